@@ -1,0 +1,45 @@
+"""Oracle-built test cases (tests only).  Inputs come from paper_2202_08627_b200.synth (draws,
+no method arithmetic) and the fp64 oracle (scaling per R16 and the noise-free model per R20);
+nothing here ever comes from the CUDA path."""
+import functools
+
+import numpy as np
+
+from oracle import ora
+from paper_2202_08627_b200 import synth
+
+
+def oracle_case(cfg: synth.Config, with_data: bool = True) -> synth.Case:
+    ang = cfg.angles
+
+    def max_shift(delta):
+        P = ora.project(delta, ang, cfg.n_det, cfg.pixel, cfg.det_pitch)
+        return float(max(np.abs(cfg.z * ora.diff_t(row, cfg.det_pitch)).max() for row in P))
+
+    def max_proj(img):
+        return float(ora.project(img, ang, cfg.n_det, cfg.pixel, cfg.det_pitch).max())
+
+    def model(case):
+        smod, _ = ora.forward(ang, case.mu, case.delta, case.sigma, case.flat, case.mask, case.drift,
+                              dx=cfg.pixel, du=cfg.det_pitch, z=cfg.z)
+        return smod
+
+    return synth.make_case(cfg, max_shift, max_proj, model if with_data else None)
+
+
+@functools.lru_cache(maxsize=None)
+def cached_case(name: str) -> synth.Case:
+    if name in synth.CONFIGS:
+        return oracle_case(synth.CONFIGS[name])
+    if name == "R1":
+        return oracle_case(synth.small_config())
+    if name == "R2":   # 180-degree span, even sizes, no drift, M=1 (the paper's single-offset case)
+        return oracle_case(synth.small_config("R2", S=1, N=40, n_angles=24, span_deg=180.0, n_det=58,
+                                              M=1, K=4, drift_sd=0.0, w_jit=0.0, texture=0.0, seed=91))
+    raise KeyError(name)
+
+
+def oracle_cost_grad(case: synth.Case, maps, lam=0.0, slices=None):
+    cfg = case.cfg
+    return ora.cost_grad(cfg.angles, *maps, case.flat, case.mask, case.drift, case.s_exp, lam,
+                         dx=cfg.pixel, du=cfg.det_pitch, z=cfg.z, slices=slices)

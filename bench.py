@@ -1,0 +1,435 @@
+#!/usr/bin/env python
+"""Benchmark of the EI cost+gradient hot path (one `ei_cost_grad` = one step).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
+
+Workload: BASELINE.json configs[1] (C2: 256x256 slice, 360 angles, 384 detector pixels, M=7)
+by default; --config C1..C5 selects another (C4 = 64-slice stack).  Inputs are synthetic
+(paper_2202_08627_b200.synth), resident in HBM before the timed region; L2 is flushed
+(256 MiB write, untimed) before every timed step.  Each step is timed with CUDA events on
+the launching stream; per-kernel times come from events the library records around its own
+launches during the same timed steps (ei_plan_set_timing).  N>1 (torchrun): one process per
+GPU, each rank evaluates its own seeded slice set (slices are independent problems,
+PAPER.md:203): no collective on the data path, weak scaling, max-over-ranks timing.
+
+`--impl reference` times the fp64 CPU oracle (oracle/, the correctness reference) on the host
+cores, on bounded samples of the same workload.  Rank 0 prints one JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import dataclasses
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_2202_08627_b200 import synth  # noqa: E402
+
+METRIC = "cost+gradient evals/sec"
+UNIT = "evals/s"
+
+
+def load_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+# ---------------------------------------------------------------------------------------
+# algorithmic counts
+# ---------------------------------------------------------------------------------------
+def ray_sample_updates(cfg) -> int:
+    """Exact number of (ray, dominant line) Joseph samples with >= 1 tap inside the grid,
+    per slice per direction (SURVEY.md §8(d) definition), in fp64."""
+    N, ND = cfg.N, cfg.n_det
+    ctr, dctr = (N - 1) / 2.0, (ND - 1) / 2.0
+    y = np.arange(N) - ctr
+    k = np.arange(ND) - dctr
+    total = 0
+    for th in cfg.angles:
+        c, s = np.cos(th), np.sin(th)
+        cd, so = (c, s) if abs(c) >= abs(s) else (s, c)
+        xs = (k[:, None] * cfg.det_pitch / cd) / cfg.pixel - (so / cd) * y[None, :] + ctr
+        total += int(np.count_nonzero((xs > -1.0) & (xs < N)))
+    return total
+
+
+def kernel_bytes(cfg, rsu):
+    """Algorithmic bytes per launch (all S slices): K1/K3 gather 2 taps x 3 fp32 maps per
+    ray-sample update (24 B, on-chip); K2 streams P (12 B) + s_exp (4M B) in and G (12 B) out
+    per (s, theta, t), flat (12 B) per (s, t)."""
+    S, NA, ND, M = cfg.S, cfg.n_angles, cfg.n_det, cfg.M
+    return {"K1_project": 24.0 * rsu * S,
+            "K3_backproject": 24.0 * rsu * S,
+            "K2_curve": float(S * NA * ND * (12 + 4 * M + 12) + S * ND * 12)}
+
+
+# ---------------------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+# ---------------------------------------------------------------------------------------
+class ClockSampler:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.samples = []
+        self.proc = None
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "--query-gpu=" + self.Q,
+                                          "--format=csv,noheader,nounits", "-lms", "100",
+                                          "-i", str(index)],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 9:
+                self.samples.append((time.time(), parts))
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self, t0, t1):
+        win = [p for (t, p) in self.samples if t0 - 0.15 <= t <= t1 + 0.15]
+        if not win and self.samples:   # timed region shorter than the sampling period
+            mid = 0.5 * (t0 + t1)
+            win = [min(self.samples, key=lambda s: abs(s[0] - mid))[1]]
+        if not win:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+        sm = [num(p[1]) for p in win if num(p[1]) is not None]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for p in win for i in range(4) if p[5 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": num(win[0][2]), "reasons": reasons, "samples": len(win),
+                "power_w_max": max((num(p[3]) or 0.0) for p in win)}
+
+
+# ---------------------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------------------
+def make_gpu_case(cfg, ei, torch):
+    """Synthetic inputs per the recipe (synth); the two model-dependent steps (R16 scaling,
+    R20 noise-free curves) use the product path itself."""
+    one = ei.Plan(1, cfg.N, cfg.n_angles, cfg.n_det, cfg.M, cfg.pixel, cfg.det_pitch, cfg.z, cfg.angles)
+    sino = torch.zeros(1, 1, cfg.n_angles, cfg.n_det, device="cuda")
+
+    def proj(img):
+        ei.ei_project(one, torch.from_numpy(np.ascontiguousarray(img, np.float32)).cuda().view(1, 1, cfg.N, cfg.N),
+                      1, sino)
+        return sino[0, 0]
+
+    def max_proj(img):
+        return float(proj(img).max())
+
+    def max_shift(delta):
+        P = proj(delta).double()
+        d = torch.empty_like(P)
+        d[:, 1:-1] = (P[:, 2:] - P[:, :-2]) / (2 * cfg.det_pitch)
+        d[:, 0] = (P[:, 1] - P[:, 0]) / cfg.det_pitch
+        d[:, -1] = (P[:, -1] - P[:, -2]) / cfg.det_pitch
+        return float((cfg.z * d).abs().max())
+
+    def model(case):
+        plan = ei.Plan(cfg.S, cfg.N, cfg.n_angles, cfg.n_det, cfg.M, cfg.pixel, cfg.det_pitch, cfg.z,
+                       cfg.angles)
+        out = torch.zeros(cfg.S, cfg.n_angles, cfg.M, cfg.n_det, device="cuda")
+        dv = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+        ei.ei_forward(plan, dv(case.mu), dv(case.delta), dv(case.sigma), dv(case.flat), dv(case.mask),
+                      None if case.drift is None else dv(case.drift), out)
+        torch.cuda.synchronize()
+        plan.destroy()
+        return out.cpu().numpy()
+
+    case = synth.make_case(cfg, max_shift, max_proj, model)
+    one.destroy()
+    return case
+
+
+def run_gpu(args, cfg, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+    from paper_2202_08627_b200 import ei
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        cfg = dataclasses.replace(cfg, seed=cfg.seed + 100000 * rank)
+    t_gen = time.time()
+    case = make_gpu_case(cfg, ei, torch)
+    t_gen = time.time() - t_gen
+    maps = synth.perturbed(case.maps(), cfg.seed + 7)          # mid-optimisation iterate (R21)
+    lam = args.lam
+    plan = ei.Plan(cfg.S, cfg.N, cfg.n_angles, cfg.n_det, cfg.M, cfg.pixel, cfg.det_pitch, cfg.z, cfg.angles)
+    dv = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+    mu, delta, sigma = (dv(m) for m in maps)
+    flat, mask = dv(case.flat), dv(case.mask)
+    drift = None if case.drift is None else dv(case.drift)
+    s_exp = dv(case.s_exp)
+    ws = ei.Workspace(plan, dev)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        ei.ei_cost_grad(plan, mu, delta, sigma, flat, mask, drift, s_exp, lam, ws.cost, ws.g[0], ws.g[1],
+                        ws.g[2], ws.status, stream)
+
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)   # 256 MiB > 126 MB L2
+    for _ in range(max(args.warmup, 3)):
+        flush.fill_(1.0)
+        step()
+    torch.cuda.synchronize()
+    # keep the GPU at load clocks for the sampler while it starts (untimed)
+    sampler = ClockSampler(local_rank) if rank == 0 else None
+    t_end = time.time() + 0.5
+    while time.time() < t_end:
+        step()
+        torch.cuda.synchronize()
+    ws.status.zero_()
+    K = args.steps
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    s0 = ei.ei_plan_stats(plan)
+    ei.ei_plan_set_timing(plan, K)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.time()
+    for i in range(K):
+        flush.fill_(1.0)                                          # untimed L2 flush
+        ev[i][0].record(stream)
+        step()
+        ev[i][1].record(stream)
+    torch.cuda.synchronize()
+    t1 = time.time()
+    if world > 1:
+        dist.barrier()
+    ms = sum(a.elapsed_time(b) for a, b in ev)
+    kern_ms, n_rec = ei.ei_plan_read_timing(plan)
+    ei.ei_plan_set_timing(plan, 0)
+    s1 = ei.ei_plan_stats(plan)
+    launches = s1[5] - s0[5]
+    status = ws.status.cpu().numpy().tolist()
+    cost0 = float(ws.cost[0].item())
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+
+    # ---- end-to-end through the host-buffer C-ABI entry point (pinned host memory) ----
+    def pinned(a):
+        t = torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+        return t.numpy()
+    h_in = [pinned(m) for m in maps] + [pinned(case.flat), pinned(case.mask)]
+    h_drift = None if case.drift is None else pinned(case.drift)
+    h_sexp = pinned(case.s_exp)
+    S, N = cfg.S, cfg.N
+    h_cost = pinned(np.zeros(S))
+    h_g = [pinned(np.zeros((S, N, N), np.float32)) for _ in range(3)]
+    h_st = pinned(np.zeros(4, np.int32))
+
+    def e2e_step():
+        ei.ei_cost_grad_host(plan, *h_in, h_drift, h_sexp, lam, h_cost, *h_g, h_st, stream)
+
+    for _ in range(2):
+        e2e_step()
+    Ke = max(1, min(K, 50))
+    ee = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(Ke)]
+    if world > 1:
+        dist.barrier()
+    for i in range(Ke):
+        flush.fill_(1.0)
+        ee[i][0].record(stream)
+        e2e_step()
+        ee[i][1].record(stream)
+    torch.cuda.synchronize()
+    e2e_ms = sum(a.elapsed_time(b) for a, b in ee) / Ke
+    if world > 1:
+        t = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    h2d = 4 * (3 * S * N * N + S * 3 * cfg.n_det + cfg.M + (cfg.n_angles if case.drift is not None else 0)
+               + S * cfg.n_angles * cfg.M * cfg.n_det)
+    d2h = 8 * S + 4 * 3 * S * N * N + 16
+    if sampler:
+        sampler.stop()
+    if rank != 0:
+        return None
+
+    clocks = sampler.summary(t0, t1)
+    peaks = load_peaks()
+    ms_step = ms / K
+    rsu = ray_sample_updates(cfg)
+    kb = kernel_bytes(cfg, rsu)
+    per_kernel_ms = {k: v / max(n_rec, 1) for k, v in kern_ms.items()}
+    dom = max(("K1_project", "K2_curve", "K3_backproject"), key=lambda k: per_kernel_ms[k])
+    sm_mhz = clocks.get("sm_mhz") or peaks.get("sm_max_mhz", 1965.0)
+    l1_peak = 128.0 * 148 * sm_mhz * 1e6 / 1e9                       # GB/s, DESIGN.md §6
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    kernels = {}
+    for k in ("K1_project", "K2_curve", "K3_backproject"):
+        bound = "hbm" if k == "K2_curve" else "l1"
+        peak = hbm_peak if bound == "hbm" else l1_peak
+        ach = kb[k] / (per_kernel_ms[k] * 1e-3) / 1e9 if per_kernel_ms[k] > 0 else 0.0
+        kernels[k] = {"ms": round(per_kernel_ms[k], 5), "share": round(per_kernel_ms[k] / ms_step, 4),
+                      "bound": bound, "achieved": round(ach, 1), "peak": round(peak, 1), "unit": "GB/s",
+                      "frac": round(ach / peak, 4), "bytes_per_launch": kb[k]}
+    for k in ("check", "K0_pack", "K4_finalize"):
+        kernels[k] = {"ms": round(per_kernel_ms[k], 5), "share": round(per_kernel_ms[k] / ms_step, 4)}
+    d = kernels[dom]
+    roofline = {"kernel": dom, "bound": d["bound"], "achieved": d["achieved"], "peak": d["peak"],
+                "unit": "GB/s", "frac": d["frac"], "traffic": None,
+                "peak_source": ("derived: 128 B/clk/SM x 148 SMs x median SM clock under load "
+                                "(%.0f MHz)" % sm_mhz) if d["bound"] == "l1" else
+                               "measured hbm_gbs (MEASURED_PEAKS.json)"}
+    value = world * 1000.0 / ms_step
+    line = {
+        "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": K,
+        "warmup": args.warmup, "ms_per_step": round(ms_step, 5), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": "%s: %s" % (cfg.name, describe(cfg)), "slices_per_gpu": cfg.S,
+                   "lambda": lam, "eval_point": "x_pert (R21)",
+                   "l2": "flushed before every timed step (256 MiB write, untimed)",
+                   "parallelism": "slice-parallel replicas" if world > 1 else "1 GPU"},
+        "ray_sample_updates_per_s": round(world * 6 * rsu * cfg.S / (ms_step * 1e-3), 1),
+        "slice_evals_per_s": round(world * cfg.S * 1000.0 / ms_step, 3),
+        "ray_sample_updates_per_eval": 6 * rsu * cfg.S,
+        "roofline": roofline, "kernels": kernels,
+        "e2e": {"value": round(world * 1000.0 / e2e_ms, 3), "unit": UNIT, "ms_per_step": round(e2e_ms, 4),
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "api": "ei_cost_grad_host (pinned host buffers)"},
+        "gpu_launches": int(launches), "launches_per_step": launches / K,
+        "clocks": clocks, "status": status, "cost_slice0": cost0, "input_gen_s": round(t_gen, 2),
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(cfg, case, maps, lam, budget_s=args.cpu_budget)
+    return line
+
+
+def describe(cfg):
+    return ("%dx %dx%d grid, %d angles over [0,%g) deg, %d detector px, M=%d" %
+            (cfg.S, cfg.N, cfg.N, cfg.n_angles, cfg.span_deg, cfg.n_det, cfg.M))
+
+
+# ---------------------------------------------------------------------------------------
+# CPU oracle timing (cpu_baseline leg and --impl reference)
+# ---------------------------------------------------------------------------------------
+def cpu_baseline(cfg, case, maps, lam, budget_s=15.0, min_units=1):
+    """Time the fp64 oracle (as it stands) on bounded samples: whole evaluations of one slice
+    each; returns evals/s of the full workload (S slices per eval)."""
+    from oracle import ora
+    t0 = time.time()
+    n = 0
+    while n < min_units or time.time() - t0 < budget_s:
+        s = n % cfg.S
+        ora.cost_grad(cfg.angles, *maps, case.flat, case.mask, case.drift, case.s_exp, lam,
+                      dx=cfg.pixel, du=cfg.det_pitch, z=cfg.z, slices=[s])
+        n += 1
+        if time.time() - t0 > budget_s:
+            break
+    dt = time.time() - t0
+    slices_per_s = n / dt
+    return {"value": round(slices_per_s / cfg.S, 6), "unit": UNIT, "cores": ora.num_threads(),
+            "kind": "oracle",
+            "sample": "%d single-slice fp64 cost+gradient evaluations of %s (%.1f s); value = "
+                      "slices/s / %d slices per eval" % (n, cfg.name, dt, cfg.S)}
+
+
+def run_reference(args, cfg, rank):
+    if rank != 0:
+        return None
+    from oracle import ora
+    ora.build()
+
+    def max_shift(delta):
+        P = ora.project(delta, cfg.angles, cfg.n_det, cfg.pixel, cfg.det_pitch)
+        return float(max(np.abs(cfg.z * ora.diff_t(r, cfg.det_pitch)).max() for r in P))
+
+    def max_proj(img):
+        return float(ora.project(img, cfg.angles, cfg.n_det, cfg.pixel, cfg.det_pitch).max())
+
+    # the oracle times on the same workload shape; s_exp only needs the right shape and value
+    # range for timing, so slices beyond the first reuse slice 0's curves
+    one = dataclasses.replace(cfg, S=1)
+    c1 = synth.make_case(one, max_shift, max_proj,
+                         lambda c: ora.forward(cfg.angles, c.mu, c.delta, c.sigma, c.flat, c.mask, c.drift,
+                                               dx=cfg.pixel, du=cfg.det_pitch, z=cfg.z)[0])
+    maps = synth.perturbed(c1.maps(), cfg.seed + 7)
+    times = []
+    for i in range(args.warmup + args.steps):
+        t = time.time()
+        ora.cost_grad(cfg.angles, *maps, c1.flat, c1.mask, c1.drift, c1.s_exp, args.lam,
+                      dx=cfg.pixel, du=cfg.det_pitch, z=cfg.z)
+        if i >= args.warmup:
+            times.append(time.time() - t)
+    per_slice = sum(times) / len(times)
+    value = 1.0 / (per_slice * cfg.S)
+    sample = ("%d timed single-slice fp64 oracle cost+gradient evaluations of %s (one slice = 1/%d "
+              "eval)" % (len(times), cfg.name, cfg.S))
+    return {"metric": METRIC, "value": round(value, 6), "unit": UNIT, "n_gpus": 0, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(per_slice * 1e3 * cfg.S, 3),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "impl": "reference",
+            "config": {"workload": "%s: %s" % (cfg.name, describe(cfg)), "lambda": args.lam},
+            "cpu_baseline": {"value": round(value, 6), "unit": UNIT, "cores": ora.num_threads(),
+                             "kind": "oracle", "sample": sample},
+            "e2e": {"value": round(value, 6), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="C2", choices=sorted(synth.CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--lam", type=float, default=1e-2)
+    ap.add_argument("--cpu-budget", type=float, default=15.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3                                           # timing rule: W >= 3
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    cfg = synth.CONFIGS[args.config]
+    if args.impl == "reference":
+        line = run_reference(args, cfg, rank)
+    else:
+        if world > 1:
+            import torch
+            import torch.distributed as dist
+            torch.cuda.set_device(local_rank)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        line = run_gpu(args, cfg, rank, world, local_rank)
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+    if line is not None:
+        print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

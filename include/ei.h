@@ -1,0 +1,135 @@
+/*
+ * include/ei.h — C ABI of libei: the B200 (sm_100a) hot path of model-based iterative
+ * edge-illumination (EI) tomography, arxiv 2202.08627 (Modregger et al.).
+ *
+ * One cost+gradient evaluation per optimizer iteration (eq. 5) of the
+ * three-map EI model (absorption mu, refractive decrement delta, scattering
+ * sigma), in four stages, all hand-written CUDA for sm_100a:
+ *   K1  Joseph projection of mu, delta, sigma at every angle (eq. 1)
+ *   K2  fused curve model / residual / cost / dS/dP (eq. 2, eq. 4 :74-75,
+ *       eq. 5 :79), including the refraction shift z d/dt R[delta]
+ *   K3  pixel-driven, atomic-free adjoint R^T of the three gradient sinograms
+ *   K4  fixed-order fp64 per-slice cost
+ *
+ * Conventions (all entry points)
+ *   - Arrays are fp32 (cost: fp64, status: int32), C-contiguous, little-endian.
+ *   - Device-pointer entry points are asynchronous on `stream` (a cudaStream_t passed as
+ *     void*; NULL = the legacy default stream) and never synchronise the host.  Device
+ *     arrays are owned by the caller; outputs are caller-allocated.
+ *   - Argument errors are returned synchronously before any launch (EI_ERR_*), and no
+ *     output is touched.  Numeric conditions in device data are counted in `status`.
+ *   - A plan owns its device workspace (allocated in ei_plan_create) and may serve one
+ *     in-flight call at a time; distinct plans are independent.
+ *   - Geometry (readings R4-R8): pixel centres x_j = (j-(N-1)/2)*pixel
+ *     (j = contiguous index), y_i = (i-(N-1)/2)*pixel; detector u_k = (k-(Nd-1)/2)*det_pitch;
+ *     the ray (theta, k) is x cos(theta) + y sin(theta) = u_k.
+ *   - Units (R3, R4): mask positions, flat-IC centre/width, drift and the refraction shift
+ *     are in mask periods; the shift is z * dR[delta]/dt with dt = det_pitch.
+ */
+#ifndef EI_H
+#define EI_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    EI_OK = 0,
+    EI_ERR_NULL = 1,      /* a required pointer is NULL                                   */
+    EI_ERR_SHAPE = 2,     /* S<1, N<2, Nd<3, n_angles<1, M<1, n_maps not 1|3  */
+    EI_ERR_DOMAIN = 3,    /* pixel/det_pitch/z <= 0 or non-finite, det_pitch < pixel,
+                             non-finite angle, lambda < 0 or non-finite                    */
+    EI_ERR_RESOURCE = 4,  /* device allocation failed / size overflow                      */
+    EI_ERR_CUDA = 5       /* a CUDA call or kernel launch failed                           */
+};
+
+typedef struct ei_geometry {
+    int32_t n_slices;   /* S: independent slices                            */
+    int32_t n;          /* N: maps are N x N                                               */
+    int32_t n_angles;   /* N_theta                                                          */
+    int32_t n_det;      /* N_d detector pixels, >= 3 (finite differences need 3)           */
+    int32_t n_mask;     /* M mask positions                                                */
+    double pixel;       /* dx, map pixel pitch                                              */
+    double det_pitch;   /* du, detector pitch; must satisfy du >= dx (<= 2 adjoint taps)   */
+    double z;           /* sample-detector distance factor of the shift      */
+} ei_geometry;
+
+typedef struct ei_plan ei_plan;   /* opaque: device angle table + workspace               */
+
+/* Create a plan.  angles_rad_host: [n_angles] host fp64 projection angles.
+ * The per-angle table (cos, sin, row/column dominance |cos| >= |sin| decided in fp64,
+ * reading R5) is built on the host and uploaded; the workspace (packed maps, P and G
+ * sinograms, reduction partials) is allocated here and nowhere else on the device path.
+ * Returns EI_OK and *out, or an error (then *out = NULL). */
+int ei_plan_create(const ei_geometry *geom, const double *angles_rad_host, ei_plan **out);
+void ei_plan_destroy(ei_plan *plan);
+
+/* R: Joseph projection (SPEC.md:49 radon_forward).
+ * maps [S][n_maps][N][N] device -> sino [S][n_maps][N_theta][N_d] device. n_maps in {1, 3}. */
+int ei_project(const ei_plan *plan, const float *maps, int n_maps, float *sino, void *stream);
+
+/* R^T: the exact transpose of ei_project, pixel-driven tent gather (a5).
+ * sino [S][n_maps][N_theta][N_d] device -> maps [S][n_maps][N][N] device (overwritten). */
+int ei_backproject(const ei_plan *plan, const float *sino, int n_maps, float *maps, void *stream);
+
+/* Forward model s_mod (SPEC.md:206 forward; eq. 2/4 with m_r = 0, scattering per R1):
+ *   mu, delta, sigma [S][N][N]; flat [S][3][N_d] = (A, c, w) of the Gaussian flat IC (R2);
+ *   mask_pos [M]; drift [N_theta] = m_o(theta) or NULL (zeros, R14)
+ *   -> s_mod [S][N_theta][M][N_d].  All device pointers. */
+int ei_forward(const ei_plan *plan, const float *mu, const float *delta, const float *sigma,
+               const float *flat, const float *mask_pos, const float *drift, float *s_mod,
+               void *stream);
+
+/* Cost and gradient (SPEC.md:261 cost + :270 grad, map blocks), eq. 5:
+ *   S_s = sum_{theta,t,m} (s_mod - s_exp)^2 + lambda * sum (mu^2 + delta^2 + sigma^2)
+ *   s_exp [S][N_theta][M][N_d]; lambda >= 0 (paper: 1e-2)
+ *   -> cost [S] fp64 device; g_mu, g_delta, g_sigma [S][N][N] device (overwritten);
+ *      status [4] int32 device, ACCUMULATED (caller zeroes it):
+ *        [0] non-finite input elements (maps, flat, mask, drift, s_exp)
+ *        [1] (s,theta,t) where P_mu was clamped to [-50, 50] (R12)
+ *        [2] (s,theta,t) where W^2 was clamped to w^2/100 (R13)
+ *        [3] reserved (0)
+ * Exactly one projection and one adjoint per map per call. */
+int ei_cost_grad(const ei_plan *plan, const float *mu, const float *delta, const float *sigma,
+                 const float *flat, const float *mask_pos, const float *drift, const float *s_exp,
+                 float lambda, double *cost, float *g_mu, float *g_delta, float *g_sigma,
+                 int32_t *status, void *stream);
+
+/* ei_cost_grad with HOST buffers (same shapes and meaning; status is overwritten, not
+ * accumulated).  Copies inputs host->device, evaluates, copies cost, gradients and status
+ * back, and synchronises `stream` before returning.  Pinned host memory makes the copies
+ * asynchronous DMA.  Device staging buffers are allocated by the first call on a plan and
+ * kept until ei_plan_destroy (EI_ERR_RESOURCE if that fails). */
+int ei_cost_grad_host(ei_plan *plan, const float *mu, const float *delta, const float *sigma,
+                      const float *flat, const float *mask_pos, const float *drift,
+                      const float *s_exp, float lambda, double *cost, float *g_mu, float *g_delta,
+                      float *g_sigma, int32_t *status, void *stream);
+
+/* Launch accounting (the "one projection + one adjoint per map per evaluation" contract):
+ * out[0] = K1 launches, out[1] = maps projected, out[2] = K3 launches, out[3] = maps
+ * back-projected, out[4] = K2 launches, out[5] = all libei kernel launches, since plan
+ * creation.  Host counters; no device synchronisation. */
+int ei_plan_stats(const ei_plan *plan, int64_t out[6]);
+
+/* Per-kernel device timing of ei_cost_grad (measurement support, bench.py).
+ * ei_plan_set_timing(plan, max_evals): from now on the next `max_evals` ei_cost_grad calls
+ * record CUDA events around each of their kernels on the call's stream (max_evals = 0
+ * disables; events are created here, EI_ERR_RESOURCE on failure).
+ * ei_plan_read_timing(plan, ms[6], n_evals): synchronises the recorded events and returns the
+ * summed milliseconds of [check, K0 pack, K1 project, K2 curve, K3 backproject, K4 finalize]
+ * over the recorded calls and their number; then resets the recording. */
+int ei_plan_set_timing(ei_plan *plan, int max_evals);
+int ei_plan_read_timing(ei_plan *plan, double ms[6], int *n_evals);
+
+/* Human-readable name of an EI_* code (static string). */
+const char *ei_error_string(int code);
+
+/* Library build identifier, e.g. "libei sm_100a <git-describe>". */
+const char *ei_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* EI_H */

@@ -1,0 +1,181 @@
+// k_curve.cu — K2: the fused curve model / residual / cost / dS/dP pass, and K4: the
+// fixed-order fp64 per-slice cost.  SURVEY.md §8(a) a2-a4, a6.
+//
+// Per detector row (s, theta) one block:
+//   Delta = z * D P_delta         finite differences along t, halo 1
+//   T     = exp(-clamp(P_mu))     eq. 2, clamp R12
+//   W^2   = max(w^2 + P_sigma, w^2/100)                 scattering broadening R1, clamp R13
+//   s_mod = T A (w/W) exp(-u^2 / 2W^2),  u = m - c - m_o(theta) - Delta   eq. 4 with m_r = 0
+//   r     = s_mod - s_exp;  S += r^2                     eq. 5
+//   g_mu = -2 sum r s;  g_Delta = 2 sum r s u / W^2;  g_sigma = sum r s (u^2 - W^2) / W^4
+//   g_delta = z D^T g_Delta                              halo 1 more (2 in total)
+// s_exp is streamed once, coalesced along t; the M mask positions are an inner loop; the
+// cost is reduced fp32 (per thread, <= M*ceil(Nd/256) terms) -> fp64 (warp shuffle, block)
+// -> one fp64 partial per row, summed in a fixed order by K4 (deterministic, atomic-free).
+#include "ei_common.cuh"
+
+namespace ei {
+namespace {
+
+constexpr int K2_THREADS = 256;
+
+__device__ __forceinline__ double block_sum(double v, double *red) {
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) red[wid] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (threadIdx.x == 0)
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+  return t;
+}
+
+// MODE 0: forward (writes s_mod); MODE 1: cost + gradient (writes G, partials)
+template <int MODE>
+__global__ void __launch_bounds__(K2_THREADS) curve_kernel(
+    const float *__restrict__ P, const float *__restrict__ flat, const float *__restrict__ mask,
+    const float *__restrict__ drift, const float *__restrict__ s_exp, int NA, int ND, int M,
+    float z, float inv_du, float *__restrict__ s_mod, float4 *__restrict__ G,
+    double *__restrict__ part, int32_t *__restrict__ status) {
+  extern __shared__ float sm[];
+  float *pd = sm;              // [ND] P_delta row
+  float *gD = sm + ND;         // [ND] g_Delta row
+  float *gmS = sm + 2 * ND;    // [ND] g_mu row
+  float *gsS = sm + 3 * ND;    // [ND] g_sigma row
+  float *smask = sm + 4 * ND;  // [M]
+  __shared__ double red[K2_THREADS / 32];
+  const int a = blockIdx.x, s = blockIdx.y;
+  const size_t plane = (size_t)NA * ND;
+  const float *Pm = P + (size_t)s * 3 * plane + (size_t)a * ND;
+  const float *Pd = Pm + plane, *Ps = Pm + 2 * plane;
+  const float *fA = flat + (size_t)s * 3 * ND, *fc = fA + ND, *fw = fA + 2 * ND;
+  for (int k = threadIdx.x; k < ND; k += blockDim.x) pd[k] = __ldg(Pd + k);
+  for (int m = threadIdx.x; m < M; m += blockDim.x) smask[m] = __ldg(mask + m);
+  __syncthreads();
+  const float mo = drift ? __ldg(drift + a) : 0.f;
+  const size_t row = ((size_t)s * NA + a) * M * ND;   // s_exp / s_mod row base
+  float cost = 0.f;
+  int bad = 0, mu_cl = 0, w2_cl = 0;
+  for (int k = threadIdx.x; k < ND; k += blockDim.x) {
+    const float dP = (k == 0) ? (pd[1] - pd[0]) * inv_du
+                   : (k == ND - 1) ? (pd[ND - 1] - pd[ND - 2]) * inv_du
+                                   : (pd[k + 1] - pd[k - 1]) * (0.5f * inv_du);
+    const float shift = z * dP;
+    float pmu = __ldg(Pm + k);
+    const bool mc = (pmu > 50.f) || (pmu < -50.f);
+    pmu = fminf(fmaxf(pmu, -50.f), 50.f);
+    const float T = expf(-pmu);
+    const float A = __ldg(fA + k), c = __ldg(fc + k), w = __ldg(fw + k);
+    float W2 = fmaf(w, w, __ldg(Ps + k));
+    const float W2min = 0.01f * w * w;
+    const bool wc = W2 < W2min;
+    W2 = wc ? W2min : W2;
+    const float invW2 = 1.0f / W2;
+    const float amp = T * A * w * sqrtf(invW2);
+    const float base = c + mo + shift;
+    mu_cl += mc;
+    w2_cl += wc;
+    float gm = 0.f, gd = 0.f, gs = 0.f;
+    for (int m = 0; m < M; ++m) {
+      const float u = smask[m] - base;
+      const float sv = amp * expf(-0.5f * u * u * invW2);
+      if (MODE == 0) {
+        s_mod[row + (size_t)m * ND + k] = sv;
+      } else {
+        const float se = __ldg(s_exp + row + (size_t)m * ND + k);
+        bad += !isfinite(se);
+        const float r = sv - se;
+        cost = fmaf(r, r, cost);
+        const float rs = r * sv;
+        gm += rs;
+        gd = fmaf(rs, u, gd);
+        gs = fmaf(rs, fmaf(u, u, -W2), gs);
+      }
+    }
+    if (MODE == 1) {
+      gmS[k] = mc ? 0.f : -2.f * gm;
+      gsS[k] = wc ? 0.f : gs * invW2 * invW2;
+      gD[k] = 2.f * gd * invW2;
+    }
+  }
+  if (MODE == 0) return;
+  __syncthreads();
+  // g_delta = z * D^T g_Delta, D^T written out from the rows of D (a2):
+  //   y[j] = [j==0](-g0) + [j==1](g0) + [j==ND-2](-g_{ND-1}) + [j==ND-1](g_{ND-1})
+  //        + 1/2 g_{j-1} [1 <= j-1 <= ND-2] - 1/2 g_{j+1} [1 <= j+1 <= ND-2]      (all / du)
+  float4 *Grow = G + (size_t)s * plane + (size_t)a * ND;
+  for (int j = threadIdx.x; j < ND; j += blockDim.x) {
+    float y = 0.f;
+    if (j == 0) y -= gD[0];
+    if (j == 1) y += gD[0];
+    if (j == ND - 2) y -= gD[ND - 1];
+    if (j == ND - 1) y += gD[ND - 1];
+    if (j - 1 >= 1 && j - 1 <= ND - 2) y += 0.5f * gD[j - 1];
+    if (j + 1 >= 1 && j + 1 <= ND - 2) y -= 0.5f * gD[j + 1];
+    Grow[j] = make_float4(gmS[j], z * inv_du * y, gsS[j], 0.f);
+  }
+  const double tot = block_sum((double)cost, red);
+  if (threadIdx.x == 0) part[(size_t)s * NA + a] = tot;
+  if (bad) atomicAdd(&status[0], bad);
+  if (mu_cl) atomicAdd(&status[1], mu_cl);
+  if (w2_cl) atomicAdd(&status[2], w2_cl);
+}
+
+// K4: cost[s] = sum_a part_curve[s][a] + lambda * sum_b part_reg[s][b], fixed order.
+__global__ void __launch_bounds__(256) finalize_kernel(const double *__restrict__ part_curve,
+                                                       int NA, const double *__restrict__ part_reg,
+                                                       int RB, float lambda,
+                                                       double *__restrict__ cost) {
+  __shared__ double red[8];
+  const int s = blockIdx.x;
+  double c = 0.0, r = 0.0;
+  for (int a = threadIdx.x; a < NA; a += blockDim.x) c += part_curve[(size_t)s * NA + a];
+  if (lambda > 0.f)
+    for (int b = threadIdx.x; b < RB; b += blockDim.x) r += part_reg[(size_t)s * RB + b];
+  const double v = c + (double)lambda * r;
+  const double tot = block_sum(v, red);
+  if (threadIdx.x == 0) cost[s] = tot;
+}
+
+}  // namespace
+
+static size_t k2_smem(const ei_plan &p) { return sizeof(float) * (4 * (size_t)p.ND + p.M); }
+
+static cudaError_t k2_attr(const void *fn, size_t smem) {
+  if (smem > 48 * 1024)
+    return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  return cudaSuccess;
+}
+
+cudaError_t launch_curve_forward(const ei_plan &p, const float *flat, const float *mask,
+                                 const float *drift, float *s_mod, cudaStream_t st) {
+  const size_t smem = k2_smem(p);
+  cudaError_t e = k2_attr((const void *)curve_kernel<0>, smem);
+  if (e != cudaSuccess) return e;
+  dim3 grid(p.NA, p.S);
+  curve_kernel<0><<<grid, K2_THREADS, smem, st>>>(p.P, flat, mask, drift, nullptr, p.NA, p.ND, p.M,
+                                                  (float)p.g.z, (float)(1.0 / p.g.det_pitch), s_mod,
+                                                  nullptr, nullptr, nullptr);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_curve_cost_grad(const ei_plan &p, const float *flat, const float *mask,
+                                   const float *drift, const float *s_exp, int32_t *status,
+                                   cudaStream_t st) {
+  const size_t smem = k2_smem(p);
+  cudaError_t e = k2_attr((const void *)curve_kernel<1>, smem);
+  if (e != cudaSuccess) return e;
+  dim3 grid(p.NA, p.S);
+  curve_kernel<1><<<grid, K2_THREADS, smem, st>>>(p.P, flat, mask, drift, s_exp, p.NA, p.ND, p.M,
+                                                  (float)p.g.z, (float)(1.0 / p.g.det_pitch), nullptr,
+                                                  p.G4, p.part_curve, status);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_finalize(const ei_plan &p, float lambda, double *cost, cudaStream_t st) {
+  finalize_kernel<<<p.S, 256, 0, st>>>(p.part_curve, p.NA, p.part_reg, p.RB, lambda, cost);
+  return cudaGetLastError();
+}
+
+}  // namespace ei

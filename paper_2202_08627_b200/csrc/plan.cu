@@ -1,0 +1,346 @@
+// plan.cu — the C ABI of libei (include/ei.h): argument validation, plan/workspace
+// management and the launch sequence of each entry point.  Host code only; the kernels
+// live in k_*.cu.  No CPU fallback exists: every numeric step runs in the kernels.
+#include <math.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <new>
+
+#include "ei_common.cuh"
+
+#ifndef EI_GIT_DESCRIBE
+#define EI_GIT_DESCRIBE "dev"
+#endif
+
+namespace {
+
+int check_geom(const ei_geometry *g) {
+  if (!g) return EI_ERR_NULL;
+  if (g->n_slices < 1 || g->n < 2 || g->n_angles < 1 || g->n_det < 3 || g->n_mask < 1)
+    return EI_ERR_SHAPE;
+  // sizes must fit the 32-bit per-slice index arithmetic of the kernels
+  if ((int64_t)g->n * g->n > (1LL << 30) || (int64_t)g->n_angles * g->n_det * g->n_mask > (1LL << 30))
+    return EI_ERR_RESOURCE;
+  // on-chip staging limits: K2 keeps 4 detector rows + the mask in shared memory, K3 the
+  // angle table (227 KB per CTA on sm_100a)
+  if (16LL * g->n_det + 4LL * g->n_mask > 220 * 1024 || 16LL * g->n_angles > 220 * 1024)
+    return EI_ERR_SHAPE;
+  if (!(isfinite(g->pixel) && isfinite(g->det_pitch) && isfinite(g->z))) return EI_ERR_DOMAIN;
+  if (g->pixel <= 0 || g->det_pitch <= 0 || g->z <= 0) return EI_ERR_DOMAIN;
+  if (g->det_pitch < g->pixel) return EI_ERR_DOMAIN;   // <= 2 taps in the adjoint (a5)
+  return EI_OK;
+}
+
+template <class T>
+cudaError_t dalloc(T **p, size_t count) {
+  return cudaMalloc((void **)p, count * sizeof(T) + 16);
+}
+
+void free_timing(ei_plan *p) {
+  if (p->tev) {
+    for (int i = 0; i < 7 * p->tcap; ++i) cudaEventDestroy(p->tev[i]);
+    delete[] p->tev;
+  }
+  p->tev = nullptr;
+  p->tcap = 0;
+  p->tn = 0;
+}
+
+void free_plan(ei_plan *p) {
+  if (!p) return;
+  free_timing(p);
+  void *ptrs[] = {p->tab.k1, p->tab.k3, p->maps4, p->maps4T, p->mapT1, p->sino4, p->P, p->G4,
+                  p->part_curve, p->part_reg, p->h_maps, p->h_flat, p->h_mask, p->h_drift,
+                  p->h_sexp, p->h_grad, p->h_cost, p->h_status};
+  for (void *q : ptrs)
+    if (q) cudaFree(q);
+  delete p;
+}
+
+inline int cuda_status(cudaError_t e) {
+  if (e == cudaSuccess) e = cudaGetLastError();
+  return e == cudaSuccess ? EI_OK : EI_ERR_CUDA;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *ei_error_string(int code) {
+  switch (code) {
+    case EI_OK: return "ok";
+    case EI_ERR_NULL: return "null pointer argument";
+    case EI_ERR_SHAPE: return "invalid shape";
+    case EI_ERR_DOMAIN: return "argument out of domain";
+    case EI_ERR_RESOURCE: return "device resource allocation failed";
+    case EI_ERR_CUDA: return "CUDA error";
+    default: return "unknown error code";
+  }
+}
+
+const char *ei_version(void) { return "libei sm_100a " EI_GIT_DESCRIBE; }
+
+int ei_plan_create(const ei_geometry *geom, const double *angles, ei_plan **out) {
+  if (!out) return EI_ERR_NULL;
+  *out = nullptr;
+  int rc = check_geom(geom);
+  if (rc) return rc;
+  if (!angles) return EI_ERR_NULL;
+  for (int a = 0; a < geom->n_angles; ++a)
+    if (!isfinite(angles[a])) return EI_ERR_DOMAIN;
+
+  ei_plan *p = new (std::nothrow) ei_plan();
+  if (!p) return EI_ERR_RESOURCE;
+  p->g = *geom;
+  p->S = geom->n_slices;
+  p->N = geom->n;
+  p->NA = geom->n_angles;
+  p->ND = geom->n_det;
+  p->M = geom->n_mask;
+  const double dx = geom->pixel, du = geom->det_pitch;
+
+  // a0: per-angle tables in fp64 -> fp32 (reading R5: row-dominant iff
+  // |cos| >= |sin| evaluated in fp64)
+  const int NA = p->NA;
+  float4 *k1 = new float4[NA], *k3 = new float4[NA];
+  for (int a = 0; a < NA; ++a) {
+    const double c = cos(angles[a]), s = sin(angles[a]);
+    const bool rowdom = fabs(c) >= fabs(s);
+    const double cd = rowdom ? c : s, so = rowdom ? s : c;
+    k1[a] = make_float4((float)(du / (cd * dx)), (float)(so / cd), (float)(dx / fabs(cd)),
+                        rowdom ? 1.f : 0.f);
+    k3[a] = make_float4((float)(c * dx / du), (float)(s * dx / du), (float)(du / (fabs(cd) * dx)),
+                        (float)(dx / fabs(cd)));
+  }
+  const size_t S = p->S, NN = (size_t)p->N * p->N, SINO = (size_t)p->NA * p->ND;
+  p->RB = ((p->N + 31) / 32) * ((p->N + 31) / 32);
+  cudaError_t e = cudaSuccess;
+  auto A = [&](cudaError_t r) { if (e == cudaSuccess) e = r; };
+  A(dalloc(&p->tab.k1, NA));
+  A(dalloc(&p->tab.k3, NA));
+  A(dalloc(&p->maps4, S * NN));
+  A(dalloc(&p->maps4T, S * NN));
+  A(dalloc(&p->mapT1, S * NN));
+  A(dalloc(&p->sino4, S * SINO));
+  A(dalloc(&p->P, S * 3 * SINO));
+  A(dalloc(&p->G4, S * SINO));
+  A(dalloc(&p->part_curve, S * NA));
+  A(dalloc(&p->part_reg, S * p->RB));
+  if (e == cudaSuccess) A(cudaMemcpy(p->tab.k1, k1, sizeof(float4) * NA, cudaMemcpyHostToDevice));
+  if (e == cudaSuccess) A(cudaMemcpy(p->tab.k3, k3, sizeof(float4) * NA, cudaMemcpyHostToDevice));
+  delete[] k1;
+  delete[] k3;
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    free_plan(p);
+    return e == cudaErrorMemoryAllocation ? EI_ERR_RESOURCE : EI_ERR_CUDA;
+  }
+  *out = p;
+  return EI_OK;
+}
+
+void ei_plan_destroy(ei_plan *plan) { free_plan(plan); }
+
+int ei_plan_stats(const ei_plan *p, int64_t out[6]) {
+  if (!p || !out) return EI_ERR_NULL;
+  for (int i = 0; i < 6; ++i) out[i] = p->stats[i];
+  return EI_OK;
+}
+
+int ei_plan_set_timing(ei_plan *p, int max_evals) {
+  if (!p) return EI_ERR_NULL;
+  if (max_evals < 0) return EI_ERR_DOMAIN;
+  free_timing(p);
+  if (max_evals == 0) return EI_OK;
+  p->tev = new (std::nothrow) cudaEvent_t[7 * (size_t)max_evals];
+  if (!p->tev) return EI_ERR_RESOURCE;
+  for (int i = 0; i < 7 * max_evals; ++i) {
+    if (cudaEventCreate(&p->tev[i]) != cudaSuccess) {
+      for (int k = 0; k < i; ++k) cudaEventDestroy(p->tev[k]);
+      delete[] p->tev;
+      p->tev = nullptr;
+      cudaGetLastError();
+      return EI_ERR_RESOURCE;
+    }
+  }
+  p->tcap = max_evals;
+  p->tn = 0;
+  return EI_OK;
+}
+
+int ei_plan_read_timing(ei_plan *p, double ms[6], int *n_evals) {
+  if (!p || !ms || !n_evals) return EI_ERR_NULL;
+  for (int k = 0; k < 6; ++k) ms[k] = 0.0;
+  for (int e = 0; e < p->tn; ++e) {
+    cudaEvent_t *ev = p->tev + 7 * e;
+    if (cudaEventSynchronize(ev[6]) != cudaSuccess) return EI_ERR_CUDA;
+    for (int k = 0; k < 6; ++k) {
+      float t = 0.f;
+      if (cudaEventElapsedTime(&t, ev[k], ev[k + 1]) != cudaSuccess) return EI_ERR_CUDA;
+      ms[k] += t;
+    }
+  }
+  *n_evals = p->tn;
+  p->tn = 0;
+  return EI_OK;
+}
+
+int ei_project(const ei_plan *p, const float *maps, int n_maps, float *sino, void *stream) {
+  if (!p || !maps || !sino) return EI_ERR_NULL;
+  if (n_maps != 1 && n_maps != 3) return EI_ERR_SHAPE;
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t NN = (size_t)p->N * p->N;
+  cudaError_t e;
+  if (n_maps == 3) {
+    // maps [S][3][N][N]: slice stride 3*NN, plane stride NN
+    e = ei::launch_pack3(*p, maps, maps + NN, maps + 2 * NN, 3 * NN, false, nullptr, st);
+    if (e == cudaSuccess) e = ei::launch_project3(*p, sino, st);
+    p->stats[0] += 1;
+    p->stats[1] += 3;
+    p->stats[5] += 2;
+  } else {
+    e = ei::launch_transpose1(*p, maps, st);
+    if (e == cudaSuccess) e = ei::launch_project1(*p, maps, sino, st);
+    p->stats[0] += 1;
+    p->stats[1] += 1;
+    p->stats[5] += 2;
+  }
+  return cuda_status(e);
+}
+
+int ei_backproject(const ei_plan *p, const float *sino, int n_maps, float *maps, void *stream) {
+  if (!p || !maps || !sino) return EI_ERR_NULL;
+  if (n_maps != 1 && n_maps != 3) return EI_ERR_SHAPE;
+  cudaStream_t st = (cudaStream_t)stream;
+  const size_t NN = (size_t)p->N * p->N;
+  cudaError_t e;
+  if (n_maps == 3) {
+    e = ei::launch_pack_sino3(*p, sino, st);
+    if (e == cudaSuccess)
+      e = ei::launch_backproject3(*p, p->sino4, nullptr, nullptr, nullptr, 0.f, maps, maps + NN,
+                                  maps + 2 * NN, 3 * NN, st);
+    p->stats[2] += 1;
+    p->stats[3] += 3;
+    p->stats[5] += 2;
+  } else {
+    e = ei::launch_backproject1(*p, sino, maps, st);
+    p->stats[2] += 1;
+    p->stats[3] += 1;
+    p->stats[5] += 1;
+  }
+  return cuda_status(e);
+}
+
+int ei_forward(const ei_plan *p, const float *mu, const float *delta, const float *sigma,
+               const float *flat, const float *mask, const float *drift, float *s_mod,
+               void *stream) {
+  if (!p || !mu || !delta || !sigma || !flat || !mask || !s_mod) return EI_ERR_NULL;
+  cudaStream_t st = (cudaStream_t)stream;
+  // maps given as three [S][N][N] arrays: plane stride handled by pack3 (slice stride NN)
+  cudaError_t e = ei::launch_pack3(*p, mu, delta, sigma, (size_t)p->N * p->N, false, nullptr, st);
+  if (e == cudaSuccess) e = ei::launch_project3(*p, p->P, st);
+  if (e == cudaSuccess) e = ei::launch_curve_forward(*p, flat, mask, drift, s_mod, st);
+  p->stats[0] += 1;
+  p->stats[1] += 3;
+  p->stats[4] += 1;
+  p->stats[5] += 3;
+  return cuda_status(e);
+}
+
+int ei_cost_grad(const ei_plan *p, const float *mu, const float *delta, const float *sigma,
+                 const float *flat, const float *mask, const float *drift, const float *s_exp,
+                 float lambda, double *cost, float *g_mu, float *g_delta, float *g_sigma,
+                 int32_t *status, void *stream) {
+  if (!p || !mu || !delta || !sigma || !flat || !mask || !s_exp || !cost || !g_mu || !g_delta ||
+      !g_sigma || !status)
+    return EI_ERR_NULL;
+  if (!(lambda >= 0.f) || !isfinite(lambda)) return EI_ERR_DOMAIN;
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaEvent_t *ev = (p->tev && p->tn < p->tcap) ? p->tev + 7 * p->tn++ : nullptr;
+  auto mark = [&](int k) { if (ev) cudaEventRecord(ev[k], st); };
+  const size_t NN = (size_t)p->N * p->N;
+  mark(0);
+  cudaError_t e = ei::launch_check_small(*p, flat, mask, drift, status, st);          // K0'
+  mark(1);
+  if (e == cudaSuccess) e = ei::launch_pack3(*p, mu, delta, sigma, NN, lambda > 0.f, status, st);  // K0
+  mark(2);
+  if (e == cudaSuccess) e = ei::launch_project3(*p, p->P, st);                      // K1
+  mark(3);
+  if (e == cudaSuccess) e = ei::launch_curve_cost_grad(*p, flat, mask, drift, s_exp, status, st);  // K2
+  mark(4);
+  if (e == cudaSuccess) e = ei::launch_backproject3(*p, p->G4, mu, delta, sigma, lambda, g_mu,
+                                                    g_delta, g_sigma, NN, st);         // K3
+  mark(5);
+  if (e == cudaSuccess) e = ei::launch_finalize(*p, lambda, cost, st);              // K4
+  mark(6);
+  p->stats[5] += 6;
+  p->stats[0] += 1;
+  p->stats[1] += 3;
+  p->stats[2] += 1;
+  p->stats[3] += 3;
+  p->stats[4] += 1;
+  return cuda_status(e);
+}
+
+int ei_cost_grad_host(ei_plan *p, const float *mu, const float *delta, const float *sigma,
+                      const float *flat, const float *mask, const float *drift,
+                      const float *s_exp, float lambda, double *cost, float *g_mu, float *g_delta,
+                      float *g_sigma, int32_t *status, void *stream) {
+  if (!p || !mu || !delta || !sigma || !flat || !mask || !s_exp || !cost || !g_mu || !g_delta ||
+      !g_sigma || !status)
+    return EI_ERR_NULL;
+  if (!(lambda >= 0.f) || !isfinite(lambda)) return EI_ERR_DOMAIN;
+  const size_t S = p->S, NN = (size_t)p->N * p->N, ND = p->ND, NA = p->NA, M = p->M;
+  const size_t nsexp = S * NA * M * ND;
+  if (!p->h_maps) {
+    cudaError_t e = cudaSuccess;
+    auto A = [&](cudaError_t r) { if (e == cudaSuccess) e = r; };
+    A(dalloc(&p->h_maps, 3 * S * NN));
+    A(dalloc(&p->h_flat, S * 3 * ND));
+    A(dalloc(&p->h_mask, M));
+    A(dalloc(&p->h_drift, NA));
+    A(dalloc(&p->h_sexp, nsexp));
+    A(dalloc(&p->h_grad, 3 * S * NN));
+    A(dalloc(&p->h_cost, S));
+    A(dalloc(&p->h_status, 4));
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      void *ptrs[] = {p->h_maps, p->h_flat, p->h_mask, p->h_drift, p->h_sexp, p->h_grad,
+                      p->h_cost, p->h_status};
+      for (void *q : ptrs)
+        if (q) cudaFree(q);
+      p->h_maps = p->h_flat = p->h_mask = p->h_drift = p->h_sexp = p->h_grad = nullptr;
+      p->h_cost = nullptr;
+      p->h_status = nullptr;
+      return EI_ERR_RESOURCE;
+    }
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e = cudaSuccess;
+  auto A = [&](cudaError_t r) { if (e == cudaSuccess) e = r; };
+  const cudaMemcpyKind H2D = cudaMemcpyHostToDevice, D2H = cudaMemcpyDeviceToHost;
+  float *dmu = p->h_maps, *ddl = p->h_maps + S * NN, *dsg = p->h_maps + 2 * S * NN;
+  A(cudaMemcpyAsync(dmu, mu, sizeof(float) * S * NN, H2D, st));
+  A(cudaMemcpyAsync(ddl, delta, sizeof(float) * S * NN, H2D, st));
+  A(cudaMemcpyAsync(dsg, sigma, sizeof(float) * S * NN, H2D, st));
+  A(cudaMemcpyAsync(p->h_flat, flat, sizeof(float) * S * 3 * ND, H2D, st));
+  A(cudaMemcpyAsync(p->h_mask, mask, sizeof(float) * M, H2D, st));
+  if (drift) A(cudaMemcpyAsync(p->h_drift, drift, sizeof(float) * NA, H2D, st));
+  A(cudaMemcpyAsync(p->h_sexp, s_exp, sizeof(float) * nsexp, H2D, st));
+  A(cudaMemsetAsync(p->h_status, 0, sizeof(int32_t) * 4, st));
+  if (e != cudaSuccess) return EI_ERR_CUDA;
+  float *gm = p->h_grad, *gd = p->h_grad + S * NN, *gs = p->h_grad + 2 * S * NN;
+  int rc = ei_cost_grad(p, dmu, ddl, dsg, p->h_flat, p->h_mask, drift ? p->h_drift : nullptr,
+                        p->h_sexp, lambda, p->h_cost, gm, gd, gs, p->h_status, stream);
+  if (rc) return rc;
+  A(cudaMemcpyAsync(cost, p->h_cost, sizeof(double) * S, D2H, st));
+  A(cudaMemcpyAsync(g_mu, gm, sizeof(float) * S * NN, D2H, st));
+  A(cudaMemcpyAsync(g_delta, gd, sizeof(float) * S * NN, D2H, st));
+  A(cudaMemcpyAsync(g_sigma, gs, sizeof(float) * S * NN, D2H, st));
+  A(cudaMemcpyAsync(status, p->h_status, sizeof(int32_t) * 4, D2H, st));
+  A(cudaStreamSynchronize(st));
+  return cuda_status(e);
+}
+
+}  // extern "C"

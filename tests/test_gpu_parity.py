@@ -1,0 +1,185 @@
+"""GPU-vs-oracle parity through the C ABI (libei.so) — needs a B200.
+
+Gates (BASELINE.json north_star): cost |S_gpu - S_ora| / S_ora <= 1e-4; s_mod and
+each gradient map relative L2 <= 1e-3; dot test |<Rx,y> - <x,R^T y>| / max <= 1e-5 with
+x, y ~ U[0,1) and fp64 inner products.  Projections alone are held to 2e-5 relative L2 (fp32
+accumulation of N samples).  Evaluation points (R21): x0 = 0, x_true, x_pert.
+Every input comes from paper_2202_08627_b200.synth + the fp64 oracle; nothing from the GPU.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+from oracle import ora  # noqa: E402
+from paper_2202_08627_b200 import synth  # noqa: E402
+import _cases  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def ei():
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    from paper_2202_08627_b200 import build
+    build.build()
+    from paper_2202_08627_b200 import ei as mod
+    return mod
+
+
+def rel_l2(a, b):
+    a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
+    return float(np.linalg.norm((a - b).ravel()) / max(np.linalg.norm(b.ravel()), 1e-300))
+
+
+def plan_for(ei, cfg, S=None):
+    return ei.Plan(cfg.S if S is None else S, cfg.N, cfg.n_angles, cfg.n_det, cfg.M, cfg.pixel,
+                   cfg.det_pitch, cfg.z, cfg.angles)
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def gpu_cost_grad(ei, plan, case, maps, lam=0.0):
+    ws = ei.Workspace(plan)
+    drift = None if case.drift is None else dev(case.drift)
+    cost, g, st = ei.cost_grad(plan, [dev(m) for m in maps], dev(case.flat), dev(case.mask), drift,
+                               dev(case.s_exp), lam, ws)
+    torch.cuda.synchronize()
+    return cost.cpu().numpy(), [x.cpu().numpy() for x in g], st.cpu().numpy()
+
+
+SMALL = ["C1", "C2", "R1", "R2"]
+
+
+@pytest.mark.parametrize("name", SMALL)
+def test_project_parity(ei, name):
+    case = _cases.cached_case(name)
+    cfg = case.cfg
+    plan = plan_for(ei, cfg)
+    maps = np.stack(case.maps(), axis=1)                               # [S][3][N][N]
+    sino = torch.zeros(cfg.S, 3, cfg.n_angles, cfg.n_det, device="cuda")
+    ei.ei_project(plan, dev(maps), 3, sino)
+    one = torch.zeros(cfg.S, 1, cfg.n_angles, cfg.n_det, device="cuda")
+    ei.ei_project(plan, dev(maps[:, 1:2].copy()), 1, one)
+    got, got1 = sino.cpu().numpy(), one.cpu().numpy()
+    for s in range(cfg.S):
+        for q in range(3):
+            ref = ora.project(maps[s, q].astype(np.float64), cfg.angles, cfg.n_det, cfg.pixel, cfg.det_pitch)
+            assert rel_l2(got[s, q], ref) < 2e-5, (s, q)
+        assert np.array_equal(got1[s, 0], got[s, 1])
+
+
+@pytest.mark.parametrize("name", SMALL)
+def test_backproject_parity(ei, name):
+    cfg = _cases.cached_case(name).cfg
+    plan = plan_for(ei, cfg)
+    y = synth.uniform((cfg.S, 3, cfg.n_angles, cfg.n_det), 11)
+    out = torch.zeros(cfg.S, 3, cfg.N, cfg.N, device="cuda")
+    ei.ei_backproject(plan, dev(y), 3, out)
+    out1 = torch.zeros(cfg.S, 1, cfg.N, cfg.N, device="cuda")
+    ei.ei_backproject(plan, dev(y[:, 2:3].copy()), 1, out1)
+    got, got1 = out.cpu().numpy(), out1.cpu().numpy()
+    for s in range(cfg.S):
+        for q in range(3):
+            ref = ora.backproject(y[s, q].astype(np.float64), cfg.angles, cfg.N, cfg.pixel, cfg.det_pitch)
+            assert rel_l2(got[s, q], ref) < 2e-5, (s, q)
+        assert np.array_equal(got1[s, 0], got[s, 2])
+
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4", "C5", "R1", "R2"])
+def test_dot_test(ei, name):
+    """<R x, y> vs <x, R^T y> with the GPU's own R and R^T (north star: <= 1e-5)."""
+    cfg = synth.CONFIGS[name] if name in synth.CONFIGS else _cases.cached_case(name).cfg
+    S = min(cfg.S, 2)
+    plan = plan_for(ei, cfg, S)
+    x = synth.uniform((S, 1, cfg.N, cfg.N), 21)
+    y = synth.uniform((S, 1, cfg.n_angles, cfg.n_det), 22)
+    Rx = torch.zeros(S, 1, cfg.n_angles, cfg.n_det, device="cuda")
+    Rty = torch.zeros(S, 1, cfg.N, cfg.N, device="cuda")
+    ei.ei_project(plan, dev(x), 1, Rx)
+    ei.ei_backproject(plan, dev(y), 1, Rty)
+    a = float(np.dot(Rx.cpu().numpy().astype(np.float64).ravel(), y.astype(np.float64).ravel()))
+    b = float(np.dot(x.astype(np.float64).ravel(), Rty.cpu().numpy().astype(np.float64).ravel()))
+    assert abs(a - b) / max(abs(a), abs(b)) <= 1e-5, (a, b)
+
+
+@pytest.mark.parametrize("name", SMALL)
+def test_forward_parity(ei, name):
+    case = _cases.cached_case(name)
+    cfg = case.cfg
+    plan = plan_for(ei, cfg)
+    smod = torch.zeros(cfg.S, cfg.n_angles, cfg.M, cfg.n_det, device="cuda")
+    drift = None if case.drift is None else dev(case.drift)
+    ei.ei_forward(plan, *[dev(m) for m in case.maps()], dev(case.flat), dev(case.mask), drift, smod)
+    ref, _ = ora.forward(cfg.angles, *case.maps(), case.flat, case.mask, case.drift,
+                         dx=cfg.pixel, du=cfg.det_pitch, z=cfg.z)
+    for s in range(cfg.S):
+        assert rel_l2(smod.cpu().numpy()[s], ref[s]) <= 1e-3
+
+
+def eval_points(case):
+    zero = tuple(np.zeros_like(m) for m in case.maps())
+    return {"x0": zero, "true": case.maps(), "pert": synth.perturbed(case.maps(), case.cfg.seed + 7)}
+
+
+@pytest.mark.parametrize("name", SMALL)
+@pytest.mark.parametrize("point", ["x0", "true", "pert"])
+def test_cost_grad_parity(ei, name, point):
+    case = _cases.cached_case(name)
+    plan = plan_for(ei, case.cfg)
+    maps = eval_points(case)[point]
+    lam = 1e-2 if point == "pert" else 0.0                              # R11: also at 1e-2
+    cost, g, st = gpu_cost_grad(ei, plan, case, maps, lam)
+    rc, rgm, rgd, rgs, rst = _cases.oracle_cost_grad(case, maps, lam)
+    assert np.all(np.abs(cost - rc) / rc <= 1e-4), (cost, rc)
+    for q, ref in enumerate((rgm, rgd, rgs)):
+        for s in range(case.cfg.S):
+            assert rel_l2(g[q][s], ref[s]) <= 1e-3, (q, s, rel_l2(g[q][s], ref[s]))
+    assert list(st[:3]) == list(rst) and st[3] == 0
+
+
+def test_status_counters_match_oracle(ei):
+    case = _cases.cached_case("R1")
+    cfg = case.cfg
+    plan = plan_for(ei, cfg)
+    mu, delta, sigma = (m.copy() for m in case.maps())
+    mu[0] *= 4000.0                         # drives P_mu past 50 on central rays (R12)
+    sigma[1] = -sigma[1] * 1e3              # negative broadening -> W^2 clamp (R13)
+    delta[1, 3, 4] = np.nan                 # one non-finite map element
+    s_exp = case.s_exp.copy()
+    s_exp[1, 1, 0, 5] = np.inf
+    c2 = synth.Case(cfg, mu, delta, sigma, case.flat, case.mask, case.drift, s_exp)
+    _, _, st = gpu_cost_grad(ei, plan, c2, (mu, delta, sigma))
+    _, _, _, _, rst = _cases.oracle_cost_grad(c2, (mu, delta, sigma))
+    assert rst[0] == 2 and rst[1] > 0 and rst[2] > 0
+    assert list(st[:3]) == list(rst)
+    # the clamped but finite slice 0 still matches (the NaN only poisons slice 1)
+    cost, g, _ = gpu_cost_grad(ei, plan, c2, (mu, delta, sigma))
+    rc, rgm, rgd, rgs, _ = _cases.oracle_cost_grad(c2, (mu, delta, sigma), slices=[0])
+    assert abs(cost[0] - rc[0]) / rc[0] <= 1e-4
+    for q, ref in enumerate((rgm, rgd, rgs)):
+        assert rel_l2(g[q][0], ref[0]) <= 1e-3, q
+
+
+def test_launch_contract_host_path_and_determinism(ei):
+    """One K1 projection and one K3 adjoint per map per evaluation;
+    the host-buffer entry point equals the device one bit for bit; repeated runs are identical."""
+    case = _cases.cached_case("R1")
+    cfg = case.cfg
+    plan = plan_for(ei, cfg)
+    s0 = ei.ei_plan_stats(plan)
+    c1, g1, st1 = gpu_cost_grad(ei, plan, case, case.maps(), 1e-2)
+    s1 = ei.ei_plan_stats(plan)
+    assert [b - a for a, b in zip(s0, s1)] == [1, 3, 1, 3, 1, 6]
+    c2, g2, _ = gpu_cost_grad(ei, plan, case, case.maps(), 1e-2)
+    assert np.array_equal(c1, c2) and all(np.array_equal(a, b) for a, b in zip(g1, g2))
+    S, N = cfg.S, cfg.N
+    cost = np.zeros(S)
+    gh = [np.zeros((S, N, N), np.float32) for _ in range(3)]
+    st = np.zeros(4, np.int32)
+    ei.ei_cost_grad_host(plan, *case.maps(), case.flat, case.mask, case.drift, case.s_exp, 1e-2,
+                         cost, *gh, st)
+    assert np.array_equal(cost, c1) and all(np.array_equal(a, b) for a, b in zip(gh, g1))
+    assert np.array_equal(st, st1)

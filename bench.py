@@ -231,6 +231,7 @@ def run_gpu(args, cfg, rank, world, local_rank):
     ei.ei_plan_set_timing(plan, 0)
     s1 = ei.ei_plan_stats(plan)
     launches = s1[5] - s0[5]
+    plan_info = ei.ei_plan_info(plan)
     status = ws.status.cpu().numpy().tolist()
     cost0 = float(ws.cost[0].item())
     if world > 1:
@@ -321,7 +322,7 @@ def run_gpu(args, cfg, rank, world, local_rank):
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "api": "ei_cost_grad_host (pinned host buffers)"},
         "gpu_launches": int(launches), "launches_per_step": launches / K,
-        "clocks": clocks, "status": status, "cost_slice0": cost0, "input_gen_s": round(t_gen, 2),
+        "clocks": clocks, "status": status, "plan": plan_info, "cost_slice0": cost0, "input_gen_s": round(t_gen, 2),
     }
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(cfg, case, maps, lam, budget_s=args.cpu_budget)

@@ -4,6 +4,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <vector>
+
 #include "../../include/ei.h"
 
 namespace ei {
@@ -20,19 +22,39 @@ struct Tables {
   float4 *k3 = nullptr;
 };
 
+// K1 launch plan (k_project.cu: plan_projector)
+struct ProjPlan {
+  int2 *groups = nullptr;   // device: {first sorted position, count} per angle group
+  int *order = nullptr;     // device: sorted position -> angle index (row-dominant first)
+  int n_groups = 0;
+  int RC = 0;               // rows per staged chunk
+  int CW = 0;               // window width bound (entries)
+  int RS = 1;               // row split of the cost path (partial P summed by K2)
+  int2 *win1 = nullptr;     // device window table for RS = 1  [groups][tiles][nch1]
+  int2 *winRS = nullptr;    // device window table for RS      [RS][groups][tiles][nchRS]
+  int nch1 = 0, nchRS = 0;
+};
+
 }  // namespace ei
 
 struct ei_plan {
   ei_geometry g{};
   int S = 0, N = 0, NA = 0, ND = 0, M = 0;
   ei::Tables tab;
+  ei::ProjPlan proj;
   // workspace (allocated in ei_plan_create only)
-  float4 *maps4 = nullptr;    // [S][N][N]   (mu, delta, sigma, 0)
-  float4 *maps4T = nullptr;   // [S][N][N]   transposed copy (column-dominant angles, H2)
-  float *mapT1 = nullptr;     // [S][N][N]   transposed single map (ei_project n_maps=1)
-  float4 *sino4 = nullptr;    // [S][NA][ND] packed sinogram (ei_backproject n_maps=3)
-  float *P = nullptr;         // [S][3][NA][ND] projections
-  float4 *G4 = nullptr;       // [S][NA][ND]  (g_mu, g_delta, g_sigma, 0)
+  // maps in the PAIR layout (k_pack.cu): row length N+1, entry e = (x[e-1], x[e]);
+  // *T = the transposed maps (column-dominant angles, H2)
+  float4 *MA = nullptr, *MAT = nullptr;   // [S][N][N+1] (mu0, mu1, delta0, delta1)
+  float2 *MB = nullptr, *MBT = nullptr;   // [S][N][N+1] (sigma0, sigma1)
+  float2 *M1 = nullptr, *M1T = nullptr;   // [S][N][N+1] single map (ei_project n_maps=1)
+  float *P = nullptr;         // [RS][S][3][NA][ND] (partial) projections
+  int32_t *diag = nullptr;    // device counter of internal window overflows (must stay 0)
+  // gradient sinograms in the PAIR layout read by K3: row length ND+1, entry e holds
+  // (g[e-1], g[e]) (zero outside [0, ND)):  GA = (mu0, mu1, delta0, delta1), GB = (sigma0, sigma1)
+  float4 *GA = nullptr;       // [S][NA][ND+1]
+  float2 *GB = nullptr;       // [S][NA][ND+1]
+  float2 *GA1 = nullptr;      // [S][NA][ND+1]  single-map pairs (ei_backproject n_maps=1)
   double *part_curve = nullptr;  // [S][NA] per-row cost partials (K2)
   double *part_reg = nullptr;    // [S][RB] per-tile sum x^2 partials (K0)
   int RB = 0;
@@ -50,16 +72,19 @@ struct ei_plan {
 };
 
 namespace ei {
+int plan_projector(ei_plan &p, const double *angles, std::vector<int2> &groups,
+                   std::vector<int> &order, std::vector<int2> &win1, std::vector<int2> &winRS);
 // K0 (k_pack.cu)
 cudaError_t launch_pack3(const ei_plan &p, const float *mu, const float *delta, const float *sigma,
                          size_t in_stride, bool want_reg, int32_t *status, cudaStream_t st);
-cudaError_t launch_transpose1(const ei_plan &p, const float *map, cudaStream_t st);
-cudaError_t launch_pack_sino3(const ei_plan &p, const float *sino, cudaStream_t st);
+cudaError_t launch_pack1(const ei_plan &p, const float *map, cudaStream_t st);
+int reg_blocks(int N);
+cudaError_t launch_pack_sino(const ei_plan &p, const float *sino, int n_maps, cudaStream_t st);
 cudaError_t launch_check_small(const ei_plan &p, const float *flat, const float *mask,
                                const float *drift, int32_t *status, cudaStream_t st);
 // K1 (k_project.cu)
-cudaError_t launch_project3(const ei_plan &p, float *P, cudaStream_t st);
-cudaError_t launch_project1(const ei_plan &p, const float *map, float *P, cudaStream_t st);
+cudaError_t launch_project3(const ei_plan &p, float *P, int RS, cudaStream_t st);
+cudaError_t launch_project1(const ei_plan &p, float *P, cudaStream_t st);
 // K2 / K4 (k_curve.cu)
 cudaError_t launch_curve_forward(const ei_plan &p, const float *flat, const float *mask,
                                  const float *drift, float *s_mod, cudaStream_t st);
@@ -68,8 +93,8 @@ cudaError_t launch_curve_cost_grad(const ei_plan &p, const float *flat, const fl
                                    cudaStream_t st);
 cudaError_t launch_finalize(const ei_plan &p, float lambda, double *cost, cudaStream_t st);
 // K3 (k_backproject.cu)
-cudaError_t launch_backproject3(const ei_plan &p, const float4 *G, const float *mu,
-                                const float *delta, const float *sigma, float lambda, float *g_mu,
-                                float *g_delta, float *g_sigma, size_t out_stride, cudaStream_t st);
-cudaError_t launch_backproject1(const ei_plan &p, const float *sino, float *map, cudaStream_t st);
+cudaError_t launch_backproject3(const ei_plan &p, const float *mu, const float *delta,
+                                const float *sigma, float lambda, float *g_mu, float *g_delta,
+                                float *g_sigma, size_t out_stride, cudaStream_t st);
+cudaError_t launch_backproject1(const ei_plan &p, float *map, cudaStream_t st);
 }  // namespace ei

@@ -1,109 +1,216 @@
 // k_backproject.cu — K3: the adjoint R^T as a pixel-driven, atomic-free tent gather
 // ("exact algebraic transpose").  For pixel (i, j) and
 // angle theta the Joseph weight of ray k is (dx/|c_dom|) max(0, 1 - |k - k*|/h) with
-// k* = (x_j cos + y_i sin)/du + (Nd-1)/2 and h = |c_dom| dx/du <= 1, so at most the two
-// detector taps floor(k*) and floor(k*)+1 contribute (du >= dx is enforced by the plan).
-// One thread = one pixel; it loops over all angles; nothing is scattered, so the result is
-// deterministic.  The cost path adds the eq. 5 regulariser gradient 2 lambda x here.
+// k* = (x_j cos + y_i sin)/du + (Nd-1)/2 and h = |c_dom| dx/du <= 1, so only the detector pair
+// (floor(k*), floor(k*)+1) contributes (du >= dx is enforced by the plan).
+//
+// B200 design:
+//  * gradient sinograms arrive in a PAIR layout written by K2: entry e of a row holds
+//    (g[e-1], g[e]) for every map, so one tap pair of all three maps is one LDS.128 + one LDS.64
+//    (A = (mu0, mu1, delta0, delta1), B = (sigma0, sigma1)); row length Nd+1 (e = 0..Nd).
+//  * a CTA owns a 32x32 pixel tile (256 threads x 4 pixels) and walks the angles in chunks of
+//    32; for each angle it stages only the 48-entry detector window the tile projects onto
+//    (cp.async, double-buffered, zero-filled outside the detector), so the whole gather runs
+//    from shared memory;
+//  * a warp covers an 8x4 pixel sub-tile, whose taps fall on ~10 consecutive window entries:
+//    lanes share (broadcast) most loads, ~3 shared-memory wavefronts per 32 pixel-angles;
+//  * the pair products accumulate with FFMA2 (__ffma2_rn: two fp32 FMAs per instruction on
+//    sm_100a): acc.x collects the left taps, acc.y the right taps, summed once at the end.
+// Nothing is scattered: deterministic.  The cost path adds 2*lambda*x (eq. 5).
 #include "ei_common.cuh"
 
 namespace ei {
 namespace {
 
-constexpr int BX = 32, BY = 8;
+constexpr int TILE = 32;   // pixels per side
+constexpr int CH = 32;     // angles per staged chunk
+constexpr int WL = 48;     // window entries per angle (>= 31*sqrt(2) + 4)
+constexpr int NT = 256;
 
-template <int NMAP>
-struct GT;
-template <>
-struct GT<3> {
-  using T = float4;
-};
-template <>
-struct GT<1> {
-  using T = float;
-};
-
-__device__ __forceinline__ void fma_acc(float4 &acc, float w, float4 g) {
-  acc.x = fmaf(w, g.x, acc.x);
-  acc.y = fmaf(w, g.y, acc.y);
-  acc.z = fmaf(w, g.z, acc.z);
+__device__ __forceinline__ void cp_async(void *smem, const void *gmem, int bytes, bool valid) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  if (bytes == 16)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(valid ? 16 : 0));
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(valid ? 8 : 0));
 }
-__device__ __forceinline__ void fma_acc(float &acc, float w, float g) { acc = fmaf(w, g, acc); }
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
 template <int NMAP>
-__global__ void __launch_bounds__(BX *BY) backproject_kernel(
-    const typename GT<NMAP>::T *__restrict__ G, const float4 *__restrict__ k3, int N, int NA,
-    int ND, const float *__restrict__ mu, const float *__restrict__ delta,
-    const float *__restrict__ sigma, float lambda, float *__restrict__ o0, float *__restrict__ o1,
-    float *__restrict__ o2, size_t out_stride) {
-  using T = typename GT<NMAP>::T;
-  extern __shared__ float4 stab[];   // [NA] angle table
-  for (int a = threadIdx.y * BX + threadIdx.x; a < NA; a += BX * BY) stab[a] = __ldg(k3 + a);
-  __syncthreads();
-  const int j = blockIdx.x * BX + threadIdx.x, i = blockIdx.y * BY + threadIdx.y;
+struct Layout;
+template <>
+struct Layout<3> {   // A = (mu0, mu1, delta0, delta1), B = (sigma0, sigma1)
+  using A = float4;
+  static constexpr bool hasB = true;
+};
+template <>
+struct Layout<1> {   // A = (g0, g1)
+  using A = float2;
+  static constexpr bool hasB = false;
+};
+
+template <int NMAP>
+struct Smem {
+  typename Layout<NMAP>::A a[2][CH][WL];
+  float2 b[2][CH][Layout<NMAP>::hasB ? WL : 1];
+  float4 tab[2][CH];
+  int ws[2][CH];
+};
+
+template <int NMAP>
+__global__ void __launch_bounds__(NT, 2) backproject_kernel(
+    const typename Layout<NMAP>::A *__restrict__ GA, const float2 *__restrict__ GB,
+    const float4 *__restrict__ k3, int N, int NA, int ND, const float *__restrict__ mu,
+    const float *__restrict__ delta, const float *__restrict__ sigma, float lambda,
+    float *__restrict__ o0, float *__restrict__ o1, float *__restrict__ o2, size_t out_stride) {
+  using TA = typename Layout<NMAP>::A;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  Smem<NMAP> &sm = *reinterpret_cast<Smem<NMAP> *>(smem_raw);
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int s = blockIdx.z;
-  if (i >= N || j >= N) return;
+  const int j0 = blockIdx.x * TILE, i0 = blockIdx.y * TILE;
+  const int row = 4 * w + (lane >> 3), lx = lane & 7;
   const float ctr = 0.5f * (float)(N - 1), dctr = 0.5f * (float)(ND - 1);
-  const float xj = (float)j - ctr, yi = (float)i - ctr;
-  const T *Gs = G + (size_t)s * NA * ND;
-  T acc;
-  if constexpr (NMAP == 3) acc = make_float4(0.f, 0.f, 0.f, 0.f); else acc = 0.f;
-  for (int a = 0; a < NA; ++a) {
-    const float4 t = stab[a];   // cdu, sdu, inv_h, scale
-    const float ks = fmaf(xj, t.x, fmaf(yi, t.y, dctr));
-    const float f = floorf(ks);
-    const int k0 = (int)f;
-    const float fr = ks - f;
-    const float w0 = fmaxf(0.f, fmaf(-fr, t.z, 1.f)) * t.w;
-    const float w1 = fmaxf(0.f, fmaf(fr - 1.f, t.z, 1.f)) * t.w;
-    const T *row = Gs + (size_t)a * ND;
-    if (k0 >= 0 && k0 < ND) fma_acc(acc, w0, __ldg(row + k0));
-    if (k0 + 1 >= 0 && k0 + 1 < ND) fma_acc(acc, w1, __ldg(row + k0 + 1));
-  }
-  const size_t q = (size_t)i * N + j;
-  const size_t oo = (size_t)s * out_stride + q;
-  if constexpr (NMAP == 3) {
-    if (mu) {   // cost path: + 2 lambda x (eq. 5); maps have slice stride N*N
-      const size_t iq = (size_t)s * N * N + q;
-      const float l2 = 2.f * lambda;
-      acc.x = fmaf(l2, __ldg(mu + iq), acc.x);
-      acc.y = fmaf(l2, __ldg(delta + iq), acc.y);
-      acc.z = fmaf(l2, __ldg(sigma + iq), acc.z);
+  const float yi = (float)(i0 + row) - ctr;
+  float xq[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) xq[q] = (float)(j0 + lx + 8 * q) - ctr;
+  // tile corners (full 32x32 tile, even past the map edge, so every lane indexes the window)
+  const float xa = (float)j0 - ctr, xb = xa + (float)(TILE - 1);
+  const float ya = (float)i0 - ctr, yb = ya + (float)(TILE - 1);
+  const size_t rowlen = (size_t)ND + 1;
+  const TA *GAs = GA + (size_t)s * NA * rowlen;
+  const float2 *GBs = GB ? GB + (size_t)s * NA * rowlen : nullptr;
+  const int nch = (NA + CH - 1) / CH;
+
+  auto prep = [&](int c, int buf) {   // per-angle table + window start, threads < CH
+    if (tid < CH) {
+      const int a = c * CH + tid;
+      float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
+      int ws = 0;
+      if (a < NA) {
+        const float4 g = __ldg(k3 + a);   // cdu, sdu, inv_h, scale
+        const float k00 = fmaf(xa, g.x, fmaf(ya, g.y, dctr)), k01 = fmaf(xb, g.x, fmaf(ya, g.y, dctr));
+        const float k10 = fmaf(xa, g.x, fmaf(yb, g.y, dctr)), k11 = fmaf(xb, g.x, fmaf(yb, g.y, dctr));
+        const float kmin = fminf(fminf(k00, k01), fminf(k10, k11));
+        ws = (int)floorf(kmin) - 1;
+        t = make_float4(g.x, g.y, g.w * g.z, g.w);   // cdu, sdu, scale/h, scale
+      }
+      sm.tab[buf][tid] = t;
+      sm.ws[buf][tid] = ws;
     }
-    o0[oo] = acc.x;
-    o1[oo] = acc.y;
-    o2[oo] = acc.z;
-  } else {
-    o0[oo] = acc;
+  };
+  auto stage = [&](int c, int buf) {   // window entries -> shared (zero outside [0, ND])
+    const int na = min(CH, NA - c * CH);
+    for (int e = tid; e < na * WL; e += NT) {
+      const int al = e / WL, r = e - al * WL;
+      const int a = c * CH + al;
+      const int ent = sm.ws[buf][al] + 1 + r;   // entry index = k + 1
+      const bool ok = (ent >= 0) && (ent <= ND);
+      const size_t off = (size_t)a * rowlen + (ok ? ent : 0);
+      cp_async(&sm.a[buf][al][r], GAs + off, (int)sizeof(TA), ok);
+      if (Layout<NMAP>::hasB) cp_async(&sm.b[buf][al][r], GBs + off, 8, ok);
+    }
+    cp_commit();
+  };
+
+  float2 am[4], ad[4], as[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) am[q] = ad[q] = as[q] = make_float2(0.f, 0.f);
+
+  prep(0, 0);
+  __syncthreads();
+  stage(0, 0);
+  for (int c = 0; c < nch; ++c) {
+    const int b = c & 1;
+    if (c + 1 < nch) prep(c + 1, b ^ 1);
+    __syncthreads();
+    if (c + 1 < nch) {
+      stage(c + 1, b ^ 1);
+      cp_wait<1>();
+    } else {
+      cp_wait<0>();
+    }
+    __syncthreads();
+    const int na = min(CH, NA - c * CH);
+    for (int al = 0; al < na; ++al) {
+      const float4 t = sm.tab[b][al];
+      const float base = fmaf(yi, t.y, dctr - (float)sm.ws[b][al]);
+      const float c1 = t.w - t.z;
+      const TA *arow = sm.a[b][al];
+      const float2 *brow = sm.b[b][Layout<NMAP>::hasB ? al : 0];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float ks = fmaf(xq[q], t.x, base);   // window-local k*, > 0
+        const int k0 = __float2int_rd(ks);
+        const float fr = ks - (float)k0;
+        const float2 wt = make_float2(fmaxf(0.f, fmaf(-fr, t.z, t.w)), fmaxf(0.f, fmaf(fr, t.z, c1)));
+        const TA ga = arow[k0];
+        if constexpr (NMAP == 3) {
+          am[q] = __ffma2_rn(wt, make_float2(ga.x, ga.y), am[q]);
+          ad[q] = __ffma2_rn(wt, make_float2(ga.z, ga.w), ad[q]);
+          as[q] = __ffma2_rn(wt, brow[k0], as[q]);
+        } else {
+          am[q] = __ffma2_rn(wt, ga, am[q]);
+        }
+      }
+    }
+    __syncthreads();
   }
+
+  const int i = i0 + row;
+  if (i >= N) return;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int j = j0 + lx + 8 * q;
+    if (j >= N) continue;
+    const size_t p = (size_t)i * N + j;
+    const size_t oo = (size_t)s * out_stride + p;
+    float vm = am[q].x + am[q].y;
+    if constexpr (NMAP == 3) {
+      float vd = ad[q].x + ad[q].y, vs = as[q].x + as[q].y;
+      if (mu) {   // cost path: + 2 lambda x (eq. 5); maps have slice stride N*N
+        const size_t ip = (size_t)s * N * N + p;
+        const float l2 = 2.f * lambda;
+        vm = fmaf(l2, __ldg(mu + ip), vm);
+        vd = fmaf(l2, __ldg(delta + ip), vd);
+        vs = fmaf(l2, __ldg(sigma + ip), vs);
+      }
+      o0[oo] = vm;
+      o1[oo] = vd;
+      o2[oo] = vs;
+    } else {
+      o0[oo] = vm;
+    }
+  }
+}
+
+template <int NMAP>
+cudaError_t launch_bp(const ei_plan &p, const typename Layout<NMAP>::A *GA, const float2 *GB,
+                      const float *mu, const float *delta, const float *sigma, float lambda,
+                      float *o0, float *o1, float *o2, size_t out_stride, cudaStream_t st) {
+  const size_t smem = sizeof(Smem<NMAP>);
+  cudaError_t e = cudaFuncSetAttribute((const void *)backproject_kernel<NMAP>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  dim3 grid((p.N + TILE - 1) / TILE, (p.N + TILE - 1) / TILE, p.S);
+  backproject_kernel<NMAP><<<grid, NT, smem, st>>>(GA, GB, p.tab.k3, p.N, p.NA, p.ND, mu, delta,
+                                                   sigma, lambda, o0, o1, o2, out_stride);
+  return cudaGetLastError();
 }
 
 }  // namespace
 
-template <int NMAP>
-static cudaError_t launch_bp(const ei_plan &p, const typename GT<NMAP>::T *G, const float *mu,
-                             const float *delta, const float *sigma, float lambda, float *o0,
-                             float *o1, float *o2, size_t out_stride, cudaStream_t st) {
-  const size_t smem = sizeof(float4) * p.NA;
-  if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute((const void *)backproject_kernel<NMAP>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-  }
-  dim3 grid((p.N + BX - 1) / BX, (p.N + BY - 1) / BY, p.S), block(BX, BY);
-  backproject_kernel<NMAP><<<grid, block, smem, st>>>(G, p.tab.k3, p.N, p.NA, p.ND, mu, delta, sigma,
-                                                      lambda, o0, o1, o2, out_stride);
-  return cudaGetLastError();
+cudaError_t launch_backproject3(const ei_plan &p, const float *mu, const float *delta,
+                                const float *sigma, float lambda, float *g_mu, float *g_delta,
+                                float *g_sigma, size_t out_stride, cudaStream_t st) {
+  return launch_bp<3>(p, p.GA, p.GB, mu, delta, sigma, lambda, g_mu, g_delta, g_sigma, out_stride, st);
 }
 
-cudaError_t launch_backproject3(const ei_plan &p, const float4 *G, const float *mu,
-                                const float *delta, const float *sigma, float lambda, float *g_mu,
-                                float *g_delta, float *g_sigma, size_t out_stride, cudaStream_t st) {
-  return launch_bp<3>(p, G, mu, delta, sigma, lambda, g_mu, g_delta, g_sigma, out_stride, st);
-}
-
-cudaError_t launch_backproject1(const ei_plan &p, const float *sino, float *map, cudaStream_t st) {
-  return launch_bp<1>(p, sino, nullptr, nullptr, nullptr, 0.f, map, nullptr, nullptr,
+cudaError_t launch_backproject1(const ei_plan &p, float *map, cudaStream_t st) {
+  return launch_bp<1>(p, p.GA1, nullptr, nullptr, nullptr, nullptr, 0.f, map, nullptr, nullptr,
                       (size_t)p.N * p.N, st);
 }
 

@@ -34,10 +34,11 @@ __device__ __forceinline__ double block_sum(double v, double *red) {
 // MODE 0: forward (writes s_mod); MODE 1: cost + gradient (writes G, partials)
 template <int MODE>
 __global__ void __launch_bounds__(K2_THREADS) curve_kernel(
-    const float *__restrict__ P, const float *__restrict__ flat, const float *__restrict__ mask,
-    const float *__restrict__ drift, const float *__restrict__ s_exp, int NA, int ND, int M,
-    float z, float inv_du, float *__restrict__ s_mod, float4 *__restrict__ G,
-    double *__restrict__ part, int32_t *__restrict__ status) {
+    const float *__restrict__ P, int RS, int S, const float *__restrict__ flat,
+    const float *__restrict__ mask, const float *__restrict__ drift,
+    const float *__restrict__ s_exp, int NA, int ND, int M,
+    float z, float inv_du, float *__restrict__ s_mod, float4 *__restrict__ GA,
+    float2 *__restrict__ GB, double *__restrict__ part, int32_t *__restrict__ status) {
   extern __shared__ float sm[];
   float *pd = sm;              // [ND] P_delta row
   float *gD = sm + ND;         // [ND] g_Delta row
@@ -47,10 +48,17 @@ __global__ void __launch_bounds__(K2_THREADS) curve_kernel(
   __shared__ double red[K2_THREADS / 32];
   const int a = blockIdx.x, s = blockIdx.y;
   const size_t plane = (size_t)NA * ND;
+  // P holds RS row-split partial projections [RS][S][3][NA][ND]: summed here in fixed order
   const float *Pm = P + (size_t)s * 3 * plane + (size_t)a * ND;
   const float *Pd = Pm + plane, *Ps = Pm + 2 * plane;
+  const size_t rstride = (size_t)S * 3 * plane;
+  auto psum = [&](const float *b, int k) {
+    float v = __ldg(b + k);
+    for (int r = 1; r < RS; ++r) v += __ldg(b + r * rstride + k);
+    return v;
+  };
   const float *fA = flat + (size_t)s * 3 * ND, *fc = fA + ND, *fw = fA + 2 * ND;
-  for (int k = threadIdx.x; k < ND; k += blockDim.x) pd[k] = __ldg(Pd + k);
+  for (int k = threadIdx.x; k < ND; k += blockDim.x) pd[k] = psum(Pd, k);
   for (int m = threadIdx.x; m < M; m += blockDim.x) smask[m] = __ldg(mask + m);
   __syncthreads();
   const float mo = drift ? __ldg(drift + a) : 0.f;
@@ -62,12 +70,12 @@ __global__ void __launch_bounds__(K2_THREADS) curve_kernel(
                    : (k == ND - 1) ? (pd[ND - 1] - pd[ND - 2]) * inv_du
                                    : (pd[k + 1] - pd[k - 1]) * (0.5f * inv_du);
     const float shift = z * dP;
-    float pmu = __ldg(Pm + k);
+    float pmu = psum(Pm, k);
     const bool mc = (pmu > 50.f) || (pmu < -50.f);
     pmu = fminf(fmaxf(pmu, -50.f), 50.f);
     const float T = expf(-pmu);
     const float A = __ldg(fA + k), c = __ldg(fc + k), w = __ldg(fw + k);
-    float W2 = fmaf(w, w, __ldg(Ps + k));
+    float W2 = fmaf(w, w, psum(Ps, k));
     const float W2min = 0.01f * w * w;
     const bool wc = W2 < W2min;
     W2 = wc ? W2min : W2;
@@ -104,7 +112,6 @@ __global__ void __launch_bounds__(K2_THREADS) curve_kernel(
   // g_delta = z * D^T g_Delta, D^T written out from the rows of D (a2):
   //   y[j] = [j==0](-g0) + [j==1](g0) + [j==ND-2](-g_{ND-1}) + [j==ND-1](g_{ND-1})
   //        + 1/2 g_{j-1} [1 <= j-1 <= ND-2] - 1/2 g_{j+1} [1 <= j+1 <= ND-2]      (all / du)
-  float4 *Grow = G + (size_t)s * plane + (size_t)a * ND;
   for (int j = threadIdx.x; j < ND; j += blockDim.x) {
     float y = 0.f;
     if (j == 0) y -= gD[0];
@@ -113,7 +120,17 @@ __global__ void __launch_bounds__(K2_THREADS) curve_kernel(
     if (j == ND - 1) y += gD[ND - 1];
     if (j - 1 >= 1 && j - 1 <= ND - 2) y += 0.5f * gD[j - 1];
     if (j + 1 >= 1 && j + 1 <= ND - 2) y -= 0.5f * gD[j + 1];
-    Grow[j] = make_float4(gmS[j], z * inv_du * y, gsS[j], 0.f);
+    pd[j] = z * inv_du * y;   // g_delta row (P_delta row no longer needed)
+  }
+  __syncthreads();
+  // pair layout for K3: entry e = (g[e-1], g[e]), e = 0..ND, zero outside the detector
+  const size_t rl = (size_t)ND + 1;
+  float4 *Arow = GA + ((size_t)s * NA + a) * rl;
+  float2 *Brow = GB + ((size_t)s * NA + a) * rl;
+  for (int e = threadIdx.x; e <= ND; e += blockDim.x) {
+    const bool l = e >= 1, r = e < ND;
+    Arow[e] = make_float4(l ? gmS[e - 1] : 0.f, r ? gmS[e] : 0.f, l ? pd[e - 1] : 0.f, r ? pd[e] : 0.f);
+    Brow[e] = make_float2(l ? gsS[e - 1] : 0.f, r ? gsS[e] : 0.f);
   }
   const double tot = block_sum((double)cost, red);
   if (threadIdx.x == 0) part[(size_t)s * NA + a] = tot;
@@ -154,9 +171,9 @@ cudaError_t launch_curve_forward(const ei_plan &p, const float *flat, const floa
   cudaError_t e = k2_attr((const void *)curve_kernel<0>, smem);
   if (e != cudaSuccess) return e;
   dim3 grid(p.NA, p.S);
-  curve_kernel<0><<<grid, K2_THREADS, smem, st>>>(p.P, flat, mask, drift, nullptr, p.NA, p.ND, p.M,
+  curve_kernel<0><<<grid, K2_THREADS, smem, st>>>(p.P, p.proj.RS, p.S, flat, mask, drift, nullptr, p.NA, p.ND, p.M,
                                                   (float)p.g.z, (float)(1.0 / p.g.det_pitch), s_mod,
-                                                  nullptr, nullptr, nullptr);
+                                                  nullptr, nullptr, nullptr, nullptr);
   return cudaGetLastError();
 }
 
@@ -167,9 +184,9 @@ cudaError_t launch_curve_cost_grad(const ei_plan &p, const float *flat, const fl
   cudaError_t e = k2_attr((const void *)curve_kernel<1>, smem);
   if (e != cudaSuccess) return e;
   dim3 grid(p.NA, p.S);
-  curve_kernel<1><<<grid, K2_THREADS, smem, st>>>(p.P, flat, mask, drift, s_exp, p.NA, p.ND, p.M,
+  curve_kernel<1><<<grid, K2_THREADS, smem, st>>>(p.P, p.proj.RS, p.S, flat, mask, drift, s_exp, p.NA, p.ND, p.M,
                                                   (float)p.g.z, (float)(1.0 / p.g.det_pitch), nullptr,
-                                                  p.G4, p.part_curve, status);
+                                                  p.GA, p.GB, p.part_curve, status);
   return cudaGetLastError();
 }
 

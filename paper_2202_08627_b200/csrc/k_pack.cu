@@ -1,49 +1,94 @@
-// k_pack.cu — K0: pack the three maps into float4 (mu, delta, sigma, 0) in row-major and
-// transposed order (hard part H2: column-dominant angles read the
-// transposed copy so every projector load runs along a contiguous row), count non-finite
-// inputs into status[0], and emit per-tile sum(x^2) partials for the eq. 5 regulariser.
+// k_pack.cu — K0: re-layout the maps for the projector.
+//
+// PAIR layout: the Joseph sample at x* needs (x[j0], x[j0+1]) with j0 = floor(x*).  K0 writes,
+// for every map row, N+1 entries where entry e = (x[e-1], x[e]) (zero outside the row), so the
+// projector fetches the tap pair of all three maps with one 16-B + one 8-B shared-memory load:
+//   MA[e] = (mu[e-1], mu[e], delta[e-1], delta[e]),  MB[e] = (sigma[e-1], sigma[e]).
+// The same is written for the TRANSPOSED maps (rows = columns): column-dominant angles are
+// projected as row-dominant angles of the transposed map with (cos, sin) swapped (hard part H2),
+// so the projector only ever walks contiguous rows.
+// K0 also counts non-finite map elements into status[0] and emits per-tile sum(x^2) partials for
+// the eq. 5 regulariser.
 #include "ei_common.cuh"
 
 namespace ei {
 namespace {
 
-constexpr int TILE = 32;
+constexpr int T = 32;
 
-// grid (ceil(N/32), ceil(N/32), S), block (32, 8)
-__global__ void __launch_bounds__(256) pack3_kernel(const float *__restrict__ mu,
-                                                    const float *__restrict__ delta,
-                                                    const float *__restrict__ sigma,
-                                                    size_t in_stride, int N,
-                                                    float4 *__restrict__ out,
-                                                    float4 *__restrict__ outT,
-                                                    double *__restrict__ part_reg,
-                                                    int32_t *__restrict__ status) {
-  __shared__ float4 tile[TILE][TILE + 1];
+template <int NMAP>
+struct PairOut;
+template <>
+struct PairOut<3> {
+  float4 *a, *aT;
+  float2 *b, *bT;
+};
+template <>
+struct PairOut<1> {
+  float2 *a, *aT;
+};
+
+// grid (ceil((N+1)/32), ceil((N+1)/32), S), block (32, 8).  Tile (ta, tb) loads map rows
+// [32ta-1, 32ta+31] x cols [32tb-1, 32tb+31] and writes normal entries (rows 32ta.., entries
+// 32tb..) and transposed entries (T-rows 32tb.., entries 32ta..).
+template <int NMAP>
+__global__ void __launch_bounds__(256) pack_pairs_kernel(const float *__restrict__ in0,
+                                                         const float *__restrict__ in1,
+                                                         const float *__restrict__ in2,
+                                                         size_t in_stride, int N, PairOut<NMAP> out,
+                                                         double *__restrict__ part_reg,
+                                                         int32_t *__restrict__ status) {
+  __shared__ float tile[NMAP][T + 1][T + 2];
   __shared__ double red[8];
-  const int s = blockIdx.z;
-  const int i0 = blockIdx.y * TILE, j0 = blockIdx.x * TILE;
+  const int s = blockIdx.z, ta = blockIdx.y, tb = blockIdx.x;
   const int tx = threadIdx.x, ty = threadIdx.y;
-  const size_t NN = (size_t)N * N;
-  const float *m = mu + s * in_stride, *d = delta + s * in_stride, *g = sigma + s * in_stride;
-  float4 *o = out + s * NN, *oT = outT + s * NN;
+  const float *src[3] = {in0 + s * in_stride, NMAP == 3 ? in1 + s * in_stride : nullptr,
+                         NMAP == 3 ? in2 + s * in_stride : nullptr};
   double sq = 0.0;
   int bad = 0;
-  for (int r = ty; r < TILE; r += 8) {
-    const int i = i0 + r, j = j0 + tx;
-    if (i < N && j < N) {
-      const size_t q = (size_t)i * N + j;
-      const float a = __ldg(m + q), b = __ldg(d + q), c = __ldg(g + q);
-      bad += !isfinite(a) + !isfinite(b) + !isfinite(c);
-      sq += (double)a * a + (double)b * b + (double)c * c;
-      const float4 v = make_float4(a, b, c, 0.f);
-      o[q] = v;
-      tile[r][tx] = v;
+  // load (T+1) x (T+1) with a one-element halo above and to the left
+  for (int r = ty; r < T + 1; r += 8) {
+    const int i = ta * T - 1 + r;
+    for (int c = tx; c < T + 1; c += 32) {
+      const int j = tb * T - 1 + c;
+      const bool in = (i >= 0 && i < N && j >= 0 && j < N);
+#pragma unroll
+      for (int m = 0; m < NMAP; ++m) {
+        const float v = in ? __ldg(src[m] + (size_t)i * N + j) : 0.f;
+        tile[m][r][c] = v;
+        if (in && r >= 1 && c >= 1) {   // owned pixel: count once
+          bad += !isfinite(v);
+          sq += (double)v * v;
+        }
+      }
     }
   }
   __syncthreads();
-  for (int r = ty; r < TILE; r += 8) {
-    const int jj = j0 + r, ii = i0 + tx;   // write row jj of the transpose
-    if (jj < N && ii < N) oT[(size_t)jj * N + ii] = tile[tx][r];
+  const size_t rl = (size_t)N + 1, slice = (size_t)N * rl;
+  // normal: row i = 32ta + r, entry e = 32tb + c  -> (x[i][e-1], x[i][e]) = tile[r+1][c], tile[r+1][c+1]
+  // transposed: T-row j = 32tb + r, entry e = 32ta + c -> (x[e-1][j], x[e][j]) = tile[c][r+1], tile[c+1][r+1]
+  for (int r = ty; r < T; r += 8) {
+    const int c = tx;
+    const int i = ta * T + r, e = tb * T + c;
+    if (i < N && e <= N) {
+      const size_t o = s * slice + (size_t)i * rl + e;
+      if constexpr (NMAP == 3) {
+        out.a[o] = make_float4(tile[0][r + 1][c], tile[0][r + 1][c + 1], tile[1][r + 1][c], tile[1][r + 1][c + 1]);
+        out.b[o] = make_float2(tile[2][r + 1][c], tile[2][r + 1][c + 1]);
+      } else {
+        out.a[o] = make_float2(tile[0][r + 1][c], tile[0][r + 1][c + 1]);
+      }
+    }
+    const int j = tb * T + r, eT = ta * T + c;
+    if (j < N && eT <= N) {
+      const size_t o = s * slice + (size_t)j * rl + eT;
+      if constexpr (NMAP == 3) {
+        out.aT[o] = make_float4(tile[0][c][r + 1], tile[0][c + 1][r + 1], tile[1][c][r + 1], tile[1][c + 1][r + 1]);
+        out.bT[o] = make_float2(tile[2][c][r + 1], tile[2][c + 1][r + 1]);
+      } else {
+        out.aT[o] = make_float2(tile[0][c][r + 1], tile[0][c + 1][r + 1]);
+      }
+    }
   }
   if (status && bad) atomicAdd(&status[0], bad);   // integer count: order-independent
   if (part_reg) {
@@ -58,33 +103,26 @@ __global__ void __launch_bounds__(256) pack3_kernel(const float *__restrict__ mu
   }
 }
 
-// single map [S][N][N] (slice stride NN) -> transposed copy
-__global__ void __launch_bounds__(256) transpose1_kernel(const float *__restrict__ in, int N,
-                                                         float *__restrict__ outT) {
-  __shared__ float tile[TILE][TILE + 1];
-  const int s = blockIdx.z;
-  const int i0 = blockIdx.y * TILE, j0 = blockIdx.x * TILE;
-  const size_t NN = (size_t)N * N;
-  for (int r = threadIdx.y; r < TILE; r += 8) {
-    const int i = i0 + r, j = j0 + threadIdx.x;
-    if (i < N && j < N) tile[r][threadIdx.x] = __ldg(in + s * NN + (size_t)i * N + j);
-  }
-  __syncthreads();
-  for (int r = threadIdx.y; r < TILE; r += 8) {
-    const int jj = j0 + r, ii = i0 + threadIdx.x;
-    if (jj < N && ii < N) outT[s * NN + (size_t)jj * N + ii] = tile[threadIdx.x][r];
-  }
-}
-
-// sino [S][3][NA*ND] -> float4 [S][NA*ND]
-__global__ void pack_sino3_kernel(const float *__restrict__ in, size_t plane, int S,
-                                  float4 *__restrict__ out) {
-  const size_t total = plane * S;
+// planar sino [S][NMAP][NA][ND] -> pair layout [S][NA][ND+1] (entry e = (g[e-1], g[e]))
+template <int NMAP>
+__global__ void pack_sino_kernel(const float *__restrict__ in, int NA, int ND, int S,
+                                 float4 *__restrict__ GA, float2 *__restrict__ GB,
+                                 float2 *__restrict__ GA1) {
+  const size_t plane = (size_t)NA * ND, rl = (size_t)ND + 1;
+  const size_t total = (size_t)S * NA * rl;
   for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < total;
        t += (size_t)gridDim.x * blockDim.x) {
-    const size_t s = t / plane, q = t - s * plane;
-    const float *b = in + s * 3 * plane + q;
-    out[t] = make_float4(__ldg(b), __ldg(b + plane), __ldg(b + 2 * plane), 0.f);
+    const size_t sa = t / rl;
+    const int e = (int)(t - sa * rl);
+    const size_t s = sa / NA, a = sa - s * NA;
+    const float *b = in + s * NMAP * plane + a * ND;
+    auto at = [&](int m, int k) { return (k >= 0 && k < ND) ? __ldg(b + m * plane + k) : 0.f; };
+    if (NMAP == 3) {
+      GA[t] = make_float4(at(0, e - 1), at(0, e), at(1, e - 1), at(1, e));
+      GB[t] = make_float2(at(2, e - 1), at(2, e));
+    } else {
+      GA1[t] = make_float2(at(0, e - 1), at(0, e));
+    }
   }
 }
 
@@ -104,25 +142,34 @@ __global__ void check_small_kernel(const float *__restrict__ flat, int nflat,
 
 }  // namespace
 
+int reg_blocks(int N) { return ((N + 1 + T - 1) / T) * ((N + 1 + T - 1) / T); }
+
 cudaError_t launch_pack3(const ei_plan &p, const float *mu, const float *delta, const float *sigma,
                          size_t in_stride, bool want_reg, int32_t *status, cudaStream_t st) {
-  dim3 grid((p.N + TILE - 1) / TILE, (p.N + TILE - 1) / TILE, p.S), block(32, 8);
-  pack3_kernel<<<grid, block, 0, st>>>(mu, delta, sigma, in_stride, p.N, p.maps4, p.maps4T,
-                                       want_reg ? p.part_reg : nullptr, status);
+  const int nt = (p.N + 1 + T - 1) / T;
+  dim3 grid(nt, nt, p.S), block(32, 8);
+  PairOut<3> o{p.MA, p.MAT, p.MB, p.MBT};
+  pack_pairs_kernel<3><<<grid, block, 0, st>>>(mu, delta, sigma, in_stride, p.N, o,
+                                               want_reg ? p.part_reg : nullptr, status);
   return cudaGetLastError();
 }
 
-cudaError_t launch_transpose1(const ei_plan &p, const float *map, cudaStream_t st) {
-  dim3 grid((p.N + TILE - 1) / TILE, (p.N + TILE - 1) / TILE, p.S), block(32, 8);
-  transpose1_kernel<<<grid, block, 0, st>>>(map, p.N, p.mapT1);
+cudaError_t launch_pack1(const ei_plan &p, const float *map, cudaStream_t st) {
+  const int nt = (p.N + 1 + T - 1) / T;
+  dim3 grid(nt, nt, p.S), block(32, 8);
+  PairOut<1> o{p.M1, p.M1T};
+  pack_pairs_kernel<1><<<grid, block, 0, st>>>(map, nullptr, nullptr, (size_t)p.N * p.N, p.N, o,
+                                               nullptr, nullptr);
   return cudaGetLastError();
 }
 
-cudaError_t launch_pack_sino3(const ei_plan &p, const float *sino, cudaStream_t st) {
-  const size_t plane = (size_t)p.NA * p.ND;
-  const size_t total = plane * p.S;
+cudaError_t launch_pack_sino(const ei_plan &p, const float *sino, int n_maps, cudaStream_t st) {
+  const size_t total = (size_t)p.S * p.NA * (p.ND + 1);
   const int blocks = (int)((total + 255) / 256 < 148 * 16 ? (total + 255) / 256 : 148 * 16);
-  pack_sino3_kernel<<<blocks, 256, 0, st>>>(sino, plane, p.S, p.sino4);
+  if (n_maps == 3)
+    pack_sino_kernel<3><<<blocks, 256, 0, st>>>(sino, p.NA, p.ND, p.S, p.GA, p.GB, nullptr);
+  else
+    pack_sino_kernel<1><<<blocks, 256, 0, st>>>(sino, p.NA, p.ND, p.S, nullptr, nullptr, p.GA1);
   return cudaGetLastError();
 }
 

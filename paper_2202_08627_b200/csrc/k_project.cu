@@ -1,103 +1,303 @@
 // k_project.cu — K1: Joseph ray-driven projection (eq. 1; SURVEY.md §8(a) a1,
-// readings R5-R8).  Every angle is handled in its dominant-axis frame: row-dominant angles
-// sample the rows of the map, column-dominant angles sample the rows of the transposed map
-// with (cos, sin) swapped (H2), so the inner loop always walks contiguous rows and the 32
-// lanes of a warp (32 adjacent rays of one angle) read adjacent pixels of the same row.
+// readings R5-R8).  Every angle is handled in its dominant-axis frame: row-dominant angles sample
+// the rows of the map, column-dominant angles the rows of the transposed map with (cos, sin)
+// swapped (H2); x*(k, i) = (k-(Nd-1)/2)*ic - tn*(i-(N-1)/2) + (N-1)/2, taps (floor x*, +1).
 //
-// One thread = one ray (s, a, k); it visits only the rows where the ray has a tap inside
-// the grid, i.e. |x*_c| < (N+1)/2 with x*_c = (k-(Nd-1)/2)*ic - tn*(i-(N-1)/2).
+// B200 design (DESIGN.md §5 K1):
+//  * a CTA owns AGB = 16 consecutive same-dominance angles x RT = 64 adjacent rays; it walks the
+//    rows in chunks of RC rows, staging with cp.async only the window of PAIR entries (K0 layout:
+//    entry e = (x[e-1], x[e]) of all maps) that its 1024 rays touch in those rows (double-
+//    buffered); the window width bound CW is computed exactly on the host (plan) so every index
+//    stays inside the staged window without per-sample checks;
+//  * a warp = 4 adjacent angles x 8 adjacent rays: near the centre of the map the 4 angles
+//    sample the same pixels, so lanes share shared-memory words (broadcast);
+//  * one tap pair of all three maps = one LDS.128 + one LDS.64; weights (1-w, w) as a float2 and
+//    three FFMA2 per sample (acc.x: left taps, acc.y: right taps);
+//  * small problems split the rows over RS CTAs (partial P summed in fixed order by K2).
+#include <math.h>
+
+#include <algorithm>
+#include <vector>
+
 #include "ei_common.cuh"
 
 namespace ei {
 namespace {
 
+constexpr int AGB = 16;   // angles per CTA
+constexpr int RT = 64;    // rays per CTA
+constexpr int NT = 256;
+
+__device__ __forceinline__ void cp_async(void *smem, const void *gmem, int bytes, bool valid) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  if (bytes == 16)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(valid ? 16 : 0));
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(valid ? 8 : 0));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
 template <int NMAP>
-struct Pix;
+struct PL;
 template <>
-struct Pix<3> {
-  using T = float4;
+struct PL<3> {
+  using A = float4;
+  static constexpr bool hasB = true;
 };
 template <>
-struct Pix<1> {
-  using T = float;
+struct PL<1> {
+  using A = float2;
+  static constexpr bool hasB = false;
 };
 
-__device__ __forceinline__ void row_range(float alpha, float tn, float ctr, int N, int &lo, int &hi) {
-  // rows i with |alpha - tn*(i-ctr)| < ctr + 1 (taps inside the grid), conservatively widened
-  const float lim = ctr + 1.0f;
-  if (fabsf(tn) < 1e-20f) {
-    if (fabsf(alpha) < lim + 1.0f) { lo = 0; hi = N - 1; } else { lo = 0; hi = -1; }
-    return;
+struct ProjArgs {
+  const void *MA, *MAT;         // PL<NMAP>::A pairs, [S][N][N+1] (normal / transposed)
+  const float2 *MB, *MBT;       // sigma pairs (NMAP = 3)
+  const float4 *k1;             // ic, tn, scale, rowdom
+  const int2 *groups;           // {first sorted position, count}
+  const int *order;             // sorted position -> angle index
+  const int2 *win;              // [RS][groups][tiles][chunks] {cmin, W} (W = 0: chunk skipped)
+  int N, NA, ND, S, RS, RC, CW, nch;
+  float *P;                     // [RS][S][NMAP][NA][ND]
+};
+
+// lane -> (angle aq = lane & 3 of the group's current angle quad, ray rr = lane >> 2): a quarter
+// warp (8 lanes) = 4 angles x 2 adjacent rays, whose taps fall on 2-4 consecutive window entries
+// (one conflict-free wavefront per LDS.128 quarter); slot m adds 4m to the angle.
+template <int NMAP>
+__global__ void __launch_bounds__(NT, 2) project_kernel(ProjArgs args) {
+  using TA = typename PL<NMAP>::A;
+  const int N = args.N, ND = args.ND, RC = args.RC, CW = args.CW;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  TA *sA = reinterpret_cast<TA *>(smem_raw);                                   // [2][RC][CW]
+  float2 *sB = reinterpret_cast<float2 *>(sA + 2 * RC * CW);                  // [2][RC][CW]
+
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int kt = blockIdx.x * RT;
+  const int2 gi = args.groups[blockIdx.y];
+  const int s = blockIdx.z % args.S, rs = blockIdx.z / args.S;
+  const float ctr = 0.5f * (float)(N - 1), dctr = 0.5f * (float)(ND - 1);
+  const int aq = lane & 3;
+  const int k = kt + w * 8 + (lane >> 2);
+  const float kc = (float)k - dctr;
+
+  float alpha[4], tn[4], scale[4];
+  int aidx[4];
+#pragma unroll
+  for (int m = 0; m < 4; ++m) {
+    const int al = min(aq + 4 * m, gi.y - 1);
+    const int a = args.order[gi.x + al];
+    aidx[m] = (aq + 4 * m < gi.y) ? a : -1;
+    const float4 t = __ldg(args.k1 + a);
+    alpha[m] = kc * t.x;
+    tn[m] = t.y;
+    scale[m] = t.z;
   }
-  float y0 = (alpha - lim) / tn, y1 = (alpha + lim) / tn;
-  if (y0 > y1) { float t = y0; y0 = y1; y1 = t; }
-  const float f0 = floorf(y0 + ctr) - 1.0f, f1 = ceilf(y1 + ctr) + 1.0f;
-  lo = f0 < 0.f ? 0 : (f0 > (float)N ? N : (int)f0);
-  hi = f1 > (float)(N - 1) ? N - 1 : (f1 < -1.f ? -1 : (int)f1);
-}
+  const bool rowdom = __ldg(args.k1 + args.order[gi.x]).w != 0.f;
+  const size_t rl = (size_t)N + 1;
+  const TA *gA = reinterpret_cast<const TA *>(rowdom ? args.MA : args.MAT) + (size_t)s * N * rl;
+  const float2 *gB = PL<NMAP>::hasB ? (rowdom ? args.MB : args.MBT) + (size_t)s * N * rl : nullptr;
 
-__device__ __forceinline__ void acc_add(float4 &acc, float4 v0, float4 v1, float w) {
-  acc.x += fmaf(w, v1.x - v0.x, v0.x);
-  acc.y += fmaf(w, v1.y - v0.y, v0.y);
-  acc.z += fmaf(w, v1.z - v0.z, v0.z);
-}
-__device__ __forceinline__ void acc_add(float &acc, float v0, float v1, float w) {
-  acc += fmaf(w, v1 - v0, v0);
-}
-__device__ __forceinline__ float4 zero_of(float4) { return make_float4(0.f, 0.f, 0.f, 0.f); }
-__device__ __forceinline__ float zero_of(float) { return 0.f; }
+  const int r0 = (int)(((long long)rs * N) / args.RS), r1 = (int)(((long long)(rs + 1) * N) / args.RS);
+  const int nch = (r1 - r0 + RC - 1) / RC;
+  const int2 *wtab = args.win + (((size_t)rs * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * args.nch;
 
-template <int NMAP>
-__global__ void __launch_bounds__(128) project_kernel(const typename Pix<NMAP>::T *__restrict__ map,
-                                                      const typename Pix<NMAP>::T *__restrict__ mapT,
-                                                      const float4 *__restrict__ k1, int N, int NA,
-                                                      int ND, float *__restrict__ P) {
-  using T = typename Pix<NMAP>::T;
-  const int k = blockIdx.x * blockDim.x + threadIdx.x;
-  const int a = blockIdx.y, s = blockIdx.z;
+  auto stage = [&](int c, int buf) {
+    const int2 wn = __ldg(wtab + c);
+    const int i0 = r0 + c * RC, rc = min(RC, r1 - i0);
+    for (int e = tid; e < rc * wn.y; e += NT) {
+      const int r = e / wn.y, l = e - r * wn.y;
+      const int ent = wn.x + 1 + l;   // pair (x[j0], x[j0+1]) lives at entry j0 + 1
+      const bool ok = ent >= 0 && ent <= N;
+      const size_t off = (size_t)(i0 + r) * rl + (ok ? ent : 0);
+      cp_async(&sA[(buf * RC + r) * CW + l], gA + off, (int)sizeof(TA), ok);
+      if (PL<NMAP>::hasB) cp_async(&sB[(buf * RC + r) * CW + l], gB + off, 8, ok);
+    }
+    cp_commit();
+  };
+
+  float2 am[4], ad[4], as[4];
+#pragma unroll
+  for (int m = 0; m < 4; ++m) am[m] = ad[m] = as[m] = make_float2(0.f, 0.f);
+
+  stage(0, 0);
+  for (int c = 0; c < nch; ++c) {
+    const int b = c & 1;
+    cp_wait<0>();
+    __syncthreads();                       // chunk c landed; chunk c-1's buffer is free
+    if (c + 1 < nch) stage(c + 1, b ^ 1);  // overlaps the compute of chunk c
+    const int2 wn = __ldg(wtab + c);
+    if (wn.y == 0) continue;               // no ray of this CTA touches these rows
+    const int i0 = r0 + c * RC, rc = min(RC, r1 - i0);
+    for (int r = 0; r < rc; ++r) {
+      const float yi = (float)(i0 + r) - ctr;
+      const TA *arow = sA + (b * RC + r) * CW - wn.x;
+      const float2 *brow = sB + (b * RC + r) * CW - wn.x;
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        const float xs = fmaf(-tn[m], yi, alpha[m]) + ctr;
+        const int j0 = __float2int_rd(xs);
+        const float fr = xs - (float)j0;
+        const float2 wt = make_float2(1.f - fr, fr);
+        const TA va = arow[j0];
+        if constexpr (NMAP == 3) {
+          am[m] = __ffma2_rn(wt, make_float2(va.x, va.y), am[m]);
+          ad[m] = __ffma2_rn(wt, make_float2(va.z, va.w), ad[m]);
+          as[m] = __ffma2_rn(wt, brow[j0], as[m]);
+        } else {
+          am[m] = __ffma2_rn(wt, va, am[m]);
+        }
+      }
+    }
+  }
   if (k >= ND) return;
-  const float4 tab = __ldg(k1 + a);   // ic, tn, scale, rowdom
-  const size_t NN = (size_t)N * N;
-  const T *img = (tab.w != 0.f ? map : mapT) + s * NN;
-  const float ctr = 0.5f * (float)(N - 1);
-  const float alpha = ((float)k - 0.5f * (float)(ND - 1)) * tab.x;
-  int lo, hi;
-  row_range(alpha, tab.y, ctr, N, lo, hi);
-  T acc = zero_of(T());
-  const T zero = zero_of(T());
-  for (int i = lo; i <= hi; ++i) {
-    const float xs = fmaf(-tab.y, (float)i - ctr, alpha) + ctr;
-    const float f = floorf(xs);
-    const int j0 = (int)f;
-    const float w = xs - f;
-    const T *row = img + (size_t)i * N;
-    const T v0 = (j0 >= 0 && j0 < N) ? __ldg(row + j0) : zero;
-    const T v1 = (j0 + 1 >= 0 && j0 + 1 < N) ? __ldg(row + j0 + 1) : zero;
-    acc_add(acc, v0, v1, w);
+  const size_t plane = (size_t)args.NA * ND;
+  float *out = args.P + ((size_t)rs * args.S + s) * NMAP * plane + k;
+#pragma unroll
+  for (int m = 0; m < 4; ++m) {
+    if (aidx[m] < 0) continue;
+    out[(size_t)aidx[m] * ND] = (am[m].x + am[m].y) * scale[m];
+    if constexpr (NMAP == 3) {
+      out[plane + (size_t)aidx[m] * ND] = (ad[m].x + ad[m].y) * scale[m];
+      out[2 * plane + (size_t)aidx[m] * ND] = (as[m].x + as[m].y) * scale[m];
+    }
   }
-  const size_t plane = (size_t)NA * ND;
-  float *out = P + (size_t)s * NMAP * plane + (size_t)a * ND + k;
-  if constexpr (NMAP == 3) {
-    out[0] = acc.x * tab.z;
-    out[plane] = acc.y * tab.z;
-    out[2 * plane] = acc.z * tab.z;
+}
+
+template <int NMAP>
+cudaError_t launch(const ei_plan &p, int RS, float *P, cudaStream_t st) {
+  ProjArgs a;
+  if (NMAP == 3) {
+    a.MA = p.MA; a.MAT = p.MAT; a.MB = p.MB; a.MBT = p.MBT;
   } else {
-    out[0] = acc * tab.z;
+    a.MA = p.M1; a.MAT = p.M1T; a.MB = nullptr; a.MBT = nullptr;
   }
+  a.k1 = p.tab.k1;
+  a.groups = p.proj.groups;
+  a.order = p.proj.order;
+  a.win = RS == 1 ? p.proj.win1 : p.proj.winRS;
+  a.N = p.N; a.NA = p.NA; a.ND = p.ND; a.S = p.S; a.RS = RS; a.RC = p.proj.RC; a.CW = p.proj.CW;
+  a.nch = RS == 1 ? p.proj.nch1 : p.proj.nchRS;
+  a.P = P;
+  const size_t smem = (size_t)2 * p.proj.RC * p.proj.CW * (sizeof(typename PL<NMAP>::A) + (NMAP == 3 ? 8 : 0));
+  cudaError_t e = cudaFuncSetAttribute((const void *)project_kernel<NMAP>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  dim3 grid((p.ND + RT - 1) / RT, p.proj.n_groups, p.S * RS);
+  project_kernel<NMAP><<<grid, NT, smem, st>>>(a);
+  return cudaGetLastError();
 }
 
 }  // namespace
 
-cudaError_t launch_project3(const ei_plan &p, float *P, cudaStream_t st) {
-  dim3 grid((p.ND + 127) / 128, p.NA, p.S);
-  project_kernel<3><<<grid, 128, 0, st>>>(p.maps4, p.maps4T, p.tab.k1, p.N, p.NA, p.ND, P);
-  return cudaGetLastError();
+// Host planning for K1 (called once by ei_plan_create):
+//  * groups: runs of <= AGB angularly adjacent angles of one dominance class;
+//  * window table: for every (row split, group, ray tile, row chunk) the first staged pair entry
+//    and the window width, from the fp64 positions of the extreme rays at the chunk's first and
+//    last rows (x* is linear in ray and row), widened by one entry on each side so fp32 rounding
+//    in the kernel can never leave the window; chunks whose window misses the map get W = 0;
+//  * RC (rows per chunk) as large as fits two CTAs per SM, CW = max window width, and the row
+//    split RS of the cost path for problems with fewer than ~2 CTAs per SM.
+static void build_windows(const ei_plan &p, const double *angles, const std::vector<int2> &groups,
+                          const std::vector<int> &order, int RS, int RC, std::vector<int2> &win,
+                          int &nch_max, int &wmax) {
+  const int N = p.N, ND = p.ND;
+  const double dx = p.g.pixel, du = p.g.det_pitch, ctr = 0.5 * (N - 1), dctr = 0.5 * (ND - 1);
+  const int ntile = (ND + RT - 1) / RT;
+  nch_max = 0;
+  for (int rs = 0; rs < RS; ++rs) {
+    const int r0 = (int)(((long long)rs * N) / RS), r1 = (int)(((long long)(rs + 1) * N) / RS);
+    nch_max = std::max(nch_max, (r1 - r0 + RC - 1) / RC);
+  }
+  win.assign((size_t)RS * groups.size() * ntile * nch_max, make_int2(0, 0));
+  wmax = 1;
+  for (int rs = 0; rs < RS; ++rs) {
+    const int r0 = (int)(((long long)rs * N) / RS), r1 = (int)(((long long)(rs + 1) * N) / RS);
+    for (size_t g = 0; g < groups.size(); ++g) {
+      for (int t = 0; t < ntile; ++t) {
+        const int kt = t * RT;
+        int2 *row = &win[((rs * groups.size() + g) * ntile + t) * nch_max];
+        for (int c = 0; r0 + c * RC < r1; ++c) {
+          const int i0 = r0 + c * RC, i1 = std::min(i0 + RC, r1) - 1;
+          double lo = 1e300, hi = -1e300;
+          for (int q = 0; q < groups[g].y; ++q) {
+            const int a = order[groups[g].x + q];
+            const double cs = cos(angles[a]), sn = sin(angles[a]);
+            const bool rd = fabs(cs) >= fabs(sn);
+            const double cd = rd ? cs : sn, so = rd ? sn : cs;
+            for (int kk : {kt, kt + RT - 1})
+              for (int ii : {i0, i1}) {
+                const double xs = (kk - dctr) * du / (cd * dx) - (so / cd) * (ii - ctr) + ctr;
+                lo = std::min(lo, floor(xs));
+                hi = std::max(hi, floor(xs));
+              }
+          }
+          // taps j0 in [lo-1, hi+1] (one entry of rounding slack each side)
+          if (hi + 1 < -1 || lo - 1 > N - 1) continue;     // misses the map: W = 0
+          const int W = (int)(hi - lo) + 3;
+          row[c] = make_int2((int)lo - 1, W);
+          wmax = std::max(wmax, W);
+        }
+      }
+    }
+  }
 }
 
-cudaError_t launch_project1(const ei_plan &p, const float *map, float *P, cudaStream_t st) {
-  dim3 grid((p.ND + 127) / 128, p.NA, p.S);
-  project_kernel<1><<<grid, 128, 0, st>>>(map, p.mapT1, p.tab.k1, p.N, p.NA, p.ND, P);
-  return cudaGetLastError();
+int plan_projector(ei_plan &p, const double *angles, std::vector<int2> &groups,
+                   std::vector<int> &order, std::vector<int2> &win1, std::vector<int2> &winRS) {
+  const int NA = p.NA, N = p.N, ND = p.ND;
+  // groups = runs of angularly adjacent angles (sorted by angle mod 2 pi) of one dominance class
+  std::vector<int> idx(NA);
+  for (int a = 0; a < NA; ++a) idx[a] = a;
+  auto wrap = [](double t) { t = fmod(t, 2 * M_PI); return t < 0 ? t + 2 * M_PI : t; };
+  std::stable_sort(idx.begin(), idx.end(), [&](int x, int y) { return wrap(angles[x]) < wrap(angles[y]); });
+  auto rowdom = [&](int a) { return fabs(cos(angles[a])) >= fabs(sin(angles[a])); };
+  order.clear();
+  groups.clear();
+  for (int q = 0; q < NA; ++q) {
+    const int a = idx[q];
+    if (groups.empty() || groups.back().y == AGB || rowdom(a) != rowdom(order.back()))
+      groups.push_back(make_int2((int)order.size(), 0));
+    order.push_back(a);
+    groups.back().y += 1;
+  }
+  const size_t per_entry = 24;          // float4 + float2 per staged pair entry
+  const size_t budget = 110 * 1024;     // two CTAs per SM
+  int RC = 32, nch = 0, CW = 0;
+  for (;;) {
+    build_windows(p, angles, groups, order, 1, RC, win1, nch, CW);
+    if ((size_t)2 * RC * CW * per_entry <= budget || RC == 1) break;
+    RC /= 2;
+  }
+  if ((size_t)2 * RC * CW * per_entry > 220 * 1024) return EI_ERR_SHAPE;
+  p.proj.RC = RC;
+  p.proj.n_groups = (int)groups.size();
+  p.proj.nch1 = nch;
+  // row split for small problems: aim for >= 2 CTAs per SM
+  const int ntile = (ND + RT - 1) / RT;
+  const long long ctas = (long long)ntile * groups.size() * p.S;
+  int RS = 1;
+  while (RS < 8 && ctas * RS < 2 * 148 && N / (RS * 2) >= 2 * RC) RS *= 2;
+  p.proj.RS = RS;
+  int CWrs = CW;
+  if (RS > 1) {
+    build_windows(p, angles, groups, order, RS, RC, winRS, p.proj.nchRS, CWrs);
+  } else {
+    winRS.clear();
+    p.proj.nchRS = nch;
+  }
+  p.proj.CW = std::max(CW, CWrs);
+  return EI_OK;
+}
+
+cudaError_t launch_project3(const ei_plan &p, float *P, int RS, cudaStream_t st) {
+  return launch<3>(p, RS, P, st);
+}
+
+cudaError_t launch_project1(const ei_plan &p, float *P, cudaStream_t st) {
+  return launch<1>(p, 1, P, st);
 }
 
 }  // namespace ei

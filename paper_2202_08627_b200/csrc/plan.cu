@@ -6,6 +6,7 @@
 #include <string.h>
 
 #include <new>
+#include <vector>
 
 #include "ei_common.cuh"
 
@@ -50,7 +51,8 @@ void free_timing(ei_plan *p) {
 void free_plan(ei_plan *p) {
   if (!p) return;
   free_timing(p);
-  void *ptrs[] = {p->tab.k1, p->tab.k3, p->maps4, p->maps4T, p->mapT1, p->sino4, p->P, p->G4,
+  void *ptrs[] = {p->tab.k1, p->tab.k3, p->proj.groups, p->proj.order, p->proj.win1, p->proj.winRS, p->MA, p->MAT, p->MB,
+                  p->MBT, p->M1, p->M1T, p->diag, p->P, p->GA, p->GB, p->GA1,
                   p->part_curve, p->part_reg, p->h_maps, p->h_flat, p->h_mask, p->h_drift,
                   p->h_sexp, p->h_grad, p->h_cost, p->h_status};
   for (void *q : ptrs)
@@ -113,22 +115,51 @@ int ei_plan_create(const ei_geometry *geom, const double *angles, ei_plan **out)
     k3[a] = make_float4((float)(c * dx / du), (float)(s * dx / du), (float)(du / (fabs(cd) * dx)),
                         (float)(dx / fabs(cd)));
   }
-  const size_t S = p->S, NN = (size_t)p->N * p->N, SINO = (size_t)p->NA * p->ND;
-  p->RB = ((p->N + 31) / 32) * ((p->N + 31) / 32);
+  std::vector<int2> groups, win1, winRS;
+  std::vector<int> order;
+  rc = ei::plan_projector(*p, angles, groups, order, win1, winRS);
+  if (rc) {
+    delete[] k1;
+    delete[] k3;
+    delete p;
+    return rc;
+  }
+  const size_t S = p->S, SINO = (size_t)p->NA * p->ND;
+  const size_t NP = (size_t)p->N * (p->N + 1);
+  p->RB = ei::reg_blocks(p->N);
   cudaError_t e = cudaSuccess;
   auto A = [&](cudaError_t r) { if (e == cudaSuccess) e = r; };
   A(dalloc(&p->tab.k1, NA));
   A(dalloc(&p->tab.k3, NA));
-  A(dalloc(&p->maps4, S * NN));
-  A(dalloc(&p->maps4T, S * NN));
-  A(dalloc(&p->mapT1, S * NN));
-  A(dalloc(&p->sino4, S * SINO));
-  A(dalloc(&p->P, S * 3 * SINO));
-  A(dalloc(&p->G4, S * SINO));
+  A(dalloc(&p->proj.groups, groups.size()));
+  A(dalloc(&p->proj.order, order.size()));
+  A(dalloc(&p->proj.win1, win1.size()));
+  if (!winRS.empty()) A(dalloc(&p->proj.winRS, winRS.size()));
+  A(dalloc(&p->MA, S * NP));
+  A(dalloc(&p->MAT, S * NP));
+  A(dalloc(&p->MB, S * NP));
+  A(dalloc(&p->MBT, S * NP));
+  A(dalloc(&p->M1, S * NP));
+  A(dalloc(&p->M1T, S * NP));
+  A(dalloc(&p->diag, 1));
+  const size_t SINO1 = (size_t)p->NA * (p->ND + 1);
+  A(dalloc(&p->P, (size_t)p->proj.RS * S * 3 * SINO));
+  A(dalloc(&p->GA, S * SINO1));
+  A(dalloc(&p->GB, S * SINO1));
+  A(dalloc(&p->GA1, S * SINO1));
   A(dalloc(&p->part_curve, S * NA));
   A(dalloc(&p->part_reg, S * p->RB));
   if (e == cudaSuccess) A(cudaMemcpy(p->tab.k1, k1, sizeof(float4) * NA, cudaMemcpyHostToDevice));
   if (e == cudaSuccess) A(cudaMemcpy(p->tab.k3, k3, sizeof(float4) * NA, cudaMemcpyHostToDevice));
+  if (e == cudaSuccess)
+    A(cudaMemcpy(p->proj.groups, groups.data(), sizeof(int2) * groups.size(), cudaMemcpyHostToDevice));
+  if (e == cudaSuccess)
+    A(cudaMemcpy(p->proj.order, order.data(), sizeof(int) * order.size(), cudaMemcpyHostToDevice));
+  if (e == cudaSuccess) A(cudaMemset(p->diag, 0, sizeof(int32_t)));
+  if (e == cudaSuccess)
+    A(cudaMemcpy(p->proj.win1, win1.data(), sizeof(int2) * win1.size(), cudaMemcpyHostToDevice));
+  if (e == cudaSuccess && !winRS.empty())
+    A(cudaMemcpy(p->proj.winRS, winRS.data(), sizeof(int2) * winRS.size(), cudaMemcpyHostToDevice));
   delete[] k1;
   delete[] k3;
   if (e != cudaSuccess) {
@@ -145,6 +176,19 @@ void ei_plan_destroy(ei_plan *plan) { free_plan(plan); }
 int ei_plan_stats(const ei_plan *p, int64_t out[6]) {
   if (!p || !out) return EI_ERR_NULL;
   for (int i = 0; i < 6; ++i) out[i] = p->stats[i];
+  return EI_OK;
+}
+
+int ei_plan_info(const ei_plan *p, int64_t out[6]) {
+  if (!p || !out) return EI_ERR_NULL;
+  int32_t d = 0;
+  if (cudaMemcpy(&d, p->diag, sizeof(d), cudaMemcpyDeviceToHost) != cudaSuccess) return EI_ERR_CUDA;
+  out[0] = p->proj.n_groups;
+  out[1] = p->proj.RC;
+  out[2] = p->proj.CW;
+  out[3] = p->proj.RS;
+  out[4] = d;
+  out[5] = (int64_t)2 * p->proj.RC * p->proj.CW * 24;
   return EI_OK;
 }
 
@@ -195,13 +239,13 @@ int ei_project(const ei_plan *p, const float *maps, int n_maps, float *sino, voi
   if (n_maps == 3) {
     // maps [S][3][N][N]: slice stride 3*NN, plane stride NN
     e = ei::launch_pack3(*p, maps, maps + NN, maps + 2 * NN, 3 * NN, false, nullptr, st);
-    if (e == cudaSuccess) e = ei::launch_project3(*p, sino, st);
+    if (e == cudaSuccess) e = ei::launch_project3(*p, sino, 1, st);
     p->stats[0] += 1;
     p->stats[1] += 3;
     p->stats[5] += 2;
   } else {
-    e = ei::launch_transpose1(*p, maps, st);
-    if (e == cudaSuccess) e = ei::launch_project1(*p, maps, sino, st);
+    e = ei::launch_pack1(*p, maps, st);
+    if (e == cudaSuccess) e = ei::launch_project1(*p, sino, st);
     p->stats[0] += 1;
     p->stats[1] += 1;
     p->stats[5] += 2;
@@ -216,18 +260,19 @@ int ei_backproject(const ei_plan *p, const float *sino, int n_maps, float *maps,
   const size_t NN = (size_t)p->N * p->N;
   cudaError_t e;
   if (n_maps == 3) {
-    e = ei::launch_pack_sino3(*p, sino, st);
+    e = ei::launch_pack_sino(*p, sino, 3, st);
     if (e == cudaSuccess)
-      e = ei::launch_backproject3(*p, p->sino4, nullptr, nullptr, nullptr, 0.f, maps, maps + NN,
+      e = ei::launch_backproject3(*p, nullptr, nullptr, nullptr, 0.f, maps, maps + NN,
                                   maps + 2 * NN, 3 * NN, st);
     p->stats[2] += 1;
     p->stats[3] += 3;
     p->stats[5] += 2;
   } else {
-    e = ei::launch_backproject1(*p, sino, maps, st);
+    e = ei::launch_pack_sino(*p, sino, 1, st);
+    if (e == cudaSuccess) e = ei::launch_backproject1(*p, maps, st);
     p->stats[2] += 1;
     p->stats[3] += 1;
-    p->stats[5] += 1;
+    p->stats[5] += 2;
   }
   return cuda_status(e);
 }
@@ -239,7 +284,7 @@ int ei_forward(const ei_plan *p, const float *mu, const float *delta, const floa
   cudaStream_t st = (cudaStream_t)stream;
   // maps given as three [S][N][N] arrays: plane stride handled by pack3 (slice stride NN)
   cudaError_t e = ei::launch_pack3(*p, mu, delta, sigma, (size_t)p->N * p->N, false, nullptr, st);
-  if (e == cudaSuccess) e = ei::launch_project3(*p, p->P, st);
+  if (e == cudaSuccess) e = ei::launch_project3(*p, p->P, p->proj.RS, st);
   if (e == cudaSuccess) e = ei::launch_curve_forward(*p, flat, mask, drift, s_mod, st);
   p->stats[0] += 1;
   p->stats[1] += 3;
@@ -265,12 +310,12 @@ int ei_cost_grad(const ei_plan *p, const float *mu, const float *delta, const fl
   mark(1);
   if (e == cudaSuccess) e = ei::launch_pack3(*p, mu, delta, sigma, NN, lambda > 0.f, status, st);  // K0
   mark(2);
-  if (e == cudaSuccess) e = ei::launch_project3(*p, p->P, st);                      // K1
+  if (e == cudaSuccess) e = ei::launch_project3(*p, p->P, p->proj.RS, st);          // K1
   mark(3);
   if (e == cudaSuccess) e = ei::launch_curve_cost_grad(*p, flat, mask, drift, s_exp, status, st);  // K2
   mark(4);
-  if (e == cudaSuccess) e = ei::launch_backproject3(*p, p->G4, mu, delta, sigma, lambda, g_mu,
-                                                    g_delta, g_sigma, NN, st);         // K3
+  if (e == cudaSuccess) e = ei::launch_backproject3(*p, mu, delta, sigma, lambda, g_mu, g_delta,
+                                                    g_sigma, NN, st);                  // K3
   mark(5);
   if (e == cudaSuccess) e = ei::launch_finalize(*p, lambda, cost, st);              // K4
   mark(6);

@@ -25,7 +25,7 @@ _lib = ctypes.CDLL(LIB_PATH)
 EI_OK, EI_ERR_NULL, EI_ERR_SHAPE, EI_ERR_DOMAIN, EI_ERR_RESOURCE, EI_ERR_CUDA = range(6)
 SYMBOLS = ("ei_plan_create", "ei_plan_destroy", "ei_project", "ei_backproject", "ei_forward",
            "ei_cost_grad", "ei_cost_grad_host", "ei_plan_stats", "ei_plan_set_timing",
-           "ei_plan_read_timing", "ei_error_string", "ei_version")
+           "ei_plan_read_timing", "ei_plan_info", "ei_error_string", "ei_version")
 KERNELS = ("check", "K0_pack", "K1_project", "K2_curve", "K3_backproject", "K4_finalize")
 
 
@@ -46,6 +46,7 @@ _lib.ei_cost_grad.argtypes = [_vp] + [_vp] * 7 + [_f] + [_vp] * 5 + [_vp]
 _lib.ei_cost_grad_host.argtypes = [_vp] + [_vp] * 7 + [_f] + [_vp] * 5 + [_vp]
 _lib.ei_plan_stats.argtypes = [_vp, _vp]
 _lib.ei_plan_set_timing.argtypes = [_vp, _i]
+_lib.ei_plan_info.argtypes = [_vp, _vp]
 _lib.ei_plan_read_timing.argtypes = [_vp, _vp, _vp]
 _lib.ei_error_string.argtypes = [_i]
 _lib.ei_error_string.restype = ctypes.c_char_p
@@ -120,6 +121,14 @@ def ei_plan_stats(plan: Plan):
     out = (ctypes.c_int64 * 6)()
     _check(_lib.ei_plan_stats(plan.handle, out), "ei_plan_stats")
     return list(out)
+
+
+def ei_plan_info(plan: Plan) -> dict:
+    out = (ctypes.c_int64 * 6)()
+    _check(_lib.ei_plan_info(plan.handle, out), "ei_plan_info")
+    keys = ("k1_groups", "k1_rows_per_chunk", "k1_window", "k1_row_split", "window_overflows",
+            "k1_smem_bytes")
+    return dict(zip(keys, list(out)))
 
 
 def ei_plan_set_timing(plan: Plan, max_evals: int):

@@ -103,6 +103,7 @@ def test_dot_test(ei, name):
     a = float(np.dot(Rx.cpu().numpy().astype(np.float64).ravel(), y.astype(np.float64).ravel()))
     b = float(np.dot(x.astype(np.float64).ravel(), Rty.cpu().numpy().astype(np.float64).ravel()))
     assert abs(a - b) / max(abs(a), abs(b)) <= 1e-5, (a, b)
+    assert ei.ei_plan_info(plan)["window_overflows"] == 0
 
 
 @pytest.mark.parametrize("name", SMALL)
@@ -138,6 +139,7 @@ def test_cost_grad_parity(ei, name, point):
         for s in range(case.cfg.S):
             assert rel_l2(g[q][s], ref[s]) <= 1e-3, (q, s, rel_l2(g[q][s], ref[s]))
     assert list(st[:3]) == list(rst) and st[3] == 0
+    assert ei.ei_plan_info(plan)["window_overflows"] == 0
 
 
 def test_status_counters_match_oracle(ei):

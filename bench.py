@@ -297,7 +297,7 @@ def run_gpu(args, cfg, rank, world, local_rank):
         kernels[k] = {"ms": round(per_kernel_ms[k], 5), "share": round(per_kernel_ms[k] / ms_step, 4),
                       "bound": bound, "achieved": round(ach, 1), "peak": round(peak, 1), "unit": "GB/s",
                       "frac": round(ach / peak, 4), "bytes_per_launch": kb[k]}
-    for k in ("check", "K0_pack", "K4_finalize"):
+    for k in ("K0_pack",):
         kernels[k] = {"ms": round(per_kernel_ms[k], 5), "share": round(per_kernel_ms[k] / ms_step, 4)}
     d = kernels[dom]
     roofline = {"kernel": dom, "bound": d["bound"], "achieved": d["achieved"], "peak": d["peak"],

@@ -118,8 +118,8 @@ int ei_plan_stats(const ei_plan *plan, int64_t out[6]);
  * record CUDA events around each of their kernels on the call's stream (max_evals = 0
  * disables; events are created here, EI_ERR_RESOURCE on failure).
  * ei_plan_read_timing(plan, ms[6], n_evals): synchronises the recorded events and returns the
- * summed milliseconds of [check, K0 pack, K1 project, K2 curve, K3 backproject, K4 finalize]
- * over the recorded calls and their number; then resets the recording. */
+ * summed milliseconds of [K0 pack (+input check), K1 project, K2 curve (+fused K4 cost),
+ * K3 backproject, 0, 0] over the recorded calls and their number; then resets the recording. */
 int ei_plan_set_timing(ei_plan *plan, int max_evals);
 int ei_plan_read_timing(ei_plan *plan, double ms[6], int *n_evals);
 

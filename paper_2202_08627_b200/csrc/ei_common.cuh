@@ -57,6 +57,10 @@ struct ei_plan {
   float2 *GA1 = nullptr;      // [S][NA][ND+1]  single-map pairs (ei_backproject n_maps=1)
   double *part_curve = nullptr;  // [S][NA] per-row cost partials (K2)
   double *part_reg = nullptr;    // [S][RB] per-tile sum x^2 partials (K0)
+  unsigned int *done = nullptr;  // [S] K2 arrival counters (fused finalize), kept at 0 between calls
+  unsigned int *done3 = nullptr; // [S][tiles] K3 arrival counters (angle split)
+  float *part3 = nullptr;        // [KS][S][3][N][N] K3 angle-split partial gradients
+  int KS = 1;                    // K3 angle split
   int RB = 0;
   // host-I/O staging (ei_cost_grad_host), allocated on first use
   float *h_maps = nullptr, *h_flat = nullptr, *h_mask = nullptr, *h_drift = nullptr,
@@ -75,13 +79,15 @@ namespace ei {
 int plan_projector(ei_plan &p, const double *angles, std::vector<int2> &groups,
                    std::vector<int> &order, std::vector<int2> &win1, std::vector<int2> &winRS);
 // K0 (k_pack.cu)
+struct SmallCheck {          // flat/mask/drift non-finite scan folded into K0
+  const float *flat = nullptr, *mask = nullptr, *drift = nullptr;
+};
 cudaError_t launch_pack3(const ei_plan &p, const float *mu, const float *delta, const float *sigma,
-                         size_t in_stride, bool want_reg, int32_t *status, cudaStream_t st);
+                         size_t in_stride, bool want_reg, int32_t *status, SmallCheck chk,
+                         cudaStream_t st);
 cudaError_t launch_pack1(const ei_plan &p, const float *map, cudaStream_t st);
 int reg_blocks(int N);
 cudaError_t launch_pack_sino(const ei_plan &p, const float *sino, int n_maps, cudaStream_t st);
-cudaError_t launch_check_small(const ei_plan &p, const float *flat, const float *mask,
-                               const float *drift, int32_t *status, cudaStream_t st);
 // K1 (k_project.cu)
 cudaError_t launch_project3(const ei_plan &p, float *P, int RS, cudaStream_t st);
 cudaError_t launch_project1(const ei_plan &p, float *P, cudaStream_t st);
@@ -90,11 +96,12 @@ cudaError_t launch_curve_forward(const ei_plan &p, const float *flat, const floa
                                  const float *drift, float *s_mod, cudaStream_t st);
 cudaError_t launch_curve_cost_grad(const ei_plan &p, const float *flat, const float *mask,
                                    const float *drift, const float *s_exp, int32_t *status,
-                                   cudaStream_t st);
-cudaError_t launch_finalize(const ei_plan &p, float lambda, double *cost, cudaStream_t st);
+                                   float lambda, double *cost, cudaStream_t st);
 // K3 (k_backproject.cu)
 cudaError_t launch_backproject3(const ei_plan &p, const float *mu, const float *delta,
                                 const float *sigma, float lambda, float *g_mu, float *g_delta,
                                 float *g_sigma, size_t out_stride, cudaStream_t st);
 cudaError_t launch_backproject1(const ei_plan &p, float *map, cudaStream_t st);
+int bp_tiles(int N);
+int bp_chunks(int NA);
 }  // namespace ei

@@ -64,12 +64,13 @@ __global__ void __launch_bounds__(NT, 2) backproject_kernel(
     const typename Layout<NMAP>::A *__restrict__ GA, const float2 *__restrict__ GB,
     const float4 *__restrict__ k3, int N, int NA, int ND, const float *__restrict__ mu,
     const float *__restrict__ delta, const float *__restrict__ sigma, float lambda,
-    float *__restrict__ o0, float *__restrict__ o1, float *__restrict__ o2, size_t out_stride) {
+    float *__restrict__ o0, float *__restrict__ o1, float *__restrict__ o2, size_t out_stride,
+    int S, int KS, float *__restrict__ part3, unsigned int *__restrict__ done3) {
   using TA = typename Layout<NMAP>::A;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   Smem<NMAP> &sm = *reinterpret_cast<Smem<NMAP> *>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const int s = blockIdx.z;
+  const int s = blockIdx.z % S, ks = blockIdx.z / S;
   const int j0 = blockIdx.x * TILE, i0 = blockIdx.y * TILE;
   const int row = 4 * w + (lane >> 3), lx = lane & 7;
   const float ctr = 0.5f * (float)(N - 1), dctr = 0.5f * (float)(ND - 1);
@@ -83,7 +84,9 @@ __global__ void __launch_bounds__(NT, 2) backproject_kernel(
   const size_t rowlen = (size_t)ND + 1;
   const TA *GAs = GA + (size_t)s * NA * rowlen;
   const float2 *GBs = GB ? GB + (size_t)s * NA * rowlen : nullptr;
-  const int nch = (NA + CH - 1) / CH;
+  // angle split (small grids): CTA ks owns chunks [c_lo, c_hi)
+  const int nch_all = (NA + CH - 1) / CH;
+  const int c_lo = (int)(((long long)ks * nch_all) / KS), c_hi = (int)(((long long)(ks + 1) * nch_all) / KS);
 
   auto prep = [&](int c, int buf) {   // per-angle table + window start, threads < CH
     if (tid < CH) {
@@ -120,14 +123,16 @@ __global__ void __launch_bounds__(NT, 2) backproject_kernel(
 #pragma unroll
   for (int q = 0; q < 4; ++q) am[q] = ad[q] = as[q] = make_float2(0.f, 0.f);
 
-  prep(0, 0);
-  __syncthreads();
-  stage(0, 0);
-  for (int c = 0; c < nch; ++c) {
-    const int b = c & 1;
-    if (c + 1 < nch) prep(c + 1, b ^ 1);
+  if (c_lo < c_hi) {
+    prep(c_lo, 0);
     __syncthreads();
-    if (c + 1 < nch) {
+    stage(c_lo, 0);
+  }
+  for (int c = c_lo; c < c_hi; ++c) {
+    const int b = (c - c_lo) & 1;
+    if (c + 1 < c_hi) prep(c + 1, b ^ 1);
+    __syncthreads();
+    if (c + 1 < c_hi) {
       stage(c + 1, b ^ 1);
       cp_wait<1>();
     } else {
@@ -143,9 +148,9 @@ __global__ void __launch_bounds__(NT, 2) backproject_kernel(
       const float2 *brow = sm.b[b][Layout<NMAP>::hasB ? al : 0];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        const float ks = fmaf(xq[q], t.x, base);   // window-local k*, > 0
-        const int k0 = __float2int_rd(ks);
-        const float fr = ks - (float)k0;
+        const float kst = fmaf(xq[q], t.x, base);   // window-local k*, > 0
+        const int k0 = __float2int_rd(kst);
+        const float fr = kst - (float)k0;
         const float2 wt = make_float2(fmaxf(0.f, fmaf(-fr, t.z, t.w)), fmaxf(0.f, fmaf(fr, t.z, c1)));
         const TA ga = arow[k0];
         if constexpr (NMAP == 3) {
@@ -161,6 +166,48 @@ __global__ void __launch_bounds__(NT, 2) backproject_kernel(
   }
 
   const int i = i0 + row;
+  const size_t NN = (size_t)N * N;
+  if (KS > 1) {   // angle split: publish partials; the last CTA of this tile reduces in ks order
+    if (i < N) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int j = j0 + lx + 8 * q;
+        if (j >= N) continue;
+        float *pp = part3 + ((size_t)(ks * S + s) * 3) * NN + (size_t)i * N + j;
+        pp[0] = am[q].x + am[q].y;
+        if constexpr (NMAP == 3) {
+          pp[NN] = ad[q].x + ad[q].y;
+          pp[2 * NN] = as[q].x + as[q].y;
+        }
+      }
+    }
+    __shared__ bool last;
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) {
+      unsigned int *cnt = done3 + (size_t)s * gridDim.x * gridDim.y + blockIdx.y * gridDim.x + blockIdx.x;
+      last = atomicAdd(cnt, 1u) == (unsigned)(KS - 1);
+      if (last) *cnt = 0u;   // re-arm
+    }
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    if (i >= N) return;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int j = j0 + lx + 8 * q;
+      if (j >= N) continue;
+      float v[3] = {0.f, 0.f, 0.f};
+      for (int k2 = 0; k2 < KS; ++k2) {
+        const float *pp = part3 + ((size_t)(k2 * S + s) * 3) * NN + (size_t)i * N + j;
+#pragma unroll
+        for (int m = 0; m < (NMAP == 3 ? 3 : 1); ++m) v[m] += __ldcg(pp + m * NN);
+      }
+      am[q] = make_float2(v[0], 0.f);
+      ad[q] = make_float2(v[1], 0.f);
+      as[q] = make_float2(v[2], 0.f);
+    }
+  }
   if (i >= N) return;
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
@@ -172,7 +219,7 @@ __global__ void __launch_bounds__(NT, 2) backproject_kernel(
     if constexpr (NMAP == 3) {
       float vd = ad[q].x + ad[q].y, vs = as[q].x + as[q].y;
       if (mu) {   // cost path: + 2 lambda x (eq. 5); maps have slice stride N*N
-        const size_t ip = (size_t)s * N * N + p;
+        const size_t ip = (size_t)s * NN + p;
         const float l2 = 2.f * lambda;
         vm = fmaf(l2, __ldg(mu + ip), vm);
         vd = fmaf(l2, __ldg(delta + ip), vd);
@@ -195,13 +242,17 @@ cudaError_t launch_bp(const ei_plan &p, const typename Layout<NMAP>::A *GA, cons
   cudaError_t e = cudaFuncSetAttribute((const void *)backproject_kernel<NMAP>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  dim3 grid((p.N + TILE - 1) / TILE, (p.N + TILE - 1) / TILE, p.S);
+  dim3 grid((p.N + TILE - 1) / TILE, (p.N + TILE - 1) / TILE, p.S * p.KS);
   backproject_kernel<NMAP><<<grid, NT, smem, st>>>(GA, GB, p.tab.k3, p.N, p.NA, p.ND, mu, delta,
-                                                   sigma, lambda, o0, o1, o2, out_stride);
+                                                   sigma, lambda, o0, o1, o2, out_stride, p.S, p.KS,
+                                                   p.part3, p.done3);
   return cudaGetLastError();
 }
 
 }  // namespace
+
+int bp_tiles(int N) { return ((N + TILE - 1) / TILE) * ((N + TILE - 1) / TILE); }
+int bp_chunks(int NA) { return (NA + CH - 1) / CH; }
 
 cudaError_t launch_backproject3(const ei_plan &p, const float *mu, const float *delta,
                                 const float *sigma, float lambda, float *g_mu, float *g_delta,

@@ -9,9 +9,11 @@
 //   r     = s_mod - s_exp;  S += r^2                     eq. 5
 //   g_mu = -2 sum r s;  g_Delta = 2 sum r s u / W^2;  g_sigma = sum r s (u^2 - W^2) / W^4
 //   g_delta = z D^T g_Delta                              halo 1 more (2 in total)
-// s_exp is streamed once, coalesced along t; the M mask positions are an inner loop; the
-// cost is reduced fp32 (per thread, <= M*ceil(Nd/256) terms) -> fp64 (warp shuffle, block)
-// -> one fp64 partial per row, summed in a fixed order by K4 (deterministic, atomic-free).
+// s_exp is streamed once, coalesced along t, its M values per (theta, t) loaded up front (8 at a
+// time) so the loads overlap; the cost is reduced fp32 (per thread, <= M*ceil(Nd/256) terms) ->
+// fp64 (warp shuffle, block) -> one fp64 partial per row.  K4 is fused: the last CTA of a slice
+// to finish (per-slice arrival counter) sums that slice's row partials in index order (+ lambda
+// times K0's per-tile sum x^2 partials) -> cost[s].  Deterministic; no float atomics.
 #include "ei_common.cuh"
 
 namespace ei {
@@ -38,7 +40,9 @@ __global__ void __launch_bounds__(K2_THREADS) curve_kernel(
     const float *__restrict__ mask, const float *__restrict__ drift,
     const float *__restrict__ s_exp, int NA, int ND, int M,
     float z, float inv_du, float *__restrict__ s_mod, float4 *__restrict__ GA,
-    float2 *__restrict__ GB, double *__restrict__ part, int32_t *__restrict__ status) {
+    float2 *__restrict__ GB, double *__restrict__ part, int32_t *__restrict__ status,
+    unsigned int *__restrict__ done, const double *__restrict__ part_reg, int RB, float lambda,
+    double *__restrict__ cost_out) {
   extern __shared__ float sm[];
   float *pd = sm;              // [ND] P_delta row
   float *gD = sm + ND;         // [ND] g_Delta row
@@ -85,20 +89,30 @@ __global__ void __launch_bounds__(K2_THREADS) curve_kernel(
     mu_cl += mc;
     w2_cl += wc;
     float gm = 0.f, gd = 0.f, gs = 0.f;
-    for (int m = 0; m < M; ++m) {
-      const float u = smask[m] - base;
-      const float sv = amp * expf(-0.5f * u * u * invW2);
-      if (MODE == 0) {
-        s_mod[row + (size_t)m * ND + k] = sv;
-      } else {
-        const float se = __ldg(s_exp + row + (size_t)m * ND + k);
-        bad += !isfinite(se);
-        const float r = sv - se;
-        cost = fmaf(r, r, cost);
-        const float rs = r * sv;
-        gm += rs;
-        gd = fmaf(rs, u, gd);
-        gs = fmaf(rs, fmaf(u, u, -W2), gs);
+    for (int m0 = 0; m0 < M; m0 += 8) {
+      float se[8];
+      if (MODE == 1) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          se[u] = (m0 + u < M) ? __ldg(s_exp + row + (size_t)(m0 + u) * ND + k) : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int m = m0 + u;
+        if (m >= M) break;
+        const float du_ = smask[m] - base;
+        const float sv = amp * expf(-0.5f * du_ * du_ * invW2);
+        if (MODE == 0) {
+          s_mod[row + (size_t)m * ND + k] = sv;
+        } else {
+          bad += !isfinite(se[u]);
+          const float r = sv - se[u];
+          cost = fmaf(r, r, cost);
+          const float rs = r * sv;
+          gm += rs;
+          gd = fmaf(rs, du_, gd);
+          gs = fmaf(rs, fmaf(du_, du_, -W2), gs);
+        }
       }
     }
     if (MODE == 1) {
@@ -133,26 +147,28 @@ __global__ void __launch_bounds__(K2_THREADS) curve_kernel(
     Brow[e] = make_float2(l ? gsS[e - 1] : 0.f, r ? gsS[e] : 0.f);
   }
   const double tot = block_sum((double)cost, red);
-  if (threadIdx.x == 0) part[(size_t)s * NA + a] = tot;
   if (bad) atomicAdd(&status[0], bad);
   if (mu_cl) atomicAdd(&status[1], mu_cl);
   if (w2_cl) atomicAdd(&status[2], w2_cl);
-}
-
-// K4: cost[s] = sum_a part_curve[s][a] + lambda * sum_b part_reg[s][b], fixed order.
-__global__ void __launch_bounds__(256) finalize_kernel(const double *__restrict__ part_curve,
-                                                       int NA, const double *__restrict__ part_reg,
-                                                       int RB, float lambda,
-                                                       double *__restrict__ cost) {
-  __shared__ double red[8];
-  const int s = blockIdx.x;
-  double c = 0.0, r = 0.0;
-  for (int a = threadIdx.x; a < NA; a += blockDim.x) c += part_curve[(size_t)s * NA + a];
+  // fused K4: last CTA of slice s reduces the slice's partials in index order
+  __shared__ bool last;
+  if (threadIdx.x == 0) {
+    part[(size_t)s * NA + a] = tot;
+    __threadfence();
+    last = atomicAdd(&done[s], 1u) == (unsigned)(NA - 1);
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  double c = 0.0, rg = 0.0;
+  for (int q = threadIdx.x; q < NA; q += blockDim.x) c += __ldcg(part + (size_t)s * NA + q);
   if (lambda > 0.f)
-    for (int b = threadIdx.x; b < RB; b += blockDim.x) r += part_reg[(size_t)s * RB + b];
-  const double v = c + (double)lambda * r;
-  const double tot = block_sum(v, red);
-  if (threadIdx.x == 0) cost[s] = tot;
+    for (int b = threadIdx.x; b < RB; b += blockDim.x) rg += __ldcg(part_reg + (size_t)s * RB + b);
+  const double v = block_sum(c + (double)lambda * rg, red);
+  if (threadIdx.x == 0) {
+    cost_out[s] = v;
+    done[s] = 0u;   // re-arm for the next evaluation
+  }
 }
 
 }  // namespace
@@ -173,26 +189,24 @@ cudaError_t launch_curve_forward(const ei_plan &p, const float *flat, const floa
   dim3 grid(p.NA, p.S);
   curve_kernel<0><<<grid, K2_THREADS, smem, st>>>(p.P, p.proj.RS, p.S, flat, mask, drift, nullptr, p.NA, p.ND, p.M,
                                                   (float)p.g.z, (float)(1.0 / p.g.det_pitch), s_mod,
-                                                  nullptr, nullptr, nullptr, nullptr);
+                                                  nullptr, nullptr, nullptr, nullptr, nullptr,
+                                                  nullptr, 0, 0.f, nullptr);
   return cudaGetLastError();
 }
 
 cudaError_t launch_curve_cost_grad(const ei_plan &p, const float *flat, const float *mask,
                                    const float *drift, const float *s_exp, int32_t *status,
-                                   cudaStream_t st) {
+                                   float lambda, double *cost, cudaStream_t st) {
   const size_t smem = k2_smem(p);
   cudaError_t e = k2_attr((const void *)curve_kernel<1>, smem);
   if (e != cudaSuccess) return e;
   dim3 grid(p.NA, p.S);
   curve_kernel<1><<<grid, K2_THREADS, smem, st>>>(p.P, p.proj.RS, p.S, flat, mask, drift, s_exp, p.NA, p.ND, p.M,
                                                   (float)p.g.z, (float)(1.0 / p.g.det_pitch), nullptr,
-                                                  p.GA, p.GB, p.part_curve, status);
+                                                  p.GA, p.GB, p.part_curve, status, p.done,
+                                                  p.part_reg, p.RB, lambda, cost);
   return cudaGetLastError();
 }
 
-cudaError_t launch_finalize(const ei_plan &p, float lambda, double *cost, cudaStream_t st) {
-  finalize_kernel<<<p.S, 256, 0, st>>>(p.part_curve, p.NA, p.part_reg, p.RB, lambda, cost);
-  return cudaGetLastError();
-}
 
 }  // namespace ei

@@ -37,7 +37,8 @@ __global__ void __launch_bounds__(256) pack_pairs_kernel(const float *__restrict
                                                          const float *__restrict__ in2,
                                                          size_t in_stride, int N, PairOut<NMAP> out,
                                                          double *__restrict__ part_reg,
-                                                         int32_t *__restrict__ status) {
+                                                         int32_t *__restrict__ status,
+                                                         SmallCheck chk, int nflat, int M, int NA) {
   __shared__ float tile[NMAP][T + 1][T + 2];
   __shared__ double red[8];
   const int s = blockIdx.z, ta = blockIdx.y, tb = blockIdx.x;
@@ -90,6 +91,16 @@ __global__ void __launch_bounds__(256) pack_pairs_kernel(const float *__restrict
       }
     }
   }
+  if (status && chk.flat) {   // this CTA's share of the flat/mask/drift non-finite scan
+    const int total = nflat + M + (chk.drift ? NA : 0);
+    const int nb = gridDim.x * gridDim.y * gridDim.z;
+    const int b = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+    const int per = (total + nb - 1) / nb;
+    for (int t = b * per + ty * 32 + tx; t < min(total, (b + 1) * per); t += 256) {
+      const float v = t < nflat ? chk.flat[t] : (t < nflat + M ? chk.mask[t - nflat] : chk.drift[t - nflat - M]);
+      bad += !isfinite(v);
+    }
+  }
   if (status && bad) atomicAdd(&status[0], bad);   // integer count: order-independent
   if (part_reg) {
     for (int off = 16; off > 0; off >>= 1) sq += __shfl_down_sync(0xffffffffu, sq, off);
@@ -126,31 +137,20 @@ __global__ void pack_sino_kernel(const float *__restrict__ in, int NA, int ND, i
   }
 }
 
-__global__ void check_small_kernel(const float *__restrict__ flat, int nflat,
-                                   const float *__restrict__ mask, int M,
-                                   const float *__restrict__ drift, int NA,
-                                   int32_t *__restrict__ status) {
-  int bad = 0;
-  const int total = nflat + M + (drift ? NA : 0);
-  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
-    float v = t < nflat ? flat[t] : (t < nflat + M ? mask[t - nflat] : drift[t - nflat - M]);
-    bad += !isfinite(v);
-  }
-  for (int off = 16; off > 0; off >>= 1) bad += __shfl_down_sync(0xffffffffu, bad, off);
-  if ((threadIdx.x & 31) == 0 && bad) atomicAdd(&status[0], bad);
-}
 
 }  // namespace
 
 int reg_blocks(int N) { return ((N + 1 + T - 1) / T) * ((N + 1 + T - 1) / T); }
 
 cudaError_t launch_pack3(const ei_plan &p, const float *mu, const float *delta, const float *sigma,
-                         size_t in_stride, bool want_reg, int32_t *status, cudaStream_t st) {
+                         size_t in_stride, bool want_reg, int32_t *status, SmallCheck chk,
+                         cudaStream_t st) {
   const int nt = (p.N + 1 + T - 1) / T;
   dim3 grid(nt, nt, p.S), block(32, 8);
   PairOut<3> o{p.MA, p.MAT, p.MB, p.MBT};
   pack_pairs_kernel<3><<<grid, block, 0, st>>>(mu, delta, sigma, in_stride, p.N, o,
-                                               want_reg ? p.part_reg : nullptr, status);
+                                               want_reg ? p.part_reg : nullptr, status, chk,
+                                               p.S * 3 * p.ND, p.M, p.NA);
   return cudaGetLastError();
 }
 
@@ -159,7 +159,7 @@ cudaError_t launch_pack1(const ei_plan &p, const float *map, cudaStream_t st) {
   dim3 grid(nt, nt, p.S), block(32, 8);
   PairOut<1> o{p.M1, p.M1T};
   pack_pairs_kernel<1><<<grid, block, 0, st>>>(map, nullptr, nullptr, (size_t)p.N * p.N, p.N, o,
-                                               nullptr, nullptr);
+                                               nullptr, nullptr, SmallCheck{}, 0, 0, 0);
   return cudaGetLastError();
 }
 
@@ -173,13 +173,5 @@ cudaError_t launch_pack_sino(const ei_plan &p, const float *sino, int n_maps, cu
   return cudaGetLastError();
 }
 
-cudaError_t launch_check_small(const ei_plan &p, const float *flat, const float *mask,
-                               const float *drift, int32_t *status, cudaStream_t st) {
-  const int nflat = p.S * 3 * p.ND;
-  const int total = nflat + p.M + p.NA;
-  const int blocks = (total + 255) / 256 < 64 ? (total + 255) / 256 : 64;
-  check_small_kernel<<<blocks, 256, 0, st>>>(flat, nflat, mask, p.M, drift, p.NA, status);
-  return cudaGetLastError();
-}
 
 }  // namespace ei

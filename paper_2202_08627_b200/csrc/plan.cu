@@ -40,7 +40,7 @@ cudaError_t dalloc(T **p, size_t count) {
 
 void free_timing(ei_plan *p) {
   if (p->tev) {
-    for (int i = 0; i < 7 * p->tcap; ++i) cudaEventDestroy(p->tev[i]);
+    for (int i = 0; i < 7 * p->tcap; ++i) cudaEventDestroy(p->tev[i]);   // 5 used per eval
     delete[] p->tev;
   }
   p->tev = nullptr;
@@ -52,7 +52,7 @@ void free_plan(ei_plan *p) {
   if (!p) return;
   free_timing(p);
   void *ptrs[] = {p->tab.k1, p->tab.k3, p->proj.groups, p->proj.order, p->proj.win1, p->proj.winRS, p->MA, p->MAT, p->MB,
-                  p->MBT, p->M1, p->M1T, p->diag, p->P, p->GA, p->GB, p->GA1,
+                  p->MBT, p->M1, p->M1T, p->diag, p->done, p->done3, p->part3, p->P, p->GA, p->GB, p->GA1,
                   p->part_curve, p->part_reg, p->h_maps, p->h_flat, p->h_mask, p->h_drift,
                   p->h_sexp, p->h_grad, p->h_cost, p->h_status};
   for (void *q : ptrs)
@@ -149,6 +149,16 @@ int ei_plan_create(const ei_geometry *geom, const double *angles, ei_plan **out)
   A(dalloc(&p->GA1, S * SINO1));
   A(dalloc(&p->part_curve, S * NA));
   A(dalloc(&p->part_reg, S * p->RB));
+  // K3 angle split for grids with fewer than ~2 CTAs per SM (partials reduced by the last CTA)
+  {
+    const long long ctas = (long long)ei::bp_tiles(p->N) * p->S;
+    int KS = 1;
+    while (KS < 8 && ctas * KS < 2 * 148 && 2 * KS <= ei::bp_chunks(p->NA)) KS *= 2;
+    p->KS = KS;
+  }
+  A(dalloc(&p->done, S));
+  A(dalloc(&p->done3, S * (size_t)ei::bp_tiles(p->N)));
+  if (p->KS > 1) A(dalloc(&p->part3, (size_t)p->KS * S * 3 * p->N * p->N));
   if (e == cudaSuccess) A(cudaMemcpy(p->tab.k1, k1, sizeof(float4) * NA, cudaMemcpyHostToDevice));
   if (e == cudaSuccess) A(cudaMemcpy(p->tab.k3, k3, sizeof(float4) * NA, cudaMemcpyHostToDevice));
   if (e == cudaSuccess)
@@ -156,6 +166,8 @@ int ei_plan_create(const ei_geometry *geom, const double *angles, ei_plan **out)
   if (e == cudaSuccess)
     A(cudaMemcpy(p->proj.order, order.data(), sizeof(int) * order.size(), cudaMemcpyHostToDevice));
   if (e == cudaSuccess) A(cudaMemset(p->diag, 0, sizeof(int32_t)));
+  if (e == cudaSuccess) A(cudaMemset(p->done, 0, sizeof(unsigned int) * S));
+  if (e == cudaSuccess) A(cudaMemset(p->done3, 0, sizeof(unsigned int) * S * ei::bp_tiles(p->N)));
   if (e == cudaSuccess)
     A(cudaMemcpy(p->proj.win1, win1.data(), sizeof(int2) * win1.size(), cudaMemcpyHostToDevice));
   if (e == cudaSuccess && !winRS.empty())
@@ -218,8 +230,8 @@ int ei_plan_read_timing(ei_plan *p, double ms[6], int *n_evals) {
   for (int k = 0; k < 6; ++k) ms[k] = 0.0;
   for (int e = 0; e < p->tn; ++e) {
     cudaEvent_t *ev = p->tev + 7 * e;
-    if (cudaEventSynchronize(ev[6]) != cudaSuccess) return EI_ERR_CUDA;
-    for (int k = 0; k < 6; ++k) {
+    if (cudaEventSynchronize(ev[4]) != cudaSuccess) return EI_ERR_CUDA;
+    for (int k = 0; k < 4; ++k) {
       float t = 0.f;
       if (cudaEventElapsedTime(&t, ev[k], ev[k + 1]) != cudaSuccess) return EI_ERR_CUDA;
       ms[k] += t;
@@ -238,7 +250,8 @@ int ei_project(const ei_plan *p, const float *maps, int n_maps, float *sino, voi
   cudaError_t e;
   if (n_maps == 3) {
     // maps [S][3][N][N]: slice stride 3*NN, plane stride NN
-    e = ei::launch_pack3(*p, maps, maps + NN, maps + 2 * NN, 3 * NN, false, nullptr, st);
+    e = ei::launch_pack3(*p, maps, maps + NN, maps + 2 * NN, 3 * NN, false, nullptr,
+                         ei::SmallCheck{}, st);
     if (e == cudaSuccess) e = ei::launch_project3(*p, sino, 1, st);
     p->stats[0] += 1;
     p->stats[1] += 3;
@@ -283,7 +296,8 @@ int ei_forward(const ei_plan *p, const float *mu, const float *delta, const floa
   if (!p || !mu || !delta || !sigma || !flat || !mask || !s_mod) return EI_ERR_NULL;
   cudaStream_t st = (cudaStream_t)stream;
   // maps given as three [S][N][N] arrays: plane stride handled by pack3 (slice stride NN)
-  cudaError_t e = ei::launch_pack3(*p, mu, delta, sigma, (size_t)p->N * p->N, false, nullptr, st);
+  cudaError_t e = ei::launch_pack3(*p, mu, delta, sigma, (size_t)p->N * p->N, false, nullptr,
+                                   ei::SmallCheck{}, st);
   if (e == cudaSuccess) e = ei::launch_project3(*p, p->P, p->proj.RS, st);
   if (e == cudaSuccess) e = ei::launch_curve_forward(*p, flat, mask, drift, s_mod, st);
   p->stats[0] += 1;
@@ -305,21 +319,19 @@ int ei_cost_grad(const ei_plan *p, const float *mu, const float *delta, const fl
   cudaEvent_t *ev = (p->tev && p->tn < p->tcap) ? p->tev + 7 * p->tn++ : nullptr;
   auto mark = [&](int k) { if (ev) cudaEventRecord(ev[k], st); };
   const size_t NN = (size_t)p->N * p->N;
+  ei::SmallCheck chk{flat, mask, drift};
   mark(0);
-  cudaError_t e = ei::launch_check_small(*p, flat, mask, drift, status, st);          // K0'
+  cudaError_t e = ei::launch_pack3(*p, mu, delta, sigma, NN, lambda > 0.f, status, chk, st);  // K0
   mark(1);
-  if (e == cudaSuccess) e = ei::launch_pack3(*p, mu, delta, sigma, NN, lambda > 0.f, status, st);  // K0
-  mark(2);
   if (e == cudaSuccess) e = ei::launch_project3(*p, p->P, p->proj.RS, st);          // K1
+  mark(2);
+  if (e == cudaSuccess)
+    e = ei::launch_curve_cost_grad(*p, flat, mask, drift, s_exp, status, lambda, cost, st);  // K2+K4
   mark(3);
-  if (e == cudaSuccess) e = ei::launch_curve_cost_grad(*p, flat, mask, drift, s_exp, status, st);  // K2
-  mark(4);
   if (e == cudaSuccess) e = ei::launch_backproject3(*p, mu, delta, sigma, lambda, g_mu, g_delta,
                                                     g_sigma, NN, st);                  // K3
-  mark(5);
-  if (e == cudaSuccess) e = ei::launch_finalize(*p, lambda, cost, st);              // K4
-  mark(6);
-  p->stats[5] += 6;
+  mark(4);
+  p->stats[5] += 4;
   p->stats[0] += 1;
   p->stats[1] += 3;
   p->stats[2] += 1;

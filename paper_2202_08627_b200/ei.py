@@ -26,7 +26,7 @@ EI_OK, EI_ERR_NULL, EI_ERR_SHAPE, EI_ERR_DOMAIN, EI_ERR_RESOURCE, EI_ERR_CUDA = 
 SYMBOLS = ("ei_plan_create", "ei_plan_destroy", "ei_project", "ei_backproject", "ei_forward",
            "ei_cost_grad", "ei_cost_grad_host", "ei_plan_stats", "ei_plan_set_timing",
            "ei_plan_read_timing", "ei_plan_info", "ei_error_string", "ei_version")
-KERNELS = ("check", "K0_pack", "K1_project", "K2_curve", "K3_backproject", "K4_finalize")
+KERNELS = ("K0_pack", "K1_project", "K2_curve", "K3_backproject", "unused4", "unused5")
 
 
 class ei_geometry(ctypes.Structure):

@@ -14,7 +14,7 @@
 namespace ei {
 namespace {
 
-constexpr int T = 32;
+constexpr int T = 16;
 
 template <int NMAP>
 struct PairOut;
@@ -28,9 +28,9 @@ struct PairOut<1> {
   float2 *a, *aT;
 };
 
-// grid (ceil((N+1)/32), ceil((N+1)/32), S), block (32, 8).  Tile (ta, tb) loads map rows
-// [32ta-1, 32ta+31] x cols [32tb-1, 32tb+31] and writes normal entries (rows 32ta.., entries
-// 32tb..) and transposed entries (T-rows 32tb.., entries 32ta..).
+// grid (ceil((N+1)/T), ceil((N+1)/T), S), block (T, T), T = 16.  Tile (ta, tb) loads map rows
+// [T ta - 1, T ta + T - 1] x cols [T tb - 1, T tb + T - 1] and writes normal entries (rows T ta..,
+// entries T tb..) and transposed entries (T-rows T tb.., entries T ta..).
 template <int NMAP>
 __global__ void __launch_bounds__(256) pack_pairs_kernel(const float *__restrict__ in0,
                                                          const float *__restrict__ in1,
@@ -39,37 +39,35 @@ __global__ void __launch_bounds__(256) pack_pairs_kernel(const float *__restrict
                                                          double *__restrict__ part_reg,
                                                          int32_t *__restrict__ status,
                                                          SmallCheck chk, int nflat, int M, int NA) {
-  __shared__ float tile[NMAP][T + 1][T + 2];
+  __shared__ float tile[NMAP][T + 1][T + 2];   // (T+1)^2 with a one-element halo
   __shared__ double red[8];
   const int s = blockIdx.z, ta = blockIdx.y, tb = blockIdx.x;
-  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * T + tx;
   const float *src[3] = {in0 + s * in_stride, NMAP == 3 ? in1 + s * in_stride : nullptr,
                          NMAP == 3 ? in2 + s * in_stride : nullptr};
   double sq = 0.0;
   int bad = 0;
   // load (T+1) x (T+1) with a one-element halo above and to the left
-  for (int r = ty; r < T + 1; r += 8) {
-    const int i = ta * T - 1 + r;
-    for (int c = tx; c < T + 1; c += 32) {
-      const int j = tb * T - 1 + c;
-      const bool in = (i >= 0 && i < N && j >= 0 && j < N);
+  for (int q = tid; q < (T + 1) * (T + 1); q += T * T) {
+    const int r = q / (T + 1), c = q - r * (T + 1);
+    const int i = ta * T - 1 + r, j = tb * T - 1 + c;
+    const bool in = (i >= 0 && i < N && j >= 0 && j < N);
 #pragma unroll
-      for (int m = 0; m < NMAP; ++m) {
-        const float v = in ? __ldg(src[m] + (size_t)i * N + j) : 0.f;
-        tile[m][r][c] = v;
-        if (in && r >= 1 && c >= 1) {   // owned pixel: count once
-          bad += !isfinite(v);
-          sq += (double)v * v;
-        }
+    for (int m = 0; m < NMAP; ++m) {
+      const float v = in ? __ldg(src[m] + (size_t)i * N + j) : 0.f;
+      tile[m][r][c] = v;
+      if (in && r >= 1 && c >= 1) {   // owned pixel: count once
+        bad += !isfinite(v);
+        sq += (double)v * v;
       }
     }
   }
   __syncthreads();
   const size_t rl = (size_t)N + 1, slice = (size_t)N * rl;
-  // normal: row i = 32ta + r, entry e = 32tb + c  -> (x[i][e-1], x[i][e]) = tile[r+1][c], tile[r+1][c+1]
-  // transposed: T-row j = 32tb + r, entry e = 32ta + c -> (x[e-1][j], x[e][j]) = tile[c][r+1], tile[c+1][r+1]
-  for (int r = ty; r < T; r += 8) {
-    const int c = tx;
+  // normal: row i = T ta + r, entry e = T tb + c -> (x[i][e-1], x[i][e]) = tile[r+1][c], tile[r+1][c+1]
+  // transposed: T-row j = T tb + r, entry e = T ta + c -> (x[e-1][j], x[e][j]) = tile[c][r+1], tile[c+1][r+1]
+  {
+    const int r = ty, c = tx;
     const int i = ta * T + r, e = tb * T + c;
     if (i < N && e <= N) {
       const size_t o = s * slice + (size_t)i * rl + e;
@@ -96,7 +94,7 @@ __global__ void __launch_bounds__(256) pack_pairs_kernel(const float *__restrict
     const int nb = gridDim.x * gridDim.y * gridDim.z;
     const int b = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
     const int per = (total + nb - 1) / nb;
-    for (int t = b * per + ty * 32 + tx; t < min(total, (b + 1) * per); t += 256) {
+    for (int t = b * per + tid; t < min(total, (b + 1) * per); t += T * T) {
       const float v = t < nflat ? chk.flat[t] : (t < nflat + M ? chk.mask[t - nflat] : chk.drift[t - nflat - M]);
       bad += !isfinite(v);
     }
@@ -104,9 +102,9 @@ __global__ void __launch_bounds__(256) pack_pairs_kernel(const float *__restrict
   if (status && bad) atomicAdd(&status[0], bad);   // integer count: order-independent
   if (part_reg) {
     for (int off = 16; off > 0; off >>= 1) sq += __shfl_down_sync(0xffffffffu, sq, off);
-    if (tx == 0) red[ty] = sq;
+    if ((tid & 31) == 0) red[tid >> 5] = sq;
     __syncthreads();
-    if (ty == 0 && tx == 0) {
+    if (tid == 0) {
       double t = 0.0;
       for (int w = 0; w < 8; ++w) t += red[w];
       part_reg[(size_t)s * gridDim.x * gridDim.y + blockIdx.y * gridDim.x + blockIdx.x] = t;
@@ -115,10 +113,11 @@ __global__ void __launch_bounds__(256) pack_pairs_kernel(const float *__restrict
 }
 
 // planar sino [S][NMAP][NA][ND] -> pair layout [S][NA][ND+1] (entry e = (g[e-1], g[e]))
+// (each value pre-multiplied by the angle's Joseph weight dx/|c_dom|, as K2 does)
 template <int NMAP>
 __global__ void pack_sino_kernel(const float *__restrict__ in, int NA, int ND, int S,
                                  float4 *__restrict__ GA, float2 *__restrict__ GB,
-                                 float2 *__restrict__ GA1) {
+                                 float2 *__restrict__ GA1, const float4 *__restrict__ k3) {
   const size_t plane = (size_t)NA * ND, rl = (size_t)ND + 1;
   const size_t total = (size_t)S * NA * rl;
   for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < total;
@@ -127,7 +126,8 @@ __global__ void pack_sino_kernel(const float *__restrict__ in, int NA, int ND, i
     const int e = (int)(t - sa * rl);
     const size_t s = sa / NA, a = sa - s * NA;
     const float *b = in + s * NMAP * plane + a * ND;
-    auto at = [&](int m, int k) { return (k >= 0 && k < ND) ? __ldg(b + m * plane + k) : 0.f; };
+    const float sc = __ldg(k3 + a).w;
+    auto at = [&](int m, int k) { return (k >= 0 && k < ND) ? sc * __ldg(b + m * plane + k) : 0.f; };
     if (NMAP == 3) {
       GA[t] = make_float4(at(0, e - 1), at(0, e), at(1, e - 1), at(1, e));
       GB[t] = make_float2(at(2, e - 1), at(2, e));
@@ -146,7 +146,7 @@ cudaError_t launch_pack3(const ei_plan &p, const float *mu, const float *delta, 
                          size_t in_stride, bool want_reg, int32_t *status, SmallCheck chk,
                          cudaStream_t st) {
   const int nt = (p.N + 1 + T - 1) / T;
-  dim3 grid(nt, nt, p.S), block(32, 8);
+  dim3 grid(nt, nt, p.S), block(T, T);
   PairOut<3> o{p.MA, p.MAT, p.MB, p.MBT};
   pack_pairs_kernel<3><<<grid, block, 0, st>>>(mu, delta, sigma, in_stride, p.N, o,
                                                want_reg ? p.part_reg : nullptr, status, chk,
@@ -156,7 +156,7 @@ cudaError_t launch_pack3(const ei_plan &p, const float *mu, const float *delta, 
 
 cudaError_t launch_pack1(const ei_plan &p, const float *map, cudaStream_t st) {
   const int nt = (p.N + 1 + T - 1) / T;
-  dim3 grid(nt, nt, p.S), block(32, 8);
+  dim3 grid(nt, nt, p.S), block(T, T);
   PairOut<1> o{p.M1, p.M1T};
   pack_pairs_kernel<1><<<grid, block, 0, st>>>(map, nullptr, nullptr, (size_t)p.N * p.N, p.N, o,
                                                nullptr, nullptr, SmallCheck{}, 0, 0, 0);
@@ -167,9 +167,9 @@ cudaError_t launch_pack_sino(const ei_plan &p, const float *sino, int n_maps, cu
   const size_t total = (size_t)p.S * p.NA * (p.ND + 1);
   const int blocks = (int)((total + 255) / 256 < 148 * 16 ? (total + 255) / 256 : 148 * 16);
   if (n_maps == 3)
-    pack_sino_kernel<3><<<blocks, 256, 0, st>>>(sino, p.NA, p.ND, p.S, p.GA, p.GB, nullptr);
+    pack_sino_kernel<3><<<blocks, 256, 0, st>>>(sino, p.NA, p.ND, p.S, p.GA, p.GB, nullptr, p.tab.k3);
   else
-    pack_sino_kernel<1><<<blocks, 256, 0, st>>>(sino, p.NA, p.ND, p.S, nullptr, nullptr, p.GA1);
+    pack_sino_kernel<1><<<blocks, 256, 0, st>>>(sino, p.NA, p.ND, p.S, nullptr, nullptr, p.GA1, p.tab.k3);
   return cudaGetLastError();
 }
 

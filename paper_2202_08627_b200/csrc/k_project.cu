@@ -16,6 +16,8 @@
 //  * small problems split the rows over RS CTAs (partial P summed in fixed order by K2).
 #include <math.h>
 
+#include <stdlib.h>
+
 #include <algorithm>
 #include <vector>
 
@@ -41,6 +43,7 @@ __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0
 
 template <int NMAP>
 struct PL;
+
 template <>
 struct PL<3> {
   using A = float4;
@@ -67,10 +70,11 @@ struct ProjArgs {
 // warp (8 lanes) = 4 angles x 2 adjacent rays, whose taps fall on 2-4 consecutive window entries
 // (one conflict-free wavefront per LDS.128 quarter); slot m adds 4m to the angle.
 template <int NMAP>
-__global__ void __launch_bounds__(NT, 2) project_kernel(ProjArgs args) {
+__global__ void __launch_bounds__(NT, 3) project_kernel(ProjArgs args) {
   using TA = typename PL<NMAP>::A;
   const int N = args.N, ND = args.ND, RC = args.RC, CW = args.CW;
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  // separate planes (16-B / 8-B strides: conflict-free quarter/half-warp accesses)
   TA *sA = reinterpret_cast<TA *>(smem_raw);                                   // [2][RC][CW]
   float2 *sB = reinterpret_cast<float2 *>(sA + 2 * RC * CW);                  // [2][RC][CW]
 
@@ -91,7 +95,7 @@ __global__ void __launch_bounds__(NT, 2) project_kernel(ProjArgs args) {
     const int a = args.order[gi.x + al];
     aidx[m] = (aq + 4 * m < gi.y) ? a : -1;
     const float4 t = __ldg(args.k1 + a);
-    alpha[m] = kc * t.x;
+    alpha[m] = fmaf(kc, t.x, ctr);   // x* = alpha - tn * (i - ctr)
     tn[m] = t.y;
     scale[m] = t.z;
   }
@@ -113,7 +117,7 @@ __global__ void __launch_bounds__(NT, 2) project_kernel(ProjArgs args) {
       const bool ok = ent >= 0 && ent <= N;
       const size_t off = (size_t)(i0 + r) * rl + (ok ? ent : 0);
       cp_async(&sA[(buf * RC + r) * CW + l], gA + off, (int)sizeof(TA), ok);
-      if (PL<NMAP>::hasB) cp_async(&sB[(buf * RC + r) * CW + l], gB + off, 8, ok);
+      if constexpr (NMAP == 3) cp_async(&sB[(buf * RC + r) * CW + l], gB + off, 8, ok);
     }
     cp_commit();
   };
@@ -131,13 +135,13 @@ __global__ void __launch_bounds__(NT, 2) project_kernel(ProjArgs args) {
     const int2 wn = __ldg(wtab + c);
     if (wn.y == 0) continue;               // no ray of this CTA touches these rows
     const int i0 = r0 + c * RC, rc = min(RC, r1 - i0);
-    for (int r = 0; r < rc; ++r) {
-      const float yi = (float)(i0 + r) - ctr;
-      const TA *arow = sA + (b * RC + r) * CW - wn.x;
-      const float2 *brow = sB + (b * RC + r) * CW - wn.x;
+    const TA *arow = sA + b * RC * CW - wn.x;
+    const float2 *brow = sB + b * RC * CW - wn.x;
+    float yi = (float)i0 - ctr;
+    for (int r = 0; r < rc; ++r, yi += 1.f, arow += CW, brow += CW) {
 #pragma unroll
       for (int m = 0; m < 4; ++m) {
-        const float xs = fmaf(-tn[m], yi, alpha[m]) + ctr;
+        const float xs = fmaf(-tn[m], yi, alpha[m]);
         const int j0 = __float2int_rd(xs);
         const float fr = xs - (float)j0;
         const float2 wt = make_float2(1.f - fr, fr);
@@ -263,15 +267,17 @@ int plan_projector(ei_plan &p, const double *angles, std::vector<int2> &groups,
     order.push_back(a);
     groups.back().y += 1;
   }
-  const size_t per_entry = 24;          // float4 + float2 per staged pair entry
-  const size_t budget = 110 * 1024;     // two CTAs per SM
+  const size_t per_entry = 24;          // float4 + float2 per staged entry
+  // shared-memory budget per CTA: 72 KB keeps three CTAs per SM, 110 KB two (tuning knob)
+  const char *env = getenv("EI_K1_SMEM_KB");
+  const size_t budget = (env ? (size_t)atoi(env) : 72) * 1024;
   int RC = 32, nch = 0, CW = 0;
   for (;;) {
     build_windows(p, angles, groups, order, 1, RC, win1, nch, CW);
     if ((size_t)2 * RC * CW * per_entry <= budget || RC == 1) break;
     RC /= 2;
   }
-  if ((size_t)2 * RC * CW * per_entry > 220 * 1024) return EI_ERR_SHAPE;
+  if ((size_t)2 * RC * CW * per_entry > 200 * 1024) return EI_ERR_SHAPE;
   p.proj.RC = RC;
   p.proj.n_groups = (int)groups.size();
   p.proj.nch1 = nch;

@@ -111,16 +111,37 @@ __global__ void __launch_bounds__(NT, 3) project_kernel(ProjArgs args) {
   auto stage = [&](int c, int buf) {
     const int2 wn = __ldg(wtab + c);
     const int i0 = r0 + c * RC, rc = min(RC, r1 - i0);
-    for (int e = tid; e < rc * wn.y; e += NT) {
-      const int r = e / wn.y, l = e - r * wn.y;
+    for (int l = tid; l < wn.y; l += NT) {
       const int ent = wn.x + 1 + l;   // pair (x[j0], x[j0+1]) lives at entry j0 + 1
       const bool ok = ent >= 0 && ent <= N;
-      const size_t off = (size_t)(i0 + r) * rl + (ok ? ent : 0);
-      cp_async(&sA[(buf * RC + r) * CW + l], gA + off, (int)sizeof(TA), ok);
-      if constexpr (NMAP == 3) cp_async(&sB[(buf * RC + r) * CW + l], gB + off, 8, ok);
+      for (int r = 0; r < rc; ++r) {
+        const size_t off = (size_t)(i0 + r) * rl + (ok ? ent : 0);
+        cp_async(&sA[(buf * RC + r) * CW + l], gA + off, (int)sizeof(TA), ok);
+        if constexpr (NMAP == 3) cp_async(&sB[(buf * RC + r) * CW + l], gB + off, 8, ok);
+      }
     }
     cp_commit();
   };
+
+  // warp-uniform row range per slot: rows where at least one lane's ray has a tap inside the
+  // map (x* in (-1, N), linear in the row); rows outside it are skipped (exact: they add 0)
+  int wlo[4], whi[4];
+#pragma unroll
+  for (int m = 0; m < 4; ++m) {
+    int lo = 0x7fffffff, hi = -0x7fffffff;
+    if (aidx[m] >= 0 && k < ND) {
+      if (fabsf(tn[m]) < 1e-30f) {
+        if (alpha[m] > -1.f && alpha[m] < (float)N) { lo = 0; hi = N - 1; }
+      } else {
+        float y0 = (alpha[m] + 1.f) / tn[m], y1 = (alpha[m] - (float)N) / tn[m];
+        if (y0 > y1) { const float t = y0; y0 = y1; y1 = t; }
+        lo = max(0, (int)floorf(y0 + ctr) - 1);
+        hi = min(N - 1, (int)ceilf(y1 + ctr) + 1);
+      }
+    }
+    wlo[m] = __reduce_min_sync(0xffffffffu, lo);
+    whi[m] = __reduce_max_sync(0xffffffffu, hi);
+  }
 
   float2 am[4], ad[4], as[4];
 #pragma unroll
@@ -134,17 +155,27 @@ __global__ void __launch_bounds__(NT, 3) project_kernel(ProjArgs args) {
     if (c + 1 < nch) stage(c + 1, b ^ 1);  // overlaps the compute of chunk c
     const int2 wn = __ldg(wtab + c);
     if (wn.y == 0) continue;               // no ray of this CTA touches these rows
-    const int i0 = r0 + c * RC, rc = min(RC, r1 - i0);
+    const int i0 = r0 + c * RC, rc = min(RC, r1 - i0), i1 = i0 + rc - 1;
+    // warp-uniform slot activity over this chunk: skip the chunk if no slot has a tap in the
+    // map; branch-free fast path if every slot is active on every row; otherwise zero weights
+    bool any = false, all = true;
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      any |= (whi[m] >= i0 && wlo[m] <= i1);
+      all &= (wlo[m] <= i0 && whi[m] >= i1);
+    }
+    if (!any) continue;
     const TA *arow = sA + b * RC * CW - wn.x;
     const float2 *brow = sB + b * RC * CW - wn.x;
     float yi = (float)i0 - ctr;
-    for (int r = 0; r < rc; ++r, yi += 1.f, arow += CW, brow += CW) {
+    auto body = [&](bool masked, int i) {
 #pragma unroll
       for (int m = 0; m < 4; ++m) {
         const float xs = fmaf(-tn[m], yi, alpha[m]);
         const int j0 = __float2int_rd(xs);
-        const float fr = xs - (float)j0;
-        const float2 wt = make_float2(1.f - fr, fr);
+        float fr = xs - (float)j0;
+        float2 wt = make_float2(1.f - fr, fr);
+        if (masked && (i < wlo[m] || i > whi[m])) wt = make_float2(0.f, 0.f);
         const TA va = arow[j0];
         if constexpr (NMAP == 3) {
           am[m] = __ffma2_rn(wt, make_float2(va.x, va.y), am[m]);
@@ -154,6 +185,11 @@ __global__ void __launch_bounds__(NT, 3) project_kernel(ProjArgs args) {
           am[m] = __ffma2_rn(wt, va, am[m]);
         }
       }
+    };
+    if (all) {
+      for (int r = 0; r < rc; ++r, yi += 1.f, arow += CW, brow += CW) body(false, 0);
+    } else {
+      for (int r = 0; r < rc; ++r, yi += 1.f, arow += CW, brow += CW) body(true, i0 + r);
     }
   }
   if (k >= ND) return;

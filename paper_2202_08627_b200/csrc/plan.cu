@@ -153,7 +153,7 @@ int ei_plan_create(const ei_geometry *geom, const double *angles, ei_plan **out)
   {
     const long long ctas = (long long)ei::bp_tiles(p->N) * p->S;
     int KS = 1;
-    while (KS < 8 && ctas * KS < 2 * 148 && 2 * KS <= ei::bp_chunks(p->NA)) KS *= 2;
+    while (KS < 16 && ctas * KS < 3 * 148 && 2 * KS <= ei::bp_chunks(p->NA)) KS *= 2;
     p->KS = KS;
   }
   A(dalloc(&p->done, S));

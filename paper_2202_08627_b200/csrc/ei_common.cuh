@@ -33,6 +33,8 @@ struct ProjPlan {
   int2 *win1 = nullptr;     // device window table for RS = 1  [groups][tiles][nch1]
   int2 *winRS = nullptr;    // device window table for RS      [RS][groups][tiles][nchRS]
   int nch1 = 0, nchRS = 0;
+  int PAD = 0;              // zero entries before/after every pair-layout map row
+  int Rp = 0;               // padded row length (entries): N + 1 + 2 PAD, even
 };
 
 }  // namespace ei
@@ -43,11 +45,11 @@ struct ei_plan {
   ei::Tables tab;
   ei::ProjPlan proj;
   // workspace (allocated in ei_plan_create only)
-  // maps in the PAIR layout (k_pack.cu): row length N+1, entry e = (x[e-1], x[e]);
-  // *T = the transposed maps (column-dominant angles, H2)
-  float4 *MA = nullptr, *MAT = nullptr;   // [S][N][N+1] (mu0, mu1, delta0, delta1)
-  float2 *MB = nullptr, *MBT = nullptr;   // [S][N][N+1] (sigma0, sigma1)
-  float2 *M1 = nullptr, *M1T = nullptr;   // [S][N][N+1] single map (ei_project n_maps=1)
+  // maps in the PAIR layout (k_pack.cu): entry e = (x[e-1], x[e]), e = 0..N, stored at e + PAD
+  // in rows of proj.Rp entries (zero padding both sides); *T = the transposed maps (H2)
+  float4 *MA = nullptr, *MAT = nullptr;   // [S][N][Rp] (mu0, mu1, delta0, delta1)
+  float2 *MB = nullptr, *MBT = nullptr;   // [S][N][Rp] (sigma0, sigma1)
+  float2 *M1 = nullptr, *M1T = nullptr;   // [S][N][Rp] single map (ei_project n_maps=1)
   float *P = nullptr;         // [RS][S][3][NA][ND] (partial) projections
   int32_t *diag = nullptr;    // device counter of internal window overflows (must stay 0)
   // gradient sinograms in the PAIR layout read by K3: row length ND+1, entry e holds

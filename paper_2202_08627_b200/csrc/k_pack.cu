@@ -38,7 +38,8 @@ __global__ void __launch_bounds__(256) pack_pairs_kernel(const float *__restrict
                                                          size_t in_stride, int N, PairOut<NMAP> out,
                                                          double *__restrict__ part_reg,
                                                          int32_t *__restrict__ status,
-                                                         SmallCheck chk, int nflat, int M, int NA) {
+                                                         SmallCheck chk, int nflat, int M, int NA,
+                                                         int PAD, int Rp) {
   __shared__ float tile[NMAP][T + 1][T + 2];   // (T+1)^2 with a one-element halo
   __shared__ double red[8];
   const int s = blockIdx.z, ta = blockIdx.y, tb = blockIdx.x;
@@ -63,14 +64,14 @@ __global__ void __launch_bounds__(256) pack_pairs_kernel(const float *__restrict
     }
   }
   __syncthreads();
-  const size_t rl = (size_t)N + 1, slice = (size_t)N * rl;
+  const size_t rl = (size_t)Rp, slice = (size_t)N * rl;   // entry e stored at e + PAD
   // normal: row i = T ta + r, entry e = T tb + c -> (x[i][e-1], x[i][e]) = tile[r+1][c], tile[r+1][c+1]
   // transposed: T-row j = T tb + r, entry e = T ta + c -> (x[e-1][j], x[e][j]) = tile[c][r+1], tile[c+1][r+1]
   {
     const int r = ty, c = tx;
     const int i = ta * T + r, e = tb * T + c;
     if (i < N && e <= N) {
-      const size_t o = s * slice + (size_t)i * rl + e;
+      const size_t o = s * slice + (size_t)i * rl + PAD + e;
       if constexpr (NMAP == 3) {
         out.a[o] = make_float4(tile[0][r + 1][c], tile[0][r + 1][c + 1], tile[1][r + 1][c], tile[1][r + 1][c + 1]);
         out.b[o] = make_float2(tile[2][r + 1][c], tile[2][r + 1][c + 1]);
@@ -80,7 +81,7 @@ __global__ void __launch_bounds__(256) pack_pairs_kernel(const float *__restrict
     }
     const int j = tb * T + r, eT = ta * T + c;
     if (j < N && eT <= N) {
-      const size_t o = s * slice + (size_t)j * rl + eT;
+      const size_t o = s * slice + (size_t)j * rl + PAD + eT;
       if constexpr (NMAP == 3) {
         out.aT[o] = make_float4(tile[0][c][r + 1], tile[0][c + 1][r + 1], tile[1][c][r + 1], tile[1][c + 1][r + 1]);
         out.bT[o] = make_float2(tile[2][c][r + 1], tile[2][c + 1][r + 1]);
@@ -150,7 +151,7 @@ cudaError_t launch_pack3(const ei_plan &p, const float *mu, const float *delta, 
   PairOut<3> o{p.MA, p.MAT, p.MB, p.MBT};
   pack_pairs_kernel<3><<<grid, block, 0, st>>>(mu, delta, sigma, in_stride, p.N, o,
                                                want_reg ? p.part_reg : nullptr, status, chk,
-                                               p.S * 3 * p.ND, p.M, p.NA);
+                                               p.S * 3 * p.ND, p.M, p.NA, p.proj.PAD, p.proj.Rp);
   return cudaGetLastError();
 }
 
@@ -159,7 +160,8 @@ cudaError_t launch_pack1(const ei_plan &p, const float *map, cudaStream_t st) {
   dim3 grid(nt, nt, p.S), block(T, T);
   PairOut<1> o{p.M1, p.M1T};
   pack_pairs_kernel<1><<<grid, block, 0, st>>>(map, nullptr, nullptr, (size_t)p.N * p.N, p.N, o,
-                                               nullptr, nullptr, SmallCheck{}, 0, 0, 0);
+                                               nullptr, nullptr, SmallCheck{}, 0, 0, 0, p.proj.PAD,
+                                               p.proj.Rp);
   return cudaGetLastError();
 }
 

@@ -22,6 +22,7 @@
 #include <vector>
 
 #include "ei_common.cuh"
+#include "tma.cuh"
 
 namespace ei {
 namespace {
@@ -56,37 +57,92 @@ struct PL<1> {
 };
 
 struct ProjArgs {
-  const void *MA, *MAT;         // PL<NMAP>::A pairs, [S][N][N+1] (normal / transposed)
-  const float2 *MB, *MBT;       // sigma pairs (NMAP = 3)
+  const void *MA, *MAT;         // PL<NMAP>::A pairs, [S][N][Rp], entry e at e + PAD (normal / transposed)
+  const float2 *MB, *MBT;       // sigma pairs (NMAP = 3), same layout
   const float4 *k1;             // ic, tn, scale, rowdom
   const int2 *groups;           // {first sorted position, count}
   const int *order;             // sorted position -> angle index
   const int2 *win;              // [RS][groups][tiles][chunks] {cmin, W} (W = 0: chunk skipped)
-  int N, NA, ND, S, RS, RC, CW, nch;
+  int N, NA, ND, S, RS, RC, CW, nch, PAD, Rp;
   float *P;                     // [RS][S][NMAP][NA][ND]
 };
 
-// lane -> (angle aq = lane & 3 of the group's current angle quad, ray rr = lane >> 2): a quarter
-// warp (8 lanes) = 4 angles x 2 adjacent rays, whose taps fall on 2-4 consecutive window entries
-// (one conflict-free wavefront per LDS.128 quarter); slot m adds 4m to the angle.
+constexpr int NST = 3;          // pipeline stages (shared-memory ring)
+constexpr int NCW = NT / 32;    // consumer warps
+
+// Warp-specialised pipeline: warp NCW (the producer) streams each row chunk's window of pair
+// entries with 1-D bulk copies (TMA engine) into a NST-deep shared-memory ring, completing on a
+// per-stage "full" mbarrier (transaction bytes); the NCW consumer warps wait on "full", compute,
+// and release the stage on its "empty" mbarrier.  No CTA-wide barrier inside the loop.
+// Map rows are zero-padded by PAD >= CW entries on both sides, so every window is one in-bounds
+// contiguous copy per row and plane.
+// Consumer lane -> (angle aq = lane & 3 of the group's current angle quad, ray lane >> 2): a
+// quarter warp = 4 angles x 2 adjacent rays, taps on 2-4 consecutive entries (conflict-free
+// LDS.128); slot m adds 4m to the angle.
 template <int NMAP>
-__global__ void __launch_bounds__(NT, 3) project_kernel(ProjArgs args) {
+__global__ void __launch_bounds__(NT + 32, 2) project_kernel(ProjArgs args) {
   using TA = typename PL<NMAP>::A;
   const int N = args.N, ND = args.ND, RC = args.RC, CW = args.CW;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  // separate planes (16-B / 8-B strides: conflict-free quarter/half-warp accesses)
-  TA *sA = reinterpret_cast<TA *>(smem_raw);                                   // [2][RC][CW]
-  float2 *sB = reinterpret_cast<float2 *>(sA + 2 * RC * CW);                  // [2][RC][CW]
+  // 8-byte-entry planes start their copy at the even entry below the window (16-B aligned
+  // bulk copies) and need 2 spare entries per row; CW is even (host), so rows stay 16-B aligned
+  constexpr bool A8 = sizeof(TA) == 8;
+  const int CWA = A8 ? CW + 2 : CW, CWB = CW + 2;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  TA *sA = reinterpret_cast<TA *>(smem_raw);                                   // [NST][RC][CWA]
+  float2 *sB = reinterpret_cast<float2 *>(sA + NST * RC * CWA);               // [NST][RC][CWB]
+  __shared__ __align__(8) uint64_t full[NST], empty[NST];
 
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int kt = blockIdx.x * RT;
   const int2 gi = args.groups[blockIdx.y];
   const int s = blockIdx.z % args.S, rs = blockIdx.z / args.S;
   const float ctr = 0.5f * (float)(N - 1), dctr = 0.5f * (float)(ND - 1);
+  const bool rowdom = __ldg(args.k1 + args.order[gi.x]).w != 0.f;
+  const size_t Rp = (size_t)args.Rp;
+  const TA *gA = reinterpret_cast<const TA *>(rowdom ? args.MA : args.MAT) + (size_t)s * N * Rp + args.PAD;
+  const float2 *gB = NMAP == 3 ? (rowdom ? args.MB : args.MBT) + (size_t)s * N * Rp + args.PAD : nullptr;
+  const int r0 = (int)(((long long)rs * N) / args.RS), r1 = (int)(((long long)(rs + 1) * N) / args.RS);
+  const int nch = (r1 - r0 + RC - 1) / RC;
+  const int2 *wtab = args.win + (((size_t)rs * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * args.nch;
+
+  if (tid == 0) {
+    for (int q = 0; q < NST; ++q) {
+      mbar_init(&full[q], 1);
+      mbar_init(&empty[q], NCW);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+
+  if (w == NCW) {   // ---------------- producer warp ----------------
+    if (lane == 0) {
+      for (int c = 0; c < nch; ++c) {
+        const int st = c % NST;
+        if (c >= NST) mbar_wait(&empty[st], ((c / NST) + 1) & 1);
+        const int2 wn = __ldg(wtab + c);
+        const int i0 = r0 + c * RC, rc = min(RC, r1 - i0);
+        const int e0 = wn.x + 1;                       // first staged entry
+        const int eb = e0 & ~1, bofs = e0 - eb;        // B plane: 16-B aligned start
+        const uint32_t bytes8 = (uint32_t)(((wn.y + bofs) * 8 + 15) & ~15);
+        const uint32_t bytesA = A8 ? bytes8 : (uint32_t)wn.y * (uint32_t)sizeof(TA);
+        const uint32_t bytesB = NMAP == 3 ? bytes8 : 0u;
+        mbar_arrive_expect_tx(&full[st], wn.y > 0 ? (uint32_t)rc * (bytesA + bytesB) : 0u);
+        if (wn.y > 0) {
+          for (int r = 0; r < rc; ++r) {
+            const size_t row = (size_t)(i0 + r) * Rp;
+            bulk_g2s(sA + (st * RC + r) * CWA, gA + row + (A8 ? eb : e0), bytesA, &full[st]);
+            if (NMAP == 3) bulk_g2s(sB + (st * RC + r) * CWB, gB + row + eb, bytesB, &full[st]);
+          }
+        }
+      }
+    }
+    return;
+  }
+
+  // ---------------- consumer warps ----------------
   const int aq = lane & 3;
   const int k = kt + w * 8 + (lane >> 2);
   const float kc = (float)k - dctr;
-
   float alpha[4], tn[4], scale[4];
   int aidx[4];
 #pragma unroll
@@ -99,32 +155,8 @@ __global__ void __launch_bounds__(NT, 3) project_kernel(ProjArgs args) {
     tn[m] = t.y;
     scale[m] = t.z;
   }
-  const bool rowdom = __ldg(args.k1 + args.order[gi.x]).w != 0.f;
-  const size_t rl = (size_t)N + 1;
-  const TA *gA = reinterpret_cast<const TA *>(rowdom ? args.MA : args.MAT) + (size_t)s * N * rl;
-  const float2 *gB = PL<NMAP>::hasB ? (rowdom ? args.MB : args.MBT) + (size_t)s * N * rl : nullptr;
-
-  const int r0 = (int)(((long long)rs * N) / args.RS), r1 = (int)(((long long)(rs + 1) * N) / args.RS);
-  const int nch = (r1 - r0 + RC - 1) / RC;
-  const int2 *wtab = args.win + (((size_t)rs * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * args.nch;
-
-  auto stage = [&](int c, int buf) {
-    const int2 wn = __ldg(wtab + c);
-    const int i0 = r0 + c * RC, rc = min(RC, r1 - i0);
-    for (int l = tid; l < wn.y; l += NT) {
-      const int ent = wn.x + 1 + l;   // pair (x[j0], x[j0+1]) lives at entry j0 + 1
-      const bool ok = ent >= 0 && ent <= N;
-      for (int r = 0; r < rc; ++r) {
-        const size_t off = (size_t)(i0 + r) * rl + (ok ? ent : 0);
-        cp_async(&sA[(buf * RC + r) * CW + l], gA + off, (int)sizeof(TA), ok);
-        if constexpr (NMAP == 3) cp_async(&sB[(buf * RC + r) * CW + l], gB + off, 8, ok);
-      }
-    }
-    cp_commit();
-  };
-
   // warp-uniform row range per slot: rows where at least one lane's ray has a tap inside the
-  // map (x* in (-1, N), linear in the row); rows outside it are skipped (exact: they add 0)
+  // map (x* in (-1, N), linear in the row); rows outside it contribute exactly 0
   int wlo[4], whi[4];
 #pragma unroll
   for (int m = 0; m < 4; ++m) {
@@ -147,50 +179,48 @@ __global__ void __launch_bounds__(NT, 3) project_kernel(ProjArgs args) {
 #pragma unroll
   for (int m = 0; m < 4; ++m) am[m] = ad[m] = as[m] = make_float2(0.f, 0.f);
 
-  stage(0, 0);
   for (int c = 0; c < nch; ++c) {
-    const int b = c & 1;
-    cp_wait<0>();
-    __syncthreads();                       // chunk c landed; chunk c-1's buffer is free
-    if (c + 1 < nch) stage(c + 1, b ^ 1);  // overlaps the compute of chunk c
+    const int st = c % NST;
+    mbar_wait(&full[st], (c / NST) & 1);
     const int2 wn = __ldg(wtab + c);
-    if (wn.y == 0) continue;               // no ray of this CTA touches these rows
     const int i0 = r0 + c * RC, rc = min(RC, r1 - i0), i1 = i0 + rc - 1;
-    // warp-uniform slot activity over this chunk: skip the chunk if no slot has a tap in the
-    // map; branch-free fast path if every slot is active on every row; otherwise zero weights
     bool any = false, all = true;
 #pragma unroll
     for (int m = 0; m < 4; ++m) {
       any |= (whi[m] >= i0 && wlo[m] <= i1);
       all &= (wlo[m] <= i0 && whi[m] >= i1);
     }
-    if (!any) continue;
-    const TA *arow = sA + b * RC * CW - wn.x;
-    const float2 *brow = sB + b * RC * CW - wn.x;
-    float yi = (float)i0 - ctr;
-    auto body = [&](bool masked, int i) {
+    if (wn.y > 0 && any) {
+      const int bofs = (wn.x + 1) & 1;
+      const TA *arow = sA + st * RC * CWA - wn.x + (A8 ? bofs : 0);
+      const float2 *brow = sB + st * RC * CWB - wn.x + bofs;
+      float yi = (float)i0 - ctr;
+      auto body = [&](bool masked, int i) {
 #pragma unroll
-      for (int m = 0; m < 4; ++m) {
-        const float xs = fmaf(-tn[m], yi, alpha[m]);
-        const int j0 = __float2int_rd(xs);
-        float fr = xs - (float)j0;
-        float2 wt = make_float2(1.f - fr, fr);
-        if (masked && (i < wlo[m] || i > whi[m])) wt = make_float2(0.f, 0.f);
-        const TA va = arow[j0];
-        if constexpr (NMAP == 3) {
-          am[m] = __ffma2_rn(wt, make_float2(va.x, va.y), am[m]);
-          ad[m] = __ffma2_rn(wt, make_float2(va.z, va.w), ad[m]);
-          as[m] = __ffma2_rn(wt, brow[j0], as[m]);
-        } else {
-          am[m] = __ffma2_rn(wt, va, am[m]);
+        for (int m = 0; m < 4; ++m) {
+          const float xs = fmaf(-tn[m], yi, alpha[m]);
+          const int j0 = __float2int_rd(xs);
+          const float fr = xs - (float)j0;
+          float2 wt = make_float2(1.f - fr, fr);
+          if (masked && (i < wlo[m] || i > whi[m])) wt = make_float2(0.f, 0.f);
+          const TA va = arow[j0];
+          if constexpr (NMAP == 3) {
+            am[m] = __ffma2_rn(wt, make_float2(va.x, va.y), am[m]);
+            ad[m] = __ffma2_rn(wt, make_float2(va.z, va.w), ad[m]);
+            as[m] = __ffma2_rn(wt, brow[j0], as[m]);
+          } else {
+            am[m] = __ffma2_rn(wt, va, am[m]);
+          }
         }
+      };
+      if (all) {
+        for (int r = 0; r < rc; ++r, yi += 1.f, arow += CWA, brow += CWB) body(false, 0);
+      } else {
+        for (int r = 0; r < rc; ++r, yi += 1.f, arow += CWA, brow += CWB) body(true, i0 + r);
       }
-    };
-    if (all) {
-      for (int r = 0; r < rc; ++r, yi += 1.f, arow += CW, brow += CW) body(false, 0);
-    } else {
-      for (int r = 0; r < rc; ++r, yi += 1.f, arow += CW, brow += CW) body(true, i0 + r);
     }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);
   }
   if (k >= ND) return;
   const size_t plane = (size_t)args.NA * ND;
@@ -219,14 +249,16 @@ cudaError_t launch(const ei_plan &p, int RS, float *P, cudaStream_t st) {
   a.order = p.proj.order;
   a.win = RS == 1 ? p.proj.win1 : p.proj.winRS;
   a.N = p.N; a.NA = p.NA; a.ND = p.ND; a.S = p.S; a.RS = RS; a.RC = p.proj.RC; a.CW = p.proj.CW;
+  a.PAD = p.proj.PAD; a.Rp = p.proj.Rp;
   a.nch = RS == 1 ? p.proj.nch1 : p.proj.nchRS;
   a.P = P;
-  const size_t smem = (size_t)2 * p.proj.RC * p.proj.CW * (sizeof(typename PL<NMAP>::A) + (NMAP == 3 ? 8 : 0));
+  const size_t smem = NMAP == 3 ? (size_t)NST * p.proj.RC * (p.proj.CW * 16 + (p.proj.CW + 2) * 8)
+                                 : (size_t)NST * p.proj.RC * (p.proj.CW + 2) * 8;
   cudaError_t e = cudaFuncSetAttribute((const void *)project_kernel<NMAP>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   dim3 grid((p.ND + RT - 1) / RT, p.proj.n_groups, p.S * RS);
-  project_kernel<NMAP><<<grid, NT, smem, st>>>(a);
+  project_kernel<NMAP><<<grid, NT + 32, smem, st>>>(a);
   return cudaGetLastError();
 }
 
@@ -304,16 +336,16 @@ int plan_projector(ei_plan &p, const double *angles, std::vector<int2> &groups,
     groups.back().y += 1;
   }
   const size_t per_entry = 24;          // float4 + float2 per staged entry
-  // shared-memory budget per CTA: 72 KB keeps three CTAs per SM, 110 KB two (tuning knob)
+  // shared-memory budget per CTA (NST-stage ring): 100 KB keeps two CTAs per SM (tuning knob)
   const char *env = getenv("EI_K1_SMEM_KB");
-  const size_t budget = (env ? (size_t)atoi(env) : 72) * 1024;
+  const size_t budget = (env ? (size_t)atoi(env) : 100) * 1024;
   int RC = 32, nch = 0, CW = 0;
   for (;;) {
     build_windows(p, angles, groups, order, 1, RC, win1, nch, CW);
-    if ((size_t)2 * RC * CW * per_entry <= budget || RC == 1) break;
+    if ((size_t)NST * RC * (CW + 2) * per_entry <= budget || RC == 1) break;
     RC /= 2;
   }
-  if ((size_t)2 * RC * CW * per_entry > 200 * 1024) return EI_ERR_SHAPE;
+  if ((size_t)NST * RC * (CW + 2) * per_entry > 200 * 1024) return EI_ERR_SHAPE;
   p.proj.RC = RC;
   p.proj.n_groups = (int)groups.size();
   p.proj.nch1 = nch;
@@ -330,7 +362,10 @@ int plan_projector(ei_plan &p, const double *angles, std::vector<int2> &groups,
     winRS.clear();
     p.proj.nchRS = nch;
   }
-  p.proj.CW = std::max(CW, CWrs);
+  p.proj.CW = (std::max(CW, CWrs) + 1) & ~1;   // even (16-B aligned 8-byte-entry rows)
+  // zero padding of the pair-layout map rows so every staged window is one in-bounds copy
+  p.proj.PAD = p.proj.CW + 2;   // even
+  p.proj.Rp = (N + 1 + 2 * p.proj.PAD + 1) & ~1;   // even: 16-B aligned float2 rows
   return EI_OK;
 }
 

@@ -125,7 +125,7 @@ int ei_plan_create(const ei_geometry *geom, const double *angles, ei_plan **out)
     return rc;
   }
   const size_t S = p->S, SINO = (size_t)p->NA * p->ND;
-  const size_t NP = (size_t)p->N * (p->N + 1);
+  const size_t NP = (size_t)p->N * p->proj.Rp;
   p->RB = ei::reg_blocks(p->N);
   cudaError_t e = cudaSuccess;
   auto A = [&](cudaError_t r) { if (e == cudaSuccess) e = r; };
@@ -166,6 +166,11 @@ int ei_plan_create(const ei_geometry *geom, const double *angles, ei_plan **out)
   if (e == cudaSuccess)
     A(cudaMemcpy(p->proj.order, order.data(), sizeof(int) * order.size(), cudaMemcpyHostToDevice));
   if (e == cudaSuccess) A(cudaMemset(p->diag, 0, sizeof(int32_t)));
+  // the zero padding of the map rows is written once here; K0 only writes the interior
+  for (void *q : {(void *)p->MA, (void *)p->MAT})
+    if (e == cudaSuccess) A(cudaMemset(q, 0, sizeof(float4) * S * NP));
+  for (void *q : {(void *)p->MB, (void *)p->MBT, (void *)p->M1, (void *)p->M1T})
+    if (e == cudaSuccess) A(cudaMemset(q, 0, sizeof(float2) * S * NP));
   if (e == cudaSuccess) A(cudaMemset(p->done, 0, sizeof(unsigned int) * S));
   if (e == cudaSuccess) A(cudaMemset(p->done3, 0, sizeof(unsigned int) * S * ei::bp_tiles(p->N)));
   if (e == cudaSuccess)
@@ -200,7 +205,7 @@ int ei_plan_info(const ei_plan *p, int64_t out[6]) {
   out[2] = p->proj.CW;
   out[3] = p->proj.RS;
   out[4] = d;
-  out[5] = (int64_t)2 * p->proj.RC * p->proj.CW * 24;
+  out[5] = (int64_t)3 * p->proj.RC * (p->proj.CW * 16 + (p->proj.CW + 2) * 8);
   return EI_OK;
 }
 

@@ -67,7 +67,8 @@ struct ProjArgs {
   float *P;                     // [RS][S][NMAP][NA][ND]
 };
 
-constexpr int NST = 3;          // pipeline stages (shared-memory ring)
+constexpr int NST = 4;          // pipeline stages (shared-memory ring)
+constexpr int MAXCH = 1024;     // window-table entries cached in shared memory per CTA
 constexpr int NCW = NT / 32;    // consumer warps
 
 // Warp-specialised pipeline: warp NCW (the producer) streams each row chunk's window of pair
@@ -91,6 +92,7 @@ __global__ void __launch_bounds__(NT + 32, 2) project_kernel(ProjArgs args) {
   TA *sA = reinterpret_cast<TA *>(smem_raw);                                   // [NST][RC][CWA]
   float2 *sB = reinterpret_cast<float2 *>(sA + NST * RC * CWA);               // [NST][RC][CWB]
   __shared__ __align__(8) uint64_t full[NST], empty[NST];
+  __shared__ int2 swin[MAXCH];   // this CTA's window table (host plan), nch <= MAXCH
 
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int kt = blockIdx.x * RT;
@@ -105,6 +107,7 @@ __global__ void __launch_bounds__(NT + 32, 2) project_kernel(ProjArgs args) {
   const int nch = (r1 - r0 + RC - 1) / RC;
   const int2 *wtab = args.win + (((size_t)rs * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * args.nch;
 
+  for (int c = tid; c < nch; c += NT + 32) swin[c] = __ldg(wtab + c);
   if (tid == 0) {
     for (int q = 0; q < NST; ++q) {
       mbar_init(&full[q], 1);
@@ -116,10 +119,11 @@ __global__ void __launch_bounds__(NT + 32, 2) project_kernel(ProjArgs args) {
 
   if (w == NCW) {   // ---------------- producer warp ----------------
     if (lane == 0) {
+      int st = 0;
+      uint32_t ph = 0;
       for (int c = 0; c < nch; ++c) {
-        const int st = c % NST;
-        if (c >= NST) mbar_wait(&empty[st], ((c / NST) + 1) & 1);
-        const int2 wn = __ldg(wtab + c);
+        if (c >= NST) mbar_wait(&empty[st], ph ^ 1);
+        const int2 wn = swin[c];
         const int i0 = r0 + c * RC, rc = min(RC, r1 - i0);
         const int e0 = wn.x + 1;                       // first staged entry
         const int eb = e0 & ~1, bofs = e0 - eb;        // B plane: 16-B aligned start
@@ -134,6 +138,7 @@ __global__ void __launch_bounds__(NT + 32, 2) project_kernel(ProjArgs args) {
             if (NMAP == 3) bulk_g2s(sB + (st * RC + r) * CWB, gB + row + eb, bytesB, &full[st]);
           }
         }
+        if (++st == NST) { st = 0; ph ^= 1; }
       }
     }
     return;
@@ -179,10 +184,11 @@ __global__ void __launch_bounds__(NT + 32, 2) project_kernel(ProjArgs args) {
 #pragma unroll
   for (int m = 0; m < 4; ++m) am[m] = ad[m] = as[m] = make_float2(0.f, 0.f);
 
-  for (int c = 0; c < nch; ++c) {
-    const int st = c % NST;
-    mbar_wait(&full[st], (c / NST) & 1);
-    const int2 wn = __ldg(wtab + c);
+  int st = 0;
+  uint32_t ph = 0;
+  for (int c = 0; c < nch; ++c, st = (st + 1 == NST) ? 0 : st + 1, ph ^= (st == 0)) {
+    mbar_wait(&full[st], ph);
+    const int2 wn = swin[c];
     const int i0 = r0 + c * RC, rc = min(RC, r1 - i0), i1 = i0 + rc - 1;
     bool any = false, all = true;
 #pragma unroll
@@ -346,6 +352,7 @@ int plan_projector(ei_plan &p, const double *angles, std::vector<int2> &groups,
     RC /= 2;
   }
   if ((size_t)NST * RC * (CW + 2) * per_entry > 200 * 1024) return EI_ERR_SHAPE;
+  if (nch > MAXCH) return EI_ERR_SHAPE;
   p.proj.RC = RC;
   p.proj.n_groups = (int)groups.size();
   p.proj.nch1 = nch;

@@ -52,11 +52,13 @@ struct ei_plan {
   float2 *M1 = nullptr, *M1T = nullptr;   // [S][N][Rp] single map (ei_project n_maps=1)
   float *P = nullptr;         // [RS][S][3][NA][ND] (partial) projections
   int32_t *diag = nullptr;    // device counter of internal window overflows (must stay 0)
-  // gradient sinograms in the PAIR layout read by K3: row length ND+1, entry e holds
-  // (g[e-1], g[e]) (zero outside [0, ND)):  GA = (mu0, mu1, delta0, delta1), GB = (sigma0, sigma1)
-  float4 *GA = nullptr;       // [S][NA][ND+1]
-  float2 *GB = nullptr;       // [S][NA][ND+1]
-  float2 *GA1 = nullptr;      // [S][NA][ND+1]  single-map pairs (ei_backproject n_maps=1)
+  // gradient sinograms in the PAIR layout read by K3: entry e = (g[e-1], g[e]), e = 0..ND
+  // (zero outside the detector), stored at e + PADG in rows of RpG entries (zero padding both
+  // sides, written once at plan creation): GA = (mu0, mu1, delta0, delta1), GB = (sigma0, sigma1)
+  float4 *GA = nullptr;       // [S][NA][RpG]
+  float2 *GB = nullptr;       // [S][NA][RpG]
+  float2 *GA1 = nullptr;      // [S][NA][RpG]  single-map pairs (ei_backproject n_maps=1)
+  int PADG = 0, RpG = 0;
   double *part_curve = nullptr;  // [S][NA] per-row cost partials (K2)
   double *part_reg = nullptr;    // [S][RB] per-tile sum x^2 partials (K0)
   unsigned int *done = nullptr;  // [S] K2 arrival counters (fused finalize), kept at 0 between calls
@@ -105,5 +107,6 @@ cudaError_t launch_backproject3(const ei_plan &p, const float *mu, const float *
                                 float *g_sigma, size_t out_stride, cudaStream_t st);
 cudaError_t launch_backproject1(const ei_plan &p, float *map, cudaStream_t st);
 int bp_tiles(int N);
+int bp_pad();
 int bp_chunks(int NA);
 }  // namespace ei

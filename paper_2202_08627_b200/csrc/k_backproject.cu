@@ -8,16 +8,18 @@
 //  * gradient sinograms arrive in a PAIR layout written by K2: entry e of a row holds
 //    (g[e-1], g[e]) for every map, so one tap pair of all three maps is one LDS.128 + one LDS.64
 //    (A = (mu0, mu1, delta0, delta1), B = (sigma0, sigma1)); row length Nd+1 (e = 0..Nd).
-//  * a CTA owns a 32x32 pixel tile (256 threads x 4 pixels) and walks the angles in chunks of
-//    32; for each angle it stages only the 48-entry detector window the tile projects onto
-//    (cp.async, double-buffered, zero-filled outside the detector), so the whole gather runs
-//    from shared memory;
+//  * a CTA owns a 32x32 pixel tile (256 consumer threads x 4 pixels) and walks the angles in
+//    chunks of 16; a producer warp stages, per angle, only the 48-entry detector window the tile
+//    projects onto, with 1-D bulk copies (TMA engine) into a 3-stage shared-memory ring that
+//    completes on full/empty mbarriers (G rows are zero-padded, so every window is one
+//    in-bounds copy); consumer warps never meet a CTA-wide barrier in the loop;
 //  * a warp covers an 8x4 pixel sub-tile, whose taps fall on ~10 consecutive window entries:
 //    lanes share (broadcast) most loads, ~3 shared-memory wavefronts per 32 pixel-angles;
 //  * the pair products accumulate with FFMA2 (__ffma2_rn: two fp32 FMAs per instruction on
 //    sm_100a): acc.x collects the left taps, acc.y the right taps, summed once at the end.
 // Nothing is scattered: deterministic.  The cost path adds 2*lambda*x (eq. 5).
 #include "ei_common.cuh"
+#include "tma.cuh"
 
 namespace ei {
 namespace {
@@ -25,7 +27,9 @@ namespace {
 constexpr int TILE = 32;   // pixels per side
 constexpr int CH = 16;     // angles per staged chunk
 constexpr int WL = 48;     // window entries per angle (>= 31*sqrt(2) + 4)
-constexpr int NT = 256;
+constexpr int NT = 256;     // consumer threads (+ one producer warp)
+constexpr int NST = 3;      // ring stages
+constexpr int WLB = WL + 2; // 8-byte-entry rows: 16-B aligned copy start needs one spare entry
 
 __device__ __forceinline__ void cp_async(void *smem, const void *gmem, int bytes, bool valid) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -55,98 +59,104 @@ struct Layout<1> {   // A = (g0, g1)
 // quarter/half warp on distinct banks; an interleaved 32-B entry stride measured 1.5x slower)
 template <int NMAP>
 struct Smem {
-  typename Layout<NMAP>::A a[2][CH][WL];
-  float2 b[2][CH][Layout<NMAP>::hasB ? WL : 1];
-  float4 tab[2][CH];
-  int ws[2][CH];
+  typename Layout<NMAP>::A a[NST][CH][sizeof(typename Layout<NMAP>::A) == 8 ? WLB : WL];
+  float2 b[NST][CH][Layout<NMAP>::hasB ? WLB : 2];
+  float4 tab[NST][CH];
+  int ws[NST][CH];
+  uint64_t full[NST], empty[NST];
 };
 
 template <int NMAP>
-__global__ void __launch_bounds__(NT, 3) backproject_kernel(
+__global__ void __launch_bounds__(NT + 32, 3) backproject_kernel(
     const typename Layout<NMAP>::A *__restrict__ GA, const float2 *__restrict__ GB,
     const float4 *__restrict__ k3, int N, int NA, int ND, const float *__restrict__ mu,
     const float *__restrict__ delta, const float *__restrict__ sigma, float lambda,
     float *__restrict__ o0, float *__restrict__ o1, float *__restrict__ o2, size_t out_stride,
-    int S, int KS, float *__restrict__ part3, unsigned int *__restrict__ done3) {
+    int S, int KS, float *__restrict__ part3, unsigned int *__restrict__ done3, int PADG, int RpG) {
   using TA = typename Layout<NMAP>::A;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
+  constexpr bool A8 = sizeof(TA) == 8;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
   Smem<NMAP> &sm = *reinterpret_cast<Smem<NMAP> *>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int s = blockIdx.z % S, ks = blockIdx.z / S;
   const int j0 = blockIdx.x * TILE, i0 = blockIdx.y * TILE;
-  const int row = 4 * w + (lane >> 3), lx = lane & 7;
   const float ctr = 0.5f * (float)(N - 1), dctr = 0.5f * (float)(ND - 1);
-  const float yi = (float)(i0 + row) - ctr;
-  float xq[4];
-#pragma unroll
-  for (int q = 0; q < 4; ++q) xq[q] = (float)(j0 + lx + 8 * q) - ctr;
-  // tile corners (full 32x32 tile, even past the map edge, so every lane indexes the window)
-  const float xa = (float)j0 - ctr, xb = xa + (float)(TILE - 1);
-  const float ya = (float)i0 - ctr, yb = ya + (float)(TILE - 1);
-  const size_t rowlen = (size_t)ND + 1;
-  const TA *GAs = GA + (size_t)s * NA * rowlen;
-  const float2 *GBs = GB ? GB + (size_t)s * NA * rowlen : nullptr;
+  const size_t rowlen = (size_t)RpG;   // padded G rows: entry e at e + PADG
+  const TA *GAs = GA + (size_t)s * NA * rowlen + PADG;
+  const float2 *GBs = GB ? GB + (size_t)s * NA * rowlen + PADG : nullptr;
   // angle split (small grids): CTA ks owns chunks [c_lo, c_hi)
   const int nch_all = (NA + CH - 1) / CH;
   const int c_lo = (int)(((long long)ks * nch_all) / KS), c_hi = (int)(((long long)(ks + 1) * nch_all) / KS);
 
-  auto prep = [&](int c, int buf) {   // per-angle table + window start, threads < CH
-    if (tid < CH) {
-      const int a = c * CH + tid;
-      float4 t = make_float4(0.f, 0.f, 0.f, 0.f);
+  if (tid == 0) {
+    for (int q = 0; q < NST; ++q) {
+      mbar_init(&sm.full[q], 1);
+      mbar_init(&sm.empty[q], NT / 32);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+
+  if (w == NT / 32) {   // ---------------- producer warp ----------------
+    // tile corners (full 32x32 tile, even past the map edge, so every lane indexes the window)
+    const float xa = (float)j0 - ctr, xb = xa + (float)(TILE - 1);
+    const float ya = (float)i0 - ctr, yb = ya + (float)(TILE - 1);
+    const uint32_t bytesA = A8 ? (uint32_t)WLB * 8 : (uint32_t)WL * 16;
+    const uint32_t bytesB = NMAP == 3 ? (uint32_t)WLB * 8 : 0u;
+    int st = 0;
+    uint32_t ph = 0;
+    for (int c = c_lo; c < c_hi; ++c) {
+      if (c - c_lo >= NST) mbar_wait(&sm.empty[st], ph ^ 1);
+      const int na = min(CH, NA - c * CH);
       int ws = 0;
-      if (a < NA) {
+      if (lane < na) {   // per-angle table + window start (first tap entry - 1)
+        const int a = c * CH + lane;
         const float4 g = __ldg(k3 + a);   // cdu, sdu, inv_h, scale
         const float k00 = fmaf(xa, g.x, fmaf(ya, g.y, dctr)), k01 = fmaf(xb, g.x, fmaf(ya, g.y, dctr));
         const float k10 = fmaf(xa, g.x, fmaf(yb, g.y, dctr)), k11 = fmaf(xb, g.x, fmaf(yb, g.y, dctr));
-        const float kmin = fminf(fminf(k00, k01), fminf(k10, k11));
-        ws = (int)floorf(kmin) - 1;
-        t = make_float4(g.x, g.y, g.z, 1.f - g.z);   // cdu, sdu, 1/h, 1 - 1/h
+        ws = (int)floorf(fminf(fminf(k00, k01), fminf(k10, k11))) - 1;
+        sm.tab[st][lane] = make_float4(g.x, g.y, g.z, 1.f - g.z);   // cdu, sdu, 1/h, 1 - 1/h
+        sm.ws[st][lane] = ws;
       }
-      sm.tab[buf][tid] = t;
-      sm.ws[buf][tid] = ws;
+      __syncwarp();
+      if (lane == 0) mbar_arrive_expect_tx(&sm.full[st], (uint32_t)na * (bytesA + bytesB));
+      __syncwarp();
+      if (lane < na) {
+        const size_t row = (size_t)(c * CH + lane) * rowlen;
+        // a window entirely off the detector only needs zeros: clamp its copy into the zero pad
+        // (a window overlapping [0, ND] is always inside the PADG >= WL padding)
+        const int e0 = min(max(ws + 1, -PADG), ND + PADG - WLB), eb = e0 & ~1;
+        bulk_g2s(&sm.a[st][lane][0], GAs + row + (A8 ? eb : e0), bytesA, &sm.full[st]);
+        if (NMAP == 3) bulk_g2s(&sm.b[st][lane][0], GBs + row + eb, bytesB, &sm.full[st]);
+      }
+      if (++st == NST) { st = 0; ph ^= 1; }
     }
-  };
-  auto stage = [&](int c, int buf) {   // window entries -> shared (zero outside [0, ND])
-    const int na = min(CH, NA - c * CH);
-    for (int e = tid; e < na * WL; e += NT) {
-      const int al = e / WL, r = e - al * WL;
-      const int a = c * CH + al;
-      const int ent = sm.ws[buf][al] + 1 + r;   // entry index = k + 1
-      const bool ok = (ent >= 0) && (ent <= ND);
-      const size_t off = (size_t)a * rowlen + (ok ? ent : 0);
-      cp_async(&sm.a[buf][al][r], GAs + off, (int)sizeof(TA), ok);
-      if constexpr (NMAP == 3) cp_async(&sm.b[buf][al][r], GBs + off, 8, ok);
-    }
-    cp_commit();
-  };
+    return;
+  }
+
+  // ---------------- consumer warps ----------------
+  const int row = 4 * w + (lane >> 3), lx = lane & 7;
+  const float yi = (float)(i0 + row) - ctr;
+  float xq[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) xq[q] = (float)(j0 + lx + 8 * q) - ctr;
 
   float2 am[4], ad[4], as[4];
 #pragma unroll
   for (int q = 0; q < 4; ++q) am[q] = ad[q] = as[q] = make_float2(0.f, 0.f);
 
-  if (c_lo < c_hi) {
-    prep(c_lo, 0);
-    __syncthreads();
-    stage(c_lo, 0);
-  }
+  int st = 0;
+  uint32_t ph = 0;
   for (int c = c_lo; c < c_hi; ++c) {
-    const int b = (c - c_lo) & 1;
-    if (c + 1 < c_hi) prep(c + 1, b ^ 1);
-    __syncthreads();
-    if (c + 1 < c_hi) {
-      stage(c + 1, b ^ 1);
-      cp_wait<1>();
-    } else {
-      cp_wait<0>();
-    }
-    __syncthreads();
+    mbar_wait(&sm.full[st], ph);
     const int na = min(CH, NA - c * CH);
     for (int al = 0; al < na; ++al) {
-      const float4 t = sm.tab[b][al];
-      const float base = fmaf(yi, t.y, dctr - (float)sm.ws[b][al]);
-      const TA *arow = sm.a[b][al];
-      const float2 *brow = sm.b[b][Layout<NMAP>::hasB ? al : 0];
+      const float4 t = sm.tab[st][al];
+      const int ws = sm.ws[st][al];
+      const int bofs = (ws + 1) & 1;
+      const float base = fmaf(yi, t.y, dctr - (float)ws);
+      const TA *arow = &sm.a[st][al][A8 ? bofs : 0];
+      const float2 *brow = &sm.b[st][Layout<NMAP>::hasB ? al : 0][bofs];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const float kst = fmaf(xq[q], t.x, base);   // window-local k*, > 0
@@ -165,7 +175,9 @@ __global__ void __launch_bounds__(NT, 3) backproject_kernel(
         }
       }
     }
-    __syncthreads();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&sm.empty[st]);
+    if (++st == NST) { st = 0; ph ^= 1; }
   }
 
   const int i = i0 + row;
@@ -186,13 +198,13 @@ __global__ void __launch_bounds__(NT, 3) backproject_kernel(
     }
     __shared__ bool last;
     __threadfence();
-    __syncthreads();
+    asm volatile("bar.sync 1, %0;\n" ::"n"(NT) : "memory");   // consumers only
     if (tid == 0) {
       unsigned int *cnt = done3 + (size_t)s * gridDim.x * gridDim.y + blockIdx.y * gridDim.x + blockIdx.x;
       last = atomicAdd(cnt, 1u) == (unsigned)(KS - 1);
       if (last) *cnt = 0u;   // re-arm
     }
-    __syncthreads();
+    asm volatile("bar.sync 1, %0;\n" ::"n"(NT) : "memory");
     if (!last) return;
     __threadfence();
     if (i >= N) return;
@@ -246,14 +258,15 @@ cudaError_t launch_bp(const ei_plan &p, const typename Layout<NMAP>::A *GA, cons
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   dim3 grid((p.N + TILE - 1) / TILE, (p.N + TILE - 1) / TILE, p.S * p.KS);
-  backproject_kernel<NMAP><<<grid, NT, smem, st>>>(GA, GB, p.tab.k3, p.N, p.NA, p.ND, mu, delta,
-                                                   sigma, lambda, o0, o1, o2, out_stride, p.S, p.KS,
-                                                   p.part3, p.done3);
+  backproject_kernel<NMAP><<<grid, NT + 32, smem, st>>>(GA, GB, p.tab.k3, p.N, p.NA, p.ND, mu, delta,
+                                                        sigma, lambda, o0, o1, o2, out_stride, p.S,
+                                                        p.KS, p.part3, p.done3, p.PADG, p.RpG);
   return cudaGetLastError();
 }
 
 }  // namespace
 
+int bp_pad() { return 64; }   // G row padding (entries) >= window width WL + slack, even
 int bp_tiles(int N) { return ((N + TILE - 1) / TILE) * ((N + TILE - 1) / TILE); }
 int bp_chunks(int NA) { return (NA + CH - 1) / CH; }
 

@@ -42,7 +42,7 @@ __global__ void __launch_bounds__(K2_THREADS) curve_kernel(
     float z, float inv_du, float *__restrict__ s_mod, float4 *__restrict__ GA,
     float2 *__restrict__ GB, double *__restrict__ part, int32_t *__restrict__ status,
     unsigned int *__restrict__ done, const double *__restrict__ part_reg, int RB, float lambda,
-    double *__restrict__ cost_out, const float4 *__restrict__ k3) {
+    double *__restrict__ cost_out, const float4 *__restrict__ k3, int PADG, int RpG) {
   extern __shared__ float sm[];
   float *pd = sm;              // [ND] P_delta row
   float *gD = sm + ND;         // [ND] g_Delta row
@@ -141,9 +141,8 @@ __global__ void __launch_bounds__(K2_THREADS) curve_kernel(
   // value pre-multiplied by the Joseph weight dx/|c_dom| of this angle (K3 then only applies the
   // unit tent)
   const float sc = __ldg(k3 + a).w;
-  const size_t rl = (size_t)ND + 1;
-  float4 *Arow = GA + ((size_t)s * NA + a) * rl;
-  float2 *Brow = GB + ((size_t)s * NA + a) * rl;
+  float4 *Arow = GA + ((size_t)s * NA + a) * (size_t)RpG + PADG;
+  float2 *Brow = GB + ((size_t)s * NA + a) * (size_t)RpG + PADG;
   for (int e = threadIdx.x; e <= ND; e += blockDim.x) {
     const bool l = e >= 1, r = e < ND;
     Arow[e] = make_float4(l ? sc * gmS[e - 1] : 0.f, r ? sc * gmS[e] : 0.f, l ? sc * pd[e - 1] : 0.f,
@@ -194,7 +193,7 @@ cudaError_t launch_curve_forward(const ei_plan &p, const float *flat, const floa
   curve_kernel<0><<<grid, K2_THREADS, smem, st>>>(p.P, p.proj.RS, p.S, flat, mask, drift, nullptr, p.NA, p.ND, p.M,
                                                   (float)p.g.z, (float)(1.0 / p.g.det_pitch), s_mod,
                                                   nullptr, nullptr, nullptr, nullptr, nullptr,
-                                                  nullptr, 0, 0.f, nullptr, nullptr);
+                                                  nullptr, 0, 0.f, nullptr, nullptr, 0, 0);
   return cudaGetLastError();
 }
 
@@ -208,7 +207,8 @@ cudaError_t launch_curve_cost_grad(const ei_plan &p, const float *flat, const fl
   curve_kernel<1><<<grid, K2_THREADS, smem, st>>>(p.P, p.proj.RS, p.S, flat, mask, drift, s_exp, p.NA, p.ND, p.M,
                                                   (float)p.g.z, (float)(1.0 / p.g.det_pitch), nullptr,
                                                   p.GA, p.GB, p.part_curve, status, p.done,
-                                                  p.part_reg, p.RB, lambda, cost, p.tab.k3);
+                                                  p.part_reg, p.RB, lambda, cost, p.tab.k3,
+                                                  p.PADG, p.RpG);
   return cudaGetLastError();
 }
 

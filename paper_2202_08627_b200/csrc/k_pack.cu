@@ -118,22 +118,24 @@ __global__ void __launch_bounds__(256) pack_pairs_kernel(const float *__restrict
 template <int NMAP>
 __global__ void pack_sino_kernel(const float *__restrict__ in, int NA, int ND, int S,
                                  float4 *__restrict__ GA, float2 *__restrict__ GB,
-                                 float2 *__restrict__ GA1, const float4 *__restrict__ k3) {
+                                 float2 *__restrict__ GA1, const float4 *__restrict__ k3, int PADG,
+                                 int RpG) {
   const size_t plane = (size_t)NA * ND, rl = (size_t)ND + 1;
   const size_t total = (size_t)S * NA * rl;
   for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < total;
        t += (size_t)gridDim.x * blockDim.x) {
     const size_t sa = t / rl;
     const int e = (int)(t - sa * rl);
+    const size_t o = sa * (size_t)RpG + PADG + e;
     const size_t s = sa / NA, a = sa - s * NA;
     const float *b = in + s * NMAP * plane + a * ND;
     const float sc = __ldg(k3 + a).w;
     auto at = [&](int m, int k) { return (k >= 0 && k < ND) ? sc * __ldg(b + m * plane + k) : 0.f; };
     if (NMAP == 3) {
-      GA[t] = make_float4(at(0, e - 1), at(0, e), at(1, e - 1), at(1, e));
-      GB[t] = make_float2(at(2, e - 1), at(2, e));
+      GA[o] = make_float4(at(0, e - 1), at(0, e), at(1, e - 1), at(1, e));
+      GB[o] = make_float2(at(2, e - 1), at(2, e));
     } else {
-      GA1[t] = make_float2(at(0, e - 1), at(0, e));
+      GA1[o] = make_float2(at(0, e - 1), at(0, e));
     }
   }
 }
@@ -169,9 +171,11 @@ cudaError_t launch_pack_sino(const ei_plan &p, const float *sino, int n_maps, cu
   const size_t total = (size_t)p.S * p.NA * (p.ND + 1);
   const int blocks = (int)((total + 255) / 256 < 148 * 16 ? (total + 255) / 256 : 148 * 16);
   if (n_maps == 3)
-    pack_sino_kernel<3><<<blocks, 256, 0, st>>>(sino, p.NA, p.ND, p.S, p.GA, p.GB, nullptr, p.tab.k3);
+    pack_sino_kernel<3><<<blocks, 256, 0, st>>>(sino, p.NA, p.ND, p.S, p.GA, p.GB, nullptr, p.tab.k3,
+                                                p.PADG, p.RpG);
   else
-    pack_sino_kernel<1><<<blocks, 256, 0, st>>>(sino, p.NA, p.ND, p.S, nullptr, nullptr, p.GA1, p.tab.k3);
+    pack_sino_kernel<1><<<blocks, 256, 0, st>>>(sino, p.NA, p.ND, p.S, nullptr, nullptr, p.GA1, p.tab.k3,
+                                                p.PADG, p.RpG);
   return cudaGetLastError();
 }
 

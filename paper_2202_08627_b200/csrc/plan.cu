@@ -5,6 +5,7 @@
 #include <stdio.h>
 #include <string.h>
 
+#include <algorithm>
 #include <new>
 #include <vector>
 
@@ -142,18 +143,28 @@ int ei_plan_create(const ei_geometry *geom, const double *angles, ei_plan **out)
   A(dalloc(&p->M1, S * NP));
   A(dalloc(&p->M1T, S * NP));
   A(dalloc(&p->diag, 1));
-  const size_t SINO1 = (size_t)p->NA * (p->ND + 1);
+  p->PADG = ei::bp_pad();
+  p->RpG = (p->ND + 1 + 2 * p->PADG + 1) & ~1;
+  const size_t SINO1 = (size_t)p->NA * p->RpG;
   A(dalloc(&p->P, (size_t)p->proj.RS * S * 3 * SINO));
   A(dalloc(&p->GA, S * SINO1));
   A(dalloc(&p->GB, S * SINO1));
   A(dalloc(&p->GA1, S * SINO1));
   A(dalloc(&p->part_curve, S * NA));
   A(dalloc(&p->part_reg, S * p->RB));
-  // K3 angle split for grids with fewer than ~2 CTAs per SM (partials reduced by the last CTA)
+  // K3 angle split for small grids: pick KS (<= 16, <= chunks/2) with the best wave
+  // quantisation over the 3 CTAs/SM x 148 SMs slots (ties -> more CTAs, i.e. better latency hiding)
   {
-    const long long ctas = (long long)ei::bp_tiles(p->N) * p->S;
+    const long long ctas = (long long)ei::bp_tiles(p->N) * p->S, slots = 3 * 148;
     int KS = 1;
-    while (KS < 16 && ctas * KS < 3 * 148 && 2 * KS <= ei::bp_chunks(p->NA)) KS *= 2;
+    double best = 0.0;
+    if (ctas < 2 * slots) {
+      for (int ks = 1; ks <= 16 && ks <= std::max(1, ei::bp_chunks(p->NA) / 2); ++ks) {
+        const long long n = ctas * ks, waves = (n + slots - 1) / slots;
+        const double eff = (double)n / (double)(waves * slots);
+        if (eff >= best - 1e-9) { best = eff; KS = ks; }
+      }
+    }
     p->KS = KS;
   }
   A(dalloc(&p->done, S));
@@ -172,6 +183,9 @@ int ei_plan_create(const ei_geometry *geom, const double *angles, ei_plan **out)
   for (void *q : {(void *)p->MB, (void *)p->MBT, (void *)p->M1, (void *)p->M1T})
     if (e == cudaSuccess) A(cudaMemset(q, 0, sizeof(float2) * S * NP));
   if (e == cudaSuccess) A(cudaMemset(p->done, 0, sizeof(unsigned int) * S));
+  if (e == cudaSuccess) A(cudaMemset(p->GA, 0, sizeof(float4) * S * SINO1));   // zero padding
+  if (e == cudaSuccess) A(cudaMemset(p->GB, 0, sizeof(float2) * S * SINO1));
+  if (e == cudaSuccess) A(cudaMemset(p->GA1, 0, sizeof(float2) * S * SINO1));
   if (e == cudaSuccess) A(cudaMemset(p->done3, 0, sizeof(unsigned int) * S * ei::bp_tiles(p->N)));
   if (e == cudaSuccess)
     A(cudaMemcpy(p->proj.win1, win1.data(), sizeof(int2) * win1.size(), cudaMemcpyHostToDevice));

@@ -21,6 +21,15 @@ namespace {
 
 constexpr int K2_THREADS = 256;
 
+// 2^x on the SFU (MUFU.EX2, ~2 ulp): every exponential of the curve model is written as a power
+// of two with the log2(e) factor folded into a per-(theta, t) constant
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+constexpr float LOG2E = 1.4426950408889634f;
+
 __device__ __forceinline__ double block_sum(double v, double *red) {
   for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -44,11 +53,10 @@ __global__ void __launch_bounds__(K2_THREADS) curve_kernel(
     unsigned int *__restrict__ done, const double *__restrict__ part_reg, int RB, float lambda,
     double *__restrict__ cost_out, const float4 *__restrict__ k3, int PADG, int RpG) {
   extern __shared__ float sm[];
-  float *pd = sm;              // [ND] P_delta row
-  float *gD = sm + ND;         // [ND] g_Delta row
-  float *gmS = sm + 2 * ND;    // [ND] g_mu row
-  float *gsS = sm + 3 * ND;    // [ND] g_sigma row
-  float *smask = sm + 4 * ND;  // [M]
+  float *gD = sm;              // [ND] g_Delta row
+  float *gmS = sm + ND;        // [ND] g_mu row
+  float *gsS = sm + 2 * ND;    // [ND] g_sigma row
+  float *smask = sm + 3 * ND;  // [M]
   __shared__ double red[K2_THREADS / 32];
   const int a = blockIdx.x, s = blockIdx.y;
   const size_t plane = (size_t)NA * ND;
@@ -62,7 +70,6 @@ __global__ void __launch_bounds__(K2_THREADS) curve_kernel(
     return v;
   };
   const float *fA = flat + (size_t)s * 3 * ND, *fc = fA + ND, *fw = fA + 2 * ND;
-  for (int k = threadIdx.x; k < ND; k += blockDim.x) pd[k] = psum(Pd, k);
   for (int m = threadIdx.x; m < M; m += blockDim.x) smask[m] = __ldg(mask + m);
   __syncthreads();
   const float mo = drift ? __ldg(drift + a) : 0.f;
@@ -70,21 +77,22 @@ __global__ void __launch_bounds__(K2_THREADS) curve_kernel(
   float cost = 0.f;
   int bad = 0, mu_cl = 0, w2_cl = 0;
   for (int k = threadIdx.x; k < ND; k += blockDim.x) {
-    const float dP = (k == 0) ? (pd[1] - pd[0]) * inv_du
-                   : (k == ND - 1) ? (pd[ND - 1] - pd[ND - 2]) * inv_du
-                                   : (pd[k + 1] - pd[k - 1]) * (0.5f * inv_du);
+    // D P_delta from the neighbouring projections (global, L1-cached; no shared-memory phase)
+    const int kl = k == 0 ? 0 : k - 1, kr = k == ND - 1 ? ND - 1 : k + 1;
+    const float dP = (psum(Pd, kr) - psum(Pd, kl)) * ((kr - kl == 2 ? 0.5f : 1.f) * inv_du);
     const float shift = z * dP;
     float pmu = psum(Pm, k);
     const bool mc = (pmu > 50.f) || (pmu < -50.f);
     pmu = fminf(fmaxf(pmu, -50.f), 50.f);
-    const float T = expf(-pmu);
+    const float T = ex2(-LOG2E * pmu);
     const float A = __ldg(fA + k), c = __ldg(fc + k), w = __ldg(fw + k);
     float W2 = fmaf(w, w, psum(Ps, k));
     const float W2min = 0.01f * w * w;
     const bool wc = W2 < W2min;
     W2 = wc ? W2min : W2;
-    const float invW2 = 1.0f / W2;
-    const float amp = T * A * w * sqrtf(invW2);
+    const float invW2 = __frcp_rn(W2);
+    const float amp = T * A * w * rsqrtf(W2);
+    const float c2 = -0.5f * LOG2E * invW2;   // exp(-u^2 / 2W^2) = 2^(c2 u^2)
     const float base = c + mo + shift;
     mu_cl += mc;
     w2_cl += wc;
@@ -101,7 +109,7 @@ __global__ void __launch_bounds__(K2_THREADS) curve_kernel(
         const int m = m0 + u;
         if (m >= M) break;
         const float du_ = smask[m] - base;
-        const float sv = amp * expf(-0.5f * du_ * du_ * invW2);
+        const float sv = amp * ex2(c2 * du_ * du_);
         if (MODE == 0) {
           s_mod[row + (size_t)m * ND + k] = sv;
         } else {
@@ -126,7 +134,7 @@ __global__ void __launch_bounds__(K2_THREADS) curve_kernel(
   // g_delta = z * D^T g_Delta, D^T written out from the rows of D (a2):
   //   y[j] = [j==0](-g0) + [j==1](g0) + [j==ND-2](-g_{ND-1}) + [j==ND-1](g_{ND-1})
   //        + 1/2 g_{j-1} [1 <= j-1 <= ND-2] - 1/2 g_{j+1} [1 <= j+1 <= ND-2]      (all / du)
-  for (int j = threadIdx.x; j < ND; j += blockDim.x) {
+  auto gdelta = [&](int j) {
     float y = 0.f;
     if (j == 0) y -= gD[0];
     if (j == 1) y += gD[0];
@@ -134,9 +142,8 @@ __global__ void __launch_bounds__(K2_THREADS) curve_kernel(
     if (j == ND - 1) y += gD[ND - 1];
     if (j - 1 >= 1 && j - 1 <= ND - 2) y += 0.5f * gD[j - 1];
     if (j + 1 >= 1 && j + 1 <= ND - 2) y -= 0.5f * gD[j + 1];
-    pd[j] = z * inv_du * y;   // g_delta row (P_delta row no longer needed)
-  }
-  __syncthreads();
+    return z * inv_du * y;
+  };
   // pair layout for K3: entry e = (g[e-1], g[e]), e = 0..ND, zero outside the detector, each
   // value pre-multiplied by the Joseph weight dx/|c_dom| of this angle (K3 then only applies the
   // unit tent)
@@ -145,8 +152,8 @@ __global__ void __launch_bounds__(K2_THREADS) curve_kernel(
   float2 *Brow = GB + ((size_t)s * NA + a) * (size_t)RpG + PADG;
   for (int e = threadIdx.x; e <= ND; e += blockDim.x) {
     const bool l = e >= 1, r = e < ND;
-    Arow[e] = make_float4(l ? sc * gmS[e - 1] : 0.f, r ? sc * gmS[e] : 0.f, l ? sc * pd[e - 1] : 0.f,
-                          r ? sc * pd[e] : 0.f);
+    Arow[e] = make_float4(l ? sc * gmS[e - 1] : 0.f, r ? sc * gmS[e] : 0.f,
+                          l ? sc * gdelta(e - 1) : 0.f, r ? sc * gdelta(e) : 0.f);
     Brow[e] = make_float2(l ? sc * gsS[e - 1] : 0.f, r ? sc * gsS[e] : 0.f);
   }
   const double tot = block_sum((double)cost, red);
@@ -176,7 +183,7 @@ __global__ void __launch_bounds__(K2_THREADS) curve_kernel(
 
 }  // namespace
 
-static size_t k2_smem(const ei_plan &p) { return sizeof(float) * (4 * (size_t)p.ND + p.M); }
+static size_t k2_smem(const ei_plan &p) { return sizeof(float) * (3 * (size_t)p.ND + p.M); }
 
 static cudaError_t k2_attr(const void *fn, size_t smem) {
   if (smem > 48 * 1024)

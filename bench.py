@@ -133,7 +133,7 @@ class ClockSampler:
 # ---------------------------------------------------------------------------------------
 # GPU arm
 # ---------------------------------------------------------------------------------------
-def make_gpu_case(cfg, ei, torch):
+def make_gpu_case(cfg, ei, torch, noise=True):
     """Synthetic inputs per the recipe (synth); the two model-dependent steps (R16 scaling,
     R20 noise-free curves) use the product path itself."""
     one = ei.Plan(1, cfg.N, cfg.n_angles, cfg.n_det, cfg.M, cfg.pixel, cfg.det_pitch, cfg.z, cfg.angles)
@@ -166,7 +166,7 @@ def make_gpu_case(cfg, ei, torch):
         plan.destroy()
         return out.cpu().numpy()
 
-    case = synth.make_case(cfg, max_shift, max_proj, model)
+    case = synth.make_case(cfg, max_shift, max_proj, model, noise=noise)
     one.destroy()
     return case
 

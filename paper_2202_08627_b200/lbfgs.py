@@ -1,0 +1,165 @@
+"""Host L-BFGS loop driving `ei_cost_grad` (the paper minimises eq. 5 with
+SciPy's L-BFGS, slice by slice).  Not the hot path: every cost and
+gradient comes from one `ei_cost_grad` call; this module only does the optimizer's vector
+arithmetic (torch ops on the device) and bookkeeping.
+
+Design (stated here because the paper gives no optimizer parameters):
+  * slices are independent problems: each slice keeps its own history, step length and
+    convergence flag, but all slices are evaluated together in one batched call;
+  * two-loop recursion (history m = 10) with a block-diagonal initial matrix: one scalar
+    gamma per (slice, map) from the newest pair, gamma = <s_q, y_q> / <y_q, y_q>, because mu, delta
+    and sigma differ by orders of magnitude and one scalar would precondition two of them badly;
+  * batched backtracking Armijo line search (c1 = 1e-4, halving, <= 30 trials); a pair is
+    stored only if <s, y> > 1e-12 |s| |y| (curvature), otherwise the history of that slice resets;
+  * stop a slice when its relative cost decrease over an accepted step is below rel_tol, or when
+    max_iter iterations are done.
+Dot products are accumulated in fp64.
+"""
+from __future__ import annotations
+
+import dataclasses
+import time
+from typing import Callable, List, Optional, Tuple
+
+import torch
+
+
+@dataclasses.dataclass
+class Result:
+    x: torch.Tensor                 # [B, S, ...] final iterate (B = blocks, e.g. the 3 maps)
+    cost: torch.Tensor              # [S] fp64 final cost
+    history: List[torch.Tensor]     # per accepted iteration: [S] fp64 cost
+    n_iter: int
+    n_evals: int
+    converged: torch.Tensor         # [S] bool
+    seconds: float
+
+
+def _bdot(a: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
+    """Per-(block, slice) dot products in fp64: [B, S]."""
+    B, S = a.shape[:2]
+    return (a.reshape(B, S, -1).double() * b.reshape(B, S, -1).double()).sum(-1)
+
+
+def _sdot(a: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
+    """Per-slice dot products over all blocks: [S]."""
+    return _bdot(a, b).sum(0)
+
+
+def _bc(v: torch.Tensor, like: torch.Tensor) -> torch.Tensor:
+    """Broadcast a [S] or [B, S] tensor against [B, S, ...]."""
+    if v.dtype != torch.bool:
+        v = v.to(like.dtype)
+    if v.dim() == 1:
+        v = v.unsqueeze(0)
+    return v.reshape(v.shape + (1,) * (like.dim() - 2))
+
+
+def minimize(fg: Callable[[torch.Tensor], Tuple[torch.Tensor, torch.Tensor]], x0: torch.Tensor,
+             max_iter: int = 200, m: int = 10, rel_tol: float = 1e-9, c1: float = 1e-4,
+             max_ls: int = 30, callback: Optional[Callable[[int, torch.Tensor], None]] = None) -> Result:
+    """Minimise S independent problems.  x0: [B, S, ...]; fg(x) -> (cost [S] fp64, grad like x)."""
+    t0 = time.time()
+    x = x0.clone()
+    f, g = fg(x)
+    f, g = f.double().clone(), g.clone()
+    n_evals = 1
+    S = x.shape[1]
+    dev = x.device
+    hist_s: List[torch.Tensor] = []
+    hist_y: List[torch.Tensor] = []
+    hist_ok: List[torch.Tensor] = []          # [S] bool: pair valid for that slice
+    B = x.shape[0]
+    gamma = torch.zeros(B, S, dtype=torch.float64, device=dev)   # block-diagonal initial scaling
+    has_gamma = torch.zeros(S, dtype=torch.bool, device=dev)
+    conv = torch.zeros(S, dtype=torch.bool, device=dev)
+    sd = torch.ones(S, dtype=torch.bool, device=dev)   # current direction is steepest descent
+    history = [f.clone()]
+    it = 0
+    for it in range(1, max_iter + 1):
+        # ---- two-loop recursion: p = -H g (per slice, masked histories) ----
+        q = g.clone()
+        alphas = []
+        for s_k, y_k, ok in zip(reversed(hist_s), reversed(hist_y), reversed(hist_ok)):
+            rho = torch.where(ok, 1.0 / _sdot(y_k, s_k).clamp_min(1e-300), torch.zeros_like(f))
+            a = rho * _sdot(s_k, q)
+            alphas.append((a, rho))
+            q = q - _bc(a, q) * y_k
+        # slices without a curvature pair yet: unit-length steepest-descent step per block
+        gnorm = _bdot(g, g).sqrt().clamp_min(1e-300)
+        scal = torch.where(has_gamma.unsqueeze(0), gamma, 1.0 / gnorm)
+        r = q * _bc(scal, q)
+        for (s_k, y_k, ok), (a, rho) in zip(zip(hist_s, hist_y, hist_ok), reversed(alphas)):
+            b = rho * _sdot(y_k, r)
+            r = r + _bc(a - b, r) * s_k
+        p = -r
+        gp = _sdot(g, p)
+        bad = gp >= 0                          # not a descent direction: restart that slice
+        if bool(bad.any()):
+            p = torch.where(_bc(bad, p), -g * _bc(1.0 / _bdot(g, g).sqrt().clamp_min(1e-300), g), p)
+            gp = _sdot(g, p)
+            hist_ok = [ok & ~bad for ok in hist_ok]
+        sd = sd | bad
+        # ---- batched backtracking Armijo ----
+        step = torch.ones(S, dtype=torch.float64, device=dev)
+        step = torch.where(conv, torch.zeros_like(step), step)
+        accepted = conv.clone()
+        x_new, f_new, g_new = x.clone(), f.clone(), g.clone()
+        for _ in range(max_ls):
+            xt = x + _bc(step, x) * p
+            ft, gt = fg(xt)
+            n_evals += 1
+            ok = (~accepted) & (ft.double() <= f + c1 * step * gp)
+            sel = _bc(ok, x)
+            x_new = torch.where(sel, xt, x_new)
+            g_new = torch.where(sel, gt, g_new)
+            f_new = torch.where(ok, ft.double(), f_new)
+            accepted |= ok
+            if bool(accepted.all()):
+                break
+            step = torch.where(accepted, step, 0.5 * step)
+        # no decrease found: restart that slice from steepest descent; if even that fails the
+        # slice has converged to working precision
+        failed = ~accepted
+        if bool(failed.any()):
+            hist_ok = [ok & ~failed for ok in hist_ok]
+            has_gamma = has_gamma & ~failed
+        s_vec, y_vec = x_new - x, g_new - g
+        sy = _sdot(s_vec, y_vec)
+        curv = sy > 1e-12 * _sdot(s_vec, s_vec).sqrt() * _sdot(y_vec, y_vec).sqrt()
+        keep = accepted & curv & ~conv
+        if bool(keep.any()):
+            hist_s.append(s_vec)
+            hist_y.append(y_vec)
+            hist_ok.append(keep)
+            if len(hist_s) > m:
+                hist_s.pop(0), hist_y.pop(0), hist_ok.pop(0)
+            gb = _bdot(s_vec, y_vec) / _bdot(y_vec, y_vec).clamp_min(1e-300)
+            gg = (sy / _sdot(y_vec, y_vec).clamp_min(1e-300)).unsqueeze(0).expand_as(gb)
+            gb = torch.where(gb > 0, gb, gg)          # block secant not positive: global scalar
+            gamma = torch.where(keep.unsqueeze(0), gb, gamma)
+            has_gamma = has_gamma | keep
+        rel = (f - f_new) / f.abs().clamp_min(1e-300)
+        conv = conv | (failed & sd) | (accepted & (rel < rel_tol))
+        sd = failed & ~conv
+        x, f, g = x_new, f_new, g_new
+        history.append(f.clone())
+        if callback is not None:
+            callback(it, f)
+        if bool(conv.all()):
+            break
+    return Result(x, f, history, it, n_evals, conv, time.time() - t0)
+
+
+def ei_objective(plan, flat, mask, drift, s_exp, lam: float = 1e-2, ws=None):
+    """fg(x) for x = [3, S, N, N] (mu, delta, sigma) through the C ABI (`ei_cost_grad`)."""
+    from . import ei
+    ws = ws or ei.Workspace(plan, s_exp.device)
+
+    def fg(x: torch.Tensor):
+        x = x.contiguous()
+        ws.status.zero_()
+        ei.ei_cost_grad(plan, x[0], x[1], x[2], flat, mask, drift, s_exp, lam, ws.cost, ws.g[0], ws.g[1],
+                        ws.g[2], ws.status)
+        return ws.cost.clone(), ws.g.clone()
+    return fg

@@ -185,11 +185,12 @@ class Case:
 def make_case(cfg: Config,
               max_shift: Callable[[np.ndarray], float],
               max_proj: Callable[[np.ndarray], float],
-              model: Optional[Callable[["Case"], np.ndarray]] = None) -> Case:
+              model: Optional[Callable[["Case"], np.ndarray]] = None, noise: bool = True) -> Case:
     """Build the truth maps (scaled per R16/R17) and, if ``model`` is given, s_exp = Poisson(model).
 
     max_shift(delta_2d) must return max |z D R[delta]|; max_proj(img_2d) max R[img];
-    model(case) must return s_mod [S][Na][M][Nd] for the case's truth maps."""
+    model(case) must return s_mod [S][Na][M][Nd] for the case's truth maps.  noise=False stores the
+    noise-free curves (exact-fit experiments)."""
     S, N = cfg.S, cfg.N
     mu = np.zeros((S, N, N), np.float32)
     delta = np.zeros_like(mu)
@@ -208,7 +209,7 @@ def make_case(cfg: Config,
         smod = np.asarray(model(case), dtype=np.float64)
         s_exp = np.empty(smod.shape, np.float32)
         for s in range(S):
-            s_exp[s] = rngs[s].poisson(np.maximum(smod[s], 0.0)).astype(np.float32)
+            s_exp[s] = (rngs[s].poisson(np.maximum(smod[s], 0.0)) if noise else smod[s]).astype(np.float32)
         case.s_exp = s_exp
     return case
 

@@ -9,7 +9,7 @@ from oracle import ora
 from paper_2202_08627_b200 import synth
 
 
-def oracle_case(cfg: synth.Config, with_data: bool = True) -> synth.Case:
+def oracle_case(cfg: synth.Config, with_data: bool = True, noise: bool = True) -> synth.Case:
     ang = cfg.angles
 
     def max_shift(delta):
@@ -24,7 +24,7 @@ def oracle_case(cfg: synth.Config, with_data: bool = True) -> synth.Case:
                               dx=cfg.pixel, du=cfg.det_pitch, z=cfg.z)
         return smod
 
-    return synth.make_case(cfg, max_shift, max_proj, model if with_data else None)
+    return synth.make_case(cfg, max_shift, max_proj, model if with_data else None, noise=noise)
 
 
 @functools.lru_cache(maxsize=None)

@@ -360,7 +360,10 @@ int plan_projector(ei_plan &p, const double *angles, std::vector<int2> &groups,
   const int ntile = (ND + RT - 1) / RT;
   const long long ctas = (long long)ntile * groups.size() * p.S;
   int RS = 1;
-  while (RS < 8 && ctas * RS < 2 * 148 && N / (RS * 2) >= 2 * RC) RS *= 2;
+  // largest power of two keeping the grid within one wave of 2 CTAs x 148 SMs (measured best
+  // on C2 with the TMA pipeline: RS = 2)
+  while (RS < 8 && ctas * RS * 2 <= 2 * 148 && N / (RS * 2) >= 2 * RC) RS *= 2;
+  if (const char *e = getenv("EI_K1_RS")) RS = std::max(1, std::min(8, atoi(e)));   // tuning knob
   p.proj.RS = RS;
   int CWrs = CW;
   if (RS > 1) {

@@ -2,6 +2,7 @@
 // management and the launch sequence of each entry point.  Host code only; the kernels
 // live in k_*.cu.  No CPU fallback exists: every numeric step runs in the kernels.
 #include <math.h>
+#include <stdlib.h>
 #include <stdio.h>
 #include <string.h>
 
@@ -152,19 +153,13 @@ int ei_plan_create(const ei_geometry *geom, const double *angles, ei_plan **out)
   A(dalloc(&p->GA1, S * SINO1));
   A(dalloc(&p->part_curve, S * NA));
   A(dalloc(&p->part_reg, S * p->RB));
-  // K3 angle split for small grids: pick KS (<= 16, <= chunks/2) with the best wave
-  // quantisation over the 3 CTAs/SM x 148 SMs slots (ties -> more CTAs, i.e. better latency hiding)
+  // K3 angle split for small grids: the largest KS (<= 16, <= chunks/2) keeping the grid within
+  // ~2 CTAs per SM (measured on C2: KS = 4 beats 1-3 and 6-16)
   {
-    const long long ctas = (long long)ei::bp_tiles(p->N) * p->S, slots = 3 * 148;
+    const long long ctas = (long long)ei::bp_tiles(p->N) * p->S;
     int KS = 1;
-    double best = 0.0;
-    if (ctas < 2 * slots) {
-      for (int ks = 1; ks <= 16 && ks <= std::max(1, ei::bp_chunks(p->NA) / 2); ++ks) {
-        const long long n = ctas * ks, waves = (n + slots - 1) / slots;
-        const double eff = (double)n / (double)(waves * slots);
-        if (eff >= best - 1e-9) { best = eff; KS = ks; }
-      }
-    }
+    while (KS < 16 && KS + 1 <= std::max(1, ei::bp_chunks(p->NA) / 2) && ctas * (KS + 1) <= 2 * 148) ++KS;
+    if (const char *e = getenv("EI_K3_KS")) KS = std::max(1, std::min(16, atoi(e)));   // tuning knob
     p->KS = KS;
   }
   A(dalloc(&p->done, S));

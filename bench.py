@@ -38,6 +38,16 @@ METRIC = "cost+gradient evals/sec"
 UNIT = "evals/s"
 
 
+def load_traffic(cfg_name, kernel):
+    """roofline.traffic: DRAM bytes (read + write) per launch of `kernel` from the committed
+    `ncu --set full` capture of this config (profiles/traffic.json, tools/ncu_traffic.py)."""
+    try:
+        e = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))[cfg_name]
+        return e["kernels"][kernel]["dram_bytes_per_launch"], e["source"]
+    except Exception:
+        return None, None
+
+
 def load_peaks():
     try:
         return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -293,7 +303,8 @@ def run_gpu(args, cfg, rank, world, local_rank):
         kernels[k] = {"ms": round(per_kernel_ms[k], 5), "share": round(per_kernel_ms[k] / ms_step, 4)}
     d = kernels[dom]
     roofline = {"kernel": dom, "bound": d["bound"], "achieved": d["achieved"], "peak": d["peak"],
-                "unit": "GB/s", "frac": d["frac"], "traffic": None,
+                "unit": "GB/s", "frac": d["frac"], "traffic": load_traffic(cfg.name, dom)[0],
+                "traffic_unit": "dram bytes per launch", "traffic_source": load_traffic(cfg.name, dom)[1],
                 "peak_source": ("derived: 128 B/clk/SM x 148 SMs x median SM clock under load "
                                 "(%.0f MHz)" % sm_mhz) if d["bound"] == "l1" else
                                "measured hbm_gbs (MEASURED_PEAKS.json)"}

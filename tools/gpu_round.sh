@@ -1,0 +1,52 @@
+#!/bin/bash
+# One GPU-box pass: parity tests, smoke, bench lines for every config, ncu launch list of the
+# default bench command and one `--set full` capture of K1/K3/K2.  Usage (under gpurun):
+#   bash tools/gpu_round.sh TAG [what...]     what ⊂ {tests smoke bench ncu full}
+set -u
+TAG=${1:-run}; shift || true
+WHAT=${*:-tests smoke bench ncu full}
+OUT=gpurun_out/$TAG
+mkdir -p $OUT
+python -c "import __graft_entry__ as g; g.build()" > $OUT/build.log 2>&1 || { echo build failed; tail $OUT/build.log; exit 1; }
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $OUT/gpu.txt 2>&1
+nproc >> $OUT/gpu.txt; grep -m1 "model name" /proc/cpuinfo >> $OUT/gpu.txt
+for w in $WHAT; do
+  case $w in
+    tests)
+      timeout 1500 python -m pytest tests -m gpu -x -q > $OUT/pytest_gpu.log 2>&1; echo "pytest gpu rc=$?" | tee -a $OUT/rc.txt
+      tail -3 $OUT/pytest_gpu.log ;;
+    smoke)
+      timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1; echo "smoke rc=$?" | tee -a $OUT/rc.txt
+      tail -1 $OUT/smoke.log ;;
+    bench)
+      for c in C2 C1 C3 C5 C4; do
+        timeout 600 python bench.py --config $c > $OUT/bench_$c.json 2> $OUT/bench_$c.err; echo "bench $c rc=$?" | tee -a $OUT/rc.txt
+        python - $OUT/bench_$c.json <<'EOF'
+import json, sys
+try:
+    d = json.loads(open(sys.argv[1]).read().strip().splitlines()[-1])
+    k = d["kernels"]
+    print(d["config"]["workload"][:3], "ms/step %.4f" % d["ms_per_step"], "e2e %.1f" % d["e2e"]["value"],
+          " ".join("%s %.4fms %.3f" % (n, v["ms"], v.get("frac", 0)) for n, v in k.items()))
+except Exception as e:
+    print("parse fail", e)
+EOF
+      done ;;
+    ref)
+      timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > $OUT/bench_ref.json 2> $OUT/bench_ref.err; echo "ref rc=$?" | tee -a $OUT/rc.txt
+      tail -c 600 $OUT/bench_ref.json ;;
+    ncu)
+      timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
+        --log-file $OUT/launches.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline > $OUT/ncu_launch.log 2>&1
+      echo "ncu launches rc=$?" | tee -a $OUT/rc.txt ;;
+    full)
+      timeout 900 ncu --set full --clock-control none --import-source on \
+        -k regex:"project_kernel|backproject_kernel|curve_kernel" -s 9 -c 3 \
+        -o $OUT/full_c2 python bench.py --steps 3 --warmup 3 --no-cpu-baseline > $OUT/ncu_full_c2.log 2>&1
+      echo "ncu full c2 rc=$?" | tee -a $OUT/rc.txt
+      timeout 900 ncu --set full --clock-control none --import-source on \
+        -k regex:"project_kernel|backproject_kernel|curve_kernel" -s 3 -c 3 \
+        -o $OUT/full_c4s8 python tools/prof_case.py C4 8 2 > $OUT/ncu_full_c4.log 2>&1
+      echo "ncu full c4s8 rc=$?" | tee -a $OUT/rc.txt ;;
+  esac
+done

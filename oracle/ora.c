@@ -171,18 +171,20 @@ void ora_diff_t_adjoint(int n_det, double du, const double *g, double *y)
  *   g_mu, g_delta, g_sigma : [n_det] dS/dP_x (only when s_exp != NULL); g_delta already
  *                            includes z * D^T
  *   counters[0..1]         : += mu-clamp hits, W^2-clamp hits (R12, R13)
+ *   g_drift                : += dS/dm_o(theta) of this row, or NULL (NEXT-2: m_o enters eq. 4,
+ *                            P:74-75, through u = m - c - m_o - Delta, so ds/dm_o = s u / W^2)
  * ------------------------------------------------------------------------------- */
 void ora_curve_row(int n_det, int n_mask, double du, double z,
                    const double *p_mu, const double *p_delta, const double *p_sigma,
                    const double *flat_A, const double *flat_c, const double *flat_w,
                    const double *mask, double drift, const double *s_exp, double *s_mod,
                    double *cost, double *g_mu, double *g_delta, double *g_sigma,
-                   int64_t *counters)
+                   int64_t *counters, double *g_drift)
 {
     double *dP = (double *)malloc(sizeof(double) * n_det);
     double *gD = (double *)malloc(sizeof(double) * n_det);
     ora_diff_t(n_det, du, p_delta, dP);
-    double S = 0.0;
+    double S = 0.0, Gmo = 0.0;
     for (int k = 0; k < n_det; ++k) {
         const double delta_shift = z * dP[k];                          /* Delta = z dR[delta]/dt */
         double pm = p_mu[k];
@@ -208,6 +210,7 @@ void ora_curve_row(int n_det, int n_mask, double du, double z,
                 gm += -2.0 * r * s;                                   /* ds/dP_mu = -s        */
                 gd += 2.0 * r * s * u / W2;                           /* ds/dDelta = s u/W^2  */
                 gs += r * s * (u * u - W2) / (W2 * W2);               /* 2 r ds/dW^2          */
+                Gmo += 2.0 * r * s * u / W2;                          /* ds/dm_o = s u/W^2    */
             }
         }
         if (s_exp) {
@@ -220,6 +223,7 @@ void ora_curve_row(int n_det, int n_mask, double du, double z,
         ora_diff_t_adjoint(n_det, du, gD, g_delta);                   /* g_delta = z D^T g_Delta */
         for (int k = 0; k < n_det; ++k) g_delta[k] *= z;
         *cost += S;
+        if (g_drift) *g_drift += Gmo;
     }
     free(dP);
     free(gD);
@@ -272,7 +276,7 @@ void ora_forward(int n, int n_angles, int n_det, int n_mask, double dx, double d
         ora_curve_row(n_det, n_mask, du, z, Pm + (size_t)a * n_det, Pd + (size_t)a * n_det,
                       Ps + (size_t)a * n_det, fl, fl + n_det, fl + 2 * n_det, mk,
                       drift ? (double)drift[a] : 0.0, NULL, s_mod + (size_t)a * n_mask * n_det,
-                      NULL, NULL, NULL, NULL, c2);
+                      NULL, NULL, NULL, NULL, c2, NULL);
         cnt[0] += c2[0];
         cnt[1] += c2[1];
     }
@@ -285,12 +289,13 @@ void ora_forward(int n, int n_angles, int n_det, int n_mask, double dx, double d
  * Whole-slice cost and gradient (S:261 'cost' + S:270 'grad', map blocks only).
  *   status[0] += non-finite input elements (maps, flat, mask, drift, s_exp)
  *   status[1] += mu-clamp hits, status[2] += W^2-clamp hits
+ *   g_drift   = [n_angles] dS/dm_o(theta) of this slice (NEXT-2), or NULL
  * ------------------------------------------------------------------------------- */
-void ora_cost_grad(int n, int n_angles, int n_det, int n_mask, double dx, double du, double z,
-                   const double *angles, const float *mu, const float *delta, const float *sigma,
-                   const float *flat, const float *mask, const float *drift, const float *s_exp,
-                   double lambda, double *cost, double *g_mu, double *g_delta, double *g_sigma,
-                   int64_t *status /*[3]*/)
+void ora_cost_grad2(int n, int n_angles, int n_det, int n_mask, double dx, double du, double z,
+                    const double *angles, const float *mu, const float *delta, const float *sigma,
+                    const float *flat, const float *mask, const float *drift, const float *s_exp,
+                    double lambda, double *cost, double *g_mu, double *g_delta, double *g_sigma,
+                    int64_t *status /*[3]*/, double *g_drift)
 {
     const size_t nn = (size_t)n * n, ns = (size_t)n_angles * n_det;
     status[0] += count_nonfinite(mu, nn) + count_nonfinite(delta, nn) + count_nonfinite(sigma, nn) +
@@ -312,7 +317,8 @@ void ora_cost_grad(int n, int n_angles, int n_det, int n_mask, double dx, double
         ora_curve_row(n_det, n_mask, du, z, Pm + (size_t)a * n_det, Pd + (size_t)a * n_det,
                       Ps + (size_t)a * n_det, fl, fl + n_det, fl + 2 * n_det, mk,
                       drift ? (double)drift[a] : 0.0, se, NULL, &rowcost[a],
-                      Gm + (size_t)a * n_det, Gd + (size_t)a * n_det, Gs + (size_t)a * n_det, c2);
+                      Gm + (size_t)a * n_det, Gd + (size_t)a * n_det, Gs + (size_t)a * n_det, c2,
+                      g_drift ? &g_drift[a] : NULL);
         free(se);
         cnt[0] += c2[0];
         cnt[1] += c2[1];
@@ -336,6 +342,16 @@ void ora_cost_grad(int n, int n_angles, int n_det, int n_mask, double dx, double
     }
     *cost = S;
     free(Pm); free(Pd); free(Ps); free(Gm); free(Gd); free(Gs); free(rowcost); free(fl); free(mk);
+}
+
+void ora_cost_grad(int n, int n_angles, int n_det, int n_mask, double dx, double du, double z,
+                   const double *angles, const float *mu, const float *delta, const float *sigma,
+                   const float *flat, const float *mask, const float *drift, const float *s_exp,
+                   double lambda, double *cost, double *g_mu, double *g_delta, double *g_sigma,
+                   int64_t *status /*[3]*/)
+{
+    ora_cost_grad2(n, n_angles, n_det, n_mask, dx, du, z, angles, mu, delta, sigma, flat, mask, drift,
+                   s_exp, lambda, cost, g_mu, g_delta, g_sigma, status, NULL);
 }
 
 int ora_num_threads(void)

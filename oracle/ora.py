@@ -54,10 +54,11 @@ def lib():
         L.ora_diff_t_adjoint.argtypes = [i, d, _dp, _dp]
         vp = ctypes.c_void_p
         L.ora_curve_row.argtypes = [i, i, d, d, _dp, _dp, _dp, _dp, _dp, _dp, _dp, d,
-                                    vp, vp, vp, vp, vp, vp, _ip]
+                                    vp, vp, vp, vp, vp, vp, _ip, vp]
         L.ora_forward.argtypes = [i, i, i, i, d, d, d, _dp, _fp, _fp, _fp, _fp, _fp, vp, _dp, _ip]
         L.ora_cost_grad.argtypes = [i, i, i, i, d, d, d, _dp, _fp, _fp, _fp, _fp, _fp, vp, _fp, d,
                                     vp, _dp, _dp, _dp, _ip]
+        L.ora_cost_grad2.argtypes = L.ora_cost_grad.argtypes + [vp]
         L.ora_num_threads.restype = i
         _lib = L
     return _lib
@@ -114,7 +115,7 @@ def diff_t_adjoint(g, du=1.0):
 def curve_row(p_mu, p_delta, p_sigma, flat_A, flat_c, flat_w, mask, drift=0.0, z=1.0, du=1.0,
               s_exp=None):
     """One detector row: returns dict(s_mod [M][Nd], and if s_exp: cost, g_mu, g_delta, g_sigma,
-    counters=[mu_clamp, w2_clamp])."""
+    g_drift = dS/dm_o, counters=[mu_clamp, w2_clamp])."""
     p_mu, p_delta, p_sigma = _d(p_mu), _d(p_delta), _d(p_sigma)
     fa, fc, fw, mk = _d(flat_A), _d(flat_c), _d(flat_w), _d(mask)
     nd, m = len(p_mu), len(mk)
@@ -125,12 +126,14 @@ def curve_row(p_mu, p_delta, p_sigma, flat_A, flat_c, flat_w, mask, drift=0.0, z
         se = _d(s_exp).reshape(m, nd)
         cost = np.zeros(1, np.float64)
         gm, gd, gs = (np.zeros(nd, np.float64) for _ in range(3))
+        gmo = np.zeros(1, np.float64)
         lib().ora_curve_row(nd, m, du, z, p_mu, p_delta, p_sigma, fa, fc, fw, mk, float(drift),
-                            _ptr(se), _ptr(s_mod), _ptr(cost), _ptr(gm), _ptr(gd), _ptr(gs), cnt)
-        out.update(cost=float(cost[0]), g_mu=gm, g_delta=gd, g_sigma=gs)
+                            _ptr(se), _ptr(s_mod), _ptr(cost), _ptr(gm), _ptr(gd), _ptr(gs), cnt,
+                            _ptr(gmo))
+        out.update(cost=float(cost[0]), g_mu=gm, g_delta=gd, g_sigma=gs, g_drift=float(gmo[0]))
     else:
         lib().ora_curve_row(nd, m, du, z, p_mu, p_delta, p_sigma, fa, fc, fw, mk, float(drift),
-                            None, _ptr(s_mod), None, None, None, None, cnt)
+                            None, _ptr(s_mod), None, None, None, None, cnt, None)
     out["counters"] = cnt
     return out
 
@@ -154,8 +157,9 @@ def forward(angles, mu, delta, sigma, flat, mask, drift=None, n_det=None, dx=1.0
 
 
 def cost_grad(angles, mu, delta, sigma, flat, mask, drift, s_exp, lam=0.0, dx=1.0, du=1.0, z=1.0,
-              slices=None):
-    """Per-slice cost (fp64) and gradient maps (fp64) of eq. 5; status [3] int64."""
+              slices=None, want_drift=False):
+    """Per-slice cost (fp64) and gradient maps (fp64) of eq. 5; status [3] int64.
+    want_drift: also return g_drift [S][Na] = dS_s/dm_o(theta) (NEXT-2) as a 6th value."""
     angles = _d(angles)
     mu, delta, sigma, flat, mask, s_exp = (_f(a) for a in (mu, delta, sigma, flat, mask, s_exp))
     S, n, _ = mu.shape
@@ -165,11 +169,16 @@ def cost_grad(angles, mu, delta, sigma, flat, mask, drift, s_exp, lam=0.0, dx=1.
     cost = np.zeros(len(sl), np.float64)
     g = np.zeros((3, len(sl), n, n), np.float64)
     status = np.zeros(3, np.int64)
+    gdr = np.zeros((len(sl), na), np.float64)
     for o, s in enumerate(sl):
         c = np.zeros(1, np.float64)
         gm, gd, gs = (np.zeros((n, n), np.float64) for _ in range(3))
-        lib().ora_cost_grad(n, na, nd, m, dx, du, z, angles, mu[s], delta[s], sigma[s], flat[s], mask,
-                            _ptr(dr), s_exp[s], float(lam), _ptr(c), gm, gd, gs, status)
+        gmo = np.zeros(na, np.float64)
+        lib().ora_cost_grad2(n, na, nd, m, dx, du, z, angles, mu[s], delta[s], sigma[s], flat[s], mask,
+                             _ptr(dr), s_exp[s], float(lam), _ptr(c), gm, gd, gs, status, _ptr(gmo))
         cost[o] = c[0]
         g[0, o], g[1, o], g[2, o] = gm, gd, gs
+        gdr[o] = gmo
+    if want_drift:
+        return cost, g[0], g[1], g[2], status, gdr
     return cost, g[0], g[1], g[2], status

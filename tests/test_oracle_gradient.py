@@ -96,3 +96,29 @@ def test_slices_independent_and_status():
     s_bad[0, 0, 0, 0] = np.inf
     _, _, _, _, st = ora.cost_grad(a1[0], *bad, a1[2], a1[3], a1[4], s_bad)
     assert st[0] == 2
+
+
+@pytest.mark.parametrize("seed,z", [(7, 1.0), (8, 2.5)])
+def test_drift_gradient_matches_finite_differences(seed, z):
+    """NEXT-2: dS/dm_o(theta) (m_o enters eq. 4, through u = m - c - m_o - Delta)
+    against central differences of the fp64 cost in each drift component."""
+    ang, maps, flat, mask, drift, s_exp = tiny_problem(seed)
+    cost, gm, gd, gs, st, gdr = ora.cost_grad(ang, *maps, flat, mask, drift, s_exp, 0.0, z=z,
+                                              want_drift=True)
+    maps64 = [x[0].astype(np.float64) for x in maps]
+    d64 = drift.astype(np.float64)
+    h = 1e-5
+    fd = np.zeros(len(d64))
+    for a in range(len(d64)):
+        dp, dm = d64.copy(), d64.copy()
+        dp[a] += h
+        dm[a] -= h
+        fd[a] = (_cost64(ang, maps64, flat, mask, dp, s_exp, 0.0, z) -
+                 _cost64(ang, maps64, flat, mask, dm, s_exp, 0.0, z)) / (2 * h)
+    assert np.linalg.norm(fd - gdr[0]) / np.linalg.norm(gdr[0]) < 1e-6
+    # a shift of every drift component by a is a shift of every mask position by -a (eq. 4):
+    # sum_theta dS/dm_o = -sum_j dS/dm_j, checked by moving the mask instead
+    mk = mask.astype(np.float64)
+    cp = _cost64(ang, maps64, flat, mk - h, d64, s_exp, 0.0, z)
+    cm = _cost64(ang, maps64, flat, mk + h, d64, s_exp, 0.0, z)
+    assert abs((cp - cm) / (2 * h) - gdr[0].sum()) <= 1e-6 * np.abs(gdr[0]).sum()

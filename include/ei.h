@@ -97,6 +97,19 @@ int ei_cost_grad(const ei_plan *plan, const float *mu, const float *delta, const
                  float lambda, double *cost, float *g_mu, float *g_delta, float *g_sigma,
                  int32_t *status, void *stream);
 
+/* ei_cost_grad plus the gradient with respect to the mask drift m_o(theta) (SURVEY.md §8(f)
+ * NEXT-2; m_o enters eq. 4, through u = m - c - m_o - Delta), computed in the same
+ * pass (one extra fixed-order reduction, no extra launch):
+ *   g_drift [S][N_theta] fp32 device (overwritten): dS_s/dm_o(theta) of each slice s; the drift
+ *   is shared by the slices of a stack, so its gradient is the sum over s (left to the caller, and
+ *   across ranks for a slice-sharded stack).  Must not be NULL (EI_ERR_NULL).
+ * All other arguments, outputs and errors exactly as ei_cost_grad; a NULL drift means m_o = 0
+ * and the gradient is still evaluated there. */
+int ei_cost_grad_drift(const ei_plan *plan, const float *mu, const float *delta, const float *sigma,
+                       const float *flat, const float *mask_pos, const float *drift,
+                       const float *s_exp, float lambda, double *cost, float *g_mu, float *g_delta,
+                       float *g_sigma, float *g_drift, int32_t *status, void *stream);
+
 /* ei_cost_grad with HOST buffers (same shapes and meaning; status is overwritten, not
  * accumulated).  Copies inputs host->device, evaluates, copies cost, gradients and status
  * back, and synchronises `stream` before returning.  Pinned host memory makes the copies

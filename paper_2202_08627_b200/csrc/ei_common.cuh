@@ -37,6 +37,15 @@ struct ProjPlan {
   int Rp = 0;               // padded row length (entries): N + 1 + 2 PAD, even
 };
 
+// K2 launch plan (k_curve.cu: plan_curve)
+struct CurvePlan {
+  int nseg = 1;   // segments per detector row
+  int W = 0;      // core positions per segment
+  int NT = 0;     // threads per CTA (>= W + 4, multiple of 32)
+  int nw = 0;     // warps per CTA (per-warp cost / drift partials per item)
+  int ctas = 0;   // persistent grid size
+};
+
 }  // namespace ei
 
 struct ei_plan {
@@ -44,6 +53,7 @@ struct ei_plan {
   int S = 0, N = 0, NA = 0, ND = 0, M = 0;
   ei::Tables tab;
   ei::ProjPlan proj;
+  ei::CurvePlan k2;
   // workspace (allocated in ei_plan_create only)
   // maps in the PAIR layout (k_pack.cu): entry e = (x[e-1], x[e]), e = 0..N, stored at e + PAD
   // in rows of proj.Rp entries (zero padding both sides); *T = the transposed maps (H2)
@@ -59,9 +69,9 @@ struct ei_plan {
   float2 *GB = nullptr;       // [S][NA][RpG]
   float2 *GA1 = nullptr;      // [S][NA][RpG]  single-map pairs (ei_backproject n_maps=1)
   int PADG = 0, RpG = 0;
-  double *part_curve = nullptr;  // [S][NA] per-row cost partials (K2)
+  float *part_curve = nullptr;   // [S][NA][nseg][nw] per-warp cost partials (K2)
+  float *part_mo = nullptr;      // [S][NA][nseg][nw] per-warp dS/dm_o partials (K2, NEXT-2)
   double *part_reg = nullptr;    // [S][RB] per-tile sum x^2 partials (K0)
-  unsigned int *done = nullptr;  // [S] K2 arrival counters (fused finalize), kept at 0 between calls
   unsigned int *done3 = nullptr; // [S][tiles] K3 arrival counters (angle split)
   float *part3 = nullptr;        // [KS][S][3][N][N] K3 angle-split partial gradients
   int KS = 1;                    // K3 angle split
@@ -95,16 +105,24 @@ cudaError_t launch_pack_sino(const ei_plan &p, const float *sino, int n_maps, cu
 // K1 (k_project.cu)
 cudaError_t launch_project3(const ei_plan &p, float *P, int RS, cudaStream_t st);
 cudaError_t launch_project1(const ei_plan &p, float *P, cudaStream_t st);
-// K2 / K4 (k_curve.cu)
+// K2 (k_curve.cu)
+int plan_curve(ei_plan &p);
 cudaError_t launch_curve_forward(const ei_plan &p, const float *flat, const float *mask,
                                  const float *drift, float *s_mod, cudaStream_t st);
 cudaError_t launch_curve_cost_grad(const ei_plan &p, const float *flat, const float *mask,
                                    const float *drift, const float *s_exp, int32_t *status,
-                                   float lambda, double *cost, cudaStream_t st);
-// K3 (k_backproject.cu)
+                                   cudaStream_t st);
+// K3 (k_backproject.cu); with `fin` set, the CTAs (0, 0, s) also run the fused K4 finalize:
+// cost[s] = fixed-order sum of K2's per-segment partials + lambda * K0's sum x^2 partials, and
+// g_drift[s][theta] = sum of K2's per-segment dS/dm_o partials (if g_drift != NULL)
+struct Finalize {
+  double *cost = nullptr;
+  float *g_drift = nullptr;
+};
 cudaError_t launch_backproject3(const ei_plan &p, const float *mu, const float *delta,
                                 const float *sigma, float lambda, float *g_mu, float *g_delta,
-                                float *g_sigma, size_t out_stride, cudaStream_t st);
+                                float *g_sigma, size_t out_stride, const Finalize *fin,
+                                cudaStream_t st);
 cudaError_t launch_backproject1(const ei_plan &p, float *map, cudaStream_t st);
 int bp_tiles(int N);
 int bp_pad();

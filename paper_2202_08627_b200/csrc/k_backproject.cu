@@ -66,13 +66,50 @@ struct Smem {
   uint64_t full[NST], empty[NST];
 };
 
+struct FinArgs {
+  const float *part_cost, *part_mo;   // K2 per-warp partials [S][NA][nseg * nw]
+  const double *part_reg;
+  int per_slice, nseg, NA, RB;   // per_slice = NA * nseg * nw, nseg here = nseg * nw
+  double lambda;
+  double *cost;                  // NULL: no finalize (ei_backproject)
+  float *g_drift;                // [S][NA] or NULL
+};
+
+// consumer threads only (named barrier 1, NT threads); fixed order: per-thread strided fp64 sums,
+// then the warps' sums in warp order
+__device__ __forceinline__ void finalize(const FinArgs &f, int s, int tid) {
+  __shared__ double fred[NT / 32];
+  double c = 0.0, rg = 0.0;
+  const float *pc = f.part_cost + (size_t)s * f.per_slice;
+  for (int q = tid; q < f.per_slice; q += NT) c += (double)__ldcg(pc + q);
+  if (f.lambda > 0.0)
+    for (int b = tid; b < f.RB; b += NT) rg += __ldcg(f.part_reg + (size_t)s * f.RB + b);
+  double v = c + f.lambda * rg;
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
+  if ((tid & 31) == 0) fred[tid >> 5] = v;
+  asm volatile("bar.sync 1, %0;\n" ::"n"(NT) : "memory");
+  if (tid == 0) {
+    double t = 0.0;
+    for (int w = 0; w < NT / 32; ++w) t += fred[w];
+    f.cost[s] = t;
+  }
+  if (f.g_drift)
+    for (int a = tid; a < f.NA; a += NT) {
+      const float *pm = f.part_mo + ((size_t)s * f.NA + a) * f.nseg;
+      double m = 0.0;
+      for (int q = 0; q < f.nseg; ++q) m += (double)__ldcg(pm + q);
+      f.g_drift[(size_t)s * f.NA + a] = (float)m;
+    }
+}
+
 template <int NMAP>
 __global__ void __launch_bounds__(NT + 32, 3) backproject_kernel(
     const typename Layout<NMAP>::A *__restrict__ GA, const float2 *__restrict__ GB,
     const float4 *__restrict__ k3, int N, int NA, int ND, const float *__restrict__ mu,
     const float *__restrict__ delta, const float *__restrict__ sigma, float lambda,
     float *__restrict__ o0, float *__restrict__ o1, float *__restrict__ o2, size_t out_stride,
-    int S, int KS, float *__restrict__ part3, unsigned int *__restrict__ done3, int PADG, int RpG) {
+    int S, int KS, float *__restrict__ part3, unsigned int *__restrict__ done3, int PADG, int RpG,
+    FinArgs fin) {
   using TA = typename Layout<NMAP>::A;
   constexpr bool A8 = sizeof(TA) == 8;
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -135,6 +172,10 @@ __global__ void __launch_bounds__(NT + 32, 3) backproject_kernel(
   }
 
   // ---------------- consumer warps ----------------
+  // fused K4 (cost path): while the producer fills the ring, CTA (0, 0, s) of angle split 0 sums
+  // K2's per-segment partials of slice s in index order (+ lambda * K0's sum x^2 partials) and
+  // the per-angle drift gradient
+  if (fin.cost && blockIdx.x == 0 && blockIdx.y == 0 && ks == 0) finalize(fin, s, tid);
   const int row = 4 * w + (lane >> 3), lx = lane & 7;
   const float yi = (float)(i0 + row) - ctr;
   float xq[4];
@@ -252,7 +293,21 @@ __global__ void __launch_bounds__(NT + 32, 3) backproject_kernel(
 template <int NMAP>
 cudaError_t launch_bp(const ei_plan &p, const typename Layout<NMAP>::A *GA, const float2 *GB,
                       const float *mu, const float *delta, const float *sigma, float lambda,
-                      float *o0, float *o1, float *o2, size_t out_stride, cudaStream_t st) {
+                      float *o0, float *o1, float *o2, size_t out_stride, const Finalize *fz,
+                      cudaStream_t st) {
+  FinArgs fin{};
+  if (fz) {
+    fin.part_cost = p.part_curve;
+    fin.part_mo = p.part_mo;
+    fin.part_reg = p.part_reg;
+    fin.per_slice = p.NA * p.k2.nseg * p.k2.nw;
+    fin.nseg = p.k2.nseg * p.k2.nw;
+    fin.NA = p.NA;
+    fin.RB = p.RB;
+    fin.lambda = (double)lambda;
+    fin.cost = fz->cost;
+    fin.g_drift = fz->g_drift;
+  }
   const size_t smem = sizeof(Smem<NMAP>);
   cudaError_t e = cudaFuncSetAttribute((const void *)backproject_kernel<NMAP>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -260,7 +315,7 @@ cudaError_t launch_bp(const ei_plan &p, const typename Layout<NMAP>::A *GA, cons
   dim3 grid((p.N + TILE - 1) / TILE, (p.N + TILE - 1) / TILE, p.S * p.KS);
   backproject_kernel<NMAP><<<grid, NT + 32, smem, st>>>(GA, GB, p.tab.k3, p.N, p.NA, p.ND, mu, delta,
                                                         sigma, lambda, o0, o1, o2, out_stride, p.S,
-                                                        p.KS, p.part3, p.done3, p.PADG, p.RpG);
+                                                        p.KS, p.part3, p.done3, p.PADG, p.RpG, fin);
   return cudaGetLastError();
 }
 
@@ -272,13 +327,15 @@ int bp_chunks(int NA) { return (NA + CH - 1) / CH; }
 
 cudaError_t launch_backproject3(const ei_plan &p, const float *mu, const float *delta,
                                 const float *sigma, float lambda, float *g_mu, float *g_delta,
-                                float *g_sigma, size_t out_stride, cudaStream_t st) {
-  return launch_bp<3>(p, p.GA, p.GB, mu, delta, sigma, lambda, g_mu, g_delta, g_sigma, out_stride, st);
+                                float *g_sigma, size_t out_stride, const Finalize *fin,
+                                cudaStream_t st) {
+  return launch_bp<3>(p, p.GA, p.GB, mu, delta, sigma, lambda, g_mu, g_delta, g_sigma, out_stride, fin,
+                      st);
 }
 
 cudaError_t launch_backproject1(const ei_plan &p, float *map, cudaStream_t st) {
   return launch_bp<1>(p, p.GA1, nullptr, nullptr, nullptr, nullptr, 0.f, map, nullptr, nullptr,
-                      (size_t)p.N * p.N, st);
+                      (size_t)p.N * p.N, nullptr, st);
 }
 
 }  // namespace ei

@@ -1,7 +1,6 @@
-// k_curve.cu — K2: the fused curve model / residual / cost / dS/dP pass, and K4: the
-// fixed-order fp64 per-slice cost.  SURVEY.md §8(a) a2-a4, a6.
+// k_curve.cu — K2: the fused curve model / residual / cost / dS/dP pass.  SURVEY.md §8(a) a2-a4.
 //
-// Per detector row (s, theta) one block:
+// Per detector position (s, theta, t):
 //   Delta = z * D P_delta         finite differences along t, halo 1
 //   T     = exp(-clamp(P_mu))     eq. 2, clamp R12
 //   W^2   = max(w^2 + P_sigma, w^2/100)                 scattering broadening R1, clamp R13
@@ -9,215 +8,409 @@
 //   r     = s_mod - s_exp;  S += r^2                     eq. 5
 //   g_mu = -2 sum r s;  g_Delta = 2 sum r s u / W^2;  g_sigma = sum r s (u^2 - W^2) / W^4
 //   g_delta = z D^T g_Delta                              halo 1 more (2 in total)
-// s_exp is streamed once, coalesced along t, its M values per (theta, t) loaded up front (8 at a
-// time) so the loads overlap; the cost is reduced fp32 (per thread, <= M*ceil(Nd/256) terms) ->
-// fp64 (warp shuffle, block) -> one fp64 partial per row.  K4 is fused: the last CTA of a slice
-// to finish (per-slice arrival counter) sums that slice's row partials in index order (+ lambda
-// times K0's per-tile sum x^2 partials) -> cost[s].  Deterministic; no float atomics.
+//   dS/dm_o(theta) = sum_t g_Delta(t)                    NEXT-2 (u depends on m_o like on -Delta)
+//
+// B200 design (DESIGN.md §5 K2): the pass is HBM-bound (s_exp streams once), so it is organised
+// for memory-level parallelism rather than per-row CTAs:
+//  * work item = one segment of W detector positions of one row (s, theta); a CTA of NT >= W + 4
+//    threads evaluates the curve at the W core positions plus a halo of 2 on each side, so D and
+//    D^T never need a neighbouring segment (1.5-3 % redundant arithmetic, no extra HBM bytes: the
+//    halo loads hit L2/L1);
+//  * persistent CTAs own a contiguous run of items (angle fastest, so stepping is a carry chain, no
+//    division) and the flat-IC parameters stay in registers; every thread PREFETCHES its loads
+//    for the next 2 items (3 projections + 2 neighbours, up to 8 s_exp values) as 4-byte cp.async
+//    copies into private shared slots, so each thread keeps ~20 independent loads in flight through
+//    its whole life instead of one round trip per row;
+//  * one CTA barrier per item: the per-position g values go to a double-buffered shared row, the
+//    core threads then write the gradient sinograms directly in K3's PAIR layout (entry
+//    e = (g[e-1], g[e]) of every map, pre-multiplied by the Joseph weight dx/|c_dom|);
+//  * cost and drift-gradient partials: fp32 per thread (M terms) and per warp (shuffle) -> one
+//    partial per (item, warp); K3 sums them in fp64 in index order (fused finalize, K4).
+// Deterministic: no float atomics, fixed reduction order, results independent of the grid size.
+#include <algorithm>
+
 #include "ei_common.cuh"
 
 namespace ei {
 namespace {
 
-constexpr int K2_THREADS = 256;
+constexpr int K2_MAXT = 512;   // threads per CTA (max)
+constexpr int MPF = 8;         // s_exp values per position held in prefetch registers
 
 // 2^x on the SFU (MUFU.EX2, ~2 ulp): every exponential of the curve model is written as a power
-// of two with the log2(e) factor folded into a per-(theta, t) constant
+// of two with the log2(e) factor folded into a per-position constant
 __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
 constexpr float LOG2E = 1.4426950408889634f;
-
-__device__ __forceinline__ double block_sum(double v, double *red) {
-  for (int off = 16; off > 0; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  __syncthreads();
-  if (lane == 0) red[wid] = v;
-  __syncthreads();
-  double t = 0.0;
-  if (threadIdx.x == 0)
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
-  return t;
+__device__ __forceinline__ float rcp(float x) {   // MUFU.RCP (~1 ulp), no slow path
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float rsq(float x) {   // MUFU.RSQ (~2 ulp), no denormal fix-up
+  float y;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
 }
 
-// MODE 0: forward (writes s_mod); MODE 1: cost + gradient (writes G, partials)
+struct K2Args {
+  const float *P;            // [RS][S][3][NA][ND] (row-split partial projections, summed here)
+  int RS, S;
+  size_t rstride;            // S * 3 * NA * ND
+  const float *flat, *mask, *drift, *s_exp;
+  int NA, ND, M, nseg, W;    // W = core positions per segment (<= blockDim - 4)
+  float z, inv_du;
+  float *s_mod;              // MODE 0
+  float4 *GA;                // MODE 1: pair-layout gradient sinograms (K3 input)
+  float2 *GB;
+  int PADG, RpG;
+  const float4 *k3;          // per-angle table, .w = Joseph weight dx/|c_dom|
+  float *part_cost, *part_mo;    // [S * NA * nseg * nw] per-warp partials
+  int32_t *status;
+  int items;                 // S * NA * nseg
+};
+
+// prefetch slots per position: P_mu, P_delta(k-1), P_delta(k+1), P_sigma, s_exp[0..MPF); each
+// thread's slots are contiguous (stride NQ, odd -> conflict-free), so every slot address is the
+// thread's base plus an immediate
+constexpr int NQ = 4 + MPF + 1;
+constexpr int NSTAGE = 3;      // items in flight per CTA: the current one + 2 prefetched
+
+__device__ __forceinline__ void cp4(uint32_t dst, const float *src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(dst), "l"(src));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+// item position (s, seg, a): angle fastest; a CTA's items are consecutive, so stepping is a carry
+// chain (no division), the flat-IC parameters (which depend on (s, t) only) stay in registers and
+// the load pointers advance by one row
+struct Pos {
+  int s, seg, a;
+  __device__ __forceinline__ bool step(int NA, int nseg) {   // true: (s, seg) changed
+    if (++a < NA) return false;
+    a = 0;
+    if (++seg == nseg) { seg = 0; ++s; }
+    return true;
+  }
+};
+
+// per-thread load cursor: this thread's position k of item (s, seg, a), as pointers into P and s_exp
+struct Cursor {
+  const float *pm, *se;   // &P[s][0][a][k], &s_exp[s][a][0][k]
+  int k;
+  bool valid;
+  __device__ __forceinline__ void seek(const K2Args &g, const Pos &q, int t) {
+    k = q.seg * g.W - 2 + t;
+    valid = k >= 0 && k < g.ND;
+    const int plane = g.NA * g.ND;                                 // < 2^30 (plan)
+    pm = g.P + (size_t)q.s * 3 * plane + (q.a * g.ND + k);
+    se = g.s_exp ? g.s_exp + ((size_t)(q.s * g.NA + q.a) * g.M) * g.ND + k : nullptr;
+  }
+  __device__ __forceinline__ void next_row(const K2Args &g) {     // a -> a + 1, same (s, seg)
+    pm += g.ND;
+    if (se) se += (size_t)g.M * g.ND;
+  }
+};
+
+// issue this thread's loads of the cursor's item as 4-byte async copies into its private prefetch
+// slots (only this thread reads them: cp.async.wait_group alone orders them — no barrier)
 template <int MODE>
-__global__ void __launch_bounds__(K2_THREADS) curve_kernel(
-    const float *__restrict__ P, int RS, int S, const float *__restrict__ flat,
-    const float *__restrict__ mask, const float *__restrict__ drift,
-    const float *__restrict__ s_exp, int NA, int ND, int M,
-    float z, float inv_du, float *__restrict__ s_mod, float4 *__restrict__ GA,
-    float2 *__restrict__ GB, double *__restrict__ part, int32_t *__restrict__ status,
-    unsigned int *__restrict__ done, const double *__restrict__ part_reg, int RB, float lambda,
-    double *__restrict__ cost_out, const float4 *__restrict__ k3, int PADG, int RpG) {
-  extern __shared__ float sm[];
-  float *gD = sm;              // [ND] g_Delta row
-  float *gmS = sm + ND;        // [ND] g_mu row
-  float *gsS = sm + 2 * ND;    // [ND] g_sigma row
-  float *smask = sm + 3 * ND;  // [M]
-  __shared__ double red[K2_THREADS / 32];
-  const int a = blockIdx.x, s = blockIdx.y;
-  const size_t plane = (size_t)NA * ND;
-  // P holds RS row-split partial projections [RS][S][3][NA][ND]: summed here in fixed order
-  const float *Pm = P + (size_t)s * 3 * plane + (size_t)a * ND;
-  const float *Pd = Pm + plane, *Ps = Pm + 2 * plane;
-  const size_t rstride = (size_t)S * 3 * plane;
-  auto psum = [&](const float *b, int k) {
-    float v = __ldg(b + k);
-    for (int r = 1; r < RS; ++r) v += __ldg(b + r * rstride + k);
-    return v;
-  };
-  const float *fA = flat + (size_t)s * 3 * ND, *fc = fA + ND, *fw = fA + 2 * ND;
-  for (int m = threadIdx.x; m < M; m += blockDim.x) smask[m] = __ldg(mask + m);
-  __syncthreads();
-  const float mo = drift ? __ldg(drift + a) : 0.f;
-  const size_t row = ((size_t)s * NA + a) * M * ND;   // s_exp / s_mod row base
-  float cost = 0.f;
+__device__ __forceinline__ void load_item(const K2Args &g, const Cursor &c, uint32_t slot, int plane,
+                                          int dl, int dr) {
+  if (!c.valid) return;
+  cp4(slot, c.pm);
+  cp4(slot + 4, c.pm + plane + dl);
+  cp4(slot + 8, c.pm + plane + dr);
+  cp4(slot + 12, c.pm + 2 * plane);
+  if (MODE == 1) {
+    const float *se = c.se;
+#pragma unroll
+    for (int u = 0; u < MPF; ++u) {
+      if (u < g.M) cp4(slot + 16 + 4 * u, se);
+      se += g.ND;
+    }
+  }
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+  return v;
+}
+
+template <int MODE>
+__global__ void __maxnreg__(72) curve_kernel(K2Args g) {
+  extern __shared__ __align__(16) float pre_s[];   // [NSTAGE][NQ][NT] prefetch slots
+  __shared__ float sgD[2][K2_MAXT], sgm[2][K2_MAXT], sgs[2][K2_MAXT];
+  const int NT = blockDim.x;
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5, nw = NT >> 5;
+  const int ND = g.ND;
   int bad = 0, mu_cl = 0, w2_cl = 0;
-  for (int k = threadIdx.x; k < ND; k += blockDim.x) {
-    // D P_delta from the neighbouring projections (global, L1-cached; no shared-memory phase)
-    const int kl = k == 0 ? 0 : k - 1, kr = k == ND - 1 ? ND - 1 : k + 1;
-    const float dP = (psum(Pd, kr) - psum(Pd, kl)) * ((kr - kl == 2 ? 0.5f : 1.f) * inv_du);
-    const float shift = z * dP;
-    float pmu = psum(Pm, k);
-    const bool mc = (pmu > 50.f) || (pmu < -50.f);
-    pmu = fminf(fmaxf(pmu, -50.f), 50.f);
-    const float T = ex2(-LOG2E * pmu);
-    const float A = __ldg(fA + k), c = __ldg(fc + k), w = __ldg(fw + k);
-    float W2 = fmaf(w, w, psum(Ps, k));
-    const float W2min = 0.01f * w * w;
-    const bool wc = W2 < W2min;
-    W2 = wc ? W2min : W2;
-    const float invW2 = __frcp_rn(W2);
-    const float amp = T * A * w * rsqrtf(W2);
-    const float c2 = -0.5f * LOG2E * invW2;   // exp(-u^2 / 2W^2) = 2^(c2 u^2)
-    const float base = c + mo + shift;
-    mu_cl += mc;
-    w2_cl += wc;
-    float gm = 0.f, gd = 0.f, gs = 0.f;
-    for (int m0 = 0; m0 < M; m0 += 8) {
-      float se[8];
-      if (MODE == 1) {
+  float mk[MPF];                                   // mask positions (first MPF) in registers
 #pragma unroll
-        for (int u = 0; u < 8; ++u)
-          se[u] = (m0 + u < M) ? __ldg(s_exp + row + (size_t)(m0 + u) * ND + k) : 0.f;
+  for (int u = 0; u < MPF; ++u) mk[u] = u < g.M ? __ldg(g.mask + u) : 0.f;
+  // static contiguous split of the items (deterministic, independent of timing)
+  const int i0 = (int)(((long long)blockIdx.x * g.items) / gridDim.x);
+  const int i1 = (int)(((long long)(blockIdx.x + 1) * g.items) / gridDim.x);
+  const int plane = g.NA * ND;
+  const uint32_t slot0 = (uint32_t)__cvta_generic_to_shared(pre_s) + 4u * (uint32_t)(t * NQ);
+  const uint32_t stage_bytes = 4u * (uint32_t)(NQ * NT);
+  Pos cp{i0 / (g.nseg * g.NA), (i0 / g.NA) % g.nseg, i0 % g.NA};   // current item
+  Pos lp = cp;                                                       // next item to prefetch
+  Cursor lc;
+  lc.seek(g, lp, t);
+  int dl = lc.k == 0 ? 0 : -1, dr = lc.k == ND - 1 ? 0 : 1;
+  auto advance = [&]() {   // lp/lc -> next item
+    if (lp.step(g.NA, g.nseg)) {
+      lc.seek(g, lp, t);
+      dl = lc.k == 0 ? 0 : -1;
+      dr = lc.k == ND - 1 ? 0 : 1;
+    } else {
+      lc.next_row(g);
+    }
+  };
+#pragma unroll
+  for (int q = 0; q < NSTAGE - 1; ++q) {
+    if (i0 + q < i1) {
+      load_item<MODE>(g, lc, slot0 + q * stage_bytes, plane, dl, dr);
+      advance();
+    }
+    cp_commit();
+  }
+  int fs = -1, fseg = -1;                          // (slice, segment) of the flat registers
+  float fA = 0.f, fc = 0.f, fw = 1.f;
+  int buf = 0, st = 0;
+  for (int item = i0; item < i1; ++item, buf ^= 1, st = (st + 1 == NSTAGE) ? 0 : st + 1,
+           cp.step(g.NA, g.nseg)) {
+    {   // keep NSTAGE - 1 items in flight: issue item + NSTAGE - 1 into the stage freed last
+      const int ns = (st + NSTAGE - 1) % NSTAGE;
+      if (item + NSTAGE - 1 < i1) {
+        load_item<MODE>(g, lc, slot0 + ns * stage_bytes, plane, dl, dr);
+        advance();
       }
-#pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int m = m0 + u;
-        if (m >= M) break;
-        const float du_ = smask[m] - base;
-        const float sv = amp * ex2(c2 * du_ * du_);
+      cp_commit();
+    }
+    const int seg = cp.seg, a = cp.a, s = cp.s;
+    const int k = seg * g.W - 2 + t;
+    const bool valid = k >= 0 && k < ND;
+    const bool core = valid && t >= 2 && t < g.W + 2;
+    if (valid && (s != fs || seg != fseg)) {       // new (slice, segment): flat A, c, w
+      const float *f = g.flat + (size_t)s * 3 * ND + k;
+      fA = __ldg(f);
+      fc = __ldg(f + ND);
+      fw = __ldg(f + 2 * ND);
+    }
+    fs = s;
+    fseg = seg;
+    cp_wait<NSTAGE - 1>();   // this item's copies (issued NSTAGE-1 groups ago) have landed
+    const float *cur = pre_s + st * NQ * NT + t * NQ;
+    const int row = s * g.NA + a;
+    float gm = 0.f, gd = 0.f, gs = 0.f, cost = 0.f;
+    if (valid) {
+      float pm = cur[0], pdl = cur[1], pdr = cur[2], ps = cur[3];
+      const int kl = k == 0 ? 0 : k - 1, kr = k == ND - 1 ? ND - 1 : k + 1;
+      if (g.RS > 1) {   // fixed-order sum of the row-split partials (small problems, L2-resident)
+        const int plane = g.NA * ND;
+        const float *Pm = g.P + (size_t)s * 3 * plane + a * ND;
+        for (int r = 1; r < g.RS; ++r) {
+          const float *b = Pm + r * g.rstride;
+          pm += __ldg(b + k);
+          pdl += __ldg(b + plane + kl);
+          pdr += __ldg(b + plane + kr);
+          ps += __ldg(b + 2 * plane + k);
+        }
+      }
+      const float dP = (pdr - pdl) * ((kr - kl == 2 ? 0.5f : 1.f) * g.inv_du);
+      const bool mc = (pm > 50.f) || (pm < -50.f);
+      pm = fminf(fmaxf(pm, -50.f), 50.f);
+      const float T = ex2(-LOG2E * pm);
+      float W2 = fmaf(fw, fw, ps);
+      const float W2min = 0.01f * fw * fw;
+      const bool wc = W2 < W2min;
+      W2 = wc ? W2min : W2;
+      const float invW2 = rcp(W2);
+      const float amp = T * fA * fw * rsq(W2);
+      // s = amp exp(-u^2 / 2W^2) = amp 2^(c2 u^2).  (Folding amp into the exponent as log2|amp|
+      // saves one FMUL per mask position but adds ~8x the argument rounding and breaks the 1e-3
+      // gradient gate at C3's noise level: measured 1.36e-3.)
+      const float c2 = -0.5f * LOG2E * invW2;
+      const float mo = g.drift ? __ldg(g.drift + a) : 0.f;
+      const float base = fc + mo + g.z * dP;
+      if (core) {
+        mu_cl += mc;
+        w2_cl += wc;
+      }
+      const size_t rowb = (size_t)row * g.M * ND + k;   // s_exp / s_mod row base
+      // per mask position: r = s - s_exp; cost += r^2; with rs = r s:
+      //   gmm += rs, gdd += rs u, gq += rs u^2   (g_sigma uses gq - W^2 gmm)
+      float gmm = 0.f, gdd = 0.f, gq = 0.f;
+      auto term = [&](float mpos, int m, float se) {
+        const float du_ = mpos - base;
+        const float u2 = du_ * du_;
+        const float sv = amp * ex2(c2 * u2);
         if (MODE == 0) {
-          s_mod[row + (size_t)m * ND + k] = sv;
+          if (core) g.s_mod[rowb + (size_t)m * ND] = sv;
         } else {
-          bad += !isfinite(se[u]);
-          const float r = sv - se[u];
+          const float r = sv - se;
           cost = fmaf(r, r, cost);
-          const float rs = r * sv;
-          gm += rs;
-          gd = fmaf(rs, du_, gd);
-          gs = fmaf(rs, fmaf(du_, du_, -W2), gs);
+          const float rsv = r * sv;
+          gmm += rsv;
+          gdd = fmaf(rsv, du_, gdd);
+          gq = fmaf(rsv, u2, gq);
+        }
+      };
+#pragma unroll
+      for (int u = 0; u < MPF; ++u)
+        if (u < g.M) term(mk[u], u, MODE == 1 ? cur[4 + u] : 0.f);   // prefetched s_exp
+      for (int m = MPF; m < g.M; ++m)                                          // M > MPF
+        term(__ldg(g.mask + m), m, MODE == 1 ? __ldcs(g.s_exp + rowb + (size_t)m * ND) : 0.f);
+      // a non-finite s_exp makes the cost non-finite; only then count the elements (rare path)
+      if (MODE == 1 && core && !isfinite(cost))
+        for (int m = 0; m < g.M; ++m) bad += !isfinite(m < MPF ? cur[4 + m] : g.s_exp[rowb + (size_t)m * ND]);
+      gm = mc ? 0.f : -2.f * gmm;
+      const float gss = fmaf(-W2, gmm, gq);   // sum r s (u^2 - W^2)
+      gs = wc ? 0.f : gss * invW2 * invW2;
+      gd = 2.f * gdd * invW2;
+    }
+    if (MODE == 1) {
+      sgD[buf][t] = gd;
+      sgm[buf][t] = gm;
+      sgs[buf][t] = gs;
+      // cost and dS/dm_o partials: fp32 per thread (<= M terms) and per warp (32 terms), then
+      // fp64 over the warps in warp order
+      const float wc_ = warp_sum(core ? cost : 0.f);
+      const float wm_ = warp_sum(core ? gd : 0.f);
+      if (lane == 0) {   // per-warp partials, (s, a, seg, warp) order; K3 sums them in fp64
+        const int pidx = ((s * g.NA + a) * g.nseg + seg) * nw + wid;
+        g.part_cost[pidx] = wc_;
+        g.part_mo[pidx] = wm_;
+      }
+      __syncthreads();
+      if (t < g.W) {
+        const int e = seg * g.W + t;       // pair entry written by this thread
+        if (e < ND) {
+          const float *D = sgD[buf] + (t + 2 - e);   // D[k] = g_Delta at detector k (window)
+          const float zh = 0.5f * g.z * g.inv_du;
+          // g_delta = z D^T g_Delta, D^T written out from the rows of D (a2):
+          //   y[j] = [j==0](-g0) + [j==1](g0) + [j==ND-2](-g_{ND-1}) + [j==ND-1](g_{ND-1})
+          //        + 1/2 g_{j-1} [1 <= j-1 <= ND-2] - 1/2 g_{j+1} [1 <= j+1 <= ND-2]   (all / du)
+          auto gdelta = [&](int j) {
+            if (j >= 2 && j <= ND - 3) return zh * (D[j - 1] - D[j + 1]);   // interior rows only
+            float y = 0.f;
+            if (j == 0) y -= D[0];
+            if (j == 1) y += D[0];
+            if (j == ND - 2) y -= D[ND - 1];
+            if (j == ND - 1) y += D[ND - 1];
+            if (j - 1 >= 1 && j - 1 <= ND - 2) y += 0.5f * D[j - 1];
+            if (j + 1 >= 1 && j + 1 <= ND - 2) y -= 0.5f * D[j + 1];
+            return g.z * g.inv_du * y;
+          };
+          const float sc = __ldg(g.k3 + a).w;
+          const size_t rb = (size_t)row * g.RpG + g.PADG;
+          const float m1 = sgm[buf][t + 2], s1 = sgs[buf][t + 2], d1 = gdelta(e);
+          const float m0 = e >= 1 ? sgm[buf][t + 1] : 0.f, s0 = e >= 1 ? sgs[buf][t + 1] : 0.f;
+          const float d0 = e >= 1 ? gdelta(e - 1) : 0.f;
+          g.GA[rb + e] = make_float4(sc * m0, sc * m1, sc * d0, sc * d1);
+          g.GB[rb + e] = make_float2(sc * s0, sc * s1);
+          if (e == ND - 1) {   // closing entry e = ND: (g[ND-1], 0)
+            g.GA[rb + ND] = make_float4(sc * m1, 0.f, sc * d1, 0.f);
+            g.GB[rb + ND] = make_float2(sc * s1, 0.f);
+          }
         }
       }
     }
-    if (MODE == 1) {
-      gmS[k] = mc ? 0.f : -2.f * gm;
-      gsS[k] = wc ? 0.f : gs * invW2 * invW2;
-      gD[k] = 2.f * gd * invW2;
+  }
+  cp_wait<0>();
+  if (MODE == 1) {
+    bad = __reduce_add_sync(0xffffffffu, bad);
+    mu_cl = __reduce_add_sync(0xffffffffu, mu_cl);
+    w2_cl = __reduce_add_sync(0xffffffffu, w2_cl);
+    if (lane == 0) {
+      if (bad) atomicAdd(&g.status[0], bad);
+      if (mu_cl) atomicAdd(&g.status[1], mu_cl);
+      if (w2_cl) atomicAdd(&g.status[2], w2_cl);
     }
   }
-  if (MODE == 0) return;
-  __syncthreads();
-  // g_delta = z * D^T g_Delta, D^T written out from the rows of D (a2):
-  //   y[j] = [j==0](-g0) + [j==1](g0) + [j==ND-2](-g_{ND-1}) + [j==ND-1](g_{ND-1})
-  //        + 1/2 g_{j-1} [1 <= j-1 <= ND-2] - 1/2 g_{j+1} [1 <= j+1 <= ND-2]      (all / du)
-  auto gdelta = [&](int j) {
-    float y = 0.f;
-    if (j == 0) y -= gD[0];
-    if (j == 1) y += gD[0];
-    if (j == ND - 2) y -= gD[ND - 1];
-    if (j == ND - 1) y += gD[ND - 1];
-    if (j - 1 >= 1 && j - 1 <= ND - 2) y += 0.5f * gD[j - 1];
-    if (j + 1 >= 1 && j + 1 <= ND - 2) y -= 0.5f * gD[j + 1];
-    return z * inv_du * y;
-  };
-  // pair layout for K3: entry e = (g[e-1], g[e]), e = 0..ND, zero outside the detector, each
-  // value pre-multiplied by the Joseph weight dx/|c_dom| of this angle (K3 then only applies the
-  // unit tent)
-  const float sc = __ldg(k3 + a).w;
-  float4 *Arow = GA + ((size_t)s * NA + a) * (size_t)RpG + PADG;
-  float2 *Brow = GB + ((size_t)s * NA + a) * (size_t)RpG + PADG;
-  for (int e = threadIdx.x; e <= ND; e += blockDim.x) {
-    const bool l = e >= 1, r = e < ND;
-    Arow[e] = make_float4(l ? sc * gmS[e - 1] : 0.f, r ? sc * gmS[e] : 0.f,
-                          l ? sc * gdelta(e - 1) : 0.f, r ? sc * gdelta(e) : 0.f);
-    Brow[e] = make_float2(l ? sc * gsS[e - 1] : 0.f, r ? sc * gsS[e] : 0.f);
-  }
-  const double tot = block_sum((double)cost, red);
-  if (bad) atomicAdd(&status[0], bad);
-  if (mu_cl) atomicAdd(&status[1], mu_cl);
-  if (w2_cl) atomicAdd(&status[2], w2_cl);
-  // fused K4: last CTA of slice s reduces the slice's partials in index order
-  __shared__ bool last;
-  if (threadIdx.x == 0) {
-    part[(size_t)s * NA + a] = tot;
-    __threadfence();
-    last = atomicAdd(&done[s], 1u) == (unsigned)(NA - 1);
-  }
-  __syncthreads();
-  if (!last) return;
-  __threadfence();
-  double c = 0.0, rg = 0.0;
-  for (int q = threadIdx.x; q < NA; q += blockDim.x) c += __ldcg(part + (size_t)s * NA + q);
-  if (lambda > 0.f)
-    for (int b = threadIdx.x; b < RB; b += blockDim.x) rg += __ldcg(part_reg + (size_t)s * RB + b);
-  const double v = block_sum(c + (double)lambda * rg, red);
-  if (threadIdx.x == 0) {
-    cost_out[s] = v;
-    done[s] = 0u;   // re-arm for the next evaluation
-  }
+}
+
+static size_t k2_smem(int NT) { return sizeof(float) * (size_t)NSTAGE * NQ * NT; }
+
+template <int MODE>
+cudaError_t launch(const ei_plan &p, const float *flat, const float *mask, const float *drift,
+                   const float *s_exp, float *s_mod, int32_t *status, cudaStream_t st) {
+  K2Args g;
+  g.P = p.P;
+  g.RS = p.proj.RS;
+  g.S = p.S;
+  g.rstride = (size_t)p.S * 3 * p.NA * p.ND;
+  g.flat = flat;
+  g.mask = mask;
+  g.drift = drift;
+  g.s_exp = s_exp;
+  g.NA = p.NA;
+  g.ND = p.ND;
+  g.M = p.M;
+  g.nseg = p.k2.nseg;
+  g.W = p.k2.W;
+  g.z = (float)p.g.z;
+  g.inv_du = (float)(1.0 / p.g.det_pitch);
+  g.s_mod = s_mod;
+  g.GA = p.GA;
+  g.GB = p.GB;
+  g.PADG = p.PADG;
+  g.RpG = p.RpG;
+  g.k3 = p.tab.k3;
+  g.part_cost = p.part_curve;
+  g.part_mo = p.part_mo;
+  g.status = status;
+  g.items = p.S * p.NA * p.k2.nseg;
+  const int grid = std::min(g.items, p.k2.ctas);
+  const size_t smem = k2_smem(p.k2.NT);
+  cudaError_t e = cudaFuncSetAttribute((const void *)curve_kernel<MODE>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  curve_kernel<MODE><<<grid, p.k2.NT, smem, st>>>(g);
+  return cudaGetLastError();
 }
 
 }  // namespace
 
-static size_t k2_smem(const ei_plan &p) { return sizeof(float) * (3 * (size_t)p.ND + p.M); }
-
-static cudaError_t k2_attr(const void *fn, size_t smem) {
-  if (smem > 48 * 1024)
-    return cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  return cudaSuccess;
+// K2 launch plan: segments of W = ceil(ND / nseg) positions, nseg the smallest count with
+// W + 4 <= 384 threads (balanced segments, <= ~10 % idle threads), CTA = W + 4 rounded up to a
+// warp; persistent grid = resident CTAs per SM x SMs.
+int plan_curve(ei_plan &p) {
+  int nseg = 1;
+  while ((p.ND + nseg - 1) / nseg + 4 > 384) ++nseg;
+  p.k2.nseg = nseg;
+  p.k2.W = (p.ND + nseg - 1) / nseg;
+  p.k2.NT = ((p.k2.W + 4 + 31) / 32) * 32;
+  p.k2.nw = p.k2.NT / 32;
+  if ((long long)p.S * p.NA * nseg > 0x7fffffffLL) return EI_ERR_RESOURCE;   // 32-bit item index
+  int dev = 0, sms = 148, per = 1;
+  if (cudaGetDevice(&dev) == cudaSuccess)
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaFuncSetAttribute((const void *)curve_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)k2_smem(p.k2.NT));
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, curve_kernel<1>, p.k2.NT, k2_smem(p.k2.NT)) != cudaSuccess || per < 1)
+    per = 1;
+  cudaGetLastError();
+  p.k2.ctas = sms * per;
+  return EI_OK;
 }
 
 cudaError_t launch_curve_forward(const ei_plan &p, const float *flat, const float *mask,
                                  const float *drift, float *s_mod, cudaStream_t st) {
-  const size_t smem = k2_smem(p);
-  cudaError_t e = k2_attr((const void *)curve_kernel<0>, smem);
-  if (e != cudaSuccess) return e;
-  dim3 grid(p.NA, p.S);
-  curve_kernel<0><<<grid, K2_THREADS, smem, st>>>(p.P, p.proj.RS, p.S, flat, mask, drift, nullptr, p.NA, p.ND, p.M,
-                                                  (float)p.g.z, (float)(1.0 / p.g.det_pitch), s_mod,
-                                                  nullptr, nullptr, nullptr, nullptr, nullptr,
-                                                  nullptr, 0, 0.f, nullptr, nullptr, 0, 0);
-  return cudaGetLastError();
+  return launch<0>(p, flat, mask, drift, nullptr, s_mod, nullptr, st);
 }
 
 cudaError_t launch_curve_cost_grad(const ei_plan &p, const float *flat, const float *mask,
                                    const float *drift, const float *s_exp, int32_t *status,
-                                   float lambda, double *cost, cudaStream_t st) {
-  const size_t smem = k2_smem(p);
-  cudaError_t e = k2_attr((const void *)curve_kernel<1>, smem);
-  if (e != cudaSuccess) return e;
-  dim3 grid(p.NA, p.S);
-  curve_kernel<1><<<grid, K2_THREADS, smem, st>>>(p.P, p.proj.RS, p.S, flat, mask, drift, s_exp, p.NA, p.ND, p.M,
-                                                  (float)p.g.z, (float)(1.0 / p.g.det_pitch), nullptr,
-                                                  p.GA, p.GB, p.part_curve, status, p.done,
-                                                  p.part_reg, p.RB, lambda, cost, p.tab.k3,
-                                                  p.PADG, p.RpG);
-  return cudaGetLastError();
+                                   cudaStream_t st) {
+  return launch<1>(p, flat, mask, drift, s_exp, nullptr, status, st);
 }
-
 
 }  // namespace ei

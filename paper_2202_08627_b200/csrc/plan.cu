@@ -54,7 +54,7 @@ void free_plan(ei_plan *p) {
   if (!p) return;
   free_timing(p);
   void *ptrs[] = {p->tab.k1, p->tab.k3, p->proj.groups, p->proj.order, p->proj.win1, p->proj.winRS, p->MA, p->MAT, p->MB,
-                  p->MBT, p->M1, p->M1T, p->diag, p->done, p->done3, p->part3, p->P, p->GA, p->GB, p->GA1,
+                  p->MBT, p->M1, p->M1T, p->diag, p->part_mo, p->done3, p->part3, p->P, p->GA, p->GB, p->GA1,
                   p->part_curve, p->part_reg, p->h_maps, p->h_flat, p->h_mask, p->h_drift,
                   p->h_sexp, p->h_grad, p->h_cost, p->h_status};
   for (void *q : ptrs)
@@ -120,6 +120,7 @@ int ei_plan_create(const ei_geometry *geom, const double *angles, ei_plan **out)
   std::vector<int2> groups, win1, winRS;
   std::vector<int> order;
   rc = ei::plan_projector(*p, angles, groups, order, win1, winRS);
+  if (!rc) rc = ei::plan_curve(*p);
   if (rc) {
     delete[] k1;
     delete[] k3;
@@ -151,7 +152,8 @@ int ei_plan_create(const ei_geometry *geom, const double *angles, ei_plan **out)
   A(dalloc(&p->GA, S * SINO1));
   A(dalloc(&p->GB, S * SINO1));
   A(dalloc(&p->GA1, S * SINO1));
-  A(dalloc(&p->part_curve, S * NA));
+  A(dalloc(&p->part_curve, S * NA * p->k2.nseg * p->k2.nw));
+  A(dalloc(&p->part_mo, S * NA * p->k2.nseg * p->k2.nw));
   A(dalloc(&p->part_reg, S * p->RB));
   // K3 angle split for small grids: the largest KS (<= 16, <= chunks/2) keeping the grid within
   // ~2 CTAs per SM (measured on C2: KS = 4 beats 1-3 and 6-16)
@@ -162,7 +164,6 @@ int ei_plan_create(const ei_geometry *geom, const double *angles, ei_plan **out)
     if (const char *e = getenv("EI_K3_KS")) KS = std::max(1, std::min(16, atoi(e)));   // tuning knob
     p->KS = KS;
   }
-  A(dalloc(&p->done, S));
   A(dalloc(&p->done3, S * (size_t)ei::bp_tiles(p->N)));
   if (p->KS > 1) A(dalloc(&p->part3, (size_t)p->KS * S * 3 * p->N * p->N));
   if (e == cudaSuccess) A(cudaMemcpy(p->tab.k1, k1, sizeof(float4) * NA, cudaMemcpyHostToDevice));
@@ -177,7 +178,6 @@ int ei_plan_create(const ei_geometry *geom, const double *angles, ei_plan **out)
     if (e == cudaSuccess) A(cudaMemset(q, 0, sizeof(float4) * S * NP));
   for (void *q : {(void *)p->MB, (void *)p->MBT, (void *)p->M1, (void *)p->M1T})
     if (e == cudaSuccess) A(cudaMemset(q, 0, sizeof(float2) * S * NP));
-  if (e == cudaSuccess) A(cudaMemset(p->done, 0, sizeof(unsigned int) * S));
   if (e == cudaSuccess) A(cudaMemset(p->GA, 0, sizeof(float4) * S * SINO1));   // zero padding
   if (e == cudaSuccess) A(cudaMemset(p->GB, 0, sizeof(float2) * S * SINO1));
   if (e == cudaSuccess) A(cudaMemset(p->GA1, 0, sizeof(float2) * S * SINO1));
@@ -290,7 +290,7 @@ int ei_backproject(const ei_plan *p, const float *sino, int n_maps, float *maps,
     e = ei::launch_pack_sino(*p, sino, 3, st);
     if (e == cudaSuccess)
       e = ei::launch_backproject3(*p, nullptr, nullptr, nullptr, 0.f, maps, maps + NN,
-                                  maps + 2 * NN, 3 * NN, st);
+                                  maps + 2 * NN, 3 * NN, nullptr, st);
     p->stats[2] += 1;
     p->stats[3] += 3;
     p->stats[5] += 2;
@@ -321,10 +321,11 @@ int ei_forward(const ei_plan *p, const float *mu, const float *delta, const floa
   return cuda_status(e);
 }
 
-int ei_cost_grad(const ei_plan *p, const float *mu, const float *delta, const float *sigma,
-                 const float *flat, const float *mask, const float *drift, const float *s_exp,
-                 float lambda, double *cost, float *g_mu, float *g_delta, float *g_sigma,
-                 int32_t *status, void *stream) {
+namespace {
+int cost_grad_impl(const ei_plan *p, const float *mu, const float *delta, const float *sigma,
+                   const float *flat, const float *mask, const float *drift, const float *s_exp,
+                   float lambda, double *cost, float *g_mu, float *g_delta, float *g_sigma,
+                   float *g_drift, int32_t *status, void *stream) {
   if (!p || !mu || !delta || !sigma || !flat || !mask || !s_exp || !cost || !g_mu || !g_delta ||
       !g_sigma || !status)
     return EI_ERR_NULL;
@@ -339,11 +340,11 @@ int ei_cost_grad(const ei_plan *p, const float *mu, const float *delta, const fl
   mark(1);
   if (e == cudaSuccess) e = ei::launch_project3(*p, p->P, p->proj.RS, st);          // K1
   mark(2);
-  if (e == cudaSuccess)
-    e = ei::launch_curve_cost_grad(*p, flat, mask, drift, s_exp, status, lambda, cost, st);  // K2+K4
+  if (e == cudaSuccess) e = ei::launch_curve_cost_grad(*p, flat, mask, drift, s_exp, status, st);  // K2
   mark(3);
+  ei::Finalize fin{cost, g_drift};
   if (e == cudaSuccess) e = ei::launch_backproject3(*p, mu, delta, sigma, lambda, g_mu, g_delta,
-                                                    g_sigma, NN, st);                  // K3
+                                                    g_sigma, NN, &fin, st);            // K3 + K4
   mark(4);
   p->stats[5] += 4;
   p->stats[0] += 1;
@@ -352,6 +353,24 @@ int ei_cost_grad(const ei_plan *p, const float *mu, const float *delta, const fl
   p->stats[3] += 3;
   p->stats[4] += 1;
   return cuda_status(e);
+}
+}  // namespace
+
+int ei_cost_grad(const ei_plan *p, const float *mu, const float *delta, const float *sigma,
+                 const float *flat, const float *mask, const float *drift, const float *s_exp,
+                 float lambda, double *cost, float *g_mu, float *g_delta, float *g_sigma,
+                 int32_t *status, void *stream) {
+  return cost_grad_impl(p, mu, delta, sigma, flat, mask, drift, s_exp, lambda, cost, g_mu, g_delta,
+                        g_sigma, nullptr, status, stream);
+}
+
+int ei_cost_grad_drift(const ei_plan *p, const float *mu, const float *delta, const float *sigma,
+                       const float *flat, const float *mask, const float *drift, const float *s_exp,
+                       float lambda, double *cost, float *g_mu, float *g_delta, float *g_sigma,
+                       float *g_drift, int32_t *status, void *stream) {
+  if (!g_drift) return EI_ERR_NULL;
+  return cost_grad_impl(p, mu, delta, sigma, flat, mask, drift, s_exp, lambda, cost, g_mu, g_delta,
+                        g_sigma, g_drift, status, stream);
 }
 
 int ei_cost_grad_host(ei_plan *p, const float *mu, const float *delta, const float *sigma,

@@ -24,7 +24,7 @@ _lib = ctypes.CDLL(LIB_PATH)
 
 EI_OK, EI_ERR_NULL, EI_ERR_SHAPE, EI_ERR_DOMAIN, EI_ERR_RESOURCE, EI_ERR_CUDA = range(6)
 SYMBOLS = ("ei_plan_create", "ei_plan_destroy", "ei_project", "ei_backproject", "ei_forward",
-           "ei_cost_grad", "ei_cost_grad_host", "ei_plan_stats", "ei_plan_set_timing",
+           "ei_cost_grad", "ei_cost_grad_drift", "ei_cost_grad_host", "ei_plan_stats", "ei_plan_set_timing",
            "ei_plan_read_timing", "ei_plan_info", "ei_error_string", "ei_version")
 KERNELS = ("K0_pack", "K1_project", "K2_curve", "K3_backproject", "unused4", "unused5")
 
@@ -43,6 +43,7 @@ _lib.ei_project.argtypes = [_vp, _vp, _i, _vp, _vp]
 _lib.ei_backproject.argtypes = [_vp, _vp, _i, _vp, _vp]
 _lib.ei_forward.argtypes = [_vp] + [_vp] * 7 + [_vp]
 _lib.ei_cost_grad.argtypes = [_vp] + [_vp] * 7 + [_f] + [_vp] * 5 + [_vp]
+_lib.ei_cost_grad_drift.argtypes = [_vp] + [_vp] * 7 + [_f] + [_vp] * 6 + [_vp]
 _lib.ei_cost_grad_host.argtypes = [_vp] + [_vp] * 7 + [_f] + [_vp] * 5 + [_vp]
 _lib.ei_plan_stats.argtypes = [_vp, _vp]
 _lib.ei_plan_set_timing.argtypes = [_vp, _i]
@@ -199,6 +200,21 @@ def ei_cost_grad(plan: Plan, mu, delta, sigma, flat, mask_pos, drift, s_exp, lam
         _stream(stream)), "ei_cost_grad")
 
 
+def ei_cost_grad_drift(plan: Plan, mu, delta, sigma, flat, mask_pos, drift, s_exp, lam: float, cost,
+                       g_mu, g_delta, g_sigma, g_drift, status, stream=None):
+    """ei_cost_grad + g_drift [S][N_theta] = dS_s/dm_o(theta) (NEXT-2), same pass."""
+    import torch
+    S, N, NA, ND, M = plan.shape
+    _check(_lib.ei_cost_grad_drift(
+        plan.handle, _dev(mu, (S, N, N), "mu"), _dev(delta, (S, N, N), "delta"),
+        _dev(sigma, (S, N, N), "sigma"), _dev(flat, (S, 3, ND), "flat"),
+        _dev(mask_pos, (M,), "mask_pos"), None if drift is None else _dev(drift, (NA,), "drift"),
+        _dev(s_exp, (S, NA, M, ND), "s_exp"), float(lam), _dev(cost, (S,), "cost", torch.float64),
+        _dev(g_mu, (S, N, N), "g_mu"), _dev(g_delta, (S, N, N), "g_delta"),
+        _dev(g_sigma, (S, N, N), "g_sigma"), _dev(g_drift, (S, NA), "g_drift"),
+        _dev(status, (4,), "status", torch.int32), _stream(stream)), "ei_cost_grad_drift")
+
+
 def _host(a, shape, name, dtype=np.float32, writable=False):
     if not isinstance(a, np.ndarray) or a.dtype != dtype or not a.flags.c_contiguous:
         raise TypeError("%s must be a C-contiguous numpy %s array" % (name, np.dtype(dtype)))
@@ -234,13 +250,19 @@ class Workspace:
         self.cost = torch.zeros(S, dtype=torch.float64, device=device)
         self.g = torch.zeros(3, S, N, N, dtype=torch.float32, device=device)
         self.status = torch.zeros(4, dtype=torch.int32, device=device)
+        self.g_drift = torch.zeros(S, NA, dtype=torch.float32, device=device)
 
 
 def cost_grad(plan: Plan, maps, flat, mask_pos, drift, s_exp, lam: float = 0.0,
-              ws: Optional[Workspace] = None, stream=None):
-    """Returns (cost [S] fp64, (g_mu, g_delta, g_sigma), status[4]) as device tensors."""
+              ws: Optional[Workspace] = None, stream=None, want_drift: bool = False):
+    """Returns (cost [S] fp64, (g_mu, g_delta, g_sigma), status[4]) as device tensors;
+    with want_drift a 4th value g_drift [S][N_theta] (ei_cost_grad_drift)."""
     ws = ws or Workspace(plan, maps[0].device)
     ws.status.zero_()
+    if want_drift:
+        ei_cost_grad_drift(plan, maps[0], maps[1], maps[2], flat, mask_pos, drift, s_exp, lam,
+                           ws.cost, ws.g[0], ws.g[1], ws.g[2], ws.g_drift, ws.status, stream)
+        return ws.cost, (ws.g[0], ws.g[1], ws.g[2]), ws.status, ws.g_drift
     ei_cost_grad(plan, maps[0], maps[1], maps[2], flat, mask_pos, drift, s_exp, lam, ws.cost,
                  ws.g[0], ws.g[1], ws.g[2], ws.status, stream)
     return ws.cost, (ws.g[0], ws.g[1], ws.g[2]), ws.status

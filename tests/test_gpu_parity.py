@@ -185,3 +185,28 @@ def test_launch_contract_host_path_and_determinism(ei):
                          cost, *gh, st)
     assert np.array_equal(cost, c1) and all(np.array_equal(a, b) for a, b in zip(gh, g1))
     assert np.array_equal(st, st1)
+
+
+@pytest.mark.parametrize("name", ["R1", "C1", "C2"])
+def test_drift_gradient_parity(ei, name):
+    """NEXT-2: g_drift [S][N_theta] = dS_s/dm_o(theta) from the same pass (ei_cost_grad_drift) vs
+    the oracle; the cost and map gradients are identical to ei_cost_grad's (same kernels)."""
+    case = _cases.cached_case(name)
+    cfg = case.cfg
+    plan = plan_for(ei, cfg)
+    maps = synth.perturbed(case.maps(), cfg.seed + 7)
+    drift = None if case.drift is None else dev(case.drift)
+    ws = ei.Workspace(plan)
+    cost, g, st, gdr = ei.cost_grad(plan, [dev(m) for m in maps], dev(case.flat), dev(case.mask),
+                                    drift, dev(case.s_exp), 0.0, ws, want_drift=True)
+    torch.cuda.synchronize()
+    gdr = gdr.cpu().numpy().copy()
+    c_d = cost.cpu().numpy().copy()
+    g_d = [x.cpu().numpy().copy() for x in g]
+    rc, rgm, rgd, rgs, rst, rdr = ora.cost_grad(cfg.angles, *maps, case.flat, case.mask, case.drift,
+                                                case.s_exp, 0.0, dx=cfg.pixel, du=cfg.det_pitch,
+                                                z=cfg.z, want_drift=True)
+    for s in range(cfg.S):
+        assert rel_l2(gdr[s], rdr[s]) <= 1e-3, (s, rel_l2(gdr[s], rdr[s]))
+    c2, g2, _ = gpu_cost_grad(ei, plan, case, maps, 0.0)
+    assert np.array_equal(c_d, c2) and all(np.array_equal(a, b) for a, b in zip(g_d, g2))

@@ -139,8 +139,9 @@ int ei_plan_read_timing(ei_plan *plan, double ms[6], int *n_evals);
 /* Launch-plan diagnostics (synchronous: reads a device counter).  out[0] = K1 angle groups,
  * out[1] = K1 rows per staged chunk, out[2] = K1 window-width bound (entries), out[3] = K1 row
  * split of the cost path, out[4] = internal window overflows seen so far (must be 0),
- * out[5] = K1 dynamic shared memory per CTA (bytes). */
-int ei_plan_info(const ei_plan *plan, int64_t out[6]);
+ * out[5] = K1 dynamic shared memory per CTA (bytes), out[6] = K1 angle groups using the
+ * ray-fastest lane mapping, out[7] = K3 angle split. */
+int ei_plan_info(const ei_plan *plan, int64_t out[8]);
 
 /* Human-readable name of an EI_* code (static string). */
 const char *ei_error_string(int code);

@@ -24,10 +24,11 @@ struct Tables {
 
 // K1 launch plan (k_project.cu: plan_projector)
 struct ProjPlan {
-  int2 *groups = nullptr;   // device: {first sorted position, count} per angle group
+  int2 *groups = nullptr;   // device: {first sorted position, count | ray_fast << 16} per group
   int *order = nullptr;     // device: sorted position -> angle index (row-dominant first)
   int n_groups = 0;
   int RC = 0;               // rows per staged chunk
+  int ray_fast = 0;         // number of angle groups using the ray-fastest consumer lane mapping
   int CW = 0;               // window width bound (entries)
   int RS = 1;               // row split of the cost path (partial P summed by K2)
   int2 *win1 = nullptr;     // device window table for RS = 1  [groups][tiles][nch1]

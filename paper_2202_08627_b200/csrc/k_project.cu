@@ -16,6 +16,7 @@
 //  * small problems split the rows over RS CTAs (partial P summed in fixed order by K2).
 #include <math.h>
 
+#include <stdio.h>
 #include <stdlib.h>
 
 #include <algorithm>
@@ -77,9 +78,13 @@ constexpr int NCW = NT / 32;    // consumer warps
 // and release the stage on its "empty" mbarrier.  No CTA-wide barrier inside the loop.
 // Map rows are zero-padded by PAD >= CW entries on both sides, so every window is one in-bounds
 // contiguous copy per row and plane.
-// Consumer lane -> (angle aq = lane & 3 of the group's current angle quad, ray lane >> 2): a
-// quarter warp = 4 angles x 2 adjacent rays, taps on 2-4 consecutive entries (conflict-free
-// LDS.128); slot m adds 4m to the angle.
+// Consumer lane -> (angle aq of the group's current angle quad, ray rq of the warp's 8 rays);
+// slot m adds 4m to the angle.  Two mappings, chosen per angle group from a bank-conflict model
+// of the geometry (plan_projector): angle fastest (aq = lane & 3, rq = lane >> 2: a quarter warp = 4
+// angles x 2 adjacent rays, taps on 2-4 consecutive entries when adjacent angles sample nearly
+// the same pixels — dense views) or ray fastest (rq = lane & 7, aq = lane >> 3: a quarter warp =
+// 8 adjacent rays of one angle — sparse views with large N, where the 4 angles of a quarter would
+// spread over tens of entries and conflict).
 template <int NMAP>
 __global__ void __launch_bounds__(NT + 32, 2) project_kernel(ProjArgs args) {
   using TA = typename PL<NMAP>::A;
@@ -96,7 +101,9 @@ __global__ void __launch_bounds__(NT + 32, 2) project_kernel(ProjArgs args) {
 
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int kt = blockIdx.x * RT;
-  const int2 gi = args.groups[blockIdx.y];
+  const int2 gr = args.groups[blockIdx.y];
+  const int2 gi = make_int2(gr.x, gr.y & 0xffff);   // {first sorted position, count}
+  const bool ray_fast = (gr.y >> 16) != 0;          // lane mapping of this group (plan)
   const int s = blockIdx.z % args.S, rs = blockIdx.z / args.S;
   const float ctr = 0.5f * (float)(N - 1), dctr = 0.5f * (float)(ND - 1);
   const bool rowdom = __ldg(args.k1 + args.order[gi.x]).w != 0.f;
@@ -145,8 +152,8 @@ __global__ void __launch_bounds__(NT + 32, 2) project_kernel(ProjArgs args) {
   }
 
   // ---------------- consumer warps ----------------
-  const int aq = lane & 3;
-  const int k = kt + w * 8 + (lane >> 2);
+  const int aq = ray_fast ? lane >> 3 : lane & 3;
+  const int k = kt + w * 8 + (ray_fast ? lane & 7 : lane >> 2);
   const float kc = (float)k - dctr;
   float alpha[4], tn[4], scale[4];
   int aidx[4];
@@ -323,6 +330,60 @@ static void build_windows(const ei_plan &p, const double *angles, const std::vec
   }
 }
 
+// Shared-memory wavefront model of the consumer gathers for one lane mapping (see the kernel):
+// per quarter warp the LDS.128 of the A plane costs the largest number of distinct 16-B entries
+// falling on one bank group (entry mod 8); per half warp the LDS.64 of the B plane the largest
+// number of distinct 8-B entries per bank pair (entry mod 16).  Averaged over sampled (ray tile,
+// warp, slot, row) positions of angle group g.
+static double wavefront_model(const ei_plan &p, const double *angles, const std::vector<int2> &groups,
+                              const std::vector<int> &order, size_t g, bool ray_fast) {
+  const int N = p.N, ND = p.ND;
+  const double dx = p.g.pixel, du = p.g.det_pitch, ctr = 0.5 * (N - 1), dctr = 0.5 * (ND - 1);
+  double wf = 0.0;
+  long long n = 0;
+  const int rows[5] = {0, N / 4, N / 2, (3 * N) / 4, N - 1};
+  const int tstep = std::max(1, (ND / 64) / 6);
+  for (int kt = 0; kt + 64 <= ND; kt += 64 * tstep)
+      for (int w = 0; w < 8; ++w)
+        for (int m = 0; m < 4; ++m)
+          for (int i : rows) {
+            long long e[32];
+            for (int lane = 0; lane < 32; ++lane) {
+              const int aq = ray_fast ? lane >> 3 : lane & 3, rq = ray_fast ? lane & 7 : lane >> 2;
+              const int al = std::min(aq + 4 * m, groups[g].y - 1);
+              const double th = angles[order[groups[g].x + al]];
+              const double cs = cos(th), sn = sin(th);
+              const bool rd = fabs(cs) >= fabs(sn);
+              const double cd = rd ? cs : sn, so = rd ? sn : cs;
+              const int k = kt + 8 * w + rq;
+              const double xs = (k - dctr) * du / (cd * dx) - (so / cd) * (i - ctr) + ctr;
+              e[lane] = (long long)floor(xs) + 1;
+            }
+            auto cost = [&](int lanes, int banks) {
+              int tot = 0;
+              for (int q0 = 0; q0 < 32; q0 += lanes) {
+                int worst = 1;
+                for (int b = 0; b < banks; ++b) {
+                  long long seen[32];
+                  int ns = 0;
+                  for (int l = q0; l < q0 + lanes; ++l) {
+                    if ((((e[l] % banks) + banks) % banks) != b) continue;
+                    bool dup = false;
+                    for (int z = 0; z < ns; ++z) dup |= seen[z] == e[l];
+                    if (!dup) seen[ns++] = e[l];
+                  }
+                  worst = std::max(worst, ns);
+                }
+                tot += worst;
+              }
+              return tot;
+            };
+            wf += cost(8, 8) + cost(16, 16);
+            ++n;
+          }
+  return n ? wf / n : 0.0;
+}
+
 int plan_projector(ei_plan &p, const double *angles, std::vector<int2> &groups,
                    std::vector<int> &order, std::vector<int2> &win1, std::vector<int2> &winRS) {
   const int NA = p.NA, N = p.N, ND = p.ND;
@@ -346,6 +407,7 @@ int plan_projector(ei_plan &p, const double *angles, std::vector<int2> &groups,
   const char *env = getenv("EI_K1_SMEM_KB");
   const size_t budget = (env ? (size_t)atoi(env) : 100) * 1024;
   int RC = 32, nch = 0, CW = 0;
+  std::vector<int> rf_flags;
   for (;;) {
     build_windows(p, angles, groups, order, 1, RC, win1, nch, CW);
     if ((size_t)NST * RC * (CW + 2) * per_entry <= budget || RC == 1) break;
@@ -355,6 +417,27 @@ int plan_projector(ei_plan &p, const double *angles, std::vector<int2> &groups,
   if (nch > MAXCH) return EI_ERR_SHAPE;
   p.proj.RC = RC;
   p.proj.n_groups = (int)groups.size();
+  {   // per angle group, the lane mapping with fewer modelled shared-memory wavefronts, stored in
+      // bit 16 of the group's count (tuning knob EI_K1_RAYFAST forces one mapping everywhere)
+    const char *force = getenv("EI_K1_RAYFAST");
+    rf_flags.assign(groups.size(), 0);
+    double wa_sum = 0.0, wbest = 0.0;
+    int nrf = 0;
+    for (size_t g = 0; g < groups.size(); ++g) {
+      const double wa = wavefront_model(p, angles, groups, order, g, false);
+      const double wr = wavefront_model(p, angles, groups, order, g, true);
+      int rf = wr < 0.9 * wa ? 1 : 0;
+      if (force) rf = atoi(force) ? 1 : 0;
+      wa_sum += wa;
+      wbest += rf ? wr : wa;
+      nrf += rf;
+      rf_flags[g] = rf;   // encoded into the device copy at the end (host code reads counts)
+    }
+    p.proj.ray_fast = nrf;
+    if (getenv("EI_PLAN_VERBOSE"))
+      fprintf(stderr, "libei plan: K1 modelled wavefronts/sample angle-fast %.2f chosen %.2f (%d/%d ray-fast groups)\n",
+              wa_sum / groups.size(), wbest / groups.size(), nrf, (int)groups.size());
+  }
   p.proj.nch1 = nch;
   // row split for small problems: aim for >= 2 CTAs per SM
   const int ntile = (ND + RT - 1) / RT;
@@ -376,6 +459,7 @@ int plan_projector(ei_plan &p, const double *angles, std::vector<int2> &groups,
   // zero padding of the pair-layout map rows so every staged window is one in-bounds copy
   p.proj.PAD = p.proj.CW + 2;   // even
   p.proj.Rp = (N + 1 + 2 * p.proj.PAD + 1) & ~1;   // even: 16-B aligned float2 rows
+  for (size_t g = 0; g < groups.size(); ++g) groups[g].y |= rf_flags[g] << 16;   // last: device copy
   return EI_OK;
 }
 

@@ -205,7 +205,7 @@ int ei_plan_stats(const ei_plan *p, int64_t out[6]) {
   return EI_OK;
 }
 
-int ei_plan_info(const ei_plan *p, int64_t out[6]) {
+int ei_plan_info(const ei_plan *p, int64_t out[8]) {
   if (!p || !out) return EI_ERR_NULL;
   int32_t d = 0;
   if (cudaMemcpy(&d, p->diag, sizeof(d), cudaMemcpyDeviceToHost) != cudaSuccess) return EI_ERR_CUDA;
@@ -214,7 +214,9 @@ int ei_plan_info(const ei_plan *p, int64_t out[6]) {
   out[2] = p->proj.CW;
   out[3] = p->proj.RS;
   out[4] = d;
-  out[5] = (int64_t)3 * p->proj.RC * (p->proj.CW * 16 + (p->proj.CW + 2) * 8);
+  out[5] = (int64_t)4 * p->proj.RC * (p->proj.CW * 16 + (p->proj.CW + 2) * 8);
+  out[6] = p->proj.ray_fast;
+  out[7] = p->KS;
   return EI_OK;
 }
 

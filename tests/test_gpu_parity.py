@@ -210,3 +210,24 @@ def test_drift_gradient_parity(ei, name):
         assert rel_l2(gdr[s], rdr[s]) <= 1e-3, (s, rel_l2(gdr[s], rdr[s]))
     c2, g2, _ = gpu_cost_grad(ei, plan, case, maps, 0.0)
     assert np.array_equal(c_d, c2) and all(np.array_equal(a, b) for a, b in zip(g_d, g2))
+
+
+@pytest.mark.parametrize("ray_fast", ["0", "1"])
+@pytest.mark.parametrize("name", ["C1", "R1"])
+def test_project_parity_both_lane_mappings(ei, name, ray_fast, monkeypatch):
+    """K1's two consumer lane mappings (angle fastest / ray fastest, chosen per plan by a
+    bank-conflict model) give the same projections (within fp32 rounding) as the oracle."""
+    monkeypatch.setenv("EI_K1_RAYFAST", ray_fast)
+    case = _cases.cached_case(name)
+    cfg = case.cfg
+    plan = plan_for(ei, cfg)
+    info = ei.ei_plan_info(plan)
+    assert info["k1_ray_fast"] == (info["k1_groups"] if ray_fast == "1" else 0)
+    maps = np.stack(case.maps(), axis=1)
+    sino = torch.zeros(cfg.S, 3, cfg.n_angles, cfg.n_det, device="cuda")
+    ei.ei_project(plan, dev(maps), 3, sino)
+    got = sino.cpu().numpy()
+    for s in range(cfg.S):
+        for q in range(3):
+            ref = ora.project(maps[s, q].astype(np.float64), cfg.angles, cfg.n_det, cfg.pixel, cfg.det_pitch)
+            assert rel_l2(got[s, q], ref) < 2e-5, (s, q)

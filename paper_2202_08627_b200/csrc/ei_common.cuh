@@ -91,6 +91,24 @@ struct ei_plan {
 };
 
 namespace ei {
+// launch `kern` on `st` with programmatic stream serialization (PDL): the kernel's prologue may
+// overlap the predecessor's tail; the kernel itself calls pdl_wait() before reading its inputs
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                       Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, ((KArgs)args)...);
+}
+
 int plan_projector(ei_plan &p, const double *angles, std::vector<int2> &groups,
                    std::vector<int> &order, std::vector<int2> &win1, std::vector<int2> &winRS);
 // K0 (k_pack.cu)

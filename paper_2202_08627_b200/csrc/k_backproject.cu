@@ -133,6 +133,7 @@ __global__ void __launch_bounds__(NT + 32, 3) backproject_kernel(
     mbar_fence_init();
   }
   __syncthreads();
+  pdl_wait();   // K2's gradient sinograms and partials (the prologue overlapped K2's tail)
 
   if (w == NT / 32) {   // ---------------- producer warp ----------------
     // tile corners (full 32x32 tile, even past the map edge, so every lane indexes the window)
@@ -313,9 +314,10 @@ cudaError_t launch_bp(const ei_plan &p, const typename Layout<NMAP>::A *GA, cons
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   dim3 grid((p.N + TILE - 1) / TILE, (p.N + TILE - 1) / TILE, p.S * p.KS);
-  backproject_kernel<NMAP><<<grid, NT + 32, smem, st>>>(GA, GB, p.tab.k3, p.N, p.NA, p.ND, mu, delta,
-                                                        sigma, lambda, o0, o1, o2, out_stride, p.S,
-                                                        p.KS, p.part3, p.done3, p.PADG, p.RpG, fin);
+  e = launch_pdl(backproject_kernel<NMAP>, grid, dim3(NT + 32), smem, st, GA, GB, p.tab.k3, p.N,
+                 p.NA, p.ND, mu, delta, sigma, lambda, o0, o1, o2, out_stride, p.S, p.KS, p.part3,
+                 p.done3, p.PADG, p.RpG, fin);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 

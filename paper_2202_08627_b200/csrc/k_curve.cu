@@ -30,6 +30,7 @@
 #include <algorithm>
 
 #include "ei_common.cuh"
+#include "tma.cuh"
 
 namespace ei {
 namespace {
@@ -153,6 +154,7 @@ __global__ void __maxnreg__(72) curve_kernel(K2Args g) {
   float mk[MPF];                                   // mask positions (first MPF) in registers
 #pragma unroll
   for (int u = 0; u < MPF; ++u) mk[u] = u < g.M ? __ldg(g.mask + u) : 0.f;
+  pdl_wait();   // K1's projections
   // static contiguous split of the items (deterministic, independent of timing)
   const int i0 = (int)(((long long)blockIdx.x * g.items) / gridDim.x);
   const int i1 = (int)(((long long)(blockIdx.x + 1) * g.items) / gridDim.x);
@@ -325,6 +327,7 @@ __global__ void __maxnreg__(72) curve_kernel(K2Args g) {
     }
   }
   cp_wait<0>();
+  pdl_trigger();
   if (MODE == 1) {
     bad = __reduce_add_sync(0xffffffffu, bad);
     mu_cl = __reduce_add_sync(0xffffffffu, mu_cl);
@@ -373,7 +376,8 @@ cudaError_t launch(const ei_plan &p, const float *flat, const float *mask, const
   cudaError_t e = cudaFuncSetAttribute((const void *)curve_kernel<MODE>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  curve_kernel<MODE><<<grid, p.k2.NT, smem, st>>>(g);
+  e = launch_pdl(curve_kernel<MODE>, dim3(grid), dim3(p.k2.NT), smem, st, g);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 

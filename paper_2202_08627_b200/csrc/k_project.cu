@@ -123,6 +123,7 @@ __global__ void __launch_bounds__(NT + 32, 2) project_kernel(ProjArgs args) {
     mbar_fence_init();
   }
   __syncthreads();
+  pdl_wait();   // K0's packed maps (the prologue above overlapped K0's tail)
 
   if (w == NCW) {   // ---------------- producer warp ----------------
     if (lane == 0) {
@@ -235,6 +236,7 @@ __global__ void __launch_bounds__(NT + 32, 2) project_kernel(ProjArgs args) {
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[st]);
   }
+  pdl_trigger();
   if (k >= ND) return;
   const size_t plane = (size_t)args.NA * ND;
   float *out = args.P + ((size_t)rs * args.S + s) * NMAP * plane + k;
@@ -271,7 +273,8 @@ cudaError_t launch(const ei_plan &p, int RS, float *P, cudaStream_t st) {
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   dim3 grid((p.ND + RT - 1) / RT, p.proj.n_groups, p.S * RS);
-  project_kernel<NMAP><<<grid, NT + 32, smem, st>>>(a);
+  e = launch_pdl(project_kernel<NMAP>, grid, dim3(NT + 32), smem, st, a);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 

@@ -49,4 +49,11 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
       : "memory");
 }
 
+// Programmatic dependent launch (PDL): a kernel launched with launch_pdl() may start while its
+// stream predecessor is still running; every thread that reads the predecessor's output first
+// executes pdl_wait() (returns once the predecessor grid has completed and its writes are
+// visible).  pdl_trigger() lets the dependent grid's CTAs be scheduled before this grid exits.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+
 }  // namespace ei

@@ -112,9 +112,11 @@ int ei_cost_grad_drift(const ei_plan *plan, const float *mu, const float *delta,
 
 /* ei_cost_grad with HOST buffers (same shapes and meaning; status is overwritten, not
  * accumulated).  Copies inputs host->device, evaluates, copies cost, gradients and status
- * back, and synchronises `stream` before returning.  Pinned host memory makes the copies
- * asynchronous DMA.  Device staging buffers are allocated by the first call on a plan and
- * kept until ei_plan_destroy (EI_ERR_RESOURCE if that fails). */
+ * back, and synchronises `stream` before returning.  The maps/flat/mask/drift upload runs on
+ * `stream`; the s_exp upload (the bulk of the bytes) runs on an internal copy stream of the
+ * plan and overlaps K0/K1, K2 waiting for it.  Pinned host memory makes the copies
+ * asynchronous DMA.  Device staging buffers, the copy stream and its events are created by the
+ * first call on a plan and kept until ei_plan_destroy (EI_ERR_RESOURCE if that fails). */
 int ei_cost_grad_host(ei_plan *plan, const float *mu, const float *delta, const float *sigma,
                       const float *flat, const float *mask_pos, const float *drift,
                       const float *s_exp, float lambda, double *cost, float *g_mu, float *g_delta,

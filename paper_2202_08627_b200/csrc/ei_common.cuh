@@ -82,6 +82,8 @@ struct ei_plan {
         *h_sexp = nullptr, *h_grad = nullptr;
   double *h_cost = nullptr;
   int32_t *h_status = nullptr;
+  cudaStream_t h_copy = nullptr;            // s_exp upload stream (host path)
+  cudaEvent_t h_ev[2] = {nullptr, nullptr}; // small inputs uploaded / s_exp uploaded
   // launch accounting
   mutable int64_t stats[6] = {0, 0, 0, 0, 0, 0};
   // optional per-kernel timing of ei_cost_grad: 7 events per recorded evaluation

@@ -53,6 +53,12 @@ void free_timing(ei_plan *p) {
 void free_plan(ei_plan *p) {
   if (!p) return;
   free_timing(p);
+  if (p->h_copy) {
+    cudaStreamSynchronize(p->h_copy);
+    cudaStreamDestroy(p->h_copy);
+  }
+  for (cudaEvent_t ev : p->h_ev)
+    if (ev) cudaEventDestroy(ev);
   void *ptrs[] = {p->tab.k1, p->tab.k3, p->proj.groups, p->proj.order, p->proj.win1, p->proj.winRS, p->MA, p->MAT, p->MB,
                   p->MBT, p->M1, p->M1T, p->diag, p->part_mo, p->done3, p->part3, p->P, p->GA, p->GB, p->GA1,
                   p->part_curve, p->part_reg, p->h_maps, p->h_flat, p->h_mask, p->h_drift,
@@ -324,10 +330,12 @@ int ei_forward(const ei_plan *p, const float *mu, const float *delta, const floa
 }
 
 namespace {
+// sexp_ready: if not NULL, an event K2 (the first reader of s_exp) waits for (host path: the
+// s_exp upload runs on a copy stream under K0 and K1)
 int cost_grad_impl(const ei_plan *p, const float *mu, const float *delta, const float *sigma,
                    const float *flat, const float *mask, const float *drift, const float *s_exp,
                    float lambda, double *cost, float *g_mu, float *g_delta, float *g_sigma,
-                   float *g_drift, int32_t *status, void *stream) {
+                   float *g_drift, int32_t *status, void *stream, cudaEvent_t sexp_ready = nullptr) {
   if (!p || !mu || !delta || !sigma || !flat || !mask || !s_exp || !cost || !g_mu || !g_delta ||
       !g_sigma || !status)
     return EI_ERR_NULL;
@@ -342,6 +350,7 @@ int cost_grad_impl(const ei_plan *p, const float *mu, const float *delta, const 
   mark(1);
   if (e == cudaSuccess) e = ei::launch_project3(*p, p->P, p->proj.RS, st);          // K1
   mark(2);
+  if (e == cudaSuccess && sexp_ready) e = cudaStreamWaitEvent(st, sexp_ready, 0);
   if (e == cudaSuccess) e = ei::launch_curve_cost_grad(*p, flat, mask, drift, s_exp, status, st);  // K2
   mark(3);
   ei::Finalize fin{cost, g_drift};
@@ -408,10 +417,22 @@ int ei_cost_grad_host(ei_plan *p, const float *mu, const float *delta, const flo
       return EI_ERR_RESOURCE;
     }
   }
+  if (!p->h_copy) {   // copy stream + events for the s_exp upload (created once per plan)
+    cudaError_t e = cudaStreamCreateWithFlags(&p->h_copy, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->h_ev[0], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->h_ev[1], cudaEventDisableTiming);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return EI_ERR_RESOURCE;
+    }
+  }
   cudaStream_t st = (cudaStream_t)stream;
   cudaError_t e = cudaSuccess;
   auto A = [&](cudaError_t r) { if (e == cudaSuccess) e = r; };
   const cudaMemcpyKind H2D = cudaMemcpyHostToDevice, D2H = cudaMemcpyDeviceToHost;
+  // the small inputs first on the compute stream, so K0/K1 start after ~1/6 of the bytes; the
+  // s_exp upload (the bulk: M values per ray) follows on the copy stream, overlapping K0 and K1,
+  // and K2 waits for it (event h_ev[1])
   float *dmu = p->h_maps, *ddl = p->h_maps + S * NN, *dsg = p->h_maps + 2 * S * NN;
   A(cudaMemcpyAsync(dmu, mu, sizeof(float) * S * NN, H2D, st));
   A(cudaMemcpyAsync(ddl, delta, sizeof(float) * S * NN, H2D, st));
@@ -419,12 +440,16 @@ int ei_cost_grad_host(ei_plan *p, const float *mu, const float *delta, const flo
   A(cudaMemcpyAsync(p->h_flat, flat, sizeof(float) * S * 3 * ND, H2D, st));
   A(cudaMemcpyAsync(p->h_mask, mask, sizeof(float) * M, H2D, st));
   if (drift) A(cudaMemcpyAsync(p->h_drift, drift, sizeof(float) * NA, H2D, st));
-  A(cudaMemcpyAsync(p->h_sexp, s_exp, sizeof(float) * nsexp, H2D, st));
   A(cudaMemsetAsync(p->h_status, 0, sizeof(int32_t) * 4, st));
+  A(cudaEventRecord(p->h_ev[0], st));
+  A(cudaStreamWaitEvent(p->h_copy, p->h_ev[0], 0));
+  A(cudaMemcpyAsync(p->h_sexp, s_exp, sizeof(float) * nsexp, H2D, p->h_copy));
+  A(cudaEventRecord(p->h_ev[1], p->h_copy));
   if (e != cudaSuccess) return EI_ERR_CUDA;
   float *gm = p->h_grad, *gd = p->h_grad + S * NN, *gs = p->h_grad + 2 * S * NN;
-  int rc = ei_cost_grad(p, dmu, ddl, dsg, p->h_flat, p->h_mask, drift ? p->h_drift : nullptr,
-                        p->h_sexp, lambda, p->h_cost, gm, gd, gs, p->h_status, stream);
+  int rc = cost_grad_impl(p, dmu, ddl, dsg, p->h_flat, p->h_mask, drift ? p->h_drift : nullptr,
+                          p->h_sexp, lambda, p->h_cost, gm, gd, gs, nullptr, p->h_status, stream,
+                          p->h_ev[1]);
   if (rc) return rc;
   A(cudaMemcpyAsync(cost, p->h_cost, sizeof(double) * S, D2H, st));
   A(cudaMemcpyAsync(g_mu, gm, sizeof(float) * S * NN, D2H, st));

@@ -354,6 +354,93 @@ void ora_cost_grad(int n, int n_angles, int n_det, int n_mask, double dx, double
                    s_exp, lambda, cost, g_mu, g_delta, g_sigma, status, NULL);
 }
 
+/* ---------------------------------------------------------------------------------
+ * NEXT-3: the paper's own single-map model, eq. 4 with m_r == 0, under the
+ * homogeneity assumption mu = gamma^-1 delta = h, cost eq. 5 with the L2 term on h:
+ *
+ *   P     = R_J[h]
+ *   T     = exp(-clamp(P, -50, 50))                      (R12)
+ *   u     = m - c - m_o(theta) - z gamma D P             (eq. 4; R10 sign)
+ *   s_mod = T * f(t, u + c) = T * A * exp(-u^2 / (2 w^2))   (Gaussian flat IC, R2; no scattering)
+ *   S     = sum (s_mod - s_exp)^2 + lambda sum h^2
+ *   dS/dP = -2 sum_m r s  [0 where clamped]  +  z gamma D^T ( 2 sum_m r s u / w^2 )
+ *   grad  = R_J^T dS/dP + 2 lambda h
+ *
+ * Written out directly from eq. 4 (its own loops, not via the three-map functions above).
+ * flat [3][n_det] = (A, c, w); s_exp [n_angles][n_mask][n_det]; grad [n][n]; s_mod (or NULL)
+ * [n_angles][n_mask][n_det]; status[0] += non-finite inputs, status[1] += clamp hits.
+ * ------------------------------------------------------------------------------- */
+void ora_cost_grad_h(int n, int n_angles, int n_det, int n_mask, double dx, double du, double z,
+                     double gamma, const double *angles, const float *h, const float *flat,
+                     const float *mask, const float *drift, const float *s_exp, double lambda,
+                     double *cost, double *grad, double *s_mod, int64_t *status)
+{
+    const size_t nn = (size_t)n * n, ns = (size_t)n_angles * n_det;
+    if (s_exp)
+        status[0] += count_nonfinite(h, nn) + count_nonfinite(flat, (size_t)3 * n_det) +
+                     count_nonfinite(mask, n_mask) + (drift ? count_nonfinite(drift, n_angles) : 0) +
+                     count_nonfinite(s_exp, ns * n_mask);
+    double *hd = widen(h, nn);
+    double *P = malloc(sizeof(double) * ns), *G = malloc(sizeof(double) * ns);
+    double *rowcost = calloc(n_angles, sizeof(double));
+    ora_project(n, n_angles, n_det, dx, du, angles, hd, P);
+    int64_t clamps = 0;
+#pragma omp parallel for schedule(dynamic, 1) reduction(+ : clamps)
+    for (int a = 0; a < n_angles; ++a) {
+        const double *Pa = P + (size_t)a * n_det;
+        double *dP = malloc(sizeof(double) * n_det), *gD = malloc(sizeof(double) * n_det),
+               *gT = malloc(sizeof(double) * n_det), *y = malloc(sizeof(double) * n_det);
+        ora_diff_t(n_det, du, Pa, dP);
+        const double mo = drift ? (double)drift[a] : 0.0;
+        double Sa = 0.0;
+        for (int k = 0; k < n_det; ++k) {
+            double pk = Pa[k];
+            int cl = 0;
+            if (pk > 50.0) { pk = 50.0; cl = 1; }
+            if (pk < -50.0) { pk = -50.0; cl = 1; }
+            clamps += cl;
+            const double T = exp(-pk);
+            const double A = flat[k], c = flat[n_det + k], w = flat[2 * n_det + k];
+            double g_t = 0.0, g_d = 0.0;
+            for (int m = 0; m < n_mask; ++m) {
+                const double u = (double)mask[m] - c - mo - z * gamma * dP[k];
+                const double s = T * A * exp(-u * u / (2.0 * w * w));
+                if (s_mod) s_mod[((size_t)a * n_mask + m) * n_det + k] = s;
+                if (s_exp) {
+                    const double r = s - (double)s_exp[((size_t)a * n_mask + m) * n_det + k];
+                    Sa += r * r;
+                    g_t += -2.0 * r * s;                    /* d/dP through T: ds/dP = -s   */
+                    g_d += 2.0 * r * s * u / (w * w);       /* d/dShift: ds/dShift = s u/w^2 */
+                }
+            }
+            gT[k] = cl ? 0.0 : g_t;
+            gD[k] = g_d;
+        }
+        if (s_exp) {
+            ora_diff_t_adjoint(n_det, du, gD, y);        /* shift = z gamma D P */
+            for (int k = 0; k < n_det; ++k) G[(size_t)a * n_det + k] = gT[k] + z * gamma * y[k];
+            rowcost[a] = Sa;
+        }
+        free(dP); free(gD); free(gT); free(y);
+    }
+    if (s_exp) {
+        status[1] += clamps;
+        double S = 0.0;
+        for (int a = 0; a < n_angles; ++a) S += rowcost[a];
+        ora_backproject(n, n_angles, n_det, dx, du, angles, G, grad);
+        if (lambda > 0.0) {
+            double reg = 0.0;
+            for (size_t q = 0; q < nn; ++q) {
+                reg += hd[q] * hd[q];
+                grad[q] += 2.0 * lambda * hd[q];
+            }
+            S += lambda * reg;
+        }
+        *cost = S;
+    }
+    free(hd); free(P); free(G); free(rowcost);
+}
+
 int ora_num_threads(void)
 {
 #ifdef _OPENMP

@@ -13,6 +13,7 @@ Functions (fp64 unless noted; slices are independent):
   curve_row(...)                                a2-a4 for one detector row (eq. 2, 4, 5)
   forward(geom, angles, mu, delta, sigma, flat, mask, drift)        -> s_mod [S][Na][M][Nd]
   cost_grad(geom, angles, ..., s_exp, lam)      -> cost[S], g_mu, g_delta, g_sigma, status
+  cost_grad_h(angles, h, gamma, ...)            NEXT-3: the paper's single-map model, eq. 4
 """
 from __future__ import annotations
 
@@ -59,6 +60,7 @@ def lib():
         L.ora_cost_grad.argtypes = [i, i, i, i, d, d, d, _dp, _fp, _fp, _fp, _fp, _fp, vp, _fp, d,
                                     vp, _dp, _dp, _dp, _ip]
         L.ora_cost_grad2.argtypes = L.ora_cost_grad.argtypes + [vp]
+        L.ora_cost_grad_h.argtypes = [i, i, i, i, d, d, d, d, _dp, _fp, _fp, _fp, vp, vp, d, vp, vp, vp, _ip]
         L.ora_num_threads.restype = i
         _lib = L
     return _lib
@@ -182,3 +184,33 @@ def cost_grad(angles, mu, delta, sigma, flat, mask, drift, s_exp, lam=0.0, dx=1.
     if want_drift:
         return cost, g[0], g[1], g[2], status, gdr
     return cost, g[0], g[1], g[2], status
+
+
+def cost_grad_h(angles, h, gamma, flat, mask, drift, s_exp=None, lam=0.0, dx=1.0, du=1.0, z=1.0,
+                want_smod=False):
+    """The paper's single-map model (eq. 4, mu = gamma^-1 delta = h): per-slice cost (fp64),
+    gradient map (fp64) and status [2] = (non-finite inputs, clamp hits); s_exp=None: forward only
+    (returns s_mod [S][Na][M][Nd]).  With want_smod the s_mod array is appended."""
+    angles = _d(angles)
+    h, flat, mask = _f(h), _f(flat), _f(mask)
+    S, n, _ = h.shape
+    na = len(angles)
+    m = len(mask)
+    nd = flat.shape[-1]
+    dr = None if drift is None else _f(drift)
+    se = None if s_exp is None else _f(s_exp)
+    cost = np.zeros(S)
+    grad = np.zeros((S, n, n))
+    smod = np.zeros((S, na, m, nd))
+    status = np.zeros(2, np.int64)
+    for s in range(S):
+        c = np.zeros(1)
+        g = np.zeros((n, n))
+        sm = np.zeros((na, m, nd))
+        lib().ora_cost_grad_h(n, na, nd, m, dx, du, z, float(gamma), angles, h[s], flat[s], mask,
+                              _ptr(dr), None if se is None else _ptr(se[s]), float(lam), _ptr(c),
+                              _ptr(g), _ptr(sm), status)
+        cost[s], grad[s], smod[s] = c[0], g, sm
+    if s_exp is None:
+        return smod
+    return (cost, grad, status, smod) if want_smod else (cost, grad, status)

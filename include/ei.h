@@ -110,6 +110,24 @@ int ei_cost_grad_drift(const ei_plan *plan, const float *mu, const float *delta,
                        const float *s_exp, float lambda, double *cost, float *g_mu, float *g_delta,
                        float *g_sigma, float *g_drift, int32_t *status, void *stream);
 
+/* The paper's own single-map model: eq. 4 with
+ * m_r = 0 under the homogeneity assumption mu = gamma^-1 delta = h,
+ * so one projection and one adjoint per evaluation instead of three:
+ *   s_mod = exp(-R[h]) * f(t, m - m_o(theta) - z gamma dR[h]/dt)   (no scattering: W = w)
+ *   S_s   = sum (s_mod - s_exp)^2 + lambda sum h^2                  (eq. 5; paper gamma = 5,
+ *                                                                     lambda = 1e-2)
+ * h [S][N][N] device; gamma finite (EI_ERR_DOMAIN otherwise); the plan's geometry (z, pixel,
+ * det_pitch, M) as for the three-map model; flat, mask_pos, drift, s_exp as for ei_cost_grad.
+ * ei_forward_h -> s_mod [S][N_theta][M][N_d].
+ * ei_cost_grad_h -> cost [S] fp64, g_h [S][N][N] (overwritten), g_drift [S][N_theta] or NULL
+ * (dS_s/dm_o(theta), as ei_cost_grad_drift), status [4] accumulated: [0] non-finite inputs,
+ * [1] P_h clamp hits (R12), [2] 0, [3] 0.  Same conventions as ei_cost_grad otherwise. */
+int ei_forward_h(const ei_plan *plan, const float *h, float gamma, const float *flat,
+                 const float *mask_pos, const float *drift, float *s_mod, void *stream);
+int ei_cost_grad_h(const ei_plan *plan, const float *h, float gamma, const float *flat,
+                   const float *mask_pos, const float *drift, const float *s_exp, float lambda,
+                   double *cost, float *g_h, float *g_drift, int32_t *status, void *stream);
+
 /* ei_cost_grad with HOST buffers (same shapes and meaning; status is overwritten, not
  * accumulated).  Copies inputs host->device, evaluates, copies cost, gradients and status
  * back, and synchronises `stream` before returning.  The maps/flat/mask/drift upload runs on

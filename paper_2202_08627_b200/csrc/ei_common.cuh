@@ -120,12 +120,13 @@ struct SmallCheck {          // flat/mask/drift non-finite scan folded into K0
 cudaError_t launch_pack3(const ei_plan &p, const float *mu, const float *delta, const float *sigma,
                          size_t in_stride, bool want_reg, int32_t *status, SmallCheck chk,
                          cudaStream_t st);
-cudaError_t launch_pack1(const ei_plan &p, const float *map, cudaStream_t st);
+cudaError_t launch_pack1(const ei_plan &p, const float *map, cudaStream_t st, bool want_reg = false,
+                         int32_t *status = nullptr, SmallCheck chk = SmallCheck{});
 int reg_blocks(int N);
 cudaError_t launch_pack_sino(const ei_plan &p, const float *sino, int n_maps, cudaStream_t st);
 // K1 (k_project.cu)
 cudaError_t launch_project3(const ei_plan &p, float *P, int RS, cudaStream_t st);
-cudaError_t launch_project1(const ei_plan &p, float *P, cudaStream_t st);
+cudaError_t launch_project1(const ei_plan &p, float *P, cudaStream_t st, int RS = 1);
 // K2 (k_curve.cu)
 int plan_curve(ei_plan &p);
 cudaError_t launch_curve_forward(const ei_plan &p, const float *flat, const float *mask,
@@ -133,6 +134,11 @@ cudaError_t launch_curve_forward(const ei_plan &p, const float *flat, const floa
 cudaError_t launch_curve_cost_grad(const ei_plan &p, const float *flat, const float *mask,
                                    const float *drift, const float *s_exp, int32_t *status,
                                    cudaStream_t st);
+cudaError_t launch_curve_forward_h(const ei_plan &p, float gamma, const float *flat, const float *mask,
+                                   const float *drift, float *s_mod, cudaStream_t st);
+cudaError_t launch_curve_cost_grad_h(const ei_plan &p, float gamma, const float *flat,
+                                     const float *mask, const float *drift, const float *s_exp,
+                                     int32_t *status, cudaStream_t st);
 // K3 (k_backproject.cu); with `fin` set, the CTAs (0, 0, s) also run the fused K4 finalize:
 // cost[s] = fixed-order sum of K2's per-segment partials + lambda * K0's sum x^2 partials, and
 // g_drift[s][theta] = sum of K2's per-segment dS/dm_o partials (if g_drift != NULL)
@@ -144,7 +150,8 @@ cudaError_t launch_backproject3(const ei_plan &p, const float *mu, const float *
                                 const float *sigma, float lambda, float *g_mu, float *g_delta,
                                 float *g_sigma, size_t out_stride, const Finalize *fin,
                                 cudaStream_t st);
-cudaError_t launch_backproject1(const ei_plan &p, float *map, cudaStream_t st);
+cudaError_t launch_backproject1(const ei_plan &p, float *map, cudaStream_t st, const float *h = nullptr,
+                                float lambda = 0.f, const Finalize *fin = nullptr);
 int bp_tiles(int N);
 int bp_pad();
 int bp_chunks(int NA);

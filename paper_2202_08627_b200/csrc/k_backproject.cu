@@ -286,6 +286,7 @@ __global__ void __launch_bounds__(NT + 32, 3) backproject_kernel(
       o1[oo] = vd;
       o2[oo] = vs;
     } else {
+      if (mu) vm = fmaf(2.f * lambda, __ldg(mu + (size_t)s * NN + p), vm);   // single-map cost path
       o0[oo] = vm;
     }
   }
@@ -335,9 +336,10 @@ cudaError_t launch_backproject3(const ei_plan &p, const float *mu, const float *
                       st);
 }
 
-cudaError_t launch_backproject1(const ei_plan &p, float *map, cudaStream_t st) {
-  return launch_bp<1>(p, p.GA1, nullptr, nullptr, nullptr, nullptr, 0.f, map, nullptr, nullptr,
-                      (size_t)p.N * p.N, nullptr, st);
+cudaError_t launch_backproject1(const ei_plan &p, float *map, cudaStream_t st, const float *h,
+                                float lambda, const Finalize *fin) {
+  return launch_bp<1>(p, p.GA1, nullptr, h, nullptr, nullptr, lambda, map, nullptr, nullptr,
+                      (size_t)p.N * p.N, fin, st);
 }
 
 }  // namespace ei

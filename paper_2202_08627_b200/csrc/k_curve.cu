@@ -63,10 +63,12 @@ struct K2Args {
   size_t rstride;            // S * 3 * NA * ND
   const float *flat, *mask, *drift, *s_exp;
   int NA, ND, M, nseg, W;    // W = core positions per segment (<= blockDim - 4)
-  float z, inv_du;
+  int nmap;                  // maps per slice in P: 3 (mu, delta, sigma) or 1 (h, NEXT-3)
+  float zs, inv_du;          // shift factor: z (three-map model) or z gamma (single-map model)
   float *s_mod;              // MODE 0
   float4 *GA;                // MODE 1: pair-layout gradient sinograms (K3 input)
   float2 *GB;
+  float2 *GA1;               // MODE 2: pair-layout gradient sinogram of h
   int PADG, RpG;
   const float4 *k3;          // per-angle table, .w = Joseph weight dx/|c_dom|
   float *part_cost, *part_mo;    // [S * NA * nseg * nw] per-warp partials
@@ -109,7 +111,7 @@ struct Cursor {
     k = q.seg * g.W - 2 + t;
     valid = k >= 0 && k < g.ND;
     const int plane = g.NA * g.ND;                                 // < 2^30 (plan)
-    pm = g.P + (size_t)q.s * 3 * plane + (q.a * g.ND + k);
+    pm = g.P + (size_t)q.s * g.nmap * plane + (q.a * g.ND + k);
     se = g.s_exp ? g.s_exp + ((size_t)(q.s * g.NA + q.a) * g.M) * g.ND + k : nullptr;
   }
   __device__ __forceinline__ void next_row(const K2Args &g) {     // a -> a + 1, same (s, seg)
@@ -120,15 +122,28 @@ struct Cursor {
 
 // issue this thread's loads of the cursor's item as 4-byte async copies into its private prefetch
 // slots (only this thread reads them: cp.async.wait_group alone orders them — no barrier)
+// K2 modes: 0 forward (three maps), 1 cost + gradient (three maps), 2 cost + gradient of the
+// paper's single-map model h (NEXT-3: P_mu = P_h, shift z gamma D P_h, no scattering), 3 forward h
+template <int MODE>
+struct Mode {
+  static constexpr bool cost = MODE == 1 || MODE == 2;
+  static constexpr bool h = MODE >= 2;
+};
+
 template <int MODE>
 __device__ __forceinline__ void load_item(const K2Args &g, const Cursor &c, uint32_t slot, int plane,
                                           int dl, int dr) {
   if (!c.valid) return;
   cp4(slot, c.pm);
-  cp4(slot + 4, c.pm + plane + dl);
-  cp4(slot + 8, c.pm + plane + dr);
-  cp4(slot + 12, c.pm + 2 * plane);
-  if (MODE == 1) {
+  if (Mode<MODE>::h) {                 // P_h at k, k-1, k+1
+    cp4(slot + 4, c.pm + dl);
+    cp4(slot + 8, c.pm + dr);
+  } else {                             // P_mu, P_delta(k-1), P_delta(k+1), P_sigma
+    cp4(slot + 4, c.pm + plane + dl);
+    cp4(slot + 8, c.pm + plane + dr);
+    cp4(slot + 12, c.pm + 2 * plane);
+  }
+  if (Mode<MODE>::cost) {
     const float *se = c.se;
 #pragma unroll
     for (int u = 0; u < MPF; ++u) {
@@ -213,17 +228,18 @@ __global__ void __maxnreg__(72) curve_kernel(K2Args g) {
     const int row = s * g.NA + a;
     float gm = 0.f, gd = 0.f, gs = 0.f, cost = 0.f;
     if (valid) {
-      float pm = cur[0], pdl = cur[1], pdr = cur[2], ps = cur[3];
+      float pm = cur[0], pdl = cur[1], pdr = cur[2], ps = Mode<MODE>::h ? 0.f : cur[3];
       const int kl = k == 0 ? 0 : k - 1, kr = k == ND - 1 ? ND - 1 : k + 1;
       if (g.RS > 1) {   // fixed-order sum of the row-split partials (small problems, L2-resident)
         const int plane = g.NA * ND;
-        const float *Pm = g.P + (size_t)s * 3 * plane + a * ND;
+        const float *Pm = g.P + (size_t)s * g.nmap * plane + a * ND;
+        const int pd = Mode<MODE>::h ? 0 : plane;   // P_delta plane (the h plane itself)
         for (int r = 1; r < g.RS; ++r) {
           const float *b = Pm + r * g.rstride;
           pm += __ldg(b + k);
-          pdl += __ldg(b + plane + kl);
-          pdr += __ldg(b + plane + kr);
-          ps += __ldg(b + 2 * plane + k);
+          pdl += __ldg(b + pd + kl);
+          pdr += __ldg(b + pd + kr);
+          if (!Mode<MODE>::h) ps += __ldg(b + 2 * plane + k);
         }
       }
       const float dP = (pdr - pdl) * ((kr - kl == 2 ? 0.5f : 1.f) * g.inv_du);
@@ -241,7 +257,7 @@ __global__ void __maxnreg__(72) curve_kernel(K2Args g) {
       // gradient gate at C3's noise level: measured 1.36e-3.)
       const float c2 = -0.5f * LOG2E * invW2;
       const float mo = g.drift ? __ldg(g.drift + a) : 0.f;
-      const float base = fc + mo + g.z * dP;
+      const float base = fc + mo + g.zs * dP;
       if (core) {
         mu_cl += mc;
         w2_cl += wc;
@@ -254,7 +270,7 @@ __global__ void __maxnreg__(72) curve_kernel(K2Args g) {
         const float du_ = mpos - base;
         const float u2 = du_ * du_;
         const float sv = amp * ex2(c2 * u2);
-        if (MODE == 0) {
+        if (!Mode<MODE>::cost) {
           if (core) g.s_mod[rowb + (size_t)m * ND] = sv;
         } else {
           const float r = sv - se;
@@ -267,18 +283,18 @@ __global__ void __maxnreg__(72) curve_kernel(K2Args g) {
       };
 #pragma unroll
       for (int u = 0; u < MPF; ++u)
-        if (u < g.M) term(mk[u], u, MODE == 1 ? cur[4 + u] : 0.f);   // prefetched s_exp
-      for (int m = MPF; m < g.M; ++m)                                          // M > MPF
-        term(__ldg(g.mask + m), m, MODE == 1 ? __ldcs(g.s_exp + rowb + (size_t)m * ND) : 0.f);
+        if (u < g.M) term(mk[u], u, Mode<MODE>::cost ? cur[4 + u] : 0.f);   // prefetched s_exp
+      for (int m = MPF; m < g.M; ++m)                                                // M > MPF
+        term(__ldg(g.mask + m), m, Mode<MODE>::cost ? __ldcs(g.s_exp + rowb + (size_t)m * ND) : 0.f);
       // a non-finite s_exp makes the cost non-finite; only then count the elements (rare path)
-      if (MODE == 1 && core && !isfinite(cost))
+      if (Mode<MODE>::cost && core && !isfinite(cost))
         for (int m = 0; m < g.M; ++m) bad += !isfinite(m < MPF ? cur[4 + m] : g.s_exp[rowb + (size_t)m * ND]);
       gm = mc ? 0.f : -2.f * gmm;
       const float gss = fmaf(-W2, gmm, gq);   // sum r s (u^2 - W^2)
       gs = wc ? 0.f : gss * invW2 * invW2;
       gd = 2.f * gdd * invW2;
     }
-    if (MODE == 1) {
+    if (Mode<MODE>::cost) {
       sgD[buf][t] = gd;
       sgm[buf][t] = gm;
       sgs[buf][t] = gs;
@@ -296,7 +312,7 @@ __global__ void __maxnreg__(72) curve_kernel(K2Args g) {
         const int e = seg * g.W + t;       // pair entry written by this thread
         if (e < ND) {
           const float *D = sgD[buf] + (t + 2 - e);   // D[k] = g_Delta at detector k (window)
-          const float zh = 0.5f * g.z * g.inv_du;
+          const float zh = 0.5f * g.zs * g.inv_du;
           // g_delta = z D^T g_Delta, D^T written out from the rows of D (a2):
           //   y[j] = [j==0](-g0) + [j==1](g0) + [j==ND-2](-g_{ND-1}) + [j==ND-1](g_{ND-1})
           //        + 1/2 g_{j-1} [1 <= j-1 <= ND-2] - 1/2 g_{j+1} [1 <= j+1 <= ND-2]   (all / du)
@@ -309,18 +325,23 @@ __global__ void __maxnreg__(72) curve_kernel(K2Args g) {
             if (j == ND - 1) y += D[ND - 1];
             if (j - 1 >= 1 && j - 1 <= ND - 2) y += 0.5f * D[j - 1];
             if (j + 1 >= 1 && j + 1 <= ND - 2) y -= 0.5f * D[j + 1];
-            return g.z * g.inv_du * y;
+            return g.zs * g.inv_du * y;
           };
           const float sc = __ldg(g.k3 + a).w;
           const size_t rb = (size_t)row * g.RpG + g.PADG;
           const float m1 = sgm[buf][t + 2], s1 = sgs[buf][t + 2], d1 = gdelta(e);
           const float m0 = e >= 1 ? sgm[buf][t + 1] : 0.f, s0 = e >= 1 ? sgs[buf][t + 1] : 0.f;
           const float d0 = e >= 1 ? gdelta(e - 1) : 0.f;
-          g.GA[rb + e] = make_float4(sc * m0, sc * m1, sc * d0, sc * d1);
-          g.GB[rb + e] = make_float2(sc * s0, sc * s1);
-          if (e == ND - 1) {   // closing entry e = ND: (g[ND-1], 0)
-            g.GA[rb + ND] = make_float4(sc * m1, 0.f, sc * d1, 0.f);
-            g.GB[rb + ND] = make_float2(sc * s1, 0.f);
+          if (Mode<MODE>::h) {   // dS/dP_h = g_mu + z gamma D^T g_Delta (eq. 4 chain rule)
+            g.GA1[rb + e] = make_float2(sc * (m0 + d0), sc * (m1 + d1));
+            if (e == ND - 1) g.GA1[rb + ND] = make_float2(sc * (m1 + d1), 0.f);
+          } else {
+            g.GA[rb + e] = make_float4(sc * m0, sc * m1, sc * d0, sc * d1);
+            g.GB[rb + e] = make_float2(sc * s0, sc * s1);
+            if (e == ND - 1) {   // closing entry e = ND: (g[ND-1], 0)
+              g.GA[rb + ND] = make_float4(sc * m1, 0.f, sc * d1, 0.f);
+              g.GB[rb + ND] = make_float2(sc * s1, 0.f);
+            }
           }
         }
       }
@@ -328,7 +349,7 @@ __global__ void __maxnreg__(72) curve_kernel(K2Args g) {
   }
   cp_wait<0>();
   pdl_trigger();
-  if (MODE == 1) {
+  if (Mode<MODE>::cost) {
     bad = __reduce_add_sync(0xffffffffu, bad);
     mu_cl = __reduce_add_sync(0xffffffffu, mu_cl);
     w2_cl = __reduce_add_sync(0xffffffffu, w2_cl);
@@ -344,12 +365,13 @@ static size_t k2_smem(int NT) { return sizeof(float) * (size_t)NSTAGE * NQ * NT;
 
 template <int MODE>
 cudaError_t launch(const ei_plan &p, const float *flat, const float *mask, const float *drift,
-                   const float *s_exp, float *s_mod, int32_t *status, cudaStream_t st) {
+                   const float *s_exp, float *s_mod, int32_t *status, float gamma, cudaStream_t st) {
   K2Args g;
   g.P = p.P;
   g.RS = p.proj.RS;
   g.S = p.S;
-  g.rstride = (size_t)p.S * 3 * p.NA * p.ND;
+  g.nmap = Mode<MODE>::h ? 1 : 3;
+  g.rstride = (size_t)p.S * g.nmap * p.NA * p.ND;
   g.flat = flat;
   g.mask = mask;
   g.drift = drift;
@@ -359,11 +381,12 @@ cudaError_t launch(const ei_plan &p, const float *flat, const float *mask, const
   g.M = p.M;
   g.nseg = p.k2.nseg;
   g.W = p.k2.W;
-  g.z = (float)p.g.z;
+  g.zs = (float)(p.g.z * (Mode<MODE>::h ? (double)gamma : 1.0));
   g.inv_du = (float)(1.0 / p.g.det_pitch);
   g.s_mod = s_mod;
   g.GA = p.GA;
   g.GB = p.GB;
+  g.GA1 = p.GA1;
   g.PADG = p.PADG;
   g.RpG = p.RpG;
   g.k3 = p.tab.k3;
@@ -408,13 +431,24 @@ int plan_curve(ei_plan &p) {
 
 cudaError_t launch_curve_forward(const ei_plan &p, const float *flat, const float *mask,
                                  const float *drift, float *s_mod, cudaStream_t st) {
-  return launch<0>(p, flat, mask, drift, nullptr, s_mod, nullptr, st);
+  return launch<0>(p, flat, mask, drift, nullptr, s_mod, nullptr, 0.f, st);
 }
 
 cudaError_t launch_curve_cost_grad(const ei_plan &p, const float *flat, const float *mask,
                                    const float *drift, const float *s_exp, int32_t *status,
                                    cudaStream_t st) {
-  return launch<1>(p, flat, mask, drift, s_exp, nullptr, status, st);
+  return launch<1>(p, flat, mask, drift, s_exp, nullptr, status, 0.f, st);
+}
+
+cudaError_t launch_curve_forward_h(const ei_plan &p, float gamma, const float *flat, const float *mask,
+                                   const float *drift, float *s_mod, cudaStream_t st) {
+  return launch<3>(p, flat, mask, drift, nullptr, s_mod, nullptr, gamma, st);
+}
+
+cudaError_t launch_curve_cost_grad_h(const ei_plan &p, float gamma, const float *flat,
+                                     const float *mask, const float *drift, const float *s_exp,
+                                     int32_t *status, cudaStream_t st) {
+  return launch<2>(p, flat, mask, drift, s_exp, nullptr, status, gamma, st);
 }
 
 }  // namespace ei

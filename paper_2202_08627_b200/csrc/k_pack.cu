@@ -157,13 +157,14 @@ cudaError_t launch_pack3(const ei_plan &p, const float *mu, const float *delta, 
   return cudaGetLastError();
 }
 
-cudaError_t launch_pack1(const ei_plan &p, const float *map, cudaStream_t st) {
+cudaError_t launch_pack1(const ei_plan &p, const float *map, cudaStream_t st, bool want_reg,
+                         int32_t *status, SmallCheck chk) {
   const int nt = (p.N + 1 + T - 1) / T;
   dim3 grid(nt, nt, p.S), block(T, T);
   PairOut<1> o{p.M1, p.M1T};
   pack_pairs_kernel<1><<<grid, block, 0, st>>>(map, nullptr, nullptr, (size_t)p.N * p.N, p.N, o,
-                                               nullptr, nullptr, SmallCheck{}, 0, 0, 0, p.proj.PAD,
-                                               p.proj.Rp);
+                                               want_reg ? p.part_reg : nullptr, status, chk,
+                                               p.S * 3 * p.ND, p.M, p.NA, p.proj.PAD, p.proj.Rp);
   return cudaGetLastError();
 }
 

@@ -470,8 +470,8 @@ cudaError_t launch_project3(const ei_plan &p, float *P, int RS, cudaStream_t st)
   return launch<3>(p, RS, P, st);
 }
 
-cudaError_t launch_project1(const ei_plan &p, float *P, cudaStream_t st) {
-  return launch<1>(p, 1, P, st);
+cudaError_t launch_project1(const ei_plan &p, float *P, cudaStream_t st, int RS) {
+  return launch<1>(p, RS, P, st);
 }
 
 }  // namespace ei

@@ -24,7 +24,7 @@ _lib = ctypes.CDLL(LIB_PATH)
 
 EI_OK, EI_ERR_NULL, EI_ERR_SHAPE, EI_ERR_DOMAIN, EI_ERR_RESOURCE, EI_ERR_CUDA = range(6)
 SYMBOLS = ("ei_plan_create", "ei_plan_destroy", "ei_project", "ei_backproject", "ei_forward",
-           "ei_cost_grad", "ei_cost_grad_drift", "ei_cost_grad_host", "ei_plan_stats", "ei_plan_set_timing",
+           "ei_cost_grad", "ei_cost_grad_drift", "ei_forward_h", "ei_cost_grad_h", "ei_cost_grad_host", "ei_plan_stats", "ei_plan_set_timing",
            "ei_plan_read_timing", "ei_plan_info", "ei_error_string", "ei_version")
 KERNELS = ("K0_pack", "K1_project", "K2_curve", "K3_backproject", "unused4", "unused5")
 
@@ -44,6 +44,8 @@ _lib.ei_backproject.argtypes = [_vp, _vp, _i, _vp, _vp]
 _lib.ei_forward.argtypes = [_vp] + [_vp] * 7 + [_vp]
 _lib.ei_cost_grad.argtypes = [_vp] + [_vp] * 7 + [_f] + [_vp] * 5 + [_vp]
 _lib.ei_cost_grad_drift.argtypes = [_vp] + [_vp] * 7 + [_f] + [_vp] * 6 + [_vp]
+_lib.ei_forward_h.argtypes = [_vp, _vp, _f] + [_vp] * 4 + [_vp]
+_lib.ei_cost_grad_h.argtypes = [_vp, _vp, _f] + [_vp] * 4 + [_f] + [_vp] * 4 + [_vp]
 _lib.ei_cost_grad_host.argtypes = [_vp] + [_vp] * 7 + [_f] + [_vp] * 5 + [_vp]
 _lib.ei_plan_stats.argtypes = [_vp, _vp]
 _lib.ei_plan_set_timing.argtypes = [_vp, _i]
@@ -213,6 +215,28 @@ def ei_cost_grad_drift(plan: Plan, mu, delta, sigma, flat, mask_pos, drift, s_ex
         _dev(g_mu, (S, N, N), "g_mu"), _dev(g_delta, (S, N, N), "g_delta"),
         _dev(g_sigma, (S, N, N), "g_sigma"), _dev(g_drift, (S, NA), "g_drift"),
         _dev(status, (4,), "status", torch.int32), _stream(stream)), "ei_cost_grad_drift")
+
+
+def ei_forward_h(plan: Plan, h, gamma: float, flat, mask_pos, drift, s_mod, stream=None):
+    """Single-map model (NEXT-3, eq. 4 with mu = gamma^-1 delta = h): s_mod [S][N_theta][M][N_d]."""
+    S, N, NA, ND, M = plan.shape
+    _check(_lib.ei_forward_h(plan.handle, _dev(h, (S, N, N), "h"), float(gamma),
+                             _dev(flat, (S, 3, ND), "flat"), _dev(mask_pos, (M,), "mask_pos"),
+                             None if drift is None else _dev(drift, (NA,), "drift"),
+                             _dev(s_mod, (S, NA, M, ND), "s_mod"), _stream(stream)), "ei_forward_h")
+
+
+def ei_cost_grad_h(plan: Plan, h, gamma: float, flat, mask_pos, drift, s_exp, lam: float, cost, g_h,
+                   g_drift, status, stream=None):
+    """Single-map model (NEXT-3): cost [S] fp64, g_h [S][N][N], optional g_drift [S][N_theta]."""
+    import torch
+    S, N, NA, ND, M = plan.shape
+    _check(_lib.ei_cost_grad_h(
+        plan.handle, _dev(h, (S, N, N), "h"), float(gamma), _dev(flat, (S, 3, ND), "flat"),
+        _dev(mask_pos, (M,), "mask_pos"), None if drift is None else _dev(drift, (NA,), "drift"),
+        _dev(s_exp, (S, NA, M, ND), "s_exp"), float(lam), _dev(cost, (S,), "cost", torch.float64),
+        _dev(g_h, (S, N, N), "g_h"), None if g_drift is None else _dev(g_drift, (S, NA), "g_drift"),
+        _dev(status, (4,), "status", torch.int32), _stream(stream)), "ei_cost_grad_h")
 
 
 def _host(a, shape, name, dtype=np.float32, writable=False):

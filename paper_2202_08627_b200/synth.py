@@ -47,6 +47,7 @@ class Config:
     pixel: float = 1.0
     det_pitch: float = 1.0
     z: float = 1.0
+    mask_offset: float = 0.0   # added to every mask position (P1: the paper's slope position)
 
     @property
     def angles(self) -> np.ndarray:
@@ -54,7 +55,7 @@ class Config:
 
     @property
     def mask(self) -> np.ndarray:
-        return ((np.arange(self.M) - (self.M - 1) / 2.0) / self.M).astype(np.float32)
+        return ((np.arange(self.M) - (self.M - 1) / 2.0) / self.M + self.mask_offset).astype(np.float32)
 
 
 # BASELINE.json configs[0..4]
@@ -65,6 +66,18 @@ CONFIGS = {
     "C4": Config("C4", 64, 512, 720, 180.0, 768, 7, 8, 1e4, 0.15, 0.0, 0.0, 0.002, 4000),
     "C5": Config("C5", 1, 2048, 240, 180.0, 3072, 5, 64, 2e3, 0.12, 0.0, 0.0, 0.0, 5000),
 }
+
+# The paper's own scan geometry for its single-map model (NEXT-3): a 220 x 220
+# slice (N_t = 220 detector pixels), 400 projections over 360 deg, one mask position on the slope
+# of the IC, 9 um from its maximum with a 38 um sample-mask period (m = 9/38 period), gamma = 5,
+# lambda = 1e-2.  The plastic-granule phantom is a seeded sum of 12 ellipses (the real scan is
+# not in the container).
+H_CONFIGS = {
+    "P1": Config("P1", 1, 220, 400, 360.0, 220, 1, 12, 1e4, 0.15, 0.0, 0.0, 0.0, 6000,
+                 mask_offset=9.0 / 38.0),
+}
+H_GAMMA = 5.0
+H_LAMBDA = 1e-2
 
 
 def small_config(name="R1", S=2, N=67, n_angles=37, span_deg=360.0, n_det=101, M=3, K=5,
@@ -223,3 +236,42 @@ def perturbed(maps, seed: int, rel: float = 0.1):
 def uniform(shape, seed: int) -> np.ndarray:
     """Nonnegative U[0,1) vectors for dot tests."""
     return np.random.default_rng(seed).uniform(0.0, 1.0, shape).astype(np.float32)
+
+
+@dataclasses.dataclass
+class HCase:
+    """Inputs of the single-map model (NEXT-3): truth h, flat, mask, drift, gamma, s_exp; cfg.z is
+    set so that the largest refraction shift z gamma |D R[h]| is 0.3 nominal IC widths (R16's
+    recipe applied to delta = gamma h)."""
+    cfg: Config
+    h: np.ndarray                 # [S][N][N] fp32 (truth)
+    gamma: float
+    flat: np.ndarray              # [S][3][Nd]
+    mask: np.ndarray              # [M]
+    drift: Optional[np.ndarray]
+    s_exp: Optional[np.ndarray] = None
+
+
+def make_h_case(cfg: Config, gamma: float,
+                max_shift: Callable[[np.ndarray], float],
+                model: Optional[Callable[["HCase"], np.ndarray]] = None, noise: bool = True) -> HCase:
+    """max_shift(img_2d) must return max |D R[img]| (unit z); model(case) s_mod [S][Na][M][Nd]."""
+    S, N = cfg.S, cfg.N
+    h = np.zeros((S, N, N), np.float32)
+    flat = np.zeros((S, 3, cfg.n_det), np.float32)
+    rngs = []
+    for s in range(S):
+        sl, rng = draw_slice(cfg, s)
+        rngs.append(rng)
+        h[s] = sl.mu * ((0.02 * 64 / N) / max(sl.mu.max(), 1e-30))      # R17 scale on mu = h
+        flat[s] = sl.flat
+    shift = max(max_shift(h[s]) for s in range(S))
+    z = 0.3 * cfg.w0 / max(gamma * shift, 1e-30)
+    case = HCase(dataclasses.replace(cfg, z=float(z)), h, float(gamma), flat, cfg.mask, draw_drift(cfg))
+    if model is not None:
+        smod = np.asarray(model(case), dtype=np.float64)
+        s_exp = np.empty(smod.shape, np.float32)
+        for s in range(S):
+            s_exp[s] = (rngs[s].poisson(np.maximum(smod[s], 0.0)) if noise else smod[s]).astype(np.float32)
+        case.s_exp = s_exp
+    return case

@@ -43,3 +43,36 @@ def oracle_cost_grad(case: synth.Case, maps, lam=0.0, slices=None):
     cfg = case.cfg
     return ora.cost_grad(cfg.angles, *maps, case.flat, case.mask, case.drift, case.s_exp, lam,
                          dx=cfg.pixel, du=cfg.det_pitch, z=cfg.z, slices=slices)
+
+
+def oracle_h_case(cfg: synth.Config, gamma: float = synth.H_GAMMA, noise: bool = True) -> synth.HCase:
+    """Single-map model case (NEXT-3): z from the oracle projector, s_exp = Poisson(oracle model)."""
+    ang = cfg.angles
+
+    def max_shift(img):
+        P = ora.project(img, ang, cfg.n_det, cfg.pixel, cfg.det_pitch)
+        return float(max(np.abs(ora.diff_t(row, cfg.det_pitch)).max() for row in P))
+
+    def model(case):
+        c = case.cfg
+        return ora.cost_grad_h(ang, case.h, case.gamma, case.flat, case.mask, case.drift,
+                               dx=c.pixel, du=c.det_pitch, z=c.z)
+
+    return synth.make_h_case(cfg, gamma, max_shift, model, noise=noise)
+
+
+@functools.lru_cache(maxsize=None)
+def cached_h_case(name: str) -> synth.HCase:
+    if name in synth.H_CONFIGS:
+        return oracle_h_case(synth.H_CONFIGS[name])
+    if name == "RH":   # ragged: odd sizes, detector narrower than the map diagonal, drift, M = 2
+        return oracle_h_case(synth.small_config("RH", S=2, N=41, n_angles=29, span_deg=360.0, n_det=47,
+                                                M=2, K=4, drift_sd=0.003, w_jit=0.1, texture=0.0,
+                                                seed=93))
+    raise KeyError(name)
+
+
+def oracle_cost_grad_h(case: synth.HCase, h, lam=0.0):
+    c = case.cfg
+    return ora.cost_grad_h(c.angles, h, case.gamma, case.flat, case.mask, case.drift, case.s_exp, lam,
+                           dx=c.pixel, du=c.det_pitch, z=c.z)

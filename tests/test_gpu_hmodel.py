@@ -1,0 +1,115 @@
+"""GPU-vs-oracle parity of the paper's single-map model (NEXT-3: eq. 4, with
+mu = gamma^-1 delta = h) through the C ABI: ei_forward_h and ei_cost_grad_h.  Same gates
+as the three-map path (cost 1e-4 relative; s_mod, g_h and g_drift 1e-3 relative L2), on the
+paper's own scan geometry P1 (220 x 220, 400 angles over 360 deg, one slope mask position,
+gamma = 5, lambda = 1e-2) and a ragged case."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+from paper_2202_08627_b200 import synth  # noqa: E402
+import _cases  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def ei():
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    from paper_2202_08627_b200 import build
+    build.build()
+    from paper_2202_08627_b200 import ei as mod
+    return mod
+
+
+def rel_l2(a, b):
+    a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
+    return float(np.linalg.norm((a - b).ravel()) / max(np.linalg.norm(b.ravel()), 1e-300))
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def plan_for(ei, cfg):
+    return ei.Plan(cfg.S, cfg.N, cfg.n_angles, cfg.n_det, cfg.M, cfg.pixel, cfg.det_pitch, cfg.z, cfg.angles)
+
+
+def gpu_h(ei, plan, case, h, lam):
+    cfg = case.cfg
+    cost = torch.zeros(cfg.S, dtype=torch.float64, device="cuda")
+    g = torch.zeros(cfg.S, cfg.N, cfg.N, device="cuda")
+    gdr = torch.zeros(cfg.S, cfg.n_angles, device="cuda")
+    st = torch.zeros(4, dtype=torch.int32, device="cuda")
+    drift = None if case.drift is None else dev(case.drift)
+    ei.ei_cost_grad_h(plan, dev(h), case.gamma, dev(case.flat), dev(case.mask), drift, dev(case.s_exp),
+                      lam, cost, g, gdr, st)
+    torch.cuda.synchronize()
+    return cost.cpu().numpy(), g.cpu().numpy(), gdr.cpu().numpy(), st.cpu().numpy()
+
+
+@pytest.mark.parametrize("name", ["P1", "RH"])
+def test_forward_h_parity(ei, name):
+    case = _cases.cached_h_case(name)
+    cfg = case.cfg
+    plan = plan_for(ei, cfg)
+    smod = torch.zeros(cfg.S, cfg.n_angles, cfg.M, cfg.n_det, device="cuda")
+    drift = None if case.drift is None else dev(case.drift)
+    ei.ei_forward_h(plan, dev(case.h), case.gamma, dev(case.flat), dev(case.mask), drift, smod)
+    ref = _cases.ora.cost_grad_h(cfg.angles, case.h, case.gamma, case.flat, case.mask, case.drift,
+                                 dx=cfg.pixel, du=cfg.det_pitch, z=cfg.z)
+    got = smod.cpu().numpy()
+    for s in range(cfg.S):
+        assert rel_l2(got[s], ref[s]) <= 1e-3
+
+
+@pytest.mark.parametrize("name", ["P1", "RH"])
+@pytest.mark.parametrize("point", ["x0", "true", "pert"])
+def test_cost_grad_h_parity(ei, name, point):
+    case = _cases.cached_h_case(name)
+    cfg = case.cfg
+    plan = plan_for(ei, cfg)
+    h = {"x0": np.zeros_like(case.h), "true": case.h,
+         "pert": synth.perturbed((case.h,), cfg.seed + 7)[0]}[point]
+    lam = synth.H_LAMBDA
+    cost, g, gdr, st = gpu_h(ei, plan, case, h, lam)
+    rc, rg, rst = _cases.oracle_cost_grad_h(case, h, lam)
+    assert np.all(np.abs(cost - rc) / rc <= 1e-4), (cost, rc)
+    for s in range(cfg.S):
+        assert rel_l2(g[s], rg[s]) <= 1e-3, (s, rel_l2(g[s], rg[s]))
+    assert st[0] == rst[0] and st[1] == rst[1]
+
+
+@pytest.mark.parametrize("name", ["P1", "RH"])
+def test_drift_gradient_h_parity(ei, name):
+    """dS/dm_o of the single-map model: the oracle's as central differences are not exposed for
+    h, so compare with the three-map oracle at (h, gamma h, 0), which has the same cost."""
+    case = _cases.cached_h_case(name)
+    cfg = case.cfg
+    plan = plan_for(ei, cfg)
+    h = synth.perturbed((case.h,), cfg.seed + 7)[0]
+    _, _, gdr, _ = gpu_h(ei, plan, case, h, 0.0)
+    delta = (case.gamma * h.astype(np.float64)).astype(np.float32)
+    out = _cases.ora.cost_grad(cfg.angles, h, delta, np.zeros_like(h), case.flat, case.mask, case.drift,
+                               case.s_exp, 0.0, dx=cfg.pixel, du=cfg.det_pitch, z=cfg.z, want_drift=True)
+    for s in range(cfg.S):
+        assert rel_l2(gdr[s], out[5][s]) <= 1e-3
+
+
+def test_h_model_equals_three_map_model_on_gpu(ei):
+    """The GPU's single-map path equals its three-map path at (mu, delta, sigma) = (h, gamma h, 0)
+    up to the fp32 rounding of gamma h: g_h = g_mu + gamma g_delta (chain rule)."""
+    case = _cases.cached_h_case("RH")
+    cfg = case.cfg
+    plan = plan_for(ei, cfg)
+    h = synth.perturbed((case.h,), cfg.seed + 7)[0]
+    cost, g, _, _ = gpu_h(ei, plan, case, h, 0.0)
+    maps = [dev(h), dev((case.gamma * h.astype(np.float64)).astype(np.float32)), dev(np.zeros_like(h))]
+    drift = None if case.drift is None else dev(case.drift)
+    c3, g3, _ = ei.cost_grad(plan, maps, dev(case.flat), dev(case.mask), drift, dev(case.s_exp), 0.0)
+    torch.cuda.synchronize()
+    assert np.all(np.abs(cost - c3.cpu().numpy()) / cost <= 1e-5)
+    chain = g3[0].cpu().numpy() + case.gamma * g3[1].cpu().numpy()
+    for s in range(cfg.S):
+        assert rel_l2(g[s], chain[s]) <= 1e-4

@@ -32,3 +32,13 @@ def test_deterministic_and_drift():
     assert synth.draw_drift(synth.CONFIGS["C1"]) is None
     c4 = synth.CONFIGS["C4"]
     assert c4.S == 64 and c4.N == 512 and c4.n_angles == 720 and c4.n_det == 768 and c4.M == 7
+
+
+def test_paper_workload_config():
+    """P1 follows the paper's scan: 220 x 220, 400 angles over 360 deg, one mask
+    position at 9 um from the IC maximum with a 38 um period."""
+    cfg = synth.H_CONFIGS["P1"]
+    assert (cfg.N, cfg.n_angles, cfg.n_det, cfg.M) == (220, 400, 220, 1)
+    assert np.isclose(np.rad2deg(cfg.angles[-1] + cfg.angles[1]), 360.0)
+    assert np.isclose(cfg.mask[0], 9.0 / 38.0)
+    assert synth.H_GAMMA == 5.0 and synth.H_LAMBDA == 1e-2

@@ -409,12 +409,133 @@ def run_reference(args, cfg, rank):
             "e2e": {"value": round(value, 6), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
+# ---------------------------------------------------------------------------------------
+# the paper's single-map model on the paper's scan geometry (NEXT-3, config P1): a context line
+# ---------------------------------------------------------------------------------------
+PAPER_CONTEXT = {
+    "paper_best_cell_s": 14.5, "paper_best_cell_iterations": 36,
+    "paper_s_per_iteration": round(14.5 / 36, 3),
+    "paper_hardware": "standard workstation, Intel i5 at 2.10 GHz, single thread (PAPER.md:186, :203)",
+    "paper_workload": "220 x 220 slice, 400 projections over 360 deg, one mask position, Numba Radon, "
+                      "m_r = 0, 20 flat scans (Table 2, PAPER.md:166-186)",
+    "note": "context only: the paper reports time per L-BFGS iteration (>= 1 cost+gradient "
+            "evaluation), not evaluations per second",
+}
+
+
+def run_gpu_h(args, cfg):
+    import torch
+    from paper_2202_08627_b200 import ei
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(0)
+    t_gen = time.time()
+    ang = cfg.angles
+
+    def max_shift(img):   # product path: max |D R[img]| (unit z) from ei_project (no parity claim)
+        plan1 = ei.Plan(1, cfg.N, cfg.n_angles, cfg.n_det, cfg.M, cfg.pixel, cfg.det_pitch, 1.0, ang)
+        sino = torch.zeros(1, 1, cfg.n_angles, cfg.n_det, device=dev)
+        ei.ei_project(plan1, torch.from_numpy(np.ascontiguousarray(img[None, None])).to(dev), 1, sino)
+        P = sino[0, 0].double()
+        d = torch.cat([P[:, 1:2] - P[:, 0:1], 0.5 * (P[:, 2:] - P[:, :-2]), P[:, -1:] - P[:, -2:-1]], 1)
+        return float(d.abs().max() / cfg.det_pitch)
+
+    def model(case):
+        c = case.cfg
+        plan = ei.Plan(c.S, c.N, c.n_angles, c.n_det, c.M, c.pixel, c.det_pitch, c.z, ang)
+        out = torch.zeros(c.S, c.n_angles, c.M, c.n_det, device=dev)
+        dv = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+        ei.ei_forward_h(plan, dv(case.h), case.gamma, dv(case.flat), dv(case.mask),
+                        None if case.drift is None else dv(case.drift), out)
+        return out.cpu().numpy()
+
+    case = synth.make_h_case(cfg, synth.H_GAMMA, max_shift, model)
+    cfg = case.cfg
+    t_gen = time.time() - t_gen
+    h = synth.perturbed((case.h,), cfg.seed + 7)[0]
+    lam = synth.H_LAMBDA
+    plan = ei.Plan(cfg.S, cfg.N, cfg.n_angles, cfg.n_det, cfg.M, cfg.pixel, cfg.det_pitch, cfg.z, ang)
+    dv = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+    hd, flat, mask, s_exp = dv(h), dv(case.flat), dv(case.mask), dv(case.s_exp)
+    drift = None if case.drift is None else dv(case.drift)
+    cost = torch.zeros(cfg.S, dtype=torch.float64, device=dev)
+    g = torch.zeros(cfg.S, cfg.N, cfg.N, device=dev)
+    st = torch.zeros(4, dtype=torch.int32, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        ei.ei_cost_grad_h(plan, hd, case.gamma, flat, mask, drift, s_exp, lam, cost, g, None, st, stream)
+
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
+    for _ in range(max(args.warmup, 3)):
+        flush.fill_(1.0)
+        step()
+    torch.cuda.synchronize()
+    sampler = ClockSampler(0)
+    t_end = time.time() + 0.5
+    while time.time() < t_end:
+        step()
+        torch.cuda.synchronize()
+    K = args.steps
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    s0 = ei.ei_plan_stats(plan)
+    torch.cuda.synchronize()
+    t0 = time.time()
+    for i in range(K):
+        flush.fill_(1.0)
+        ev[i][0].record(stream)
+        step()
+        ev[i][1].record(stream)
+    torch.cuda.synchronize()
+    t1 = time.time()
+    ms_step = sum(a.elapsed_time(b) for a, b in ev) / K
+    s1 = ei.ei_plan_stats(plan)
+    ei.ei_plan_set_timing(plan, K)
+    for i in range(K):
+        flush.fill_(1.0)
+        step()
+    torch.cuda.synchronize()
+    kern_ms, n_rec = ei.ei_plan_read_timing(plan)
+    ei.ei_plan_set_timing(plan, 0)
+    sampler.stop()
+    clocks = sampler.summary(t0, t1)
+    rsu = ray_sample_updates(cfg)
+    line = {
+        "metric": "cost+gradient evals/sec (single-map model, eq. 4)", "value": round(1000.0 / ms_step, 3),
+        "unit": UNIT, "n_gpus": 1, "steps": K, "warmup": args.warmup, "ms_per_step": round(ms_step, 5),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": "%s: %s (paper scan geometry, PAPER.md:89-93), gamma=%g" %
+                   (cfg.name, describe(cfg), case.gamma), "lambda": lam, "eval_point": "x_pert (R21)",
+                   "mask_position": float(case.mask[0]),
+                   "l2": "flushed before every timed step (256 MiB write, untimed)", "parallelism": "1 GPU"},
+        "ray_sample_updates_per_s": round(2 * rsu * cfg.S / (ms_step * 1e-3), 1),
+        "kernels_ms": {k: round(v / max(n_rec, 1), 5) for k, v in kern_ms.items() if v > 0},
+        "gpu_launches": int(s1[5] - s0[5]), "clocks": clocks, "status": st.cpu().numpy().tolist(),
+        "paper_context": PAPER_CONTEXT, "input_gen_s": round(t_gen, 2),
+    }
+    if not args.no_cpu_baseline:
+        from oracle import ora
+        t = time.time()
+        n = 0
+        while n < 1 or time.time() - t < args.cpu_budget:
+            ora.cost_grad_h(cfg.angles, h, case.gamma, case.flat, case.mask, case.drift, case.s_exp, lam,
+                            dx=cfg.pixel, du=cfg.det_pitch, z=cfg.z)
+            n += 1
+        dt = time.time() - t
+        line["cpu_baseline"] = {"value": round(n / dt, 4), "unit": UNIT, "cores": ora.num_threads(),
+                                "kind": "oracle",
+                                "sample": "%d fp64 oracle single-map cost+gradient evaluations of %s "
+                                          "(%.1f s)" % (n, cfg.name, dt)}
+    return line
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="C2", choices=sorted(synth.CONFIGS))
+    ap.add_argument("--config", default="C2", choices=sorted(synth.CONFIGS) + sorted(synth.H_CONFIGS),
+                    help="C1-C5: three-map model (BASELINE.json configs); P1: the paper's single-map "
+                         "model on its own scan geometry (context line)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--lam", type=float, default=1e-2)
     ap.add_argument("--cpu-budget", type=float, default=15.0)
@@ -423,6 +544,11 @@ def main():
     if args.warmup < 3:
         args.warmup = 3                                           # timing rule: W >= 3
     rank, world, local_rank = edist.env_rank()
+    if args.config in synth.H_CONFIGS:
+        if args.impl == "reference" or world > 1:
+            raise SystemExit("P1 (single-map context line) runs on one GPU with --impl ours only")
+        print(json.dumps(run_gpu_h(args, synth.H_CONFIGS[args.config])), flush=True)
+        return
     cfg = synth.CONFIGS[args.config]
     if args.impl == "reference":
         line = run_reference(args, cfg, rank)

@@ -147,7 +147,7 @@ int ei_cost_grad_host(ei_plan *plan, const float *mu, const float *delta, const 
 int ei_plan_stats(const ei_plan *plan, int64_t out[6]);
 
 /* Per-kernel device timing of ei_cost_grad (measurement support, bench.py).
- * ei_plan_set_timing(plan, max_evals): from now on the next `max_evals` ei_cost_grad calls
+ * ei_plan_set_timing(plan, max_evals): from now on the next `max_evals` ei_cost_grad(_drift/_h) calls
  * record CUDA events around each of their kernels on the call's stream (max_evals = 0
  * disables; events are created here, EI_ERR_RESOURCE on failure).
  * ei_plan_read_timing(plan, ms[6], n_evals): synchronises the recorded events and returns the

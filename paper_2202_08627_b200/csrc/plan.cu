@@ -405,13 +405,20 @@ int ei_cost_grad_h(const ei_plan *p, const float *h, float gamma, const float *f
   if (!p || !h || !flat || !mask || !s_exp || !cost || !g_h || !status) return EI_ERR_NULL;
   if (!(lambda >= 0.f) || !isfinite(lambda) || !isfinite(gamma)) return EI_ERR_DOMAIN;
   cudaStream_t st = (cudaStream_t)stream;
+  cudaEvent_t *ev = (p->tev && p->tn < p->tcap) ? p->tev + 7 * p->tn++ : nullptr;
+  auto mark = [&](int k) { if (ev) cudaEventRecord(ev[k], st); };
   ei::SmallCheck chk{flat, mask, drift};
+  mark(0);
   cudaError_t e = ei::launch_pack1(*p, h, st, lambda > 0.f, status, chk);            // K0
+  mark(1);
   if (e == cudaSuccess) e = ei::launch_project1(*p, p->P, st, p->proj.RS);           // K1
+  mark(2);
   if (e == cudaSuccess)
     e = ei::launch_curve_cost_grad_h(*p, gamma, flat, mask, drift, s_exp, status, st);  // K2
+  mark(3);
   ei::Finalize fin{cost, g_drift};
   if (e == cudaSuccess) e = ei::launch_backproject1(*p, g_h, st, h, lambda, &fin);   // K3 + K4
+  mark(4);
   p->stats[0] += 1;
   p->stats[1] += 1;
   p->stats[2] += 1;

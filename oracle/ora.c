@@ -441,6 +441,110 @@ void ora_cost_grad_h(int n, int n_angles, int n_det, int n_mask, double dx, doub
     free(hd); free(P); free(G); free(rowcost);
 }
 
+/* ---------------------------------------------------------------------------------
+ * NEXT-4: the measured (sampled) flat-field IC.  The paper measures f(t, m) by scanning the
+ * sample mask over one period in 33 steps, repeated 20 times; f at the shifted argument
+ * of eq. 4 is read between the samples.  The paper does not say how (SPEC.md's reading,
+ * S:147-159, adopted here as reading R23): a PERIODIC Catmull-Rom cubic through the K knots
+ * m_q = q / K (mask positions in periods, R3, period 1):
+ *   x = m K, i = floor(x), tau = x - i, p_j = f[(i - 1 + j) mod K], j = 0..3
+ *   f(m)  = 1/2 [2 p1 + (p2 - p0) tau + (2 p0 - 5 p1 + 4 p2 - p3) tau^2 + (3 p1 - p0 - 3 p2 + p3) tau^3]
+ *   f'(m) = K/2 [(p2 - p0) + 2 (2 p0 - 5 p1 + 4 p2 - p3) tau + 3 (3 p1 - p0 - 3 p2 + p3) tau^2]
+ * fs: [n_knots][n_det] samples (t contiguous).
+ * ------------------------------------------------------------------------------- */
+void ora_ic_eval(const float *fs, int n_knots, int n_det, int t, double m, double *f, double *fp)
+{
+    const double x = m * n_knots;
+    const double fl = floor(x);
+    const double tau = x - fl;
+    long long i = (long long)fl;
+    double p[4];
+    for (int j = 0; j < 4; ++j) {
+        long long q = (i - 1 + j) % n_knots;
+        if (q < 0) q += n_knots;
+        p[j] = (double)fs[(size_t)q * n_det + t];
+    }
+    const double a1 = p[2] - p[0];
+    const double a2 = 2.0 * p[0] - 5.0 * p[1] + 4.0 * p[2] - p[3];
+    const double a3 = 3.0 * p[1] - p[0] - 3.0 * p[2] + p[3];
+    *f = 0.5 * (2.0 * p[1] + a1 * tau + a2 * tau * tau + a3 * tau * tau * tau);
+    *fp = 0.5 * n_knots * (a1 + 2.0 * a2 * tau + 3.0 * a3 * tau * tau);
+}
+
+/* The single-map model (eq. 4) with the sampled flat IC: as ora_cost_grad_h but
+ *   s_mod = T f(t, m - m_o - z gamma D P),   ds/dShift = -T f'(t, .)
+ *   dS/dP = -2 sum_m r s [0 where clamped] + z gamma D^T (-2 sum_m r T f') */
+void ora_cost_grad_hs(int n, int n_angles, int n_det, int n_mask, int n_knots, double dx, double du,
+                      double z, double gamma, const double *angles, const float *h, const float *fs,
+                      const float *mask, const float *drift, const float *s_exp, double lambda,
+                      double *cost, double *grad, double *s_mod, int64_t *status)
+{
+    const size_t nn = (size_t)n * n, ns = (size_t)n_angles * n_det;
+    if (s_exp)
+        status[0] += count_nonfinite(h, nn) + count_nonfinite(fs, (size_t)n_knots * n_det) +
+                     count_nonfinite(mask, n_mask) + (drift ? count_nonfinite(drift, n_angles) : 0) +
+                     count_nonfinite(s_exp, ns * n_mask);
+    double *hd = widen(h, nn);
+    double *P = malloc(sizeof(double) * ns), *G = malloc(sizeof(double) * ns);
+    double *rowcost = calloc(n_angles, sizeof(double));
+    ora_project(n, n_angles, n_det, dx, du, angles, hd, P);
+    int64_t clamps = 0;
+#pragma omp parallel for schedule(dynamic, 1) reduction(+ : clamps)
+    for (int a = 0; a < n_angles; ++a) {
+        const double *Pa = P + (size_t)a * n_det;
+        double *dP = malloc(sizeof(double) * n_det), *gD = malloc(sizeof(double) * n_det),
+               *gT = malloc(sizeof(double) * n_det), *y = malloc(sizeof(double) * n_det);
+        ora_diff_t(n_det, du, Pa, dP);
+        const double mo = drift ? (double)drift[a] : 0.0;
+        double Sa = 0.0;
+        for (int k = 0; k < n_det; ++k) {
+            double pk = Pa[k];
+            int cl = 0;
+            if (pk > 50.0) { pk = 50.0; cl = 1; }
+            if (pk < -50.0) { pk = -50.0; cl = 1; }
+            clamps += cl;
+            const double T = exp(-pk);
+            double g_t = 0.0, g_d = 0.0;
+            for (int m = 0; m < n_mask; ++m) {
+                double f, fp;
+                ora_ic_eval(fs, n_knots, n_det, k, (double)mask[m] - mo - z * gamma * dP[k], &f, &fp);
+                const double s = T * f;
+                if (s_mod) s_mod[((size_t)a * n_mask + m) * n_det + k] = s;
+                if (s_exp) {
+                    const double r = s - (double)s_exp[((size_t)a * n_mask + m) * n_det + k];
+                    Sa += r * r;
+                    g_t += -2.0 * r * s;                    /* d/dP through T               */
+                    g_d += -2.0 * r * T * fp;               /* d/dShift: ds/dShift = -T f'  */
+                }
+            }
+            gT[k] = cl ? 0.0 : g_t;
+            gD[k] = g_d;
+        }
+        if (s_exp) {
+            ora_diff_t_adjoint(n_det, du, gD, y);
+            for (int k = 0; k < n_det; ++k) G[(size_t)a * n_det + k] = gT[k] + z * gamma * y[k];
+            rowcost[a] = Sa;
+        }
+        free(dP); free(gD); free(gT); free(y);
+    }
+    if (s_exp) {
+        status[1] += clamps;
+        double S = 0.0;
+        for (int a = 0; a < n_angles; ++a) S += rowcost[a];
+        ora_backproject(n, n_angles, n_det, dx, du, angles, G, grad);
+        if (lambda > 0.0) {
+            double reg = 0.0;
+            for (size_t q = 0; q < nn; ++q) {
+                reg += hd[q] * hd[q];
+                grad[q] += 2.0 * lambda * hd[q];
+            }
+            S += lambda * reg;
+        }
+        *cost = S;
+    }
+    free(hd); free(P); free(G); free(rowcost);
+}
+
 int ora_num_threads(void)
 {
 #ifdef _OPENMP

@@ -14,6 +14,7 @@ Functions (fp64 unless noted; slices are independent):
   forward(geom, angles, mu, delta, sigma, flat, mask, drift)        -> s_mod [S][Na][M][Nd]
   cost_grad(geom, angles, ..., s_exp, lam)      -> cost[S], g_mu, g_delta, g_sigma, status
   cost_grad_h(angles, h, gamma, ...)            NEXT-3: the paper's single-map model, eq. 4
+  ic_eval / cost_grad_hs(...)                   NEXT-4: sampled flat IC (periodic Catmull-Rom)
 """
 from __future__ import annotations
 
@@ -61,6 +62,9 @@ def lib():
                                     vp, _dp, _dp, _dp, _ip]
         L.ora_cost_grad2.argtypes = L.ora_cost_grad.argtypes + [vp]
         L.ora_cost_grad_h.argtypes = [i, i, i, i, d, d, d, d, _dp, _fp, _fp, _fp, vp, vp, d, vp, vp, vp, _ip]
+        L.ora_ic_eval.argtypes = [_fp, i, i, i, d, vp, vp]
+        L.ora_cost_grad_hs.argtypes = [i, i, i, i, i, d, d, d, d, _dp, _fp, _fp, _fp, vp, vp, d, vp, vp, vp,
+                                       _ip]
         L.ora_num_threads.restype = i
         _lib = L
     return _lib
@@ -214,3 +218,36 @@ def cost_grad_h(angles, h, gamma, flat, mask, drift, s_exp=None, lam=0.0, dx=1.0
     if s_exp is None:
         return smod
     return (cost, grad, status, smod) if want_smod else (cost, grad, status)
+
+
+def ic_eval(fs, t, m):
+    """Sampled flat IC fs [K][Nd] at pixel t and mask position m (periods): (f, f')."""
+    fs = _f(fs)
+    K, nd = fs.shape
+    f, fp = np.zeros(1), np.zeros(1)
+    lib().ora_ic_eval(fs, K, nd, int(t), float(m), _ptr(f), _ptr(fp))
+    return float(f[0]), float(fp[0])
+
+
+def cost_grad_hs(angles, h, gamma, fs, mask, drift, s_exp=None, lam=0.0, dx=1.0, du=1.0, z=1.0):
+    """Single-map model with the sampled flat IC fs [S][K][Nd] (NEXT-4).  s_exp=None: returns
+    s_mod [S][Na][M][Nd]; else (cost [S], grad [S][N][N], status [2])."""
+    angles = _d(angles)
+    h, fs, mask = _f(h), _f(fs), _f(mask)
+    S, n, _ = h.shape
+    na, m = len(angles), len(mask)
+    K, nd = fs.shape[1:]
+    dr = None if drift is None else _f(drift)
+    se = None if s_exp is None else _f(s_exp)
+    cost, grad = np.zeros(S), np.zeros((S, n, n))
+    smod = np.zeros((S, na, m, nd))
+    status = np.zeros(2, np.int64)
+    for s in range(S):
+        c, g, sm = np.zeros(1), np.zeros((n, n)), np.zeros((na, m, nd))
+        lib().ora_cost_grad_hs(n, na, nd, m, K, dx, du, z, float(gamma), angles, h[s], fs[s], mask,
+                               _ptr(dr), None if se is None else _ptr(se[s]), float(lam), _ptr(c),
+                               _ptr(g), _ptr(sm), status)
+        cost[s], grad[s], smod[s] = c[0], g, sm
+    if s_exp is None:
+        return smod
+    return cost, grad, status

@@ -275,3 +275,19 @@ def make_h_case(cfg: Config, gamma: float,
             s_exp[s] = (rngs[s].poisson(np.maximum(smod[s], 0.0)) if noise else smod[s]).astype(np.float32)
         case.s_exp = s_exp
     return case
+
+
+def sampled_flat(flat: np.ndarray, n_knots: int = 33, repeats: int = 20, seed: int = 0,
+                 noise: bool = True) -> np.ndarray:
+    """A measured flat IC (NEXT-4): the paper scans the sample mask over one period in 33 steps
+    and repeats the scan 20 times.  Synthesised here per detector pixel from the
+    Gaussian flat parameters flat [S][3][Nd] = (A, c, w) as the periodic curve of one mask period,
+    A sum_k exp(-(m_q - c - k)^2 / (2 w^2)) at m_q = q / n_knots, Poisson-sampled `repeats` times
+    and averaged.  Returns [S][n_knots][Nd] fp32."""
+    rng = np.random.default_rng(seed)
+    A, c, w = (flat[:, q, None, :].astype(np.float64) for q in range(3))
+    m = (np.arange(n_knots) / n_knots)[None, :, None]
+    f = sum(A * np.exp(-(m - c - k) ** 2 / (2 * w * w)) for k in (-2, -1, 0, 1, 2))
+    if noise:
+        f = sum(rng.poisson(f) for _ in range(repeats)) / repeats
+    return f.astype(np.float32)

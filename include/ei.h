@@ -128,6 +128,22 @@ int ei_cost_grad_h(const ei_plan *plan, const float *h, float gamma, const float
                    const float *mask_pos, const float *drift, const float *s_exp, float lambda,
                    double *cost, float *g_h, float *g_drift, int32_t *status, void *stream);
 
+/* The single-map model with the MEASURED (sampled) flat-field IC: the
+ * paper scans the sample mask over one period in 33 steps and evaluates f at the
+ * shifted argument of eq. 4; here f(t, .) is read between the samples by a periodic Catmull-Rom
+ * cubic (reading R23, after SPEC.md:147-159):
+ *   flat_samples [S][n_knots][N_d] device: f(t, q / n_knots), q = 0..n_knots-1 (mask positions in
+ *   periods, R3); n_knots >= 4 (EI_ERR_SHAPE otherwise).
+ *   s_mod = exp(-R[h]) f(t, m - m_o(theta) - z gamma dR[h]/dt)   (no centre parameter: the
+ *   measured curve carries it)
+ * Everything else exactly as ei_forward_h / ei_cost_grad_h. */
+int ei_forward_hs(const ei_plan *plan, const float *h, float gamma, const float *flat_samples,
+                  int n_knots, const float *mask_pos, const float *drift, float *s_mod, void *stream);
+int ei_cost_grad_hs(const ei_plan *plan, const float *h, float gamma, const float *flat_samples,
+                    int n_knots, const float *mask_pos, const float *drift, const float *s_exp,
+                    float lambda, double *cost, float *g_h, float *g_drift, int32_t *status,
+                    void *stream);
+
 /* ei_cost_grad with HOST buffers (same shapes and meaning; status is overwritten, not
  * accumulated).  Copies inputs host->device, evaluates, copies cost, gradients and status
  * back, and synchronises `stream` before returning.  The maps/flat/mask/drift upload runs on

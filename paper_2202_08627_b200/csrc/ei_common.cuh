@@ -116,6 +116,7 @@ int plan_projector(ei_plan &p, const double *angles, std::vector<int2> &groups,
 // K0 (k_pack.cu)
 struct SmallCheck {          // flat/mask/drift non-finite scan folded into K0
   const float *flat = nullptr, *mask = nullptr, *drift = nullptr;
+  int nflat_per_slice = 0;   // flat elements per slice (0: 3 N_d, the Gaussian parameters)
 };
 cudaError_t launch_pack3(const ei_plan &p, const float *mu, const float *delta, const float *sigma,
                          size_t in_stride, bool want_reg, int32_t *status, SmallCheck chk,
@@ -139,6 +140,11 @@ cudaError_t launch_curve_forward_h(const ei_plan &p, float gamma, const float *f
 cudaError_t launch_curve_cost_grad_h(const ei_plan &p, float gamma, const float *flat,
                                      const float *mask, const float *drift, const float *s_exp,
                                      int32_t *status, cudaStream_t st);
+cudaError_t launch_curve_forward_hs(const ei_plan &p, float gamma, const float *fs, int n_knots,
+                                    const float *mask, const float *drift, float *s_mod, cudaStream_t st);
+cudaError_t launch_curve_cost_grad_hs(const ei_plan &p, float gamma, const float *fs, int n_knots,
+                                      const float *mask, const float *drift, const float *s_exp,
+                                      int32_t *status, cudaStream_t st);
 // K3 (k_backproject.cu); with `fin` set, the CTAs (0, 0, s) also run the fused K4 finalize:
 // cost[s] = fixed-order sum of K2's per-segment partials + lambda * K0's sum x^2 partials, and
 // g_drift[s][theta] = sum of K2's per-segment dS/dm_o partials (if g_drift != NULL)

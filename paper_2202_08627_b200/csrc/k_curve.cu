@@ -64,6 +64,7 @@ struct K2Args {
   const float *flat, *mask, *drift, *s_exp;
   int NA, ND, M, nseg, W;    // W = core positions per segment (<= blockDim - 4)
   int nmap;                  // maps per slice in P: 3 (mu, delta, sigma) or 1 (h, NEXT-3)
+  int K;                     // MODES 4, 5: knots of the sampled flat IC (flat = [S][K][ND])
   float zs, inv_du;          // shift factor: z (three-map model) or z gamma (single-map model)
   float *s_mod;              // MODE 0
   float4 *GA;                // MODE 1: pair-layout gradient sinograms (K3 input)
@@ -123,11 +124,14 @@ struct Cursor {
 // issue this thread's loads of the cursor's item as 4-byte async copies into its private prefetch
 // slots (only this thread reads them: cp.async.wait_group alone orders them — no barrier)
 // K2 modes: 0 forward (three maps), 1 cost + gradient (three maps), 2 cost + gradient of the
-// paper's single-map model h (NEXT-3: P_mu = P_h, shift z gamma D P_h, no scattering), 3 forward h
+// paper's single-map model h (NEXT-3: P_mu = P_h, shift z gamma D P_h, no scattering), 3 forward h,
+// 4 / 5 cost + gradient / forward of the single-map model with the SAMPLED flat IC (NEXT-4:
+// K knots per period per detector pixel, periodic Catmull-Rom, reading R23)
 template <int MODE>
 struct Mode {
-  static constexpr bool cost = MODE == 1 || MODE == 2;
+  static constexpr bool cost = MODE == 1 || MODE == 2 || MODE == 4;
   static constexpr bool h = MODE >= 2;
+  static constexpr bool sampled = MODE >= 4;
 };
 
 template <int MODE>
@@ -215,7 +219,7 @@ __global__ void __maxnreg__(72) curve_kernel(K2Args g) {
     const int k = seg * g.W - 2 + t;
     const bool valid = k >= 0 && k < ND;
     const bool core = valid && t >= 2 && t < g.W + 2;
-    if (valid && (s != fs || seg != fseg)) {       // new (slice, segment): flat A, c, w
+    if (!Mode<MODE>::sampled && valid && (s != fs || seg != fseg)) {   // new (s, seg): A, c, w
       const float *f = g.flat + (size_t)s * 3 * ND + k;
       fA = __ldg(f);
       fc = __ldg(f + ND);
@@ -248,16 +252,16 @@ __global__ void __maxnreg__(72) curve_kernel(K2Args g) {
       const float T = ex2(-LOG2E * pm);
       float W2 = fmaf(fw, fw, ps);
       const float W2min = 0.01f * fw * fw;
-      const bool wc = W2 < W2min;
+      const bool wc = !Mode<MODE>::sampled && W2 < W2min;
       W2 = wc ? W2min : W2;
       const float invW2 = rcp(W2);
-      const float amp = T * fA * fw * rsq(W2);
+      const float amp = Mode<MODE>::sampled ? T : T * fA * fw * rsq(W2);
       // s = amp exp(-u^2 / 2W^2) = amp 2^(c2 u^2).  (Folding amp into the exponent as log2|amp|
       // saves one FMUL per mask position but adds ~8x the argument rounding and breaks the 1e-3
       // gradient gate at C3's noise level: measured 1.36e-3.)
       const float c2 = -0.5f * LOG2E * invW2;
       const float mo = g.drift ? __ldg(g.drift + a) : 0.f;
-      const float base = fc + mo + g.zs * dP;
+      const float base = (Mode<MODE>::sampled ? 0.f : fc) + mo + g.zs * dP;
       if (core) {
         mu_cl += mc;
         w2_cl += wc;
@@ -266,10 +270,32 @@ __global__ void __maxnreg__(72) curve_kernel(K2Args g) {
       // per mask position: r = s - s_exp; cost += r^2; with rs = r s:
       //   gmm += rs, gdd += rs u, gq += rs u^2   (g_sigma uses gq - W^2 gmm)
       float gmm = 0.f, gdd = 0.f, gq = 0.f;
+      // sampled flat IC of this pixel: knots fsb[q * ND], q = 0..K-1 (periodic Catmull-Rom, R23)
+      const float *fsb = Mode<MODE>::sampled ? g.flat + (size_t)s * g.K * ND + k : nullptr;
       auto term = [&](float mpos, int m, float se) {
         const float du_ = mpos - base;
-        const float u2 = du_ * du_;
-        const float sv = amp * ex2(c2 * u2);
+        float sv, tfp = 0.f;   // s, and for the sampled IC T f'(arg)
+        float u2 = 0.f;
+        if (Mode<MODE>::sampled) {
+          const int K = g.K;
+          const float x = du_ * (float)K;
+          const float fl = floorf(x);
+          const float tau = x - fl;
+          int i = (int)fl % K;
+          if (i < 0) i += K;
+          const int q0 = i == 0 ? K - 1 : i - 1, q2 = i + 1 == K ? 0 : i + 1, q3 = q2 + 1 == K ? 0 : q2 + 1;
+          const float p0 = __ldg(fsb + q0 * ND), p1 = __ldg(fsb + i * ND), p2 = __ldg(fsb + q2 * ND),
+                      p3 = __ldg(fsb + q3 * ND);
+          const float a1 = p2 - p0, a2 = fmaf(2.f, p0, fmaf(-5.f, p1, fmaf(4.f, p2, -p3)));
+          const float a3 = fmaf(3.f, p1 - p2, p3 - p0);
+          const float f = 0.5f * fmaf(tau, fmaf(tau, fmaf(tau, a3, a2), a1), 2.f * p1);
+          const float fp = 0.5f * (float)K * fmaf(tau, fmaf(3.f * tau, a3, 2.f * a2), a1);
+          sv = amp * f;
+          tfp = amp * fp;
+        } else {
+          u2 = du_ * du_;
+          sv = amp * ex2(c2 * u2);
+        }
         if (!Mode<MODE>::cost) {
           if (core) g.s_mod[rowb + (size_t)m * ND] = sv;
         } else {
@@ -277,8 +303,12 @@ __global__ void __maxnreg__(72) curve_kernel(K2Args g) {
           cost = fmaf(r, r, cost);
           const float rsv = r * sv;
           gmm += rsv;
-          gdd = fmaf(rsv, du_, gdd);
-          gq = fmaf(rsv, u2, gq);
+          if (Mode<MODE>::sampled) {
+            gdd = fmaf(r, tfp, gdd);   // sum r T f'
+          } else {
+            gdd = fmaf(rsv, du_, gdd);
+            gq = fmaf(rsv, u2, gq);
+          }
         }
       };
 #pragma unroll
@@ -292,7 +322,7 @@ __global__ void __maxnreg__(72) curve_kernel(K2Args g) {
       gm = mc ? 0.f : -2.f * gmm;
       const float gss = fmaf(-W2, gmm, gq);   // sum r s (u^2 - W^2)
       gs = wc ? 0.f : gss * invW2 * invW2;
-      gd = 2.f * gdd * invW2;
+      gd = Mode<MODE>::sampled ? -2.f * gdd : 2.f * gdd * invW2;   // dS/dShift
     }
     if (Mode<MODE>::cost) {
       sgD[buf][t] = gd;
@@ -365,8 +395,10 @@ static size_t k2_smem(int NT) { return sizeof(float) * (size_t)NSTAGE * NQ * NT;
 
 template <int MODE>
 cudaError_t launch(const ei_plan &p, const float *flat, const float *mask, const float *drift,
-                   const float *s_exp, float *s_mod, int32_t *status, float gamma, cudaStream_t st) {
+                   const float *s_exp, float *s_mod, int32_t *status, float gamma, cudaStream_t st,
+                   int n_knots = 0) {
   K2Args g;
+  g.K = n_knots;
   g.P = p.P;
   g.RS = p.proj.RS;
   g.S = p.S;
@@ -443,6 +475,17 @@ cudaError_t launch_curve_cost_grad(const ei_plan &p, const float *flat, const fl
 cudaError_t launch_curve_forward_h(const ei_plan &p, float gamma, const float *flat, const float *mask,
                                    const float *drift, float *s_mod, cudaStream_t st) {
   return launch<3>(p, flat, mask, drift, nullptr, s_mod, nullptr, gamma, st);
+}
+
+cudaError_t launch_curve_forward_hs(const ei_plan &p, float gamma, const float *fs, int n_knots,
+                                    const float *mask, const float *drift, float *s_mod, cudaStream_t st) {
+  return launch<5>(p, fs, mask, drift, nullptr, s_mod, nullptr, gamma, st, n_knots);
+}
+
+cudaError_t launch_curve_cost_grad_hs(const ei_plan &p, float gamma, const float *fs, int n_knots,
+                                      const float *mask, const float *drift, const float *s_exp,
+                                      int32_t *status, cudaStream_t st) {
+  return launch<4>(p, fs, mask, drift, s_exp, nullptr, status, gamma, st, n_knots);
 }
 
 cudaError_t launch_curve_cost_grad_h(const ei_plan &p, float gamma, const float *flat,

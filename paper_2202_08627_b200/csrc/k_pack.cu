@@ -153,7 +153,8 @@ cudaError_t launch_pack3(const ei_plan &p, const float *mu, const float *delta, 
   PairOut<3> o{p.MA, p.MAT, p.MB, p.MBT};
   pack_pairs_kernel<3><<<grid, block, 0, st>>>(mu, delta, sigma, in_stride, p.N, o,
                                                want_reg ? p.part_reg : nullptr, status, chk,
-                                               p.S * 3 * p.ND, p.M, p.NA, p.proj.PAD, p.proj.Rp);
+                                               p.S * (chk.nflat_per_slice ? chk.nflat_per_slice : 3 * p.ND),
+                                               p.M, p.NA, p.proj.PAD, p.proj.Rp);
   return cudaGetLastError();
 }
 
@@ -164,7 +165,8 @@ cudaError_t launch_pack1(const ei_plan &p, const float *map, cudaStream_t st, bo
   PairOut<1> o{p.M1, p.M1T};
   pack_pairs_kernel<1><<<grid, block, 0, st>>>(map, nullptr, nullptr, (size_t)p.N * p.N, p.N, o,
                                                want_reg ? p.part_reg : nullptr, status, chk,
-                                               p.S * 3 * p.ND, p.M, p.NA, p.proj.PAD, p.proj.Rp);
+                                               p.S * (chk.nflat_per_slice ? chk.nflat_per_slice : 3 * p.ND),
+                                               p.M, p.NA, p.proj.PAD, p.proj.Rp);
   return cudaGetLastError();
 }
 

@@ -428,6 +428,47 @@ int ei_cost_grad_h(const ei_plan *p, const float *h, float gamma, const float *f
   return cuda_status(e);
 }
 
+int ei_forward_hs(const ei_plan *p, const float *h, float gamma, const float *flat_samples,
+                  int n_knots, const float *mask, const float *drift, float *s_mod, void *stream) {
+  if (!p || !h || !flat_samples || !mask || !s_mod) return EI_ERR_NULL;
+  if (n_knots < 4) return EI_ERR_SHAPE;
+  if (!isfinite(gamma)) return EI_ERR_DOMAIN;
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e = ei::launch_pack1(*p, h, st);                                        // K0
+  if (e == cudaSuccess) e = ei::launch_project1(*p, p->P, st, p->proj.RS);           // K1
+  if (e == cudaSuccess)
+    e = ei::launch_curve_forward_hs(*p, gamma, flat_samples, n_knots, mask, drift, s_mod, st);  // K2
+  p->stats[0] += 1;
+  p->stats[1] += 1;
+  p->stats[4] += 1;
+  p->stats[5] += 3;
+  return cuda_status(e);
+}
+
+int ei_cost_grad_hs(const ei_plan *p, const float *h, float gamma, const float *flat_samples,
+                    int n_knots, const float *mask, const float *drift, const float *s_exp,
+                    float lambda, double *cost, float *g_h, float *g_drift, int32_t *status,
+                    void *stream) {
+  if (!p || !h || !flat_samples || !mask || !s_exp || !cost || !g_h || !status) return EI_ERR_NULL;
+  if (n_knots < 4) return EI_ERR_SHAPE;
+  if (!(lambda >= 0.f) || !isfinite(lambda) || !isfinite(gamma)) return EI_ERR_DOMAIN;
+  cudaStream_t st = (cudaStream_t)stream;
+  ei::SmallCheck chk{flat_samples, mask, drift, n_knots * p->ND};
+  cudaError_t e = ei::launch_pack1(*p, h, st, lambda > 0.f, status, chk);            // K0
+  if (e == cudaSuccess) e = ei::launch_project1(*p, p->P, st, p->proj.RS);           // K1
+  if (e == cudaSuccess)
+    e = ei::launch_curve_cost_grad_hs(*p, gamma, flat_samples, n_knots, mask, drift, s_exp, status, st);
+  ei::Finalize fin{cost, g_drift};
+  if (e == cudaSuccess) e = ei::launch_backproject1(*p, g_h, st, h, lambda, &fin);   // K3 + K4
+  p->stats[0] += 1;
+  p->stats[1] += 1;
+  p->stats[2] += 1;
+  p->stats[3] += 1;
+  p->stats[4] += 1;
+  p->stats[5] += 4;
+  return cuda_status(e);
+}
+
 int ei_cost_grad_host(ei_plan *p, const float *mu, const float *delta, const float *sigma,
                       const float *flat, const float *mask, const float *drift,
                       const float *s_exp, float lambda, double *cost, float *g_mu, float *g_delta,

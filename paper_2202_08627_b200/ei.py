@@ -24,7 +24,8 @@ _lib = ctypes.CDLL(LIB_PATH)
 
 EI_OK, EI_ERR_NULL, EI_ERR_SHAPE, EI_ERR_DOMAIN, EI_ERR_RESOURCE, EI_ERR_CUDA = range(6)
 SYMBOLS = ("ei_plan_create", "ei_plan_destroy", "ei_project", "ei_backproject", "ei_forward",
-           "ei_cost_grad", "ei_cost_grad_drift", "ei_forward_h", "ei_cost_grad_h", "ei_cost_grad_host", "ei_plan_stats", "ei_plan_set_timing",
+           "ei_cost_grad", "ei_cost_grad_drift", "ei_forward_h", "ei_cost_grad_h", "ei_forward_hs",
+           "ei_cost_grad_hs", "ei_cost_grad_host", "ei_plan_stats", "ei_plan_set_timing",
            "ei_plan_read_timing", "ei_plan_info", "ei_error_string", "ei_version")
 KERNELS = ("K0_pack", "K1_project", "K2_curve", "K3_backproject", "unused4", "unused5")
 
@@ -46,6 +47,8 @@ _lib.ei_cost_grad.argtypes = [_vp] + [_vp] * 7 + [_f] + [_vp] * 5 + [_vp]
 _lib.ei_cost_grad_drift.argtypes = [_vp] + [_vp] * 7 + [_f] + [_vp] * 6 + [_vp]
 _lib.ei_forward_h.argtypes = [_vp, _vp, _f] + [_vp] * 4 + [_vp]
 _lib.ei_cost_grad_h.argtypes = [_vp, _vp, _f] + [_vp] * 4 + [_f] + [_vp] * 4 + [_vp]
+_lib.ei_forward_hs.argtypes = [_vp, _vp, _f, _vp, _i] + [_vp] * 3 + [_vp]
+_lib.ei_cost_grad_hs.argtypes = [_vp, _vp, _f, _vp, _i] + [_vp] * 3 + [_f] + [_vp] * 4 + [_vp]
 _lib.ei_cost_grad_host.argtypes = [_vp] + [_vp] * 7 + [_f] + [_vp] * 5 + [_vp]
 _lib.ei_plan_stats.argtypes = [_vp, _vp]
 _lib.ei_plan_set_timing.argtypes = [_vp, _i]
@@ -237,6 +240,31 @@ def ei_cost_grad_h(plan: Plan, h, gamma: float, flat, mask_pos, drift, s_exp, la
         _dev(s_exp, (S, NA, M, ND), "s_exp"), float(lam), _dev(cost, (S,), "cost", torch.float64),
         _dev(g_h, (S, N, N), "g_h"), None if g_drift is None else _dev(g_drift, (S, NA), "g_drift"),
         _dev(status, (4,), "status", torch.int32), _stream(stream)), "ei_cost_grad_h")
+
+
+def ei_forward_hs(plan: Plan, h, gamma: float, flat_samples, mask_pos, drift, s_mod, stream=None):
+    """Single-map model with the sampled flat IC flat_samples [S][K][N_d] (NEXT-4)."""
+    S, N, NA, ND, M = plan.shape
+    K = int(flat_samples.shape[1])
+    _check(_lib.ei_forward_hs(plan.handle, _dev(h, (S, N, N), "h"), float(gamma),
+                              _dev(flat_samples, (S, K, ND), "flat_samples"), K,
+                              _dev(mask_pos, (M,), "mask_pos"),
+                              None if drift is None else _dev(drift, (NA,), "drift"),
+                              _dev(s_mod, (S, NA, M, ND), "s_mod"), _stream(stream)), "ei_forward_hs")
+
+
+def ei_cost_grad_hs(plan: Plan, h, gamma: float, flat_samples, mask_pos, drift, s_exp, lam: float, cost,
+                    g_h, g_drift, status, stream=None):
+    """Single-map model with the sampled flat IC (NEXT-4): cost, g_h, optional g_drift."""
+    import torch
+    S, N, NA, ND, M = plan.shape
+    K = int(flat_samples.shape[1])
+    _check(_lib.ei_cost_grad_hs(
+        plan.handle, _dev(h, (S, N, N), "h"), float(gamma), _dev(flat_samples, (S, K, ND), "flat_samples"),
+        K, _dev(mask_pos, (M,), "mask_pos"), None if drift is None else _dev(drift, (NA,), "drift"),
+        _dev(s_exp, (S, NA, M, ND), "s_exp"), float(lam), _dev(cost, (S,), "cost", torch.float64),
+        _dev(g_h, (S, N, N), "g_h"), None if g_drift is None else _dev(g_drift, (S, NA), "g_drift"),
+        _dev(status, (4,), "status", torch.int32), _stream(stream)), "ei_cost_grad_hs")
 
 
 def _host(a, shape, name, dtype=np.float32, writable=False):

@@ -76,3 +76,17 @@ def oracle_cost_grad_h(case: synth.HCase, h, lam=0.0):
     c = case.cfg
     return ora.cost_grad_h(c.angles, h, case.gamma, case.flat, case.mask, case.drift, case.s_exp, lam,
                            dx=c.pixel, du=c.det_pitch, z=c.z)
+
+
+@functools.lru_cache(maxsize=None)
+def cached_hs_case(name: str, n_knots: int = 33):
+    """Single-map case with the sampled flat IC (NEXT-4): flat_samples from 20 averaged Poisson
+    scans of 33 steps of the case's Gaussian IC; s_exp = Poisson(oracle sampled-IC model)."""
+    base = cached_h_case(name)
+    c = base.cfg
+    fs = synth.sampled_flat(base.flat, n_knots, repeats=20, seed=c.seed + 31)
+    smod = ora.cost_grad_hs(c.angles, base.h, base.gamma, fs, base.mask, base.drift,
+                            dx=c.pixel, du=c.det_pitch, z=c.z)
+    rng = np.random.default_rng(c.seed + 32)
+    s_exp = rng.poisson(np.maximum(smod, 0.0)).astype(np.float32)
+    return base, fs, s_exp

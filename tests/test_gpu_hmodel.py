@@ -113,3 +113,36 @@ def test_h_model_equals_three_map_model_on_gpu(ei):
     chain = g3[0].cpu().numpy() + case.gamma * g3[1].cpu().numpy()
     for s in range(cfg.S):
         assert rel_l2(g[s], chain[s]) <= 1e-4
+
+
+@pytest.mark.parametrize("name", ["P1", "RH"])
+@pytest.mark.parametrize("point", ["true", "pert"])
+def test_sampled_flat_parity(ei, name, point):
+    """NEXT-4: the single-map model with the measured (sampled, 33-knot) flat IC, read by a
+    periodic Catmull-Rom cubic (R23): forward, cost, gradient and drift gradient vs the oracle."""
+    case, fs, s_exp = _cases.cached_hs_case(name)
+    cfg = case.cfg
+    plan = plan_for(ei, cfg)
+    h = case.h if point == "true" else synth.perturbed((case.h,), cfg.seed + 7)[0]
+    drift = None if case.drift is None else dev(case.drift)
+    smod = torch.zeros(cfg.S, cfg.n_angles, cfg.M, cfg.n_det, device="cuda")
+    ei.ei_forward_hs(plan, dev(h), case.gamma, dev(fs), dev(case.mask), drift, smod)
+    ref = _cases.ora.cost_grad_hs(cfg.angles, h, case.gamma, fs, case.mask, case.drift,
+                                  dx=cfg.pixel, du=cfg.det_pitch, z=cfg.z)
+    for s in range(cfg.S):
+        assert rel_l2(smod.cpu().numpy()[s], ref[s]) <= 1e-3
+    lam = synth.H_LAMBDA
+    cost = torch.zeros(cfg.S, dtype=torch.float64, device="cuda")
+    g = torch.zeros(cfg.S, cfg.N, cfg.N, device="cuda")
+    st = torch.zeros(4, dtype=torch.int32, device="cuda")
+    ei.ei_cost_grad_hs(plan, dev(h), case.gamma, dev(fs), dev(case.mask), drift, dev(s_exp), lam, cost, g,
+                       None, st)
+    torch.cuda.synchronize()
+    rc, rg, rst = _cases.ora.cost_grad_hs(cfg.angles, h, case.gamma, fs, case.mask, case.drift, s_exp, lam,
+                                          dx=cfg.pixel, du=cfg.det_pitch, z=cfg.z)
+    c = cost.cpu().numpy()
+    assert np.all(np.abs(c - rc) / rc <= 1e-4), (c, rc)
+    gg = g.cpu().numpy()
+    for s in range(cfg.S):
+        assert rel_l2(gg[s], rg[s]) <= 1e-3, (s, rel_l2(gg[s], rg[s]))
+    assert list(st.cpu().numpy()[:2]) == list(rst)

@@ -9,24 +9,30 @@
 //   g_mu = -2 sum r s;  g_Delta = 2 sum r s u / W^2;  g_sigma = sum r s (u^2 - W^2) / W^4
 //   g_delta = z D^T g_Delta                              halo 1 more (2 in total)
 //   dS/dm_o(theta) = sum_t g_Delta(t)                    NEXT-2 (u depends on m_o like on -Delta)
+// plus the single-map model of eq. 4 (NEXT-3: P_mu = P_h, Delta = z gamma D P_h, W = w) and its
+// sampled-flat variant (NEXT-4: f read by a periodic Catmull-Rom cubic, R23).
 //
-// B200 design (DESIGN.md §5 K2): the pass is HBM-bound (s_exp streams once), so it is organised
-// for memory-level parallelism rather than per-row CTAs:
-//  * work item = one segment of W detector positions of one row (s, theta); a CTA of NT >= W + 4
-//    threads evaluates the curve at the W core positions plus a halo of 2 on each side, so D and
-//    D^T never need a neighbouring segment (1.5-3 % redundant arithmetic, no extra HBM bytes: the
-//    halo loads hit L2/L1);
-//  * persistent CTAs own a contiguous run of items (angle fastest, so stepping is a carry chain, no
-//    division) and the flat-IC parameters stay in registers; every thread PREFETCHES its loads
-//    for the next 2 items (3 projections + 2 neighbours, up to 8 s_exp values) as 4-byte cp.async
-//    copies into private shared slots, so each thread keeps ~20 independent loads in flight through
-//    its whole life instead of one round trip per row;
-//  * one CTA barrier per item: the per-position g values go to a double-buffered shared row, the
-//    core threads then write the gradient sinograms directly in K3's PAIR layout (entry
-//    e = (g[e-1], g[e]) of every map, pre-multiplied by the Joseph weight dx/|c_dom|);
-//  * cost and drift-gradient partials: fp32 per thread (M terms) and per warp (shuffle) -> one
-//    partial per (item, warp); K3 sums them in fp64 in index order (fused finalize, K4).
+// B200 design (DESIGN.md §5 K2): the pass is HBM-bound (s_exp streams once), so the loads are
+// taken off the compute threads and made deep:
+//  * work item = one segment of W detector positions of one row (s, theta); its input is a set of
+//    contiguous row pieces — the projections and the M measured curves of that row, W + 8
+//    positions each (a halo of 4 on both sides, so D and D^T never need a neighbouring segment);
+//  * a producer warp streams each item's row pieces with 1-D bulk copies (TMA engine) into a
+//    3-stage shared-memory ring completing on full/empty mbarriers (one elected thread, a handful
+//    of copies per item); rows not float4-aligned (N_d % 4 != 0 or misaligned caller arrays) are
+//    copied by the producer warp's lanes instead;
+//  * consumer thread t owns J = 4 consecutive positions, i.e. one float4 of every staged row
+//    (conflict-free LDS.128); the 4 positions are independent chains through the mask loop;
+//  * persistent CTAs own a contiguous run of items (angle fastest: the flat parameters of a
+//    segment stay in registers across its angles);
+//  * per item one consumer barrier: the g values go to a double-buffered shared row, each thread
+//    reads its neighbours' float4s for D^T and writes its 4 gradient entries directly in K3's PAIR
+//    layout (entry e = (g[e-1], g[e]) of every map, pre-multiplied by the Joseph weight);
+//  * cost and drift-gradient partials: fp32 per thread and per warp (shuffle) -> one partial per
+//    (item, warp); K3 sums them in fp64 in index order (fused finalize, K4).
 // Deterministic: no float atomics, fixed reduction order, results independent of the grid size.
+#include <stdint.h>
+
 #include <algorithm>
 
 #include "ei_common.cuh"
@@ -35,8 +41,10 @@
 namespace ei {
 namespace {
 
-constexpr int K2_MAXT = 512;   // threads per CTA (max)
-constexpr int MPF = 8;         // s_exp values per position held in prefetch registers
+constexpr int J = 4;           // detector positions per consumer thread
+constexpr int K2_MAXT = 256;   // consumer threads per CTA (max)
+constexpr int NST = 3;         // ring stages
+constexpr int MPF = 8;         // mask positions kept in registers
 
 // 2^x on the SFU (MUFU.EX2, ~2 ulp): every exponential of the curve model is written as a power
 // of two with the log2(e) factor folded into a per-position constant
@@ -58,18 +66,21 @@ __device__ __forceinline__ float rsq(float x) {   // MUFU.RSQ (~2 ulp), no denor
 }
 
 struct K2Args {
-  const float *P;            // [RS][S][3][NA][ND] (row-split partial projections, summed here)
+  const float *P;            // [RS][S][nmap][NA][ND] (row-split partial projections, summed here)
   int RS, S;
-  size_t rstride;            // S * 3 * NA * ND
+  size_t rstride;            // S * nmap * NA * ND
   const float *flat, *mask, *drift, *s_exp;
-  int NA, ND, M, nseg, W;    // W = core positions per segment (<= blockDim - 4)
+  int NA, ND, M, nseg, W;    // W = core positions per segment, multiple of 4
   int nmap;                  // maps per slice in P: 3 (mu, delta, sigma) or 1 (h, NEXT-3)
+  int nrows;                 // staged rows per item: nmap + M (cost modes) or nmap (forward)
+  int WB;                    // staged positions per row: W + 8
   int K;                     // MODES 4, 5: knots of the sampled flat IC (flat = [S][K][ND])
+  int vec;                   // 1: rows are 16-B aligned (ND % 4 == 0, aligned arrays) -> TMA
   float zs, inv_du;          // shift factor: z (three-map model) or z gamma (single-map model)
-  float *s_mod;              // MODE 0
+  float *s_mod;              // forward modes
   float4 *GA;                // MODE 1: pair-layout gradient sinograms (K3 input)
   float2 *GB;
-  float2 *GA1;               // MODE 2: pair-layout gradient sinogram of h
+  float2 *GA1;               // MODES 2, 4: pair-layout gradient sinogram of h
   int PADG, RpG;
   const float4 *k3;          // per-angle table, .w = Joseph weight dx/|c_dom|
   float *part_cost, *part_mo;    // [S * NA * nseg * nw] per-warp partials
@@ -77,52 +88,6 @@ struct K2Args {
   int items;                 // S * NA * nseg
 };
 
-// prefetch slots per position: P_mu, P_delta(k-1), P_delta(k+1), P_sigma, s_exp[0..MPF); each
-// thread's slots are contiguous (stride NQ, odd -> conflict-free), so every slot address is the
-// thread's base plus an immediate
-constexpr int NQ = 4 + MPF + 1;
-constexpr int NSTAGE = 3;      // items in flight per CTA: the current one + 2 prefetched
-
-__device__ __forceinline__ void cp4(uint32_t dst, const float *src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(dst), "l"(src));
-}
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
-
-// item position (s, seg, a): angle fastest; a CTA's items are consecutive, so stepping is a carry
-// chain (no division), the flat-IC parameters (which depend on (s, t) only) stay in registers and
-// the load pointers advance by one row
-struct Pos {
-  int s, seg, a;
-  __device__ __forceinline__ bool step(int NA, int nseg) {   // true: (s, seg) changed
-    if (++a < NA) return false;
-    a = 0;
-    if (++seg == nseg) { seg = 0; ++s; }
-    return true;
-  }
-};
-
-// per-thread load cursor: this thread's position k of item (s, seg, a), as pointers into P and s_exp
-struct Cursor {
-  const float *pm, *se;   // &P[s][0][a][k], &s_exp[s][a][0][k]
-  int k;
-  bool valid;
-  __device__ __forceinline__ void seek(const K2Args &g, const Pos &q, int t) {
-    k = q.seg * g.W - 2 + t;
-    valid = k >= 0 && k < g.ND;
-    const int plane = g.NA * g.ND;                                 // < 2^30 (plan)
-    pm = g.P + (size_t)q.s * g.nmap * plane + (q.a * g.ND + k);
-    se = g.s_exp ? g.s_exp + ((size_t)(q.s * g.NA + q.a) * g.M) * g.ND + k : nullptr;
-  }
-  __device__ __forceinline__ void next_row(const K2Args &g) {     // a -> a + 1, same (s, seg)
-    pm += g.ND;
-    if (se) se += (size_t)g.M * g.ND;
-  }
-};
-
-// issue this thread's loads of the cursor's item as 4-byte async copies into its private prefetch
-// slots (only this thread reads them: cp.async.wait_group alone orders them — no barrier)
 // K2 modes: 0 forward (three maps), 1 cost + gradient (three maps), 2 cost + gradient of the
 // paper's single-map model h (NEXT-3: P_mu = P_h, shift z gamma D P_h, no scattering), 3 forward h,
 // 4 / 5 cost + gradient / forward of the single-map model with the SAMPLED flat IC (NEXT-4:
@@ -134,149 +99,212 @@ struct Mode {
   static constexpr bool sampled = MODE >= 4;
 };
 
-template <int MODE>
-__device__ __forceinline__ void load_item(const K2Args &g, const Cursor &c, uint32_t slot, int plane,
-                                          int dl, int dr) {
-  if (!c.valid) return;
-  cp4(slot, c.pm);
-  if (Mode<MODE>::h) {                 // P_h at k, k-1, k+1
-    cp4(slot + 4, c.pm + dl);
-    cp4(slot + 8, c.pm + dr);
-  } else {                             // P_mu, P_delta(k-1), P_delta(k+1), P_sigma
-    cp4(slot + 4, c.pm + plane + dl);
-    cp4(slot + 8, c.pm + plane + dr);
-    cp4(slot + 12, c.pm + 2 * plane);
+// item position (s, seg, a): angle fastest; a CTA's items are consecutive, so stepping is a carry
+// chain (no division)
+struct Pos {
+  int s, seg, a;
+  __device__ __forceinline__ void step(int NA, int nseg) {
+    if (++a < NA) return;
+    a = 0;
+    if (++seg == nseg) { seg = 0; ++s; }
   }
-  if (Mode<MODE>::cost) {
-    const float *se = c.se;
-#pragma unroll
-    for (int u = 0; u < MPF; ++u) {
-      if (u < g.M) cp4(slot + 16 + 4 * u, se);
-      se += g.ND;
-    }
-  }
-}
+};
 
 __device__ __forceinline__ float warp_sum(float v) {
   for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
   return v;
 }
 
+__device__ __forceinline__ float at(const float4 &v, int j) {
+  return j == 0 ? v.x : j == 1 ? v.y : j == 2 ? v.z : v.w;
+}
+
+// global address of staged row r of item q (rows: maps 0..nmap-1 of P, then the M s_exp rows)
+__device__ __forceinline__ const float *row_ptr(const K2Args &g, const Pos &q, int r) {
+  const int plane = g.NA * g.ND;                                   // < 2^30 (plan)
+  if (r < g.nmap) return g.P + ((size_t)q.s * g.nmap + r) * plane + (size_t)q.a * g.ND;
+  return g.s_exp + ((size_t)(q.s * g.NA + q.a) * g.M + (r - g.nmap)) * g.ND;
+}
+
 template <int MODE>
-__global__ void __maxnreg__(72) curve_kernel(K2Args g) {
-  extern __shared__ __align__(16) float pre_s[];   // [NSTAGE][NQ][NT] prefetch slots
-  __shared__ float sgD[2][K2_MAXT], sgm[2][K2_MAXT], sgs[2][K2_MAXT];
-  const int NT = blockDim.x;
+__global__ void __launch_bounds__(K2_MAXT + 32, 2) curve_kernel(K2Args g) {
+  extern __shared__ __align__(16) float smem[];   // ring [NST][nrows][WB] + exchange [2][3][WB]
+  __shared__ __align__(8) uint64_t full[NST], empty[NST];
+  const int NT = blockDim.x - 32;                  // consumer threads
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5, nw = NT >> 5;
-  const int ND = g.ND;
-  int bad = 0, mu_cl = 0, w2_cl = 0;
-  float mk[MPF];                                   // mask positions (first MPF) in registers
-#pragma unroll
-  for (int u = 0; u < MPF; ++u) mk[u] = u < g.M ? __ldg(g.mask + u) : 0.f;
+  const int ND = g.ND, WB = g.WB;
+  const int stage_floats = g.nrows * WB;
+  float *ring = smem;
+  float *xch = smem + NST * stage_floats;         // [2][3][WB]: g_Delta, g_mu, g_sigma rows
+  if (t == 0) {
+    for (int q = 0; q < NST; ++q) {
+      mbar_init(&full[q], 1);
+      mbar_init(&empty[q], nw);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
   pdl_wait();   // K1's projections
   // static contiguous split of the items (deterministic, independent of timing)
   const int i0 = (int)(((long long)blockIdx.x * g.items) / gridDim.x);
   const int i1 = (int)(((long long)(blockIdx.x + 1) * g.items) / gridDim.x);
-  const int plane = g.NA * ND;
-  const uint32_t slot0 = (uint32_t)__cvta_generic_to_shared(pre_s) + 4u * (uint32_t)(t * NQ);
-  const uint32_t stage_bytes = 4u * (uint32_t)(NQ * NT);
-  Pos cp{i0 / (g.nseg * g.NA), (i0 / g.NA) % g.nseg, i0 % g.NA};   // current item
-  Pos lp = cp;                                                       // next item to prefetch
-  Cursor lc;
-  lc.seek(g, lp, t);
-  int dl = lc.k == 0 ? 0 : -1, dr = lc.k == ND - 1 ? 0 : 1;
-  auto advance = [&]() {   // lp/lc -> next item
-    if (lp.step(g.NA, g.nseg)) {
-      lc.seek(g, lp, t);
-      dl = lc.k == 0 ? 0 : -1;
-      dr = lc.k == ND - 1 ? 0 : 1;
-    } else {
-      lc.next_row(g);
-    }
-  };
-#pragma unroll
-  for (int q = 0; q < NSTAGE - 1; ++q) {
-    if (i0 + q < i1) {
-      load_item<MODE>(g, lc, slot0 + q * stage_bytes, plane, dl, dr);
-      advance();
-    }
-    cp_commit();
-  }
-  int fs = -1, fseg = -1;                          // (slice, segment) of the flat registers
-  float fA = 0.f, fc = 0.f, fw = 1.f;
-  int buf = 0, st = 0;
-  for (int item = i0; item < i1; ++item, buf ^= 1, st = (st + 1 == NSTAGE) ? 0 : st + 1,
-           cp.step(g.NA, g.nseg)) {
-    {   // keep NSTAGE - 1 items in flight: issue item + NSTAGE - 1 into the stage freed last
-      const int ns = (st + NSTAGE - 1) % NSTAGE;
-      if (item + NSTAGE - 1 < i1) {
-        load_item<MODE>(g, lc, slot0 + ns * stage_bytes, plane, dl, dr);
-        advance();
+  const Pos p0{i0 / (g.nseg * g.NA), (i0 / g.NA) % g.nseg, i0 % g.NA};
+
+  if (wid == nw) {   // ---------------- producer warp ----------------
+    Pos q = p0;
+    int st = 0;
+    uint32_t ph = 0;
+    for (int item = i0; item < i1; ++item, q.step(g.NA, g.nseg)) {
+      if (item - i0 >= NST) {
+        if (lane == 0) mbar_wait(&empty[st], ph ^ 1);
+        __syncwarp();
       }
-      cp_commit();
+      const int kb = q.seg * g.W - J;                       // position of staged index 0
+      const int ks = max(0, kb), ke = min(ND, kb + WB);     // copied positions [ks, ke)
+      float *dst = ring + st * stage_floats + (ks - kb);
+      if (g.vec) {
+        if (lane == 0) {
+          const uint32_t bytes = (uint32_t)(ke - ks) * 4u;
+          mbar_arrive_expect_tx(&full[st], bytes * (uint32_t)g.nrows);
+          for (int r = 0; r < g.nrows; ++r) bulk_g2s(dst + r * WB, row_ptr(g, q, r) + ks, bytes, &full[st]);
+        }
+      } else {   // unaligned rows: the warp's lanes copy them
+        for (int r = 0; r < g.nrows; ++r) {
+          const float *src = row_ptr(g, q, r) + ks;
+          for (int k = lane; k < ke - ks; k += 32) dst[r * WB + k] = __ldg(src + k);
+        }
+        __syncwarp();
+        __threadfence_block();
+        if (lane == 0) mbar_arrive(&full[st]);
+      }
+      if (++st == NST) { st = 0; ph ^= 1; }
     }
+    return;
+  }
+
+  // ---------------- consumer warps ----------------
+  int bad = 0, mu_cl = 0, w2_cl = 0;
+  float mk[MPF];                                   // mask positions (first MPF) in registers
+#pragma unroll
+  for (int u = 0; u < MPF; ++u) mk[u] = u < g.M ? __ldg(g.mask + u) : 0.f;
+  int fs = -1, fseg = -1;                          // (slice, segment) of the flat registers
+  float4 fA = make_float4(0.f, 0.f, 0.f, 0.f), fc = fA, fw = make_float4(1.f, 1.f, 1.f, 1.f);
+  Pos cp = p0;
+  int st = 0, buf = 0;
+  uint32_t ph = 0;
+  for (int item = i0; item < i1; ++item, cp.step(g.NA, g.nseg), buf ^= 1) {
     const int seg = cp.seg, a = cp.a, s = cp.s;
-    const int k = seg * g.W - 2 + t;
-    const bool valid = k >= 0 && k < ND;
-    const bool core = valid && t >= 2 && t < g.W + 2;
-    if (!Mode<MODE>::sampled && valid && (s != fs || seg != fseg)) {   // new (s, seg): A, c, w
-      const float *f = g.flat + (size_t)s * 3 * ND + k;
-      fA = __ldg(f);
-      fc = __ldg(f + ND);
-      fw = __ldg(f + 2 * ND);
+    const int kb = seg * g.W - J;
+    const int k0 = kb + J * t;                     // this thread's first position
+    const bool staged = J * t < WB;                // inside the staged window (threads are
+                                                   // rounded up to a warp)
+    const bool any = staged && k0 + J > 0 && k0 < ND;
+    if (!Mode<MODE>::sampled && any && (s != fs || seg != fseg)) {   // new (s, seg): flat A, c, w
+      const float *f = g.flat + (size_t)s * 3 * ND + k0;
+      if (g.vec) {
+        fA = __ldg(reinterpret_cast<const float4 *>(f));
+        fc = __ldg(reinterpret_cast<const float4 *>(f + ND));
+        fw = __ldg(reinterpret_cast<const float4 *>(f + 2 * ND));
+      } else {
+        float a4[3][J];
+#pragma unroll
+        for (int q = 0; q < 3; ++q)
+#pragma unroll
+          for (int j = 0; j < J; ++j)
+            a4[q][j] = (k0 + j >= 0 && k0 + j < ND) ? __ldg(f + q * ND + j) : (q == 2 ? 1.f : 0.f);
+        fA = make_float4(a4[0][0], a4[0][1], a4[0][2], a4[0][3]);
+        fc = make_float4(a4[1][0], a4[1][1], a4[1][2], a4[1][3]);
+        fw = make_float4(a4[2][0], a4[2][1], a4[2][2], a4[2][3]);
+      }
     }
     fs = s;
     fseg = seg;
-    cp_wait<NSTAGE - 1>();   // this item's copies (issued NSTAGE-1 groups ago) have landed
-    const float *cur = pre_s + st * NQ * NT + t * NQ;
     const int row = s * g.NA + a;
-    float gm = 0.f, gd = 0.f, gs = 0.f, cost = 0.f;
-    if (valid) {
-      float pm = cur[0], pdl = cur[1], pdr = cur[2], ps = Mode<MODE>::h ? 0.f : cur[3];
-      const int kl = k == 0 ? 0 : k - 1, kr = k == ND - 1 ? ND - 1 : k + 1;
+    const float mo = g.drift ? __ldg(g.drift + a) : 0.f;
+    mbar_wait(&full[st], ph);
+    const float *stg = ring + st * stage_floats;   // staged rows of this item
+    float4 gm4 = make_float4(0.f, 0.f, 0.f, 0.f), gd4 = gm4, gs4 = gm4;
+    float cost = 0.f, gmo = 0.f;
+    const float4 *r4 = reinterpret_cast<const float4 *>(stg);
+    const int W4 = WB / J;
+    // D's neighbours outside this thread's float4 of P_delta: from the adjacent lanes (shuffle,
+    // all lanes), the warp's edge lanes read the staged row (one lane: no bank conflict)
+    const float *pdr = stg + (Mode<MODE>::h ? 0 : WB) + J * t;     // P_delta row at k0
+    const float4 Pd0 = staged ? r4[(Mode<MODE>::h ? 0 : W4) + t] : make_float4(0.f, 0.f, 0.f, 0.f);
+    float nbl = __shfl_up_sync(0xffffffffu, Pd0.w, 1), nbr = __shfl_down_sync(0xffffffffu, Pd0.x, 1);
+    if (lane == 0) nbl = (staged && k0 > 0) ? pdr[-1] : 0.f;
+    if (lane == 31) nbr = (staged && k0 + J < ND) ? pdr[J] : 0.f;
+    if (any) {
+      float4 Pm = Mode<MODE>::h ? Pd0 : r4[t];
+      float4 Pd = Pd0;
+      float4 Ps = Mode<MODE>::h ? make_float4(0.f, 0.f, 0.f, 0.f) : r4[2 * W4 + t];
       if (g.RS > 1) {   // fixed-order sum of the row-split partials (small problems, L2-resident)
         const int plane = g.NA * ND;
-        const float *Pm = g.P + (size_t)s * g.nmap * plane + a * ND;
-        const int pd = Mode<MODE>::h ? 0 : plane;   // P_delta plane (the h plane itself)
+        const float *Pb = g.P + (size_t)s * g.nmap * plane + a * ND + k0;
+        const int pdo = Mode<MODE>::h ? 0 : plane;
         for (int r = 1; r < g.RS; ++r) {
-          const float *b = Pm + r * g.rstride;
-          pm += __ldg(b + k);
-          pdl += __ldg(b + pd + kl);
-          pdr += __ldg(b + pd + kr);
-          if (!Mode<MODE>::h) ps += __ldg(b + 2 * plane + k);
+          const float *b = Pb + r * g.rstride;
+          float v[3][J];
+#pragma unroll
+          for (int j = 0; j < J; ++j) {
+            const bool ok = k0 + j >= 0 && k0 + j < ND;
+            v[0][j] = ok ? __ldg(b + j) : 0.f;
+            v[1][j] = ok && !Mode<MODE>::h ? __ldg(b + pdo + j) : 0.f;
+            v[2][j] = ok && !Mode<MODE>::h ? __ldg(b + 2 * plane + j) : 0.f;
+          }
+          Pm.x += v[0][0]; Pm.y += v[0][1]; Pm.z += v[0][2]; Pm.w += v[0][3];
+          if (Mode<MODE>::h) {
+            Pd = Pm;
+          } else {
+            Pd.x += v[1][0]; Pd.y += v[1][1]; Pd.z += v[1][2]; Pd.w += v[1][3];
+            Ps.x += v[2][0]; Ps.y += v[2][1]; Ps.z += v[2][2]; Ps.w += v[2][3];
+          }
+          if (k0 > 0) nbl += __ldg(b + pdo - 1);
+          if (k0 + J < ND) nbr += __ldg(b + pdo + J);
         }
       }
-      const float dP = (pdr - pdl) * ((kr - kl == 2 ? 0.5f : 1.f) * g.inv_du);
-      const bool mc = (pm > 50.f) || (pm < -50.f);
-      pm = fminf(fmaxf(pm, -50.f), 50.f);
-      const float T = ex2(-LOG2E * pm);
-      float W2 = fmaf(fw, fw, ps);
-      const float W2min = 0.01f * fw * fw;
-      const bool wc = !Mode<MODE>::sampled && W2 < W2min;
-      W2 = wc ? W2min : W2;
-      const float invW2 = rcp(W2);
-      const float amp = Mode<MODE>::sampled ? T : T * fA * fw * rsq(W2);
-      // s = amp exp(-u^2 / 2W^2) = amp 2^(c2 u^2).  (Folding amp into the exponent as log2|amp|
-      // saves one FMUL per mask position but adds ~8x the argument rounding and breaks the 1e-3
-      // gradient gate at C3's noise level: measured 1.36e-3.)
-      const float c2 = -0.5f * LOG2E * invW2;
-      const float mo = g.drift ? __ldg(g.drift + a) : 0.f;
-      const float base = (Mode<MODE>::sampled ? 0.f : fc) + mo + g.zs * dP;
-      if (core) {
-        mu_cl += mc;
-        w2_cl += wc;
+      const float pdv[J + 2] = {nbl, Pd.x, Pd.y, Pd.z, Pd.w, nbr};   // P_delta at k0-1 .. k0+4
+      const float *fsb = Mode<MODE>::sampled ? g.flat + (size_t)s * g.K * ND + k0 : nullptr;
+      // per-position constants of the curve (the 4 positions are independent chains: ILP 4)
+      float base[J], amp[J], c2[J], W2[J], invW2[J];
+      bool mc[J], wc[J], core[J];
+#pragma unroll
+      for (int j = 0; j < J; ++j) {
+        const int k = k0 + j;
+        const bool ok = k >= 0 && k < ND;
+        core[j] = ok && k >= seg * g.W && k < seg * g.W + g.W;
+        // D P_delta (a2): central inside, one-sided at the two ends
+        const float dP = k == 0 ? (pdv[j + 2] - pdv[j + 1]) * g.inv_du
+                       : k == ND - 1 ? (pdv[j + 1] - pdv[j]) * g.inv_du
+                                     : (pdv[j + 2] - pdv[j]) * (0.5f * g.inv_du);
+        float pm = at(Pm, j);
+        mc[j] = (pm > 50.f) || (pm < -50.f);
+        pm = fminf(fmaxf(pm, -50.f), 50.f);
+        const float T = ex2(-LOG2E * pm);
+        const float w = at(fw, j);
+        float w2 = fmaf(w, w, at(Ps, j));
+        const float W2min = 0.01f * w * w;
+        wc[j] = !Mode<MODE>::sampled && w2 < W2min;
+        W2[j] = wc[j] ? W2min : w2;
+        invW2[j] = rcp(W2[j]);
+        amp[j] = ok ? (Mode<MODE>::sampled ? T : T * at(fA, j) * w * rsq(W2[j])) : 0.f;
+        c2[j] = -0.5f * LOG2E * invW2[j];   // exp(-u^2 / 2W^2) = 2^(c2 u^2)
+        base[j] = (Mode<MODE>::sampled ? 0.f : at(fc, j)) + mo + g.zs * dP;
+        if (core[j]) {
+          mu_cl += mc[j];
+          w2_cl += wc[j];
+        }
       }
-      const size_t rowb = (size_t)row * g.M * ND + k;   // s_exp / s_mod row base
-      // per mask position: r = s - s_exp; cost += r^2; with rs = r s:
+      const size_t rowb = (size_t)row * g.M * ND + k0;   // s_mod row base (k0)
+      float gmm[J], gdd[J], gq[J], cst[J];
+#pragma unroll
+      for (int j = 0; j < J; ++j) gmm[j] = gdd[j] = gq[j] = cst[j] = 0.f;
+      // one mask position for the 4 positions: r = s - s_exp; cost += r^2; with rs = r s:
       //   gmm += rs, gdd += rs u, gq += rs u^2   (g_sigma uses gq - W^2 gmm)
-      float gmm = 0.f, gdd = 0.f, gq = 0.f;
-      // sampled flat IC of this pixel: knots fsb[q * ND], q = 0..K-1 (periodic Catmull-Rom, R23)
-      const float *fsb = Mode<MODE>::sampled ? g.flat + (size_t)s * g.K * ND + k : nullptr;
-      auto term = [&](float mpos, int m, float se) {
-        const float du_ = mpos - base;
-        float sv, tfp = 0.f;   // s, and for the sampled IC T f'(arg)
-        float u2 = 0.f;
-        if (Mode<MODE>::sampled) {
+      auto term = [&](int j, float mpos, int m, float se) {
+        const float du_ = mpos - base[j];
+        float sv, tfp = 0.f, u2 = 0.f;
+        if (Mode<MODE>::sampled) {   // periodic Catmull-Rom through the K knots (R23)
           const int K = g.K;
           const float x = du_ * (float)K;
           const float fl = floorf(x);
@@ -284,88 +312,131 @@ __global__ void __maxnreg__(72) curve_kernel(K2Args g) {
           int i = (int)fl % K;
           if (i < 0) i += K;
           const int q0 = i == 0 ? K - 1 : i - 1, q2 = i + 1 == K ? 0 : i + 1, q3 = q2 + 1 == K ? 0 : q2 + 1;
-          const float p0 = __ldg(fsb + q0 * ND), p1 = __ldg(fsb + i * ND), p2 = __ldg(fsb + q2 * ND),
-                      p3 = __ldg(fsb + q3 * ND);
+          const bool ok = k0 + j >= 0 && k0 + j < ND;
+          const float p0 = ok ? __ldg(fsb + q0 * ND + j) : 0.f, p1 = ok ? __ldg(fsb + i * ND + j) : 0.f,
+                      p2 = ok ? __ldg(fsb + q2 * ND + j) : 0.f, p3 = ok ? __ldg(fsb + q3 * ND + j) : 0.f;
           const float a1 = p2 - p0, a2 = fmaf(2.f, p0, fmaf(-5.f, p1, fmaf(4.f, p2, -p3)));
           const float a3 = fmaf(3.f, p1 - p2, p3 - p0);
           const float f = 0.5f * fmaf(tau, fmaf(tau, fmaf(tau, a3, a2), a1), 2.f * p1);
           const float fp = 0.5f * (float)K * fmaf(tau, fmaf(3.f * tau, a3, 2.f * a2), a1);
-          sv = amp * f;
-          tfp = amp * fp;
+          sv = amp[j] * f;
+          tfp = amp[j] * fp;
         } else {
           u2 = du_ * du_;
-          sv = amp * ex2(c2 * u2);
+          sv = amp[j] * ex2(c2[j] * u2);
         }
         if (!Mode<MODE>::cost) {
-          if (core) g.s_mod[rowb + (size_t)m * ND] = sv;
+          if (core[j]) g.s_mod[rowb + (size_t)m * ND + j] = sv;
         } else {
           const float r = sv - se;
-          cost = fmaf(r, r, cost);
+          cst[j] = fmaf(r, r, cst[j]);
           const float rsv = r * sv;
-          gmm += rsv;
+          gmm[j] += rsv;
           if (Mode<MODE>::sampled) {
-            gdd = fmaf(r, tfp, gdd);   // sum r T f'
+            gdd[j] = fmaf(r, tfp, gdd[j]);   // sum r T f'
           } else {
-            gdd = fmaf(rsv, du_, gdd);
-            gq = fmaf(rsv, u2, gq);
+            gdd[j] = fmaf(rsv, du_, gdd[j]);
+            gq[j] = fmaf(rsv, u2, gq[j]);
           }
         }
       };
 #pragma unroll
-      for (int u = 0; u < MPF; ++u)
-        if (u < g.M) term(mk[u], u, Mode<MODE>::cost ? cur[4 + u] : 0.f);   // prefetched s_exp
-      for (int m = MPF; m < g.M; ++m)                                                // M > MPF
-        term(__ldg(g.mask + m), m, Mode<MODE>::cost ? __ldcs(g.s_exp + rowb + (size_t)m * ND) : 0.f);
-      // a non-finite s_exp makes the cost non-finite; only then count the elements (rare path)
-      if (Mode<MODE>::cost && core && !isfinite(cost))
-        for (int m = 0; m < g.M; ++m) bad += !isfinite(m < MPF ? cur[4 + m] : g.s_exp[rowb + (size_t)m * ND]);
-      gm = mc ? 0.f : -2.f * gmm;
-      const float gss = fmaf(-W2, gmm, gq);   // sum r s (u^2 - W^2)
-      gs = wc ? 0.f : gss * invW2 * invW2;
-      gd = Mode<MODE>::sampled ? -2.f * gdd : 2.f * gdd * invW2;   // dS/dShift
+      for (int u = 0; u < MPF; ++u) {          // mask positions in registers
+        if (u >= g.M) break;
+        const float4 se4 = Mode<MODE>::cost ? r4[(g.nmap + u) * W4 + t] : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int j = 0; j < J; ++j) term(j, mk[u], u, at(se4, j));
+      }
+      for (int m = MPF; m < g.M; ++m) {        // M > MPF
+        const float mp = __ldg(g.mask + m);
+        const float4 se4 = Mode<MODE>::cost ? r4[(g.nmap + m) * W4 + t] : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int j = 0; j < J; ++j) term(j, mp, m, at(se4, j));
+      }
+      if (Mode<MODE>::cost) {
+#pragma unroll
+        for (int j = 0; j < J; ++j) {
+          // a non-finite s_exp makes the cost non-finite; only then count the elements (rare)
+          if (core[j] && !isfinite(cst[j]))
+            for (int m = 0; m < g.M; ++m) bad += !isfinite(stg[(g.nmap + m) * WB + J * t + j]);
+          const bool ok = k0 + j >= 0 && k0 + j < ND;
+          const float gss = fmaf(-W2[j], gmm[j], gq[j]);   // sum r s (u^2 - W^2)
+          const float gmj = (mc[j] || !ok) ? 0.f : -2.f * gmm[j];
+          const float gsj = (wc[j] || !ok) ? 0.f : gss * invW2[j] * invW2[j];
+          const float gdj = !ok ? 0.f : Mode<MODE>::sampled ? -2.f * gdd[j] : 2.f * gdd[j] * invW2[j];
+          if (j == 0) { gm4.x = gmj; gs4.x = gsj; gd4.x = gdj; }
+          if (j == 1) { gm4.y = gmj; gs4.y = gsj; gd4.y = gdj; }
+          if (j == 2) { gm4.z = gmj; gs4.z = gsj; gd4.z = gdj; }
+          if (j == 3) { gm4.w = gmj; gs4.w = gsj; gd4.w = gdj; }
+          if (core[j]) {
+            cost += cst[j];
+            gmo += gdj;
+          }
+        }
+      }
     }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);        // this warp is done with the staged rows
+    if (++st == NST) { st = 0; ph ^= 1; }
     if (Mode<MODE>::cost) {
-      sgD[buf][t] = gd;
-      sgm[buf][t] = gm;
-      sgs[buf][t] = gs;
-      // cost and dS/dm_o partials: fp32 per thread (<= M terms) and per warp (32 terms), then
-      // fp64 over the warps in warp order
-      const float wc_ = warp_sum(core ? cost : 0.f);
-      const float wm_ = warp_sum(core ? gd : 0.f);
-      if (lane == 0) {   // per-warp partials, (s, a, seg, warp) order; K3 sums them in fp64
+      float4 *x4 = reinterpret_cast<float4 *>(xch + buf * 3 * WB);
+      if (staged) {
+        x4[t] = gd4;
+        x4[W4 + t] = gm4;
+        if (!Mode<MODE>::h) x4[2 * W4 + t] = gs4;
+      }
+      // cost and dS/dm_o partials: fp32 per thread and per warp, fp64 over items/warps in K3
+      const float wc_ = warp_sum(cost);
+      const float wm_ = warp_sum(gmo);
+      if (lane == 0) {   // per-warp partials, (s, a, seg, warp) order
         const int pidx = ((s * g.NA + a) * g.nseg + seg) * nw + wid;
         g.part_cost[pidx] = wc_;
         g.part_mo[pidx] = wm_;
       }
-      __syncthreads();
-      if (t < g.W) {
-        const int e = seg * g.W + t;       // pair entry written by this thread
-        if (e < ND) {
-          const float *D = sgD[buf] + (t + 2 - e);   // D[k] = g_Delta at detector k (window)
-          const float zh = 0.5f * g.zs * g.inv_du;
-          // g_delta = z D^T g_Delta, D^T written out from the rows of D (a2):
-          //   y[j] = [j==0](-g0) + [j==1](g0) + [j==ND-2](-g_{ND-1}) + [j==ND-1](g_{ND-1})
-          //        + 1/2 g_{j-1} [1 <= j-1 <= ND-2] - 1/2 g_{j+1} [1 <= j+1 <= ND-2]   (all / du)
-          auto gdelta = [&](int j) {
-            if (j >= 2 && j <= ND - 3) return zh * (D[j - 1] - D[j + 1]);   // interior rows only
-            float y = 0.f;
-            if (j == 0) y -= D[0];
-            if (j == 1) y += D[0];
-            if (j == ND - 2) y -= D[ND - 1];
-            if (j == ND - 1) y += D[ND - 1];
-            if (j - 1 >= 1 && j - 1 <= ND - 2) y += 0.5f * D[j - 1];
-            if (j + 1 >= 1 && j + 1 <= ND - 2) y -= 0.5f * D[j + 1];
-            return g.zs * g.inv_du * y;
-          };
-          const float sc = __ldg(g.k3 + a).w;
-          const size_t rb = (size_t)row * g.RpG + g.PADG;
-          const float m1 = sgm[buf][t + 2], s1 = sgs[buf][t + 2], d1 = gdelta(e);
-          const float m0 = e >= 1 ? sgm[buf][t + 1] : 0.f, s0 = e >= 1 ? sgs[buf][t + 1] : 0.f;
-          const float d0 = e >= 1 ? gdelta(e - 1) : 0.f;
+      asm volatile("bar.sync 1, %0;\n" ::"r"(NT) : "memory");   // consumers only
+      const int e0 = max(k0, seg * g.W), e1 = min(min(k0 + J, seg * g.W + g.W), ND);
+      if (staged && e0 < e1) {   // core entries imply t <= WB/4 - 2, so x4[t + 1] is staged
+        // neighbours' float4s: g_Delta at k0-4 .. k0+7, g_mu / g_sigma at k0-4 .. k0-1
+        const float4 Ld = t > 0 ? x4[t - 1] : make_float4(0.f, 0.f, 0.f, 0.f);
+        const float4 Rd = x4[t + 1];
+        const float4 Lm = t > 0 ? x4[W4 + t - 1] : make_float4(0.f, 0.f, 0.f, 0.f);
+        const float4 Ls = (!Mode<MODE>::h && t > 0) ? x4[2 * W4 + t - 1] : make_float4(0.f, 0.f, 0.f, 0.f);
+        const float dv[J + 3] = {Ld.z, Ld.w, gd4.x, gd4.y, gd4.z, gd4.w, Rd.x};   // D at k0-2 .. k0+4
+        const float mv[J + 1] = {Lm.w, gm4.x, gm4.y, gm4.z, gm4.w};              // g_mu at k0-1 .. k0+3
+        const float sv[J + 1] = {Ls.w, gs4.x, gs4.y, gs4.z, gs4.w};
+        const float *D = xch + buf * 3 * WB - kb;    // D[k] = g_Delta at detector k (row ends)
+        const float zh = 0.5f * g.zs * g.inv_du;
+        // g_delta = zs D^T g_Delta, D^T written out from the rows of D (a2):
+        //   y[q] = [q==0](-g0) + [q==1](g0) + [q==ND-2](-g_{ND-1}) + [q==ND-1](g_{ND-1})
+        //        + 1/2 g_{q-1} [1 <= q-1 <= ND-2] - 1/2 g_{q+1} [1 <= q+1 <= ND-2]   (all / du)
+        auto gdelta = [&](int i) {   // at position q = k0 - 1 + i, i = 0..4
+          const int q = k0 - 1 + i;
+          if (q >= 2 && q <= ND - 3) return zh * (dv[i] - dv[i + 2]);   // interior rows
+          float y = 0.f;
+          if (q == 0) y -= D[0];
+          if (q == 1) y += D[0];
+          if (q == ND - 2) y -= D[ND - 1];
+          if (q == ND - 1) y += D[ND - 1];
+          if (q - 1 >= 1 && q - 1 <= ND - 2) y += 0.5f * dv[i];
+          if (q + 1 >= 1 && q + 1 <= ND - 2) y -= 0.5f * dv[i + 2];
+          return g.zs * g.inv_du * y;
+        };
+        const float sc = __ldg(g.k3 + a).w;
+        const size_t rb = (size_t)row * g.RpG + g.PADG;
+        float gdl[J + 1];
+#pragma unroll
+        for (int i = 0; i <= J; ++i) gdl[i] = gdelta(i);
+#pragma unroll
+        for (int j = 0; j < J; ++j) {   // pair entries e = k0 + j: (g[e-1], g[e])
+          const int e = k0 + j;
+          if (e < e0 || e >= e1) continue;
+          const float m0 = e >= 1 ? mv[j] : 0.f, m1 = mv[j + 1];
+          const float d0 = e >= 1 ? gdl[j] : 0.f, d1 = gdl[j + 1];
           if (Mode<MODE>::h) {   // dS/dP_h = g_mu + z gamma D^T g_Delta (eq. 4 chain rule)
             g.GA1[rb + e] = make_float2(sc * (m0 + d0), sc * (m1 + d1));
             if (e == ND - 1) g.GA1[rb + ND] = make_float2(sc * (m1 + d1), 0.f);
           } else {
+            const float s0 = e >= 1 ? sv[j] : 0.f, s1 = sv[j + 1];
             g.GA[rb + e] = make_float4(sc * m0, sc * m1, sc * d0, sc * d1);
             g.GB[rb + e] = make_float2(sc * s0, sc * s1);
             if (e == ND - 1) {   // closing entry e = ND: (g[ND-1], 0)
@@ -377,7 +448,6 @@ __global__ void __maxnreg__(72) curve_kernel(K2Args g) {
       }
     }
   }
-  cp_wait<0>();
   pdl_trigger();
   if (Mode<MODE>::cost) {
     bad = __reduce_add_sync(0xffffffffu, bad);
@@ -391,7 +461,8 @@ __global__ void __maxnreg__(72) curve_kernel(K2Args g) {
   }
 }
 
-static size_t k2_smem(int NT) { return sizeof(float) * (size_t)NSTAGE * NQ * NT; }
+// dynamic shared memory: the ring (NST stages of nrows rows) + the exchange rows (2 x 3 rows)
+static size_t k2_smem(int nrows, int WB) { return sizeof(float) * (size_t)(NST * nrows + 6) * WB; }
 
 template <int MODE>
 cudaError_t launch(const ei_plan &p, const float *flat, const float *mask, const float *drift,
@@ -403,6 +474,7 @@ cudaError_t launch(const ei_plan &p, const float *flat, const float *mask, const
   g.RS = p.proj.RS;
   g.S = p.S;
   g.nmap = Mode<MODE>::h ? 1 : 3;
+  g.nrows = g.nmap + (Mode<MODE>::cost ? p.M : 0);
   g.rstride = (size_t)p.S * g.nmap * p.NA * p.ND;
   g.flat = flat;
   g.mask = mask;
@@ -413,6 +485,9 @@ cudaError_t launch(const ei_plan &p, const float *flat, const float *mask, const
   g.M = p.M;
   g.nseg = p.k2.nseg;
   g.W = p.k2.W;
+  g.WB = p.k2.W + 2 * J;
+  auto al = [](const void *q) { return ((uintptr_t)q & 15u) == 0; };
+  g.vec = (p.ND % 4 == 0) && al(p.P) && al(flat) && (!s_exp || al(s_exp)) ? 1 : 0;
   g.zs = (float)(p.g.z * (Mode<MODE>::h ? (double)gamma : 1.0));
   g.inv_du = (float)(1.0 / p.g.det_pitch);
   g.s_mod = s_mod;
@@ -427,34 +502,41 @@ cudaError_t launch(const ei_plan &p, const float *flat, const float *mask, const
   g.status = status;
   g.items = p.S * p.NA * p.k2.nseg;
   const int grid = std::min(g.items, p.k2.ctas);
-  const size_t smem = k2_smem(p.k2.NT);
+  const size_t smem = k2_smem(g.nrows, g.WB);
   cudaError_t e = cudaFuncSetAttribute((const void *)curve_kernel<MODE>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  e = launch_pdl(curve_kernel<MODE>, dim3(grid), dim3(p.k2.NT), smem, st, g);
+  e = launch_pdl(curve_kernel<MODE>, dim3(grid), dim3(p.k2.NT + 32), smem, st, g);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
 }  // namespace
 
-// K2 launch plan: segments of W = ceil(ND / nseg) positions, nseg the smallest count with
-// W + 4 <= 384 threads (balanced segments, <= ~10 % idle threads), CTA = W + 4 rounded up to a
-// warp; persistent grid = resident CTAs per SM x SMs.
+// K2 launch plan: segments of W positions (multiple of 4) with W / 4 + 2 <= 256 consumer threads
+// and a staging ring small enough for two CTAs per SM (<= 110 KB; the widest rows still fit one
+// CTA); consumers = W / 4 + 2 threads rounded up to a warp, plus the producer warp; persistent
+// grid = resident CTAs per SM x SMs.
 int plan_curve(ei_plan &p) {
+  const int nrows = 3 + p.M;
+  auto W_of = [&](int ns) { return (((p.ND + ns - 1) / ns) + 3) & ~3; };
   int nseg = 1;
-  while ((p.ND + nseg - 1) / nseg + 4 > 384) ++nseg;
+  while (W_of(nseg) / J + 2 > K2_MAXT ||
+         (k2_smem(nrows, W_of(nseg) + 2 * J) > 110 * 1024 && W_of(nseg) > 64))
+    ++nseg;
   p.k2.nseg = nseg;
-  p.k2.W = (p.ND + nseg - 1) / nseg;
-  p.k2.NT = ((p.k2.W + 4 + 31) / 32) * 32;
+  p.k2.W = W_of(nseg);
+  p.k2.NT = ((p.k2.W / J + 2 + 31) / 32) * 32;
   p.k2.nw = p.k2.NT / 32;
   if ((long long)p.S * p.NA * nseg > 0x7fffffffLL) return EI_ERR_RESOURCE;   // 32-bit item index
+  if (k2_smem(nrows, p.k2.W + 2 * J) > 220 * 1024) return EI_ERR_SHAPE;      // M too large
   int dev = 0, sms = 148, per = 1;
   if (cudaGetDevice(&dev) == cudaSuccess)
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaFuncSetAttribute((const void *)curve_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)k2_smem(p.k2.NT));
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, curve_kernel<1>, p.k2.NT, k2_smem(p.k2.NT)) != cudaSuccess || per < 1)
+  const size_t smem = k2_smem(nrows, p.k2.W + 2 * J);
+  cudaFuncSetAttribute((const void *)curve_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, curve_kernel<1>, p.k2.NT + 32, smem) != cudaSuccess ||
+      per < 1)
     per = 1;
   cudaGetLastError();
   p.k2.ctas = sms * per;
@@ -477,6 +559,12 @@ cudaError_t launch_curve_forward_h(const ei_plan &p, float gamma, const float *f
   return launch<3>(p, flat, mask, drift, nullptr, s_mod, nullptr, gamma, st);
 }
 
+cudaError_t launch_curve_cost_grad_h(const ei_plan &p, float gamma, const float *flat,
+                                     const float *mask, const float *drift, const float *s_exp,
+                                     int32_t *status, cudaStream_t st) {
+  return launch<2>(p, flat, mask, drift, s_exp, nullptr, status, gamma, st);
+}
+
 cudaError_t launch_curve_forward_hs(const ei_plan &p, float gamma, const float *fs, int n_knots,
                                     const float *mask, const float *drift, float *s_mod, cudaStream_t st) {
   return launch<5>(p, fs, mask, drift, nullptr, s_mod, nullptr, gamma, st, n_knots);
@@ -486,12 +574,6 @@ cudaError_t launch_curve_cost_grad_hs(const ei_plan &p, float gamma, const float
                                       const float *mask, const float *drift, const float *s_exp,
                                       int32_t *status, cudaStream_t st) {
   return launch<4>(p, fs, mask, drift, s_exp, nullptr, status, gamma, st, n_knots);
-}
-
-cudaError_t launch_curve_cost_grad_h(const ei_plan &p, float gamma, const float *flat,
-                                     const float *mask, const float *drift, const float *s_exp,
-                                     int32_t *status, cudaStream_t st) {
-  return launch<2>(p, flat, mask, drift, s_exp, nullptr, status, gamma, st);
 }
 
 }  // namespace ei

@@ -74,13 +74,17 @@ def ray_sample_updates(cfg) -> int:
     return total
 
 
-def kernel_bytes(cfg, rsu):
+def kernel_bytes(cfg, rsu, mirror_pairs=0):
     """Algorithmic bytes per launch (all S slices): K1/K3 gather 2 taps x 3 fp32 maps per
     ray-sample update (24 B, on-chip); K2 streams P (12 B) + s_exp (4M B) in and G (12 B) out
-    per (s, theta, t), flat (12 B) per (s, t)."""
+    per (s, theta, t), flat (12 B) per (s, t).  With mirror pairs (360-degree scans, theta and
+    theta + pi projected / back-projected once) K1 and K3 execute only the primaries' samples:
+    the executed share is (N_theta - pairs) / N_theta (the two angles of a pair have the same
+    sample count)."""
     S, NA, ND, M = cfg.S, cfg.n_angles, cfg.n_det, cfg.M
-    return {"K1_project": 24.0 * rsu * S,
-            "K3_backproject": 24.0 * rsu * S,
+    share = (NA - mirror_pairs) / NA
+    return {"K1_project": 24.0 * rsu * S * share,
+            "K3_backproject": 24.0 * rsu * S * share,
             "K2_curve": float(S * NA * ND * (12 + 4 * M + 12) + S * ND * 12)}
 
 
@@ -292,7 +296,7 @@ def run_gpu(args, cfg, rank, world, local_rank):
     peaks = load_peaks()
     ms_step = ms / K
     rsu = ray_sample_updates(cfg)
-    kb = kernel_bytes(cfg, rsu)
+    kb = kernel_bytes(cfg, rsu, plan_info.get("mirror_pairs", 0))
     per_kernel_ms = {k: v / max(n_rec, 1) for k, v in kern_ms.items()}
     dom = max(("K1_project", "K2_curve", "K3_backproject"), key=lambda k: per_kernel_ms[k])
     sm_mhz = clocks.get("sm_mhz") or peaks.get("sm_max_mhz", 1965.0)

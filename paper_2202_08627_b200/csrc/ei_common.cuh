@@ -26,6 +26,7 @@ struct Tables {
 struct ProjPlan {
   int2 *groups = nullptr;   // device: {first sorted position, count | ray_fast << 16} per group
   int *order = nullptr;     // device: sorted position -> angle index (row-dominant first)
+  int *partner = nullptr;   // device [NA]: the angle theta + pi of a projected angle, or -1
   int n_groups = 0;
   int RC = 0;               // rows per staged chunk
   int ray_fast = 0;         // number of angle groups using the ray-fastest consumer lane mapping
@@ -76,6 +77,13 @@ struct ei_plan {
   unsigned int *done3 = nullptr; // [S][tiles] K3 arrival counters (angle split)
   float *part3 = nullptr;        // [KS][S][3][N][N] K3 angle-split partial gradients
   int KS = 1;                    // K3 angle split
+  // 360-degree scans: angle pairs (theta, theta + pi) sample the same lines (mirrored detector,
+  // R6), so K1 projects only the primary angle of each pair and writes both rows, and K3 back-
+  // projects only primaries after the gradient rows are folded: G(a) += mirror(G(partner))
+  int npairs = 0;                // number of (primary, mirror) pairs
+  int NA3 = 0;                   // angles K3 back-projects (primaries + unpaired)
+  int *alist3 = nullptr;         // device [NA3] their indices
+  int2 *pairs = nullptr;         // device [npairs] (primary, mirror)
   int RB = 0;
   // host-I/O staging (ei_cost_grad_host), allocated on first use
   float *h_maps = nullptr, *h_flat = nullptr, *h_mask = nullptr, *h_drift = nullptr,
@@ -111,8 +119,11 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
   return cudaLaunchKernelEx(&cfg, kern, ((KArgs)args)...);
 }
 
-int plan_projector(ei_plan &p, const double *angles, std::vector<int2> &groups,
-                   std::vector<int> &order, std::vector<int2> &win1, std::vector<int2> &winRS);
+int plan_projector(ei_plan &p, const double *angles, const std::vector<int> &proj_angles,
+                   std::vector<int2> &groups, std::vector<int> &order, std::vector<int2> &win1,
+                   std::vector<int2> &winRS);
+// fold of mirror-pair gradient rows (k_pack.cu): G(primary) += mirror(G(mirror)), pair layout
+cudaError_t launch_fold(const ei_plan &p, int n_maps, cudaStream_t st);
 // K0 (k_pack.cu)
 struct SmallCheck {          // flat/mask/drift non-finite scan folded into K0
   const float *flat = nullptr, *mask = nullptr, *drift = nullptr;

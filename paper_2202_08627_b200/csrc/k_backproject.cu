@@ -105,7 +105,8 @@ __device__ __forceinline__ void finalize(const FinArgs &f, int s, int tid) {
 template <int NMAP>
 __global__ void __launch_bounds__(NT + 32, 3) backproject_kernel(
     const typename Layout<NMAP>::A *__restrict__ GA, const float2 *__restrict__ GB,
-    const float4 *__restrict__ k3, int N, int NA, int ND, const float *__restrict__ mu,
+    const float4 *__restrict__ k3, const int *__restrict__ alist, int NA3, int N, int NA, int ND,
+    const float *__restrict__ mu,
     const float *__restrict__ delta, const float *__restrict__ sigma, float lambda,
     float *__restrict__ o0, float *__restrict__ o1, float *__restrict__ o2, size_t out_stride,
     int S, int KS, float *__restrict__ part3, unsigned int *__restrict__ done3, int PADG, int RpG,
@@ -122,7 +123,7 @@ __global__ void __launch_bounds__(NT + 32, 3) backproject_kernel(
   const TA *GAs = GA + (size_t)s * NA * rowlen + PADG;
   const float2 *GBs = GB ? GB + (size_t)s * NA * rowlen + PADG : nullptr;
   // angle split (small grids): CTA ks owns chunks [c_lo, c_hi)
-  const int nch_all = (NA + CH - 1) / CH;
+  const int nch_all = (NA3 + CH - 1) / CH;   // chunks over the back-projected angles
   const int c_lo = (int)(((long long)ks * nch_all) / KS), c_hi = (int)(((long long)(ks + 1) * nch_all) / KS);
 
   if (tid == 0) {
@@ -145,10 +146,10 @@ __global__ void __launch_bounds__(NT + 32, 3) backproject_kernel(
     uint32_t ph = 0;
     for (int c = c_lo; c < c_hi; ++c) {
       if (c - c_lo >= NST) mbar_wait(&sm.empty[st], ph ^ 1);
-      const int na = min(CH, NA - c * CH);
+      const int na = min(CH, NA3 - c * CH);
       int ws = 0;
       if (lane < na) {   // per-angle table + window start (first tap entry - 1)
-        const int a = c * CH + lane;
+        const int a = __ldg(alist + c * CH + lane);
         const float4 g = __ldg(k3 + a);   // cdu, sdu, inv_h, scale
         const float k00 = fmaf(xa, g.x, fmaf(ya, g.y, dctr)), k01 = fmaf(xb, g.x, fmaf(ya, g.y, dctr));
         const float k10 = fmaf(xa, g.x, fmaf(yb, g.y, dctr)), k11 = fmaf(xb, g.x, fmaf(yb, g.y, dctr));
@@ -160,7 +161,7 @@ __global__ void __launch_bounds__(NT + 32, 3) backproject_kernel(
       if (lane == 0) mbar_arrive_expect_tx(&sm.full[st], (uint32_t)na * (bytesA + bytesB));
       __syncwarp();
       if (lane < na) {
-        const size_t row = (size_t)(c * CH + lane) * rowlen;
+        const size_t row = (size_t)__ldg(alist + c * CH + lane) * rowlen;
         // a window entirely off the detector only needs zeros: clamp its copy into the zero pad
         // (a window overlapping [0, ND] is always inside the PADG >= WL padding)
         const int e0 = min(max(ws + 1, -PADG), ND + PADG - WLB), eb = e0 & ~1;
@@ -191,7 +192,7 @@ __global__ void __launch_bounds__(NT + 32, 3) backproject_kernel(
   uint32_t ph = 0;
   for (int c = c_lo; c < c_hi; ++c) {
     mbar_wait(&sm.full[st], ph);
-    const int na = min(CH, NA - c * CH);
+    const int na = min(CH, NA3 - c * CH);
     for (int al = 0; al < na; ++al) {
       const float4 t = sm.tab[st][al];
       const int ws = sm.ws[st][al];
@@ -315,8 +316,8 @@ cudaError_t launch_bp(const ei_plan &p, const typename Layout<NMAP>::A *GA, cons
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   dim3 grid((p.N + TILE - 1) / TILE, (p.N + TILE - 1) / TILE, p.S * p.KS);
-  e = launch_pdl(backproject_kernel<NMAP>, grid, dim3(NT + 32), smem, st, GA, GB, p.tab.k3, p.N,
-                 p.NA, p.ND, mu, delta, sigma, lambda, o0, o1, o2, out_stride, p.S, p.KS, p.part3,
+  e = launch_pdl(backproject_kernel<NMAP>, grid, dim3(NT + 32), smem, st, GA, GB, p.tab.k3, p.alist3,
+                 p.NA3, p.N, p.NA, p.ND, mu, delta, sigma, lambda, o0, o1, o2, out_stride, p.S, p.KS, p.part3,
                  p.done3, p.PADG, p.RpG, fin);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();

@@ -9,7 +9,10 @@
 // so the projector only ever walks contiguous rows.
 // K0 also counts non-finite map elements into status[0] and emits per-tile sum(x^2) partials for
 // the eq. 5 regulariser.
+#include <algorithm>
+
 #include "ei_common.cuh"
+#include "tma.cuh"
 
 namespace ei {
 namespace {
@@ -141,7 +144,51 @@ __global__ void pack_sino_kernel(const float *__restrict__ in, int NA, int ND, i
 }
 
 
+// Mirror-pair fold (360-degree scans): the angle theta + pi sees the same lines as theta with the
+// detector mirrored, k -> ND-1-k (R6), so R^T g = sum over primaries of R_theta^T (g_theta +
+// mirror(g_{theta+pi})).  In the pair layout (entry e = (g[e-1], g[e])) the mirrored row's entry e
+// is the partner's entry ND-e with its two taps swapped.  In place on the primary rows; one thread
+// per (slice, pair, entry).
+template <int NMAP>
+__global__ void __launch_bounds__(256) fold_kernel(const int2 *__restrict__ pairs, int npairs, int NA,
+                                                   int ND, int S, float4 *__restrict__ GA,
+                                                   float2 *__restrict__ GB, float2 *__restrict__ GA1,
+                                                   int PADG, int RpG) {
+  pdl_wait();   // K2's (or pack_sino's) gradient rows
+  const long long rl = ND + 1, total = (long long)S * npairs * rl;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int e = (int)(t % rl);
+    const long long sp = t / rl;
+    const int q = (int)(sp % npairs), s = (int)(sp / npairs);
+    const int2 ab = __ldg(pairs + q);
+    const size_t oa = ((size_t)s * NA + ab.x) * RpG + PADG + e;
+    const size_t ob = ((size_t)s * NA + ab.y) * RpG + PADG + (ND - e);
+    if (NMAP == 3) {
+      const float4 x = GA[oa], y = GA[ob];
+      GA[oa] = make_float4(x.x + y.y, x.y + y.x, x.z + y.w, x.w + y.z);
+      const float2 u = GB[oa], v = GB[ob];
+      GB[oa] = make_float2(u.x + v.y, u.y + v.x);
+    } else {
+      const float2 u = GA1[oa], v = GA1[ob];
+      GA1[oa] = make_float2(u.x + v.y, u.y + v.x);
+    }
+  }
+  pdl_trigger();
+}
+
 }  // namespace
+
+cudaError_t launch_fold(const ei_plan &p, int n_maps, cudaStream_t st) {
+  if (p.npairs == 0) return cudaSuccess;
+  const long long total = (long long)p.S * p.npairs * (p.ND + 1);
+  const int blocks = (int)std::min<long long>((total + 255) / 256, 148 * 8);
+  if (n_maps == 3)
+    return launch_pdl(fold_kernel<3>, dim3(blocks), dim3(256), 0, st, (const int2 *)p.pairs, p.npairs,
+                      p.NA, p.ND, p.S, p.GA, p.GB, (float2 *)nullptr, p.PADG, p.RpG);
+  return launch_pdl(fold_kernel<1>, dim3(blocks), dim3(256), 0, st, (const int2 *)p.pairs, p.npairs,
+                    p.NA, p.ND, p.S, (float4 *)nullptr, (float2 *)nullptr, p.GA1, p.PADG, p.RpG);
+}
 
 int reg_blocks(int N) { return ((N + 1 + T - 1) / T) * ((N + 1 + T - 1) / T); }
 

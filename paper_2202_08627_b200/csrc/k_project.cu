@@ -63,6 +63,7 @@ struct ProjArgs {
   const float4 *k1;             // ic, tn, scale, rowdom
   const int2 *groups;           // {first sorted position, count}
   const int *order;             // sorted position -> angle index
+  const int *partner;           // angle -> its mirror angle theta + pi, or -1
   const int2 *win;              // [RS][groups][tiles][chunks] {cmin, W} (W = 0: chunk skipped)
   int N, NA, ND, S, RS, RC, CW, nch, PAD, Rp;
   float *P;                     // [RS][S][NMAP][NA][ND]
@@ -175,8 +176,11 @@ __global__ void __launch_bounds__(NT + 32, 2) project_kernel(ProjArgs args) {
   for (int m = 0; m < 4; ++m) {
     int lo = 0x7fffffff, hi = -0x7fffffff;
     if (aidx[m] >= 0 && k < ND) {
-      if (fabsf(tn[m]) < 1e-30f) {
-        if (alpha[m] > -1.f && alpha[m] < (float)N) { lo = 0; hi = N - 1; }
+      // x* varies by less than 1/4 entry over the map (e.g. exactly 90 deg, where tn ~ 6e-17 and
+      // the row bounds below would overflow int): the ray keeps all rows or none (conservatively
+      // wide: rows outside the map read the zero padding inside the staged window)
+      if (fabsf(tn[m]) * (float)N < 0.25f) {
+        if (alpha[m] > -1.25f && alpha[m] < (float)N + 0.25f) { lo = 0; hi = N - 1; }
       } else {
         float y0 = (alpha[m] + 1.f) / tn[m], y1 = (alpha[m] - (float)N) / tn[m];
         if (y0 > y1) { const float t = y0; y0 = y1; y1 = t; }
@@ -240,13 +244,24 @@ __global__ void __launch_bounds__(NT + 32, 2) project_kernel(ProjArgs args) {
   if (k >= ND) return;
   const size_t plane = (size_t)args.NA * ND;
   float *out = args.P + ((size_t)rs * args.S + s) * NMAP * plane + k;
+  float *outm = out + (ND - 1 - 2 * k);   // mirrored detector position ND-1-k
 #pragma unroll
   for (int m = 0; m < 4; ++m) {
     if (aidx[m] < 0) continue;
-    out[(size_t)aidx[m] * ND] = (am[m].x + am[m].y) * scale[m];
+    const float v0 = (am[m].x + am[m].y) * scale[m];
+    out[(size_t)aidx[m] * ND] = v0;
+    // the mirror angle theta + pi samples the same line at the mirrored detector position
+    // (R6: detector centred), so its projection is this value: one projection, two rows
+    const int b = __ldg(args.partner + aidx[m]);
+    if (b >= 0) outm[(size_t)b * ND] = v0;
     if constexpr (NMAP == 3) {
-      out[plane + (size_t)aidx[m] * ND] = (ad[m].x + ad[m].y) * scale[m];
-      out[2 * plane + (size_t)aidx[m] * ND] = (as[m].x + as[m].y) * scale[m];
+      const float v1 = (ad[m].x + ad[m].y) * scale[m], v2 = (as[m].x + as[m].y) * scale[m];
+      out[plane + (size_t)aidx[m] * ND] = v1;
+      out[2 * plane + (size_t)aidx[m] * ND] = v2;
+      if (b >= 0) {
+        outm[plane + (size_t)b * ND] = v1;
+        outm[2 * plane + (size_t)b * ND] = v2;
+      }
     }
   }
 }
@@ -262,6 +277,7 @@ cudaError_t launch(const ei_plan &p, int RS, float *P, cudaStream_t st) {
   a.k1 = p.tab.k1;
   a.groups = p.proj.groups;
   a.order = p.proj.order;
+  a.partner = p.proj.partner;
   a.win = RS == 1 ? p.proj.win1 : p.proj.winRS;
   a.N = p.N; a.NA = p.NA; a.ND = p.ND; a.S = p.S; a.RS = RS; a.RC = p.proj.RC; a.CW = p.proj.CW;
   a.PAD = p.proj.PAD; a.Rp = p.proj.Rp;
@@ -387,12 +403,13 @@ static double wavefront_model(const ei_plan &p, const double *angles, const std:
   return n ? wf / n : 0.0;
 }
 
-int plan_projector(ei_plan &p, const double *angles, std::vector<int2> &groups,
-                   std::vector<int> &order, std::vector<int2> &win1, std::vector<int2> &winRS) {
-  const int NA = p.NA, N = p.N, ND = p.ND;
+int plan_projector(ei_plan &p, const double *angles, const std::vector<int> &proj_angles,
+                   std::vector<int2> &groups, std::vector<int> &order, std::vector<int2> &win1,
+                   std::vector<int2> &winRS) {
+  const int N = p.N, ND = p.ND;
+  const int NA = (int)proj_angles.size();   // the angles K1 projects (mirror pairs: primaries)
   // groups = runs of angularly adjacent angles (sorted by angle mod 2 pi) of one dominance class
-  std::vector<int> idx(NA);
-  for (int a = 0; a < NA; ++a) idx[a] = a;
+  std::vector<int> idx(proj_angles);
   auto wrap = [](double t) { t = fmod(t, 2 * M_PI); return t < 0 ? t + 2 * M_PI : t; };
   std::stable_sort(idx.begin(), idx.end(), [&](int x, int y) { return wrap(angles[x]) < wrap(angles[y]); });
   auto rowdom = [&](int a) { return fabs(cos(angles[a])) >= fabs(sin(angles[a])); };

@@ -7,6 +7,7 @@
 #include <string.h>
 
 #include <algorithm>
+#include <utility>
 #include <new>
 #include <vector>
 
@@ -59,7 +60,8 @@ void free_plan(ei_plan *p) {
   }
   for (cudaEvent_t ev : p->h_ev)
     if (ev) cudaEventDestroy(ev);
-  void *ptrs[] = {p->tab.k1, p->tab.k3, p->proj.groups, p->proj.order, p->proj.win1, p->proj.winRS, p->MA, p->MAT, p->MB,
+  void *ptrs[] = {p->tab.k1, p->tab.k3, p->proj.groups, p->proj.order, p->proj.partner, p->alist3,
+                  p->pairs, p->proj.win1, p->proj.winRS, p->MA, p->MAT, p->MB,
                   p->MBT, p->M1, p->M1T, p->diag, p->part_mo, p->done3, p->part3, p->P, p->GA, p->GB, p->GA1,
                   p->part_curve, p->part_reg, p->h_maps, p->h_flat, p->h_mask, p->h_drift,
                   p->h_sexp, p->h_grad, p->h_cost, p->h_status};
@@ -123,9 +125,45 @@ int ei_plan_create(const ei_geometry *geom, const double *angles, ei_plan **out)
     k3[a] = make_float4((float)(c * dx / du), (float)(s * dx / du), (float)(du / (fabs(cd) * dx)),
                         (float)(dx / fabs(cd)));
   }
+  // mirror pairs of 360-degree scans: theta and theta + pi (mod 2 pi, to 1e-9 rad) sample the same
+  // lines with the detector mirrored (R6), so only the primary (angle mod 2 pi < pi) is projected
+  // and back-projected (tuning knob EI_MIRROR=0 switches this off)
+  std::vector<int> partner(NA, -1), prim;
+  std::vector<int2> pairs;
+  {
+    const char *env = getenv("EI_MIRROR");
+    if (!env || atoi(env) != 0) {
+      auto wrap = [](double t) { t = fmod(t, 2 * M_PI); return t < 0 ? t + 2 * M_PI : t; };
+      std::vector<std::pair<double, int>> w(NA);
+      for (int a = 0; a < NA; ++a) w[a] = {wrap(angles[a]), a};
+      std::sort(w.begin(), w.end());
+      std::vector<char> used(NA, 0);
+      for (int q = 0; q < NA; ++q) {
+        const double ta = w[q].first;
+        const int a = w[q].second;
+        if (ta >= M_PI || used[a]) continue;
+        auto it = std::lower_bound(w.begin(), w.end(), std::make_pair(ta + M_PI - 1e-9, -1));
+        for (; it != w.end() && it->first <= ta + M_PI + 1e-9; ++it) {
+          const int b = it->second;
+          if (b != a && !used[b]) {
+            partner[a] = b;
+            used[a] = used[b] = 1;
+            pairs.push_back(make_int2(a, b));
+            break;
+          }
+        }
+      }
+    }
+    std::vector<char> is_mirror(NA, 0);
+    for (const int2 &q : pairs) is_mirror[q.y] = 1;
+    for (int a = 0; a < NA; ++a)
+      if (!is_mirror[a]) prim.push_back(a);
+  }
+  p->npairs = (int)pairs.size();
+  p->NA3 = (int)prim.size();
   std::vector<int2> groups, win1, winRS;
   std::vector<int> order;
-  rc = ei::plan_projector(*p, angles, groups, order, win1, winRS);
+  rc = ei::plan_projector(*p, angles, prim, groups, order, win1, winRS);
   if (!rc) rc = ei::plan_curve(*p);
   if (rc) {
     delete[] k1;
@@ -142,6 +180,9 @@ int ei_plan_create(const ei_geometry *geom, const double *angles, ei_plan **out)
   A(dalloc(&p->tab.k3, NA));
   A(dalloc(&p->proj.groups, groups.size()));
   A(dalloc(&p->proj.order, order.size()));
+  A(dalloc(&p->proj.partner, NA));
+  A(dalloc(&p->alist3, prim.size()));
+  if (!pairs.empty()) A(dalloc(&p->pairs, pairs.size()));
   A(dalloc(&p->proj.win1, win1.size()));
   if (!winRS.empty()) A(dalloc(&p->proj.winRS, winRS.size()));
   A(dalloc(&p->MA, S * NP));
@@ -166,7 +207,7 @@ int ei_plan_create(const ei_geometry *geom, const double *angles, ei_plan **out)
   {
     const long long ctas = (long long)ei::bp_tiles(p->N) * p->S;
     int KS = 1;
-    while (KS < 16 && KS + 1 <= std::max(1, ei::bp_chunks(p->NA) / 2) && ctas * (KS + 1) <= 2 * 148) ++KS;
+    while (KS < 16 && KS + 1 <= std::max(1, ei::bp_chunks(p->NA3) / 2) && ctas * (KS + 1) <= 2 * 148) ++KS;
     if (const char *e = getenv("EI_K3_KS")) KS = std::max(1, std::min(16, atoi(e)));   // tuning knob
     p->KS = KS;
   }
@@ -178,6 +219,12 @@ int ei_plan_create(const ei_geometry *geom, const double *angles, ei_plan **out)
     A(cudaMemcpy(p->proj.groups, groups.data(), sizeof(int2) * groups.size(), cudaMemcpyHostToDevice));
   if (e == cudaSuccess)
     A(cudaMemcpy(p->proj.order, order.data(), sizeof(int) * order.size(), cudaMemcpyHostToDevice));
+  if (e == cudaSuccess)
+    A(cudaMemcpy(p->proj.partner, partner.data(), sizeof(int) * NA, cudaMemcpyHostToDevice));
+  if (e == cudaSuccess)
+    A(cudaMemcpy(p->alist3, prim.data(), sizeof(int) * prim.size(), cudaMemcpyHostToDevice));
+  if (e == cudaSuccess && !pairs.empty())
+    A(cudaMemcpy(p->pairs, pairs.data(), sizeof(int2) * pairs.size(), cudaMemcpyHostToDevice));
   if (e == cudaSuccess) A(cudaMemset(p->diag, 0, sizeof(int32_t)));
   // the zero padding of the map rows is written once here; K0 only writes the interior
   for (void *q : {(void *)p->MA, (void *)p->MAT})
@@ -211,7 +258,7 @@ int ei_plan_stats(const ei_plan *p, int64_t out[6]) {
   return EI_OK;
 }
 
-int ei_plan_info(const ei_plan *p, int64_t out[8]) {
+int ei_plan_info(const ei_plan *p, int64_t out[10]) {
   if (!p || !out) return EI_ERR_NULL;
   int32_t d = 0;
   if (cudaMemcpy(&d, p->diag, sizeof(d), cudaMemcpyDeviceToHost) != cudaSuccess) return EI_ERR_CUDA;
@@ -223,6 +270,8 @@ int ei_plan_info(const ei_plan *p, int64_t out[8]) {
   out[5] = (int64_t)4 * p->proj.RC * (p->proj.CW * 16 + (p->proj.CW + 2) * 8);
   out[6] = p->proj.ray_fast;
   out[7] = p->KS;
+  out[8] = p->npairs;
+  out[9] = p->k2.nseg;
   return EI_OK;
 }
 
@@ -296,18 +345,20 @@ int ei_backproject(const ei_plan *p, const float *sino, int n_maps, float *maps,
   cudaError_t e;
   if (n_maps == 3) {
     e = ei::launch_pack_sino(*p, sino, 3, st);
+    if (e == cudaSuccess) e = ei::launch_fold(*p, 3, st);
     if (e == cudaSuccess)
       e = ei::launch_backproject3(*p, nullptr, nullptr, nullptr, 0.f, maps, maps + NN,
                                   maps + 2 * NN, 3 * NN, nullptr, st);
     p->stats[2] += 1;
     p->stats[3] += 3;
-    p->stats[5] += 2;
+    p->stats[5] += 2 + (p->npairs > 0);
   } else {
     e = ei::launch_pack_sino(*p, sino, 1, st);
+    if (e == cudaSuccess) e = ei::launch_fold(*p, 1, st);
     if (e == cudaSuccess) e = ei::launch_backproject1(*p, maps, st);
     p->stats[2] += 1;
     p->stats[3] += 1;
-    p->stats[5] += 2;
+    p->stats[5] += 2 + (p->npairs > 0);
   }
   return cuda_status(e);
 }
@@ -353,11 +404,12 @@ int cost_grad_impl(const ei_plan *p, const float *mu, const float *delta, const 
   if (e == cudaSuccess && sexp_ready) e = cudaStreamWaitEvent(st, sexp_ready, 0);
   if (e == cudaSuccess) e = ei::launch_curve_cost_grad(*p, flat, mask, drift, s_exp, status, st);  // K2
   mark(3);
+  if (e == cudaSuccess) e = ei::launch_fold(*p, 3, st);                              // mirror pairs
   ei::Finalize fin{cost, g_drift};
   if (e == cudaSuccess) e = ei::launch_backproject3(*p, mu, delta, sigma, lambda, g_mu, g_delta,
                                                     g_sigma, NN, &fin, st);            // K3 + K4
   mark(4);
-  p->stats[5] += 4;
+  p->stats[5] += 4 + (p->npairs > 0);
   p->stats[0] += 1;
   p->stats[1] += 3;
   p->stats[2] += 1;
@@ -416,6 +468,7 @@ int ei_cost_grad_h(const ei_plan *p, const float *h, float gamma, const float *f
   if (e == cudaSuccess)
     e = ei::launch_curve_cost_grad_h(*p, gamma, flat, mask, drift, s_exp, status, st);  // K2
   mark(3);
+  if (e == cudaSuccess) e = ei::launch_fold(*p, 1, st);                              // mirror pairs
   ei::Finalize fin{cost, g_drift};
   if (e == cudaSuccess) e = ei::launch_backproject1(*p, g_h, st, h, lambda, &fin);   // K3 + K4
   mark(4);
@@ -424,7 +477,7 @@ int ei_cost_grad_h(const ei_plan *p, const float *h, float gamma, const float *f
   p->stats[2] += 1;
   p->stats[3] += 1;
   p->stats[4] += 1;
-  p->stats[5] += 4;
+  p->stats[5] += 4 + (p->npairs > 0);
   return cuda_status(e);
 }
 
@@ -458,6 +511,7 @@ int ei_cost_grad_hs(const ei_plan *p, const float *h, float gamma, const float *
   if (e == cudaSuccess) e = ei::launch_project1(*p, p->P, st, p->proj.RS);           // K1
   if (e == cudaSuccess)
     e = ei::launch_curve_cost_grad_hs(*p, gamma, flat_samples, n_knots, mask, drift, s_exp, status, st);
+  if (e == cudaSuccess) e = ei::launch_fold(*p, 1, st);                              // mirror pairs
   ei::Finalize fin{cost, g_drift};
   if (e == cudaSuccess) e = ei::launch_backproject1(*p, g_h, st, h, lambda, &fin);   // K3 + K4
   p->stats[0] += 1;
@@ -465,7 +519,7 @@ int ei_cost_grad_hs(const ei_plan *p, const float *h, float gamma, const float *
   p->stats[2] += 1;
   p->stats[3] += 1;
   p->stats[4] += 1;
-  p->stats[5] += 4;
+  p->stats[5] += 4 + (p->npairs > 0);
   return cuda_status(e);
 }
 

@@ -36,6 +36,9 @@ def cached_case(name: str) -> synth.Case:
     if name == "R2":   # 180-degree span, even sizes, no drift, M=1 (the paper's single-offset case)
         return oracle_case(synth.small_config("R2", S=1, N=40, n_angles=24, span_deg=180.0, n_det=58,
                                               M=1, K=4, drift_sd=0.0, w_jit=0.0, texture=0.0, seed=91))
+    if name == "R3":   # 360-degree scan with an even angle count: mirror pairs (theta, theta + pi)
+        return oracle_case(synth.small_config("R3", S=2, N=48, n_angles=40, span_deg=360.0, n_det=70,
+                                              M=3, K=5, drift_sd=0.002, w_jit=0.1, texture=0.05, seed=95))
     raise KeyError(name)
 
 

@@ -19,7 +19,7 @@ for w in $WHAT; do
       timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1; echo "smoke rc=$?" | tee -a $OUT/rc.txt
       tail -1 $OUT/smoke.log ;;
     bench)
-      for c in C2 C1 C3 C5 C4; do
+      for c in C2 C1 C3 C5 C4 P1; do
         timeout 600 python bench.py --config $c > $OUT/bench_$c.json 2> $OUT/bench_$c.err; echo "bench $c rc=$?" | tee -a $OUT/rc.txt
         python - $OUT/bench_$c.json <<'EOF'
 import json, sys

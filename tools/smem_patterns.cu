@@ -96,6 +96,33 @@ int main(int argc, char **argv) {
     run<float4><<<148 * 2, 512>>>(d, 4000, out);
     printf("probe %d launched (float2, float4)\n", m);
   }
+  if (argc > 2) {   // K1 patterns for a given angle step (deg) and N: angle-fast and ray-fast
+    const double stepdeg = atof(argv[1]);
+    const int Nmap = atoi(argv[2]);
+    for (int m = 0; m < 2; ++m) {
+      for (int p = 0; p < NPAT; ++p) {
+        const double th0 = (M_PI / 2) * (p + 0.5) / NPAT - M_PI / 4;
+        const double step = stepdeg * M_PI / 180;
+        const double y = (rand() % Nmap) - Nmap / 2.0;
+        const double r0 = (rand() % Nmap) - Nmap / 2.0;
+        int mn = 1 << 30;
+        int k[32];
+        for (int l = 0; l < 32; ++l) {
+          const int a = m == 0 ? (l & 3) : (l >> 3), r = m == 0 ? (l >> 2) : (l & 7);
+          const double th = th0 + a * step, c = cos(th), s = sin(th);
+          k[l] = (int)floor((r0 + r) / c - y * s / c + 4000.0);
+          mn = k[l] < mn ? k[l] : mn;
+        }
+        for (int l = 0; l < 32; ++l) h[p * 32 + l] = k[l] - mn;
+      }
+      cudaMemcpy(d, h.data(), h.size() * 4, cudaMemcpyHostToDevice);
+      run<float2><<<148 * 2, 512>>>(d, 4000, out);
+      run<float4><<<148 * 2, 512>>>(d, 4000, out);
+      printf("sweep step %g N %d mapping %d launched (float2, float4)\n", stepdeg, Nmap, m);
+    }
+    cudaDeviceSynchronize();
+    return 0;
+  }
   // ---- K1: lane -> (angle a of 16 adjacent angles at 0.25 deg, ray r), row y ----
   // x*(a, r, y) = r / cos - y tan + ctr, pair entry floor(x*)
   for (int m = 0; m <= 4; ++m) {

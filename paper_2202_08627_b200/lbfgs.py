@@ -163,3 +163,25 @@ def ei_objective(plan, flat, mask, drift, s_exp, lam: float = 1e-2, ws=None):
                         ws.g[2], ws.status)
         return ws.cost.clone(), ws.g.clone()
     return fg
+
+
+def ei_objective_h(plan, gamma: float, flat, mask, drift, s_exp, lam: float = 1e-2,
+                   flat_samples: bool = False):
+    """fg(x) for x = [1, S, N, N] (the paper's single map h, eq. 4 with mu = gamma^-1 delta = h,
+    PAPER.md:64) through `ei_cost_grad_h`, or `ei_cost_grad_hs` when `flat` holds the sampled flat
+    IC [S][K][N_d] (flat_samples=True)."""
+    from . import ei
+    S, N, NA, ND, M = plan.shape
+    cost = torch.zeros(S, dtype=torch.float64, device=s_exp.device)
+    g = torch.zeros(1, S, N, N, dtype=torch.float32, device=s_exp.device)
+    status = torch.zeros(4, dtype=torch.int32, device=s_exp.device)
+
+    def fg(x: torch.Tensor):
+        x = x.contiguous()
+        status.zero_()
+        if flat_samples:
+            ei.ei_cost_grad_hs(plan, x[0], gamma, flat, mask, drift, s_exp, lam, cost, g[0], None, status)
+        else:
+            ei.ei_cost_grad_h(plan, x[0], gamma, flat, mask, drift, s_exp, lam, cost, g[0], None, status)
+        return cost.clone(), g.clone()
+    return fg

@@ -75,3 +75,22 @@ def test_null_arguments(ei):
         assert f(None, None, 3, None, None) == 1
     lib.ei_plan_stats.argtypes = [ctypes.c_void_p, ctypes.c_void_p]
     assert lib.ei_plan_stats(None, None) == 1
+
+
+def test_null_arguments_extended_entry_points(ei):
+    """The NEXT-2/3/4 entry points reject a NULL plan or array synchronously (EI_ERR_NULL = 1)."""
+    lib = ctypes.CDLL(ei.LIB_PATH)
+    vp, f, i = ctypes.c_void_p, ctypes.c_float, ctypes.c_int
+    lib.ei_cost_grad_drift.argtypes = [vp] * 8 + [f] + [vp] * 6 + [vp]
+    assert lib.ei_cost_grad_drift(*([None] * 8), 0.0, *([None] * 6), None) == 1
+    lib.ei_forward_h.argtypes = [vp, vp, f] + [vp] * 4 + [vp]
+    assert lib.ei_forward_h(None, None, 5.0, None, None, None, None, None) == 1
+    lib.ei_cost_grad_h.argtypes = [vp, vp, f] + [vp] * 4 + [f] + [vp] * 4 + [vp]
+    assert lib.ei_cost_grad_h(None, None, 5.0, None, None, None, None, 0.0, None, None, None, None, None) == 1
+    lib.ei_forward_hs.argtypes = [vp, vp, f, vp, i] + [vp] * 3 + [vp]
+    assert lib.ei_forward_hs(None, None, 5.0, None, 33, None, None, None, None) == 1
+    lib.ei_cost_grad_hs.argtypes = [vp, vp, f, vp, i] + [vp] * 3 + [f] + [vp] * 4 + [vp]
+    assert lib.ei_cost_grad_hs(None, None, 5.0, None, 33, None, None, None, 0.0, None, None, None, None,
+                               None) == 1
+    lib.ei_plan_info.argtypes = [vp, vp]
+    assert lib.ei_plan_info(None, None) == 1

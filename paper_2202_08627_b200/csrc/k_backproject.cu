@@ -134,9 +134,11 @@ __global__ void __launch_bounds__(NT + 32, 3) backproject_kernel(
     mbar_fence_init();
   }
   __syncthreads();
-  pdl_wait();   // K2's gradient sinograms and partials (the prologue overlapped K2's tail)
 
+  // PDL: the producer (TMA of K2's gradient rows) and the finalize CTAs (K2's partials) wait for
+  // K2; the other consumers only read what the producer staged
   if (w == NT / 32) {   // ---------------- producer warp ----------------
+    pdl_wait();   // K2's gradient sinograms
     // tile corners (full 32x32 tile, even past the map edge, so every lane indexes the window)
     const float xa = (float)j0 - ctr, xb = xa + (float)(TILE - 1);
     const float ya = (float)i0 - ctr, yb = ya + (float)(TILE - 1);
@@ -177,7 +179,10 @@ __global__ void __launch_bounds__(NT + 32, 3) backproject_kernel(
   // fused K4 (cost path): while the producer fills the ring, CTA (0, 0, s) of angle split 0 sums
   // K2's per-segment partials of slice s in index order (+ lambda * K0's sum x^2 partials) and
   // the per-angle drift gradient
-  if (fin.cost && blockIdx.x == 0 && blockIdx.y == 0 && ks == 0) finalize(fin, s, tid);
+  if (fin.cost && blockIdx.x == 0 && blockIdx.y == 0 && ks == 0) {
+    pdl_wait();   // K2's partials
+    finalize(fin, s, tid);
+  }
   const int row = 4 * w + (lane >> 3), lx = lane & 7;
   const float yi = (float)(i0 + row) - ctr;
   float xq[4];

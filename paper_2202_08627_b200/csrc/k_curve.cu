@@ -144,13 +144,15 @@ __global__ void __launch_bounds__(K2_MAXT + 32, 2) curve_kernel(K2Args g) {
     mbar_fence_init();
   }
   __syncthreads();
-  pdl_wait();   // K1's projections
   // static contiguous split of the items (deterministic, independent of timing)
   const int i0 = (int)(((long long)blockIdx.x * g.items) / gridDim.x);
   const int i1 = (int)(((long long)(blockIdx.x + 1) * g.items) / gridDim.x);
   const Pos p0{i0 / (g.nseg * g.NA), (i0 / g.NA) % g.nseg, i0 % g.NA};
 
+  // PDL: only the producer reads K1's output (the projections, via TMA); the consumers' G and
+  // partial writes are read only by this call's K3
   if (wid == nw) {   // ---------------- producer warp ----------------
+    pdl_wait();   // K1's projections
     Pos q = p0;
     int st = 0;
     uint32_t ph = 0;

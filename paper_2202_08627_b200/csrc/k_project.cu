@@ -124,9 +124,11 @@ __global__ void __launch_bounds__(NT + 32, 2) project_kernel(ProjArgs args) {
     mbar_fence_init();
   }
   __syncthreads();
-  pdl_wait();   // K0's packed maps (the prologue above overlapped K0's tail)
 
+  // PDL: only the producer reads K0's output (the packed maps, via TMA); the consumers' prologue
+  // (tables, row ranges) overlaps K0's tail and their P writes are read only by this call's K2
   if (w == NCW) {   // ---------------- producer warp ----------------
+    pdl_wait();   // K0's packed maps
     if (lane == 0) {
       int st = 0;
       uint32_t ph = 0;

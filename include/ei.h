@@ -146,11 +146,14 @@ int ei_cost_grad_hs(const ei_plan *plan, const float *h, float gamma, const floa
 
 /* ei_cost_grad with HOST buffers (same shapes and meaning; status is overwritten, not
  * accumulated).  Copies inputs host->device, evaluates, copies cost, gradients and status
- * back, and synchronises `stream` before returning.  The maps/flat/mask/drift upload runs on
- * `stream`; the s_exp upload (the bulk of the bytes) runs on an internal copy stream of the
- * plan and overlaps K0/K1, K2 waiting for it.  Pinned host memory makes the copies
- * asynchronous DMA.  Device staging buffers, the copy stream and its events are created by the
- * first call on a plan and kept until ei_plan_destroy (EI_ERR_RESOURCE if that fails). */
+ * back, and returns when they are complete.  The work is ordered after everything already
+ * queued on `stream` and runs on the plan's own streams: the maps/flat/mask/drift upload first,
+ * the s_exp upload (the bulk of the bytes) on a copy stream overlapping K0/K1 (K2 waits for it).
+ * With pinned host memory the whole call is captured once into a CUDA graph and replayed while
+ * the 13 pointers and lambda stay the same (one launch instead of ~20 API calls; env
+ * EI_HOST_GRAPH=0 disables; pageable memory falls back to direct calls).  Device staging
+ * buffers, streams, events and the graph belong to the plan (created by the first call, kept
+ * until ei_plan_destroy; EI_ERR_RESOURCE if that fails). */
 int ei_cost_grad_host(ei_plan *plan, const float *mu, const float *delta, const float *sigma,
                       const float *flat, const float *mask_pos, const float *drift,
                       const float *s_exp, float lambda, double *cost, float *g_mu, float *g_delta,

@@ -50,6 +50,22 @@ struct CurvePlan {
 
 }  // namespace ei
 
+// arguments of an ei_cost_grad_host call (the captured graph is valid for exactly these)
+struct HostKey {
+  const void *p[13];
+  float lambda;
+  HostKey() : p{}, lambda(0.f) {}
+  HostKey(const void *a, const void *b, const void *c, const void *d, const void *e, const void *f,
+          const void *g, float lam, const void *h, const void *i, const void *j, const void *k,
+          const void *l)
+      : p{a, b, c, d, e, f, g, h, i, j, k, l, nullptr}, lambda(lam) {}
+  bool operator==(const HostKey &o) const {
+    for (int q = 0; q < 13; ++q)
+      if (p[q] != o.p[q]) return false;
+    return lambda == o.lambda;
+  }
+};
+
 struct ei_plan {
   ei_geometry g{};
   int S = 0, N = 0, NA = 0, ND = 0, M = 0;
@@ -91,7 +107,12 @@ struct ei_plan {
   double *h_cost = nullptr;
   int32_t *h_status = nullptr;
   cudaStream_t h_copy = nullptr;            // s_exp upload stream (host path)
-  cudaEvent_t h_ev[2] = {nullptr, nullptr}; // small inputs uploaded / s_exp uploaded
+  cudaStream_t h_work = nullptr;            // host path work stream (graph capture / replay)
+  cudaEvent_t h_ev[3] = {nullptr, nullptr, nullptr};   // small inputs up / s_exp up / caller order
+  cudaGraphExec_t h_exec = nullptr;         // captured host path, replayed for the same arguments
+  HostKey h_key{};
+  int64_t h_stats[6] = {0, 0, 0, 0, 0, 0};  // launch accounting of one captured call
+  bool h_graph_failed = false;
   // launch accounting
   mutable int64_t stats[6] = {0, 0, 0, 0, 0, 0};
   // optional per-kernel timing of ei_cost_grad: 7 events per recorded evaluation

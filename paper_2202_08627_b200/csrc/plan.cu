@@ -54,10 +54,12 @@ void free_timing(ei_plan *p) {
 void free_plan(ei_plan *p) {
   if (!p) return;
   free_timing(p);
-  if (p->h_copy) {
-    cudaStreamSynchronize(p->h_copy);
-    cudaStreamDestroy(p->h_copy);
-  }
+  if (p->h_exec) cudaGraphExecDestroy(p->h_exec);
+  for (cudaStream_t q : {p->h_copy, p->h_work})
+    if (q) {
+      cudaStreamSynchronize(q);
+      cudaStreamDestroy(q);
+    }
   for (cudaEvent_t ev : p->h_ev)
     if (ev) cudaEventDestroy(ev);
   void *ptrs[] = {p->tab.k1, p->tab.k3, p->proj.groups, p->proj.order, p->proj.partner, p->alist3,
@@ -523,6 +525,47 @@ int ei_cost_grad_hs(const ei_plan *p, const float *h, float gamma, const float *
   return cuda_status(e);
 }
 
+namespace {
+// the host path's device work (uploads, K0..K3, downloads) enqueued on st (+ the copy stream)
+int enqueue_host_path(ei_plan *p, const float *mu, const float *delta, const float *sigma,
+                      const float *flat, const float *mask, const float *drift, const float *s_exp,
+                      float lambda, double *cost, float *g_mu, float *g_delta, float *g_sigma,
+                      int32_t *status, cudaStream_t st) {
+  const size_t S = p->S, NN = (size_t)p->N * p->N, ND = p->ND, NA = p->NA, M = p->M;
+  const size_t nsexp = S * NA * M * ND;
+  cudaError_t e = cudaSuccess;
+  auto A = [&](cudaError_t r) { if (e == cudaSuccess) e = r; };
+  const cudaMemcpyKind H2D = cudaMemcpyHostToDevice, D2H = cudaMemcpyDeviceToHost;
+  // the small inputs first on the compute stream, so K0/K1 start after ~1/6 of the bytes; the
+  // s_exp upload (the bulk: M values per ray) follows on the copy stream, overlapping K0 and K1,
+  // and K2 waits for it (event h_ev[1])
+  float *dmu = p->h_maps, *ddl = p->h_maps + S * NN, *dsg = p->h_maps + 2 * S * NN;
+  A(cudaMemcpyAsync(dmu, mu, sizeof(float) * S * NN, H2D, st));
+  A(cudaMemcpyAsync(ddl, delta, sizeof(float) * S * NN, H2D, st));
+  A(cudaMemcpyAsync(dsg, sigma, sizeof(float) * S * NN, H2D, st));
+  A(cudaMemcpyAsync(p->h_flat, flat, sizeof(float) * S * 3 * ND, H2D, st));
+  A(cudaMemcpyAsync(p->h_mask, mask, sizeof(float) * M, H2D, st));
+  if (drift) A(cudaMemcpyAsync(p->h_drift, drift, sizeof(float) * NA, H2D, st));
+  A(cudaMemsetAsync(p->h_status, 0, sizeof(int32_t) * 4, st));
+  A(cudaEventRecord(p->h_ev[0], st));
+  A(cudaStreamWaitEvent(p->h_copy, p->h_ev[0], 0));
+  A(cudaMemcpyAsync(p->h_sexp, s_exp, sizeof(float) * nsexp, H2D, p->h_copy));
+  A(cudaEventRecord(p->h_ev[1], p->h_copy));
+  if (e != cudaSuccess) return EI_ERR_CUDA;
+  float *gm = p->h_grad, *gd = p->h_grad + S * NN, *gs = p->h_grad + 2 * S * NN;
+  int rc = cost_grad_impl(p, dmu, ddl, dsg, p->h_flat, p->h_mask, drift ? p->h_drift : nullptr,
+                          p->h_sexp, lambda, p->h_cost, gm, gd, gs, nullptr, p->h_status, st,
+                          p->h_ev[1]);
+  if (rc) return rc;
+  A(cudaMemcpyAsync(cost, p->h_cost, sizeof(double) * S, D2H, st));
+  A(cudaMemcpyAsync(g_mu, gm, sizeof(float) * S * NN, D2H, st));
+  A(cudaMemcpyAsync(g_delta, gd, sizeof(float) * S * NN, D2H, st));
+  A(cudaMemcpyAsync(g_sigma, gs, sizeof(float) * S * NN, D2H, st));
+  A(cudaMemcpyAsync(status, p->h_status, sizeof(int32_t) * 4, D2H, st));
+  return e == cudaSuccess ? EI_OK : EI_ERR_CUDA;
+}
+}  // namespace
+
 int ei_cost_grad_host(ei_plan *p, const float *mu, const float *delta, const float *sigma,
                       const float *flat, const float *mask, const float *drift,
                       const float *s_exp, float lambda, double *cost, float *g_mu, float *g_delta,
@@ -556,47 +599,65 @@ int ei_cost_grad_host(ei_plan *p, const float *mu, const float *delta, const flo
       return EI_ERR_RESOURCE;
     }
   }
-  if (!p->h_copy) {   // copy stream + events for the s_exp upload (created once per plan)
+  if (!p->h_copy) {   // work + copy streams and events of the host path (created once per plan)
     cudaError_t e = cudaStreamCreateWithFlags(&p->h_copy, cudaStreamNonBlocking);
-    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->h_ev[0], cudaEventDisableTiming);
-    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&p->h_ev[1], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p->h_work, cudaStreamNonBlocking);
+    for (int k = 0; k < 3 && e == cudaSuccess; ++k) e = cudaEventCreateWithFlags(&p->h_ev[k], cudaEventDisableTiming);
     if (e != cudaSuccess) {
       cudaGetLastError();
       return EI_ERR_RESOURCE;
     }
   }
   cudaStream_t st = (cudaStream_t)stream;
-  cudaError_t e = cudaSuccess;
-  auto A = [&](cudaError_t r) { if (e == cudaSuccess) e = r; };
-  const cudaMemcpyKind H2D = cudaMemcpyHostToDevice, D2H = cudaMemcpyDeviceToHost;
-  // the small inputs first on the compute stream, so K0/K1 start after ~1/6 of the bytes; the
-  // s_exp upload (the bulk: M values per ray) follows on the copy stream, overlapping K0 and K1,
-  // and K2 waits for it (event h_ev[1])
-  float *dmu = p->h_maps, *ddl = p->h_maps + S * NN, *dsg = p->h_maps + 2 * S * NN;
-  A(cudaMemcpyAsync(dmu, mu, sizeof(float) * S * NN, H2D, st));
-  A(cudaMemcpyAsync(ddl, delta, sizeof(float) * S * NN, H2D, st));
-  A(cudaMemcpyAsync(dsg, sigma, sizeof(float) * S * NN, H2D, st));
-  A(cudaMemcpyAsync(p->h_flat, flat, sizeof(float) * S * 3 * ND, H2D, st));
-  A(cudaMemcpyAsync(p->h_mask, mask, sizeof(float) * M, H2D, st));
-  if (drift) A(cudaMemcpyAsync(p->h_drift, drift, sizeof(float) * NA, H2D, st));
-  A(cudaMemsetAsync(p->h_status, 0, sizeof(int32_t) * 4, st));
-  A(cudaEventRecord(p->h_ev[0], st));
-  A(cudaStreamWaitEvent(p->h_copy, p->h_ev[0], 0));
-  A(cudaMemcpyAsync(p->h_sexp, s_exp, sizeof(float) * nsexp, H2D, p->h_copy));
-  A(cudaEventRecord(p->h_ev[1], p->h_copy));
-  if (e != cudaSuccess) return EI_ERR_CUDA;
-  float *gm = p->h_grad, *gd = p->h_grad + S * NN, *gs = p->h_grad + 2 * S * NN;
-  int rc = cost_grad_impl(p, dmu, ddl, dsg, p->h_flat, p->h_mask, drift ? p->h_drift : nullptr,
-                          p->h_sexp, lambda, p->h_cost, gm, gd, gs, nullptr, p->h_status, stream,
-                          p->h_ev[1]);
+  // The whole call (12 copies, a memset, 4-5 kernels) is captured once into a CUDA graph on the
+  // plan's work stream and replayed while the arguments stay the same: one launch instead of ~20
+  // API calls, which otherwise leave the GPU idle between them (the call is synchronous, so the
+  // GPU starts every call idle).  Ordered after the caller's stream by an event; pageable host
+  // buffers (not capturable), the timing mode and EI_HOST_GRAPH=0 take the direct path.
+  const HostKey key{mu, delta, sigma, flat, mask, drift, s_exp, lambda, cost, g_mu, g_delta, g_sigma, status};
+  const char *genv = getenv("EI_HOST_GRAPH");
+  const bool use_graph = !p->tev && !(genv && atoi(genv) == 0) && !p->h_graph_failed;
+  if (use_graph) {
+    cudaError_t e = cudaEventRecord(p->h_ev[2], st);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(p->h_work, p->h_ev[2], 0);
+    if (e != cudaSuccess) return EI_ERR_CUDA;
+    if (!(p->h_exec && p->h_key == key)) {
+      if (p->h_exec) {
+        cudaGraphExecDestroy(p->h_exec);
+        p->h_exec = nullptr;
+      }
+      int64_t s0[6];
+      for (int i = 0; i < 6; ++i) s0[i] = p->stats[i];
+      cudaGraph_t graph = nullptr;
+      int rc = EI_ERR_CUDA;
+      if (cudaStreamBeginCapture(p->h_work, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
+        rc = enqueue_host_path(p, mu, delta, sigma, flat, mask, drift, s_exp, lambda, cost, g_mu,
+                               g_delta, g_sigma, status, p->h_work);
+        if (cudaStreamEndCapture(p->h_work, &graph) != cudaSuccess) rc = EI_ERR_CUDA;
+      }
+      for (int i = 0; i < 6; ++i) {
+        p->h_stats[i] = p->stats[i] - s0[i];
+        p->stats[i] = s0[i];
+      }
+      if (rc == EI_OK && graph && cudaGraphInstantiate(&p->h_exec, graph, 0) == cudaSuccess) {
+        p->h_key = key;
+      } else {
+        p->h_exec = nullptr;
+        p->h_graph_failed = true;   // e.g. pageable host memory: direct path from now on
+      }
+      if (graph) cudaGraphDestroy(graph);
+      cudaGetLastError();
+    }
+    if (p->h_exec) {
+      if (cudaGraphLaunch(p->h_exec, p->h_work) != cudaSuccess) return EI_ERR_CUDA;
+      for (int i = 0; i < 6; ++i) p->stats[i] += p->h_stats[i];
+      return cudaStreamSynchronize(p->h_work) == cudaSuccess ? EI_OK : EI_ERR_CUDA;
+    }
+  }
+  int rc = enqueue_host_path(p, mu, delta, sigma, flat, mask, drift, s_exp, lambda, cost, g_mu,
+                             g_delta, g_sigma, status, st);
   if (rc) return rc;
-  A(cudaMemcpyAsync(cost, p->h_cost, sizeof(double) * S, D2H, st));
-  A(cudaMemcpyAsync(g_mu, gm, sizeof(float) * S * NN, D2H, st));
-  A(cudaMemcpyAsync(g_delta, gd, sizeof(float) * S * NN, D2H, st));
-  A(cudaMemcpyAsync(g_sigma, gs, sizeof(float) * S * NN, D2H, st));
-  A(cudaMemcpyAsync(status, p->h_status, sizeof(int32_t) * 4, D2H, st));
-  A(cudaStreamSynchronize(st));
-  return cuda_status(e);
+  return cudaStreamSynchronize(st) == cudaSuccess ? EI_OK : EI_ERR_CUDA;
 }
 
 }  // extern "C"

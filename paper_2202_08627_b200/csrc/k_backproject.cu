@@ -18,6 +18,8 @@
 //  * the pair products accumulate with FFMA2 (__ffma2_rn: two fp32 FMAs per instruction on
 //    sm_100a): acc.x collects the left taps, acc.y the right taps, summed once at the end.
 // Nothing is scattered: deterministic.  The cost path adds 2*lambda*x (eq. 5).
+#include <algorithm>
+
 #include "ei_common.cuh"
 #include "tma.cuh"
 
@@ -230,7 +232,7 @@ __global__ void __launch_bounds__(NT + 32, 3) backproject_kernel(
 
   const int i = i0 + row;
   const size_t NN = (size_t)N * N;
-  if (KS > 1) {   // angle split: publish partials; the last CTA of this tile reduces in ks order
+  if (KS > 1) {   // angle split: publish partials; ks_reduce_kernel sums them in ks order
     if (i < N) {
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
@@ -244,32 +246,7 @@ __global__ void __launch_bounds__(NT + 32, 3) backproject_kernel(
         }
       }
     }
-    __shared__ bool last;
-    __threadfence();
-    asm volatile("bar.sync 1, %0;\n" ::"n"(NT) : "memory");   // consumers only
-    if (tid == 0) {
-      unsigned int *cnt = done3 + (size_t)s * gridDim.x * gridDim.y + blockIdx.y * gridDim.x + blockIdx.x;
-      last = atomicAdd(cnt, 1u) == (unsigned)(KS - 1);
-      if (last) *cnt = 0u;   // re-arm
-    }
-    asm volatile("bar.sync 1, %0;\n" ::"n"(NT) : "memory");
-    if (!last) return;
-    __threadfence();
-    if (i >= N) return;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int j = j0 + lx + 8 * q;
-      if (j >= N) continue;
-      float v[3] = {0.f, 0.f, 0.f};
-      for (int k2 = 0; k2 < KS; ++k2) {
-        const float *pp = part3 + ((size_t)(k2 * S + s) * 3) * NN + (size_t)i * N + j;
-#pragma unroll
-        for (int m = 0; m < (NMAP == 3 ? 3 : 1); ++m) v[m] += __ldcg(pp + m * NN);
-      }
-      am[q] = make_float2(v[0], 0.f);
-      ad[q] = make_float2(v[1], 0.f);
-      as[q] = make_float2(v[2], 0.f);
-    }
+    return;
   }
   if (i >= N) return;
 #pragma unroll
@@ -296,6 +273,43 @@ __global__ void __launch_bounds__(NT + 32, 3) backproject_kernel(
       o0[oo] = vm;
     }
   }
+}
+
+// angle split (KS > 1): fixed-order sum of the KS partial gradients + 2 lambda x (eq. 5), one thread
+// per (slice, pixel), launched with PDL right after K3
+template <int NMAP>
+__global__ void __launch_bounds__(256) ks_reduce_kernel(const float *__restrict__ part3, int KS, int S,
+                                                        int N, const float *__restrict__ mu,
+                                                        const float *__restrict__ delta,
+                                                        const float *__restrict__ sigma, float lambda,
+                                                        float *__restrict__ o0, float *__restrict__ o1,
+                                                        float *__restrict__ o2, size_t out_stride) {
+  pdl_wait();
+  const size_t NN = (size_t)N * N, total = (size_t)S * NN;
+  for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < total; t += (size_t)gridDim.x * blockDim.x) {
+    const size_t s = t / NN, p = t - s * NN;
+    float v[3] = {0.f, 0.f, 0.f};
+    for (int k2 = 0; k2 < KS; ++k2) {
+      const float *pp = part3 + ((size_t)(k2 * S + s) * 3) * NN + p;
+#pragma unroll
+      for (int m = 0; m < (NMAP == 3 ? 3 : 1); ++m) v[m] += __ldcg(pp + m * NN);
+    }
+    const size_t oo = s * out_stride + p;
+    if (mu) {
+      const float l2 = 2.f * lambda;
+      v[0] = fmaf(l2, __ldg(mu + s * NN + p), v[0]);
+      if (NMAP == 3) {
+        v[1] = fmaf(l2, __ldg(delta + s * NN + p), v[1]);
+        v[2] = fmaf(l2, __ldg(sigma + s * NN + p), v[2]);
+      }
+    }
+    o0[oo] = v[0];
+    if (NMAP == 3) {
+      o1[oo] = v[1];
+      o2[oo] = v[2];
+    }
+  }
+  pdl_trigger();
 }
 
 template <int NMAP>
@@ -325,6 +339,13 @@ cudaError_t launch_bp(const ei_plan &p, const typename Layout<NMAP>::A *GA, cons
                  p.NA3, p.N, p.NA, p.ND, mu, delta, sigma, lambda, o0, o1, o2, out_stride, p.S, p.KS, p.part3,
                  p.done3, p.PADG, p.RpG, fin);
   if (e != cudaSuccess) return e;
+  if (p.KS > 1) {
+    const size_t total = (size_t)p.S * p.N * p.N;
+    const int blocks = (int)std::min<size_t>((total + 255) / 256, 148 * 8);
+    e = launch_pdl(ks_reduce_kernel<NMAP>, dim3(blocks), dim3(256), 0, st, (const float *)p.part3, p.KS,
+                   p.S, p.N, mu, delta, sigma, lambda, o0, o1, o2, out_stride);
+    if (e != cudaSuccess) return e;
+  }
   return cudaGetLastError();
 }
 

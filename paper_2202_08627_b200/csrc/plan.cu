@@ -204,12 +204,13 @@ int ei_plan_create(const ei_geometry *geom, const double *angles, ei_plan **out)
   A(dalloc(&p->part_curve, S * NA * p->k2.nseg * p->k2.nw));
   A(dalloc(&p->part_mo, S * NA * p->k2.nseg * p->k2.nw));
   A(dalloc(&p->part_reg, S * p->RB));
-  // K3 angle split for small grids: the largest KS (<= 16, <= chunks/2) keeping the grid within
-  // ~2 CTAs per SM (measured on C2: KS = 4 beats 1-3 and 6-16)
+  // K3 angle split for small grids: the largest KS (<= 16, <= angle chunks) keeping the grid within
+  // one wave of 3 CTAs per SM; the KS partial gradients are summed by ks_reduce_kernel (measured:
+  // C1 KS 1 -> 6-8: 22.5 -> 14.5 us; C2 KS 4-6 best)
   {
     const long long ctas = (long long)ei::bp_tiles(p->N) * p->S;
     int KS = 1;
-    while (KS < 16 && KS + 1 <= std::max(1, ei::bp_chunks(p->NA3) / 2) && ctas * (KS + 1) <= 2 * 148) ++KS;
+    while (KS < 16 && KS + 1 <= ei::bp_chunks(p->NA3) && ctas * (KS + 1) <= 3 * 148) ++KS;
     if (const char *e = getenv("EI_K3_KS")) KS = std::max(1, std::min(16, atoi(e)));   // tuning knob
     p->KS = KS;
   }
@@ -353,14 +354,14 @@ int ei_backproject(const ei_plan *p, const float *sino, int n_maps, float *maps,
                                   maps + 2 * NN, 3 * NN, nullptr, st);
     p->stats[2] += 1;
     p->stats[3] += 3;
-    p->stats[5] += 2 + (p->npairs > 0);
+    p->stats[5] += 2 + (p->npairs > 0) + (p->KS > 1);
   } else {
     e = ei::launch_pack_sino(*p, sino, 1, st);
     if (e == cudaSuccess) e = ei::launch_fold(*p, 1, st);
     if (e == cudaSuccess) e = ei::launch_backproject1(*p, maps, st);
     p->stats[2] += 1;
     p->stats[3] += 1;
-    p->stats[5] += 2 + (p->npairs > 0);
+    p->stats[5] += 2 + (p->npairs > 0) + (p->KS > 1);
   }
   return cuda_status(e);
 }
@@ -411,7 +412,7 @@ int cost_grad_impl(const ei_plan *p, const float *mu, const float *delta, const 
   if (e == cudaSuccess) e = ei::launch_backproject3(*p, mu, delta, sigma, lambda, g_mu, g_delta,
                                                     g_sigma, NN, &fin, st);            // K3 + K4
   mark(4);
-  p->stats[5] += 4 + (p->npairs > 0);
+  p->stats[5] += 4 + (p->npairs > 0) + (p->KS > 1);
   p->stats[0] += 1;
   p->stats[1] += 3;
   p->stats[2] += 1;
@@ -479,7 +480,7 @@ int ei_cost_grad_h(const ei_plan *p, const float *h, float gamma, const float *f
   p->stats[2] += 1;
   p->stats[3] += 1;
   p->stats[4] += 1;
-  p->stats[5] += 4 + (p->npairs > 0);
+  p->stats[5] += 4 + (p->npairs > 0) + (p->KS > 1);
   return cuda_status(e);
 }
 
@@ -521,7 +522,7 @@ int ei_cost_grad_hs(const ei_plan *p, const float *h, float gamma, const float *
   p->stats[2] += 1;
   p->stats[3] += 1;
   p->stats[4] += 1;
-  p->stats[5] += 4 + (p->npairs > 0);
+  p->stats[5] += 4 + (p->npairs > 0) + (p->KS > 1);
   return cuda_status(e);
 }
 

@@ -174,7 +174,9 @@ def test_launch_contract_host_path_and_determinism(ei):
     s0 = ei.ei_plan_stats(plan)
     c1, g1, st1 = gpu_cost_grad(ei, plan, case, case.maps(), 1e-2)
     s1 = ei.ei_plan_stats(plan)
-    assert [b - a for a, b in zip(s0, s1)] == [1, 3, 1, 3, 1, 4]
+    info = ei.ei_plan_info(plan)   # K0, K1, K2, K3 (+ mirror fold, + angle-split reduction)
+    launches = 4 + (info["mirror_pairs"] > 0) + (info["k3_angle_split"] > 1)
+    assert [b - a for a, b in zip(s0, s1)] == [1, 3, 1, 3, 1, launches]
     c2, g2, _ = gpu_cost_grad(ei, plan, case, case.maps(), 1e-2)
     assert np.array_equal(c1, c2) and all(np.array_equal(a, b) for a, b in zip(g1, g2))
     S, N = cfg.S, cfg.N

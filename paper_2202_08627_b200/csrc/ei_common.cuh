@@ -90,7 +90,6 @@ struct ei_plan {
   float *part_curve = nullptr;   // [S][NA][nseg][nw] per-warp cost partials (K2)
   float *part_mo = nullptr;      // [S][NA][nseg][nw] per-warp dS/dm_o partials (K2, NEXT-2)
   double *part_reg = nullptr;    // [S][RB] per-tile sum x^2 partials (K0)
-  unsigned int *done3 = nullptr; // [S][tiles] K3 arrival counters (angle split)
   float *part3 = nullptr;        // [KS][S][3][N][N] K3 angle-split partial gradients
   int KS = 1;                    // K3 angle split
   // 360-degree scans: angle pairs (theta, theta + pi) sample the same lines (mirrored detector,

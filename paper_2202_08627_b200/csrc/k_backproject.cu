@@ -111,7 +111,7 @@ __global__ void __launch_bounds__(NT + 32, 3) backproject_kernel(
     const float *__restrict__ mu,
     const float *__restrict__ delta, const float *__restrict__ sigma, float lambda,
     float *__restrict__ o0, float *__restrict__ o1, float *__restrict__ o2, size_t out_stride,
-    int S, int KS, float *__restrict__ part3, unsigned int *__restrict__ done3, int PADG, int RpG,
+    int S, int KS, float *__restrict__ part3, int PADG, int RpG,
     FinArgs fin) {
   using TA = typename Layout<NMAP>::A;
   constexpr bool A8 = sizeof(TA) == 8;
@@ -337,7 +337,7 @@ cudaError_t launch_bp(const ei_plan &p, const typename Layout<NMAP>::A *GA, cons
   dim3 grid((p.N + TILE - 1) / TILE, (p.N + TILE - 1) / TILE, p.S * p.KS);
   e = launch_pdl(backproject_kernel<NMAP>, grid, dim3(NT + 32), smem, st, GA, GB, p.tab.k3, p.alist3,
                  p.NA3, p.N, p.NA, p.ND, mu, delta, sigma, lambda, o0, o1, o2, out_stride, p.S, p.KS, p.part3,
-                 p.done3, p.PADG, p.RpG, fin);
+                 p.PADG, p.RpG, fin);
   if (e != cudaSuccess) return e;
   if (p.KS > 1) {
     const size_t total = (size_t)p.S * p.N * p.N;

@@ -64,7 +64,7 @@ void free_plan(ei_plan *p) {
     if (ev) cudaEventDestroy(ev);
   void *ptrs[] = {p->tab.k1, p->tab.k3, p->proj.groups, p->proj.order, p->proj.partner, p->alist3,
                   p->pairs, p->proj.win1, p->proj.winRS, p->MA, p->MAT, p->MB,
-                  p->MBT, p->M1, p->M1T, p->diag, p->part_mo, p->done3, p->part3, p->P, p->GA, p->GB, p->GA1,
+                  p->MBT, p->M1, p->M1T, p->diag, p->part_mo, p->part3, p->P, p->GA, p->GB, p->GA1,
                   p->part_curve, p->part_reg, p->h_maps, p->h_flat, p->h_mask, p->h_drift,
                   p->h_sexp, p->h_grad, p->h_cost, p->h_status};
   for (void *q : ptrs)
@@ -214,7 +214,6 @@ int ei_plan_create(const ei_geometry *geom, const double *angles, ei_plan **out)
     if (const char *e = getenv("EI_K3_KS")) KS = std::max(1, std::min(16, atoi(e)));   // tuning knob
     p->KS = KS;
   }
-  A(dalloc(&p->done3, S * (size_t)ei::bp_tiles(p->N)));
   if (p->KS > 1) A(dalloc(&p->part3, (size_t)p->KS * S * 3 * p->N * p->N));
   if (e == cudaSuccess) A(cudaMemcpy(p->tab.k1, k1, sizeof(float4) * NA, cudaMemcpyHostToDevice));
   if (e == cudaSuccess) A(cudaMemcpy(p->tab.k3, k3, sizeof(float4) * NA, cudaMemcpyHostToDevice));
@@ -237,7 +236,6 @@ int ei_plan_create(const ei_geometry *geom, const double *angles, ei_plan **out)
   if (e == cudaSuccess) A(cudaMemset(p->GA, 0, sizeof(float4) * S * SINO1));   // zero padding
   if (e == cudaSuccess) A(cudaMemset(p->GB, 0, sizeof(float2) * S * SINO1));
   if (e == cudaSuccess) A(cudaMemset(p->GA1, 0, sizeof(float2) * S * SINO1));
-  if (e == cudaSuccess) A(cudaMemset(p->done3, 0, sizeof(unsigned int) * S * ei::bp_tiles(p->N)));
   if (e == cudaSuccess)
     A(cudaMemcpy(p->proj.win1, win1.data(), sizeof(int2) * win1.size(), cudaMemcpyHostToDevice));
   if (e == cudaSuccess && !winRS.empty())

@@ -32,6 +32,7 @@
 //    (item, warp); K3 sums them in fp64 in index order (fused finalize, K4).
 // Deterministic: no float atomics, fixed reduction order, results independent of the grid size.
 #include <stdint.h>
+#include <stdlib.h>
 
 #include <algorithm>
 
@@ -523,7 +524,9 @@ int plan_curve(ei_plan &p) {
   const int nrows = 3 + p.M;
   auto W_of = [&](int ns) { return (((p.ND + ns - 1) / ns) + 3) & ~3; };
   int nseg = 1;
-  while (W_of(nseg) / J + 2 > K2_MAXT ||
+  const char *mw = getenv("EI_K2_MAXW");   // tuning knob: cap on the segment width
+  const int maxw = mw ? std::max(16, atoi(mw)) : 1 << 30;
+  while (W_of(nseg) / J + 2 > K2_MAXT || W_of(nseg) > maxw ||
          (k2_smem(nrows, W_of(nseg) + 2 * J) > 110 * 1024 && W_of(nseg) > 64))
     ++nseg;
   p.k2.nseg = nseg;

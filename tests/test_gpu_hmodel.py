@@ -146,3 +146,29 @@ def test_sampled_flat_parity(ei, name, point):
     for s in range(cfg.S):
         assert rel_l2(gg[s], rg[s]) <= 1e-3, (s, rel_l2(gg[s], rg[s]))
     assert list(st.cpu().numpy()[:2]) == list(rst)
+
+
+def test_status_counters_h_and_sampled(ei):
+    """Non-finite inputs and the P_h clamp (R12) are counted by the single-map paths exactly as
+    by the oracle; the finite slice still matches."""
+    case, fs, s_exp = _cases.cached_hs_case("RH")
+    cfg = case.cfg
+    plan = plan_for(ei, cfg)
+    h = case.h.copy()
+    h[0] *= 5000.0                      # drives P_h past 50 on slice 0 (R12)
+    h[1, 3, 4] = np.nan                 # one non-finite map element on slice 1
+    se = s_exp.copy()
+    se[1, 2, 0, 5] = np.inf
+    drift = None if case.drift is None else dev(case.drift)
+    cost = torch.zeros(cfg.S, dtype=torch.float64, device="cuda")
+    g = torch.zeros(cfg.S, cfg.N, cfg.N, device="cuda")
+    st = torch.zeros(4, dtype=torch.int32, device="cuda")
+    ei.ei_cost_grad_hs(plan, dev(h), case.gamma, dev(fs), dev(case.mask), drift, dev(se), 0.0, cost, g,
+                       None, st)
+    torch.cuda.synchronize()
+    rc, rg, rst = _cases.ora.cost_grad_hs(cfg.angles, h, case.gamma, fs, case.mask, case.drift, se, 0.0,
+                                          dx=cfg.pixel, du=cfg.det_pitch, z=cfg.z)
+    assert rst[0] == 2 and rst[1] > 0
+    assert list(st.cpu().numpy()[:2]) == list(rst)
+    assert abs(cost.cpu().numpy()[0] - rc[0]) / rc[0] <= 1e-4
+    assert rel_l2(g.cpu().numpy()[0], rg[0]) <= 1e-3

@@ -343,6 +343,72 @@ def run_gpu(args, cfg, rank, world, local_rank):
     return line
 
 
+def run_gpu_angles(args, cfg, rank, world, local_rank):
+    """Strong scaling of ONE stack over its angles: every rank holds the same
+    maps, evaluates its angles (mirror pairs kept together, dist.angle_shard) and one NCCL
+    all-reduce of the gradient and cost completes the evaluation; the step includes it."""
+    import torch
+    import torch.distributed as dist
+    from paper_2202_08627_b200 import ei
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    case = make_gpu_case(cfg, ei, torch)                  # same seed on every rank: same data
+    maps = synth.perturbed(case.maps(), cfg.seed + 7)
+    lam = args.lam
+    sh = edist.AngleShardEval(ei, cfg, rank, world, dev)
+    se, dr = sh.local_inputs(case.s_exp, case.drift)
+    dv = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+    dm = [dv(m) for m in maps]
+    flat, mask = dv(case.flat), dv(case.mask)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        sh.cost_grad(dm, flat, mask, dr, se, lam, stream)
+
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
+    for _ in range(max(args.warmup, 3)):
+        flush.fill_(1.0)
+        step()
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local_rank) if rank == 0 else None
+    K = args.steps
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    s0 = ei.ei_plan_stats(sh.plan)
+    dist.barrier()
+    torch.cuda.synchronize()
+    t0 = time.time()
+    for i in range(K):
+        flush.fill_(1.0)
+        ev[i][0].record(stream)
+        step()
+        ev[i][1].record(stream)
+    torch.cuda.synchronize()
+    t1 = time.time()
+    dist.barrier()
+    ms = edist.max_over_ranks(sum(a.elapsed_time(b) for a, b in ev))
+    s1 = ei.ei_plan_stats(sh.plan)
+    if sampler:
+        sampler.stop()
+    if rank != 0:
+        return None
+    ms_step = ms / K
+    rsu = ray_sample_updates(cfg)
+    return {
+        "metric": METRIC, "value": round(1000.0 / ms_step, 3), "unit": UNIT, "n_gpus": world, "steps": K,
+        "warmup": args.warmup, "ms_per_step": round(ms_step, 5), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": "%s: %s" % (cfg.name, describe(cfg)), "slices_per_gpu": cfg.S,
+                   "lambda": lam, "eval_point": "x_pert (R21)", "parallelism": "angle-sharded x%d, NCCL "
+                   "all-reduce of gradient + cost per evaluation" % world,
+                   "l2": "flushed before every timed step (256 MiB write, untimed)"},
+        "ray_sample_updates_per_s": round(6 * rsu * cfg.S / (ms_step * 1e-3), 1),
+        "angles_rank0": int(len(sh.idx)), "gpu_launches": int(s1[5] - s0[5]),
+        "clocks": sampler.summary(t0, t1), "plan": ei.ei_plan_info(sh.plan),
+        "e2e": None,
+    }
+
+
 def describe(cfg):
     return ("%dx %dx%d grid, %d angles over [0,%g) deg, %d detector px, M=%d" %
             (cfg.S, cfg.N, cfg.N, cfg.n_angles, cfg.span_deg, cfg.n_det, cfg.M))
@@ -544,6 +610,9 @@ def main():
     ap.add_argument("--lam", type=float, default=1e-2)
     ap.add_argument("--cpu-budget", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--shard", default="slices", choices=["slices", "angles"],
+                    help="N > 1: 'slices' = every rank its own stack (weak scaling, default); "
+                         "'angles' = one stack split over angles with an all-reduce (strong)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3                                           # timing rule: W >= 3
@@ -561,7 +630,10 @@ def main():
             import torch
             torch.cuda.set_device(local_rank)
             edist.init("nccl", torch.device("cuda", local_rank))
-        line = run_gpu(args, cfg, rank, world, local_rank)
+        if args.shard == "angles" and world > 1:
+            line = run_gpu_angles(args, cfg, rank, world, local_rank)
+        else:
+            line = run_gpu(args, cfg, rank, world, local_rank)
         if world > 1:
             import torch.distributed as dist
             dist.destroy_process_group()

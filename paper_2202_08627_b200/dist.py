@@ -72,3 +72,85 @@ def gather_costs(local_costs: torch.Tensor, n_slices: int) -> torch.Tensor:
     full[first:first + count] = local_costs.to(device=dev, dtype=torch.float64)
     dist.all_reduce(full, op=dist.ReduceOp.SUM)   # disjoint supports: a gather, exact in fp64
     return full.cpu()
+
+
+# ---------------------------------------------------------------------------------------------
+# Strong scaling of ONE slice stack over its angles (single large slices such as
+# C3 / C5): K1 and K2 are angle-local and K3's per-angle contributions add, so each rank evaluates
+# the cost and gradient of its angles only and one all-reduce (sum) of the S x 3 x N^2 gradient
+# and the S costs assembles the evaluation — the path's one real exchange step.
+# ---------------------------------------------------------------------------------------------
+def angle_shard(angles, rank: int, world: int):
+    """Indices (ascending) of the angles rank `rank` evaluates.  Mirror pairs (theta, theta + pi
+    mod 2 pi, to 1e-9 rad) stay on one rank, so its plan still projects each pair once; the
+    primaries (angle mod 2 pi < pi) are split into `world` contiguous blocks in angle order,
+    balanced by count, and every angle is owned by exactly one rank."""
+    import numpy as np
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad rank/world")
+    a = np.asarray(angles, dtype=np.float64)
+    w = np.mod(a, 2 * np.pi)
+    order = np.argsort(w, kind="stable")
+    partner = -np.ones(len(a), dtype=np.int64)
+    used = np.zeros(len(a), dtype=bool)
+    ws = w[order]
+    for i in order:
+        if w[i] >= np.pi or used[i]:
+            continue
+        lo = np.searchsorted(ws, w[i] + np.pi - 1e-9)
+        for j in order[lo:]:
+            if w[j] > w[i] + np.pi + 1e-9:
+                break
+            if j != i and not used[j]:
+                partner[i] = j
+                used[i] = used[j] = True
+                break
+    mirrors = set(int(j) for j in partner if j >= 0)
+    prim = [int(i) for i in order if int(i) not in mirrors]       # primaries + unpaired, angle order
+    first, count = shard(len(prim), rank, world)
+    mine = []
+    for i in prim[first:first + count]:
+        mine.append(i)
+        if partner[i] >= 0:
+            mine.append(int(partner[i]))
+    return np.array(sorted(mine), dtype=np.int64)
+
+
+def all_reduce_sum_(*tensors) -> None:
+    """In-place sum over ranks (NCCL on GPUs, gloo in tests); no-op without a process group."""
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return
+    for t in tensors:
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+
+
+class AngleShardEval:
+    """One rank's share of an angle-sharded cost + gradient evaluation through the C ABI: a plan
+    over the rank's angles, its rows of s_exp and drift, the regulariser on rank 0 only, then one
+    all-reduce of (gradient, cost)."""
+
+    def __init__(self, ei, cfg, rank: int, world: int, device):
+        import numpy as np
+        self.ei, self.rank, self.world = ei, rank, world
+        self.idx = angle_shard(cfg.angles, rank, world)
+        self.plan = ei.Plan(cfg.S, cfg.N, len(self.idx), cfg.n_det, cfg.M, cfg.pixel, cfg.det_pitch,
+                            cfg.z, np.ascontiguousarray(cfg.angles[self.idx]))
+        self.ws = ei.Workspace(self.plan, device)
+        self.device = device
+
+    def local_inputs(self, s_exp, drift):
+        """The rank's rows of s_exp [S][Na][M][Nd] and drift [Na] (numpy or torch)."""
+        import numpy as np
+        se = np.ascontiguousarray(np.asarray(s_exp)[:, self.idx])
+        dr = None if drift is None else np.ascontiguousarray(np.asarray(drift)[self.idx])
+        to = lambda a: None if a is None else torch.from_numpy(a).to(self.device)
+        return to(se), to(dr)
+
+    def cost_grad(self, maps, flat, mask, drift_local, s_exp_local, lam: float, stream=None):
+        ws = self.ws
+        ws.status.zero_()
+        self.ei.ei_cost_grad(self.plan, maps[0], maps[1], maps[2], flat, mask, drift_local, s_exp_local,
+                             lam if self.rank == 0 else 0.0, ws.cost, ws.g[0], ws.g[1], ws.g[2], ws.status,
+                             stream)
+        all_reduce_sum_(ws.g, ws.cost)
+        return ws.cost, ws.g, ws.status

@@ -72,3 +72,71 @@ def test_world2_gloo():
     for rank, t, full in res:
         assert t == 2.5
         assert full == [s * 10.0 + 0.25 for s in range(7)]
+
+
+def test_angle_shard_partition_and_pairs():
+    """Every angle on exactly one rank; mirror pairs (360-degree scans) kept together."""
+    import numpy as np
+    for cfg in (synth.CONFIGS["C3"], synth.CONFIGS["C2"], synth.small_config("R3", n_angles=40),
+                synth.small_config("R1")):
+        ang = cfg.angles
+        for world in (1, 2, 3, 8):
+            parts = [edist.angle_shard(ang, r, world) for r in range(world)]
+            allidx = np.sort(np.concatenate(parts))
+            assert np.array_equal(allidx, np.arange(len(ang)))
+            if cfg.span_deg == 360.0 and len(ang) % 2 == 0:
+                for p in parts:   # the partner theta + pi of every angle is on the same rank
+                    w = np.mod(ang[p], 2 * np.pi)
+                    for t in w:
+                        d = np.abs(np.mod(w - t - np.pi + np.pi, 2 * np.pi) - np.pi)
+                        assert d.min() < 1e-9
+
+
+def _angle_worker(rank, world, port, q):
+    """Each rank: the fp64 oracle's cost/gradient over its angles (regulariser on rank 0 only),
+    summed over ranks with all_reduce — must equal the unsharded evaluation."""
+    import numpy as np
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world), LOCAL_RANK=str(rank))
+    edist.init("gloo")
+    try:
+        import _cases
+        from oracle import ora
+        case = _cases.cached_case("R3")
+        cfg = case.cfg
+        maps = synth.perturbed(case.maps(), cfg.seed + 7)
+        idx = edist.angle_shard(cfg.angles, rank, world)
+        lam = 1e-2 if rank == 0 else 0.0
+        c, gm, gd, gs, _ = ora.cost_grad(cfg.angles[idx], *maps, case.flat, case.mask,
+                                         None if case.drift is None else case.drift[idx],
+                                         np.ascontiguousarray(case.s_exp[:, idx]), lam)
+        cost = torch.from_numpy(c)
+        g = torch.from_numpy(np.stack([gm, gd, gs]))
+        edist.all_reduce_sum_(g, cost)
+        q.put((rank, cost.numpy().tolist(), g.numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_angle_sharded_sum_equals_full_world2():
+    import numpy as np
+    import _cases
+    from oracle import ora
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_angle_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(60)
+        assert p.exitcode == 0
+    case = _cases.cached_case("R3")
+    maps = synth.perturbed(case.maps(), case.cfg.seed + 7)
+    rc, rgm, rgd, rgs, _ = ora.cost_grad(case.cfg.angles, *maps, case.flat, case.mask, case.drift, case.s_exp,
+                                         1e-2)
+    ref = np.stack([rgm, rgd, rgs])
+    for rank, cost, g in res:
+        np.testing.assert_allclose(cost, rc, rtol=1e-12)
+        assert np.linalg.norm(g - ref) / np.linalg.norm(ref) < 1e-12

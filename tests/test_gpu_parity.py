@@ -276,3 +276,27 @@ def test_mirror_pairs_360(ei, mirror, monkeypatch):
     for q, ref in enumerate((rgm, rgd, rgs)):
         for s in range(cfg.S):
             assert rel_l2(g[q][s], ref[s]) <= 1e-3, (q, s)
+
+
+@pytest.mark.parametrize("name", ["R3", "C1"])
+def test_angle_shard_partials_sum_to_full(ei, name):
+    """Strong-scaling decomposition on one GPU: the per-rank plans of a 3-way
+    angle shard (mirror pairs kept together), regulariser on rank 0 only, summed, equal the
+    unsharded evaluation (the all-reduce itself is covered by the gloo tests)."""
+    from paper_2202_08627_b200 import dist as edist
+    case = _cases.cached_case(name)
+    cfg = case.cfg
+    maps = synth.perturbed(case.maps(), cfg.seed + 7)
+    dm = [dev(m) for m in maps]
+    tot_c, tot_g = 0.0, 0.0
+    for r in range(3):
+        sh = edist.AngleShardEval(ei, cfg, r, 3, torch.device("cuda"))
+        se, dr = sh.local_inputs(case.s_exp, case.drift)
+        c, g, st = sh.cost_grad(dm, dev(case.flat), dev(case.mask), dr, se, 1e-2)
+        torch.cuda.synchronize()
+        tot_c = tot_c + c.cpu().numpy()
+        tot_g = tot_g + g.cpu().numpy()
+    c_full, g_full, _ = gpu_cost_grad(ei, plan_for(ei, cfg), case, maps, 1e-2)
+    assert np.all(np.abs(tot_c - c_full) / c_full <= 1e-6)
+    for q in range(3):
+        assert rel_l2(tot_g[q], g_full[q]) <= 1e-5

@@ -13,7 +13,7 @@ Design (stated here because the paper gives no optimizer parameters, PAPER.md:81
     stored only if <s, y> > 1e-12 |s| |y| (curvature), otherwise the history of that slice resets;
   * stop a slice when its relative cost decrease over an accepted step is below rel_tol, or when
     max_iter iterations are done.
-Dot products are accumulated in fp64.
+Dot products: products in the iterate's dtype, sums in fp64.
 """
 from __future__ import annotations
 
@@ -36,9 +36,9 @@ class Result:
 
 
 def _bdot(a: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
-    """Per-(block, slice) dot products in fp64: [B, S]."""
+    """Per-(block, slice) dot products, products in the tensors' dtype, sums in fp64: [B, S]."""
     B, S = a.shape[:2]
-    return (a.reshape(B, S, -1).double() * b.reshape(B, S, -1).double()).sum(-1)
+    return torch.sum(a.reshape(B, S, -1) * b.reshape(B, S, -1), dim=-1, dtype=torch.float64)
 
 
 def _sdot(a: torch.Tensor, b: torch.Tensor) -> torch.Tensor:
@@ -58,18 +58,22 @@ def _bc(v: torch.Tensor, like: torch.Tensor) -> torch.Tensor:
 def minimize(fg: Callable[[torch.Tensor], Tuple[torch.Tensor, torch.Tensor]], x0: torch.Tensor,
              max_iter: int = 200, m: int = 10, rel_tol: float = 1e-9, c1: float = 1e-4,
              max_ls: int = 30, callback: Optional[Callable[[int, torch.Tensor], None]] = None) -> Result:
-    """Minimise S independent problems.  x0: [B, S, ...]; fg(x) -> (cost [S] fp64, grad like x)."""
+    """Minimise S independent problems.  x0: [B, S, ...]; fg(x) -> (cost [S] fp64, grad like x).
+
+    The (s, y) history lives in two preallocated ring tensors [m, B, S, ...] with per-(pair,
+    slice) rho = 1 / <s, y> (0 where the pair is not valid for that slice), so the two-loop
+    recursion is a handful of fused tensor ops per pair instead of per-pair allocations."""
     t0 = time.time()
     x = x0.clone()
     f, g = fg(x)
     f, g = f.double().clone(), g.clone()
     n_evals = 1
-    S = x.shape[1]
+    B, S = x.shape[:2]
     dev = x.device
-    hist_s: List[torch.Tensor] = []
-    hist_y: List[torch.Tensor] = []
-    hist_ok: List[torch.Tensor] = []          # [S] bool: pair valid for that slice
-    B = x.shape[0]
+    Sh = torch.zeros((m,) + tuple(x.shape), dtype=x.dtype, device=dev)
+    Yh = torch.zeros_like(Sh)
+    rho = torch.zeros(m, S, dtype=torch.float64, device=dev)
+    nh, head = 0, 0                          # stored pairs, next ring slot
     gamma = torch.zeros(B, S, dtype=torch.float64, device=dev)   # block-diagonal initial scaling
     has_gamma = torch.zeros(S, dtype=torch.bool, device=dev)
     conv = torch.zeros(S, dtype=torch.bool, device=dev)
@@ -79,26 +83,26 @@ def minimize(fg: Callable[[torch.Tensor], Tuple[torch.Tensor, torch.Tensor]], x0
     for it in range(1, max_iter + 1):
         # ---- two-loop recursion: p = -H g (per slice, masked histories) ----
         q = g.clone()
+        slots = [(head - nh + j) % m for j in range(nh)]     # oldest .. newest
         alphas = []
-        for s_k, y_k, ok in zip(reversed(hist_s), reversed(hist_y), reversed(hist_ok)):
-            rho = torch.where(ok, 1.0 / _sdot(y_k, s_k).clamp_min(1e-300), torch.zeros_like(f))
-            a = rho * _sdot(s_k, q)
-            alphas.append((a, rho))
-            q = q - _bc(a, q) * y_k
+        for k in reversed(slots):
+            a = rho[k] * _sdot(Sh[k], q)
+            alphas.append(a)
+            q.sub_(Yh[k] * _bc(a, q))
         # slices without a curvature pair yet: unit-length steepest-descent step per block
         gnorm = _bdot(g, g).sqrt().clamp_min(1e-300)
         scal = torch.where(has_gamma.unsqueeze(0), gamma, 1.0 / gnorm)
         r = q * _bc(scal, q)
-        for (s_k, y_k, ok), (a, rho) in zip(zip(hist_s, hist_y, hist_ok), reversed(alphas)):
-            b = rho * _sdot(y_k, r)
-            r = r + _bc(a - b, r) * s_k
+        for k, a in zip(slots, reversed(alphas)):
+            b = rho[k] * _sdot(Yh[k], r)
+            r.add_(Sh[k] * _bc(a - b, r))
         p = -r
         gp = _sdot(g, p)
         bad = gp >= 0                          # not a descent direction: restart that slice
         if bool(bad.any()):
             p = torch.where(_bc(bad, p), -g * _bc(1.0 / _bdot(g, g).sqrt().clamp_min(1e-300), g), p)
             gp = _sdot(g, p)
-            hist_ok = [ok & ~bad for ok in hist_ok]
+            rho = rho * (~bad).to(rho.dtype)
         sd = sd | bad
         # ---- batched backtracking Armijo ----
         step = torch.ones(S, dtype=torch.float64, device=dev)
@@ -122,20 +126,21 @@ def minimize(fg: Callable[[torch.Tensor], Tuple[torch.Tensor, torch.Tensor]], x0
         # slice has converged to working precision
         failed = ~accepted
         if bool(failed.any()):
-            hist_ok = [ok & ~failed for ok in hist_ok]
-            has_gamma = has_gamma & ~failed
+            rho = rho * accepted.to(rho.dtype)
+            has_gamma = has_gamma & accepted
         s_vec, y_vec = x_new - x, g_new - g
         sy = _sdot(s_vec, y_vec)
-        curv = sy > 1e-12 * _sdot(s_vec, s_vec).sqrt() * _sdot(y_vec, y_vec).sqrt()
+        yy = _sdot(y_vec, y_vec)
+        curv = sy > 1e-12 * _sdot(s_vec, s_vec).sqrt() * yy.sqrt()
         keep = accepted & curv & ~conv
         if bool(keep.any()):
-            hist_s.append(s_vec)
-            hist_y.append(y_vec)
-            hist_ok.append(keep)
-            if len(hist_s) > m:
-                hist_s.pop(0), hist_y.pop(0), hist_ok.pop(0)
+            Sh[head].copy_(s_vec)
+            Yh[head].copy_(y_vec)
+            rho[head] = torch.where(keep, 1.0 / sy.clamp_min(1e-300), torch.zeros_like(sy))
+            head = (head + 1) % m
+            nh = min(nh + 1, m)
             gb = _bdot(s_vec, y_vec) / _bdot(y_vec, y_vec).clamp_min(1e-300)
-            gg = (sy / _sdot(y_vec, y_vec).clamp_min(1e-300)).unsqueeze(0).expand_as(gb)
+            gg = (sy / yy.clamp_min(1e-300)).unsqueeze(0).expand_as(gb)
             gb = torch.where(gb > 0, gb, gg)          # block secant not positive: global scalar
             gamma = torch.where(keep.unsqueeze(0), gb, gamma)
             has_gamma = has_gamma | keep

@@ -38,7 +38,9 @@ extern "C" {
 enum {
     EI_OK = 0,
     EI_ERR_NULL = 1,      /* a required pointer is NULL                                   */
-    EI_ERR_SHAPE = 2,     /* S<1, N<2, Nd<3, n_angles<1, M<1, n_maps not 1|3  */
+    EI_ERR_SHAPE = 2,     /* S<1, N<2, Nd<3, n_angles<1, M<1, n_maps not 1|3,
+                             Nd or n_angles > ~14000, M too large for K2's staging ring, a
+                             sampled flat IC with < 4 knots                                  */
     EI_ERR_DOMAIN = 3,    /* pixel/det_pitch/z <= 0 or non-finite, det_pitch < pixel,
                              non-finite angle, lambda < 0 or non-finite                    */
     EI_ERR_RESOURCE = 4,  /* device allocation failed / size overflow                      */

@@ -200,6 +200,7 @@ __global__ void __launch_bounds__(NT + 32, 3) backproject_kernel(
   for (int c = c_lo; c < c_hi; ++c) {
     mbar_wait(&sm.full[st], ph);
     const int na = min(CH, NA3 - c * CH);
+#pragma unroll 2   // two angles in flight per warp (measured: C4 K3 8.94 -> 8.76 ms; x4 8.80)
     for (int al = 0; al < na; ++al) {
       const float4 t = sm.tab[st][al];
       const int ws = sm.ws[st][al];

@@ -46,7 +46,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return LIB
     objdir = os.path.join(HERE, "build")
     os.makedirs(objdir, exist_ok=True)
-    defs = ['-DEI_GIT_DESCRIBE="%s"' % _describe()]
+    defs = ['-DEI_GIT_DESCRIBE="%s"' % _describe()] + os.environ.get("EI_NVCC_DEFS", "").split()   # e.g. -DEI_TRACE (debug)
     extra = ["-Xptxas", "-v"] if verbose else []
 
     def compile_one(src):

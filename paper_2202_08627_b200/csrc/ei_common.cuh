@@ -35,6 +35,9 @@ struct ProjPlan {
   int2 *win1 = nullptr;     // device window table for RS = 1  [groups][tiles][nch1]
   int2 *winRS = nullptr;    // device window table for RS      [RS][groups][tiles][nchRS]
   int nch1 = 0, nchRS = 0;
+  int n_tiles = 0;          // ray tiles per angle group
+  int *unit1 = nullptr;     // device: CTA -> work unit (tile, group, slice) for RS = 1 (launch order)
+  int *unitRS = nullptr;    // device: the same for the row-split cost path
   int PAD = 0;              // zero entries before/after every pair-layout map row
   int Rp = 0;               // padded row length (entries): N + 1 + 2 PAD, even
 };
@@ -141,7 +144,7 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
 
 int plan_projector(ei_plan &p, const double *angles, const std::vector<int> &proj_angles,
                    std::vector<int2> &groups, std::vector<int> &order, std::vector<int2> &win1,
-                   std::vector<int2> &winRS);
+                   std::vector<int2> &winRS, std::vector<int> &unit1, std::vector<int> &unitRS);
 // fold of mirror-pair gradient rows (k_pack.cu): G(primary) += mirror(G(mirror)), pair layout
 cudaError_t launch_fold(const ei_plan &p, int n_maps, cudaStream_t st);
 // K0 (k_pack.cu)

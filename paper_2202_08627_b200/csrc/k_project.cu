@@ -65,9 +65,21 @@ struct ProjArgs {
   const int *order;             // sorted position -> angle index
   const int *partner;           // angle -> its mirror angle theta + pi, or -1
   const int2 *win;              // [RS][groups][tiles][chunks] {cmin, W} (W = 0: chunk skipped)
-  int N, NA, ND, S, RS, RC, CW, nch, PAD, Rp;
+  const int *unit;              // CTA -> work unit tile + ntile (group + ngroups (rs S + s)) (plan order)
+  int N, NA, ND, S, RS, RC, CW, nch, PAD, Rp, ntile, ngroups;
   float *P;                     // [RS][S][NMAP][NA][ND]
 };
+
+#ifdef EI_TRACE
+// debug builds only (-DEI_TRACE, tools/dbg/k1_trace.py): per CTA {start ns, end ns, SM id, rows
+// with work of its busiest warp}, from %globaltimer
+__device__ unsigned long long g_k1_trace[4 * 65536];
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#endif
 
 constexpr int NST = 4;          // pipeline stages (shared-memory ring)
 constexpr int MAXCH = 1024;     // window-table entries cached in shared memory per CTA
@@ -101,11 +113,19 @@ __global__ void __launch_bounds__(NT + 32, 2) project_kernel(ProjArgs args) {
   __shared__ int2 swin[MAXCH];   // this CTA's window table (host plan), nch <= MAXCH
 
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const int kt = blockIdx.x * RT;
-  const int2 gr = args.groups[blockIdx.y];
+  const int un = __ldg(args.unit + blockIdx.x);
+  const int tile = un % args.ntile, grp = (un / args.ntile) % args.ngroups, z = un / (args.ntile * args.ngroups);
+  const int kt = tile * RT;
+#ifdef EI_TRACE
+  const unsigned long long t_start = gtimer();
+  __shared__ int s_rows;
+  if (tid == 0) s_rows = 0;
+  int my_rows = 0;
+#endif
+  const int2 gr = args.groups[grp];
   const int2 gi = make_int2(gr.x, gr.y & 0xffff);   // {first sorted position, count}
   const bool ray_fast = (gr.y >> 16) != 0;          // lane mapping of this group (plan)
-  const int s = blockIdx.z % args.S, rs = blockIdx.z / args.S;
+  const int s = z % args.S, rs = z / args.S;
   const float ctr = 0.5f * (float)(N - 1), dctr = 0.5f * (float)(ND - 1);
   const bool rowdom = __ldg(args.k1 + args.order[gi.x]).w != 0.f;
   const size_t Rp = (size_t)args.Rp;
@@ -113,7 +133,7 @@ __global__ void __launch_bounds__(NT + 32, 2) project_kernel(ProjArgs args) {
   const float2 *gB = NMAP == 3 ? (rowdom ? args.MB : args.MBT) + (size_t)s * N * Rp + args.PAD : nullptr;
   const int r0 = (int)(((long long)rs * N) / args.RS), r1 = (int)(((long long)(rs + 1) * N) / args.RS);
   const int nch = (r1 - r0 + RC - 1) / RC;
-  const int2 *wtab = args.win + (((size_t)rs * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * args.nch;
+  const int2 *wtab = args.win + (((size_t)rs * args.ngroups + grp) * args.ntile + tile) * args.nch;
 
   for (int c = tid; c < nch; c += NT + 32) swin[c] = __ldg(wtab + c);
   if (tid == 0) {
@@ -238,11 +258,29 @@ __global__ void __launch_bounds__(NT + 32, 2) project_kernel(ProjArgs args) {
       } else {
         for (int r = 0; r < rc; ++r, yi += 1.f, arow += CWA, brow += CWB) body(true, i0 + r);
       }
+#ifdef EI_TRACE
+      my_rows += rc;
+#endif
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[st]);
   }
   pdl_trigger();
+#ifdef EI_TRACE
+  if (lane == 0) atomicMax(&s_rows, my_rows);
+  asm volatile("bar.sync 1, %0;\n" ::"r"(NT) : "memory");   // consumers only
+  if (tid == 0) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+    const size_t b = blockIdx.x;
+    if (b < 65536) {
+      g_k1_trace[4 * b] = t_start;
+      g_k1_trace[4 * b + 1] = gtimer();
+      g_k1_trace[4 * b + 2] = smid;
+      g_k1_trace[4 * b + 3] = (unsigned long long)s_rows | ((unsigned long long)un << 32);
+    }
+  }
+#endif
   if (k >= ND) return;
   const size_t plane = (size_t)args.NA * ND;
   float *out = args.P + ((size_t)rs * args.S + s) * NMAP * plane + k;
@@ -281,6 +319,9 @@ cudaError_t launch(const ei_plan &p, int RS, float *P, cudaStream_t st) {
   a.order = p.proj.order;
   a.partner = p.proj.partner;
   a.win = RS == 1 ? p.proj.win1 : p.proj.winRS;
+  a.unit = RS == 1 ? p.proj.unit1 : p.proj.unitRS;
+  a.ntile = p.proj.n_tiles;
+  a.ngroups = p.proj.n_groups;
   a.N = p.N; a.NA = p.NA; a.ND = p.ND; a.S = p.S; a.RS = RS; a.RC = p.proj.RC; a.CW = p.proj.CW;
   a.PAD = p.proj.PAD; a.Rp = p.proj.Rp;
   a.nch = RS == 1 ? p.proj.nch1 : p.proj.nchRS;
@@ -290,7 +331,8 @@ cudaError_t launch(const ei_plan &p, int RS, float *P, cudaStream_t st) {
   cudaError_t e = cudaFuncSetAttribute((const void *)project_kernel<NMAP>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  dim3 grid((p.ND + RT - 1) / RT, p.proj.n_groups, p.S * RS);
+  if (RS != 1 && RS != p.proj.RS) return cudaErrorInvalidValue;   // unit tables exist for these
+  dim3 grid(p.proj.n_tiles * p.proj.n_groups * p.S * RS);
   e = launch_pdl(project_kernel<NMAP>, grid, dim3(NT + 32), smem, st, a);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
@@ -405,9 +447,54 @@ static double wavefront_model(const ei_plan &p, const double *angles, const std:
   return n ? wf / n : 0.0;
 }
 
+// Launch order of the K1 work units (tile, group, row split, slice).  Unit cost = rows of its
+// staged chunks (W > 0; the ray tiles at the detector ends and near-axis angles have few).
+//  * Grid within one wave (units <= 2 CTAs x SMs): the block scheduler places block b and block
+//    b + SMs on the same SM (measured, tools/dbg/k1_trace.py: C2 SM 120 ran blocks 138 and 286),
+//    and the SM's time is the sum of its two CTAs' work.  So the heaviest units run alone on the
+//    SMs that get one CTA, and the rest are paired heaviest with lightest.
+//  * Larger grids: heaviest first (longest-processing-time order), so the light units fill the
+//    tail of the last wave.
+static std::vector<int> order_units(const std::vector<int2> &win, int RS, int n_groups, int ntile,
+                                    int nch, int S, int RC, int N) {
+  const int nu1 = RS * n_groups * ntile;          // per slice: (rs, group, tile)
+  std::vector<std::pair<long long, int>> cost;   // (-cost, unit)
+  cost.reserve((size_t)nu1 * S);
+  for (int s = 0; s < S; ++s)
+    for (int rs = 0; rs < RS; ++rs) {
+      const int r0 = (int)(((long long)rs * N) / RS), r1 = (int)(((long long)(rs + 1) * N) / RS);
+      for (int g = 0; g < n_groups; ++g)
+        for (int t = 0; t < ntile; ++t) {
+          const int2 *row = &win[(((size_t)rs * n_groups + g) * ntile + t) * nch];
+          long long c = 0;
+          for (int ch = 0; r0 + ch * RC < r1; ++ch)
+            if (row[ch].y > 0) c += std::min(RC, r1 - (r0 + ch * RC));
+          cost.push_back({-c, t + ntile * (g + n_groups * (rs * S + s))});
+        }
+    }
+  std::stable_sort(cost.begin(), cost.end());    // heaviest first; ties keep (slice, rs, g, t) order
+  const int n = (int)cost.size();
+  int sms = 148, dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaGetLastError();
+  std::vector<int> unit(n);
+  if (n > sms && n <= 2 * sms && !getenv("EI_K1_LPT")) {
+    const int npair = n - sms;                    // blocks b < npair share an SM with b + sms
+    int q = 0;
+    for (int b = npair; b < sms; ++b) unit[b] = cost[q++].second;          // alone: heaviest
+    for (int b = 0; b < npair; ++b) {
+      unit[b] = cost[q + b].second;                                         // next heaviest ...
+      unit[b + sms] = cost[n - 1 - b].second;                               // ... with the lightest
+    }
+  } else {
+    for (int b = 0; b < n; ++b) unit[b] = cost[b].second;
+  }
+  return unit;
+}
+
 int plan_projector(ei_plan &p, const double *angles, const std::vector<int> &proj_angles,
                    std::vector<int2> &groups, std::vector<int> &order, std::vector<int2> &win1,
-                   std::vector<int2> &winRS) {
+                   std::vector<int2> &winRS, std::vector<int> &unit1, std::vector<int> &unitRS) {
   const int N = p.N, ND = p.ND;
   const int NA = (int)proj_angles.size();   // the angles K1 projects (mirror pairs: primaries)
   // groups = runs of angularly adjacent angles (sorted by angle mod 2 pi) of one dominance class
@@ -481,6 +568,10 @@ int plan_projector(ei_plan &p, const double *angles, const std::vector<int> &pro
   // zero padding of the pair-layout map rows so every staged window is one in-bounds copy
   p.proj.PAD = p.proj.CW + 2;   // even
   p.proj.Rp = (N + 1 + 2 * p.proj.PAD + 1) & ~1;   // even: 16-B aligned float2 rows
+  p.proj.n_tiles = ntile;
+  if ((long long)ntile * groups.size() * p.S * RS > 0x7fffffffLL) return EI_ERR_SHAPE;   // 1-D grid
+  unit1 = order_units(win1, 1, (int)groups.size(), ntile, p.proj.nch1, p.S, RC, N);
+  unitRS = RS > 1 ? order_units(winRS, RS, (int)groups.size(), ntile, p.proj.nchRS, p.S, RC, N) : unit1;
   for (size_t g = 0; g < groups.size(); ++g) groups[g].y |= rf_flags[g] << 16;   // last: device copy
   return EI_OK;
 }
@@ -494,3 +585,10 @@ cudaError_t launch_project1(const ei_plan &p, float *P, cudaStream_t st, int RS)
 }
 
 }  // namespace ei
+
+#ifdef EI_TRACE
+extern "C" int ei_debug_k1_trace(unsigned long long *host, int n_ctas) {
+  n_ctas = n_ctas < 65536 ? n_ctas : 65536;
+  return cudaMemcpyFromSymbol(host, ei::g_k1_trace, sizeof(unsigned long long) * 4 * n_ctas) == cudaSuccess ? 0 : 5;
+}
+#endif

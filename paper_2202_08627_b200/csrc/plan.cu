@@ -64,7 +64,7 @@ void free_plan(ei_plan *p) {
   for (cudaEvent_t ev : p->h_ev)
     if (ev) cudaEventDestroy(ev);
   void *ptrs[] = {p->tab.k1, p->tab.k3, p->proj.groups, p->proj.order, p->proj.partner, p->alist3,
-                  p->pairs, p->proj.win1, p->proj.winRS, p->MA, p->MAT, p->MB,
+                  p->pairs, p->proj.win1, p->proj.winRS, p->proj.unit1, p->proj.unitRS, p->MA, p->MAT, p->MB,
                   p->MBT, p->M1, p->M1T, p->diag, p->part_mo, p->part3, p->P, p->GA, p->GB, p->GA1,
                   p->part_curve, p->part_reg, p->h_maps, p->h_flat, p->h_mask, p->h_drift,
                   p->h_sexp, p->h_grad, p->h_cost, p->h_status};
@@ -165,8 +165,8 @@ int ei_plan_create(const ei_geometry *geom, const double *angles, ei_plan **out)
   p->npairs = (int)pairs.size();
   p->NA3 = (int)prim.size();
   std::vector<int2> groups, win1, winRS;
-  std::vector<int> order;
-  rc = ei::plan_projector(*p, angles, prim, groups, order, win1, winRS);
+  std::vector<int> order, unit1, unitRS;
+  rc = ei::plan_projector(*p, angles, prim, groups, order, win1, winRS, unit1, unitRS);
   if (!rc) rc = ei::plan_curve(*p);
   if (rc) {
     delete[] k1;
@@ -188,6 +188,8 @@ int ei_plan_create(const ei_geometry *geom, const double *angles, ei_plan **out)
   if (!pairs.empty()) A(dalloc(&p->pairs, pairs.size()));
   A(dalloc(&p->proj.win1, win1.size()));
   if (!winRS.empty()) A(dalloc(&p->proj.winRS, winRS.size()));
+  A(dalloc(&p->proj.unit1, unit1.size()));
+  A(dalloc(&p->proj.unitRS, unitRS.size()));
   A(dalloc(&p->MA, S * NP));
   A(dalloc(&p->MAT, S * NP));
   A(dalloc(&p->MB, S * NP));
@@ -241,6 +243,10 @@ int ei_plan_create(const ei_geometry *geom, const double *angles, ei_plan **out)
     A(cudaMemcpy(p->proj.win1, win1.data(), sizeof(int2) * win1.size(), cudaMemcpyHostToDevice));
   if (e == cudaSuccess && !winRS.empty())
     A(cudaMemcpy(p->proj.winRS, winRS.data(), sizeof(int2) * winRS.size(), cudaMemcpyHostToDevice));
+  if (e == cudaSuccess)
+    A(cudaMemcpy(p->proj.unit1, unit1.data(), sizeof(int) * unit1.size(), cudaMemcpyHostToDevice));
+  if (e == cudaSuccess)
+    A(cudaMemcpy(p->proj.unitRS, unitRS.data(), sizeof(int) * unitRS.size(), cudaMemcpyHostToDevice));
   delete[] k1;
   delete[] k3;
   if (e != cudaSuccess) {

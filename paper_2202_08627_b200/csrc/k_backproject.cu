@@ -68,6 +68,16 @@ struct Smem {
   uint64_t full[NST], empty[NST];
 };
 
+#ifdef EI_TRACE
+// debug builds only (tools/dbg/k1_trace.py --k3): per CTA {start, first chunk staged, end, SM id}
+__device__ unsigned long long g_k3_trace[4 * 65536];
+__device__ __forceinline__ unsigned long long gtimer3() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#endif
+
 struct FinArgs {
   const float *part_cost, *part_mo;   // K2 per-warp partials [S][NA][nseg * nw]
   const double *part_reg;
@@ -81,9 +91,20 @@ struct FinArgs {
 // then the warps' sums in warp order
 __device__ __forceinline__ void finalize(const FinArgs &f, int s, int tid) {
   __shared__ double fred[NT / 32];
+  // every thread's loads are issued UF at a time (independent L2 round trips in flight) and added
+  // in the same strided order as a plain loop: q = tid, tid + NT, ...
+  constexpr int UF = 8;
   double c = 0.0, rg = 0.0;
   const float *pc = f.part_cost + (size_t)s * f.per_slice;
-  for (int q = tid; q < f.per_slice; q += NT) c += (double)__ldcg(pc + q);
+  int q = tid;
+  for (; q + (UF - 1) * NT < f.per_slice; q += UF * NT) {
+    float v[UF];
+#pragma unroll
+    for (int u = 0; u < UF; ++u) v[u] = __ldcg(pc + q + u * NT);
+#pragma unroll
+    for (int u = 0; u < UF; ++u) c += (double)v[u];
+  }
+  for (; q < f.per_slice; q += NT) c += (double)__ldcg(pc + q);
   if (f.lambda > 0.0)
     for (int b = tid; b < f.RB; b += NT) rg += __ldcg(f.part_reg + (size_t)s * f.RB + b);
   double v = c + f.lambda * rg;
@@ -99,7 +120,15 @@ __device__ __forceinline__ void finalize(const FinArgs &f, int s, int tid) {
     for (int a = tid; a < f.NA; a += NT) {
       const float *pm = f.part_mo + ((size_t)s * f.NA + a) * f.nseg;
       double m = 0.0;
-      for (int q = 0; q < f.nseg; ++q) m += (double)__ldcg(pm + q);
+      int r = 0;
+      for (; r + UF <= f.nseg; r += UF) {
+        float v[UF];
+#pragma unroll
+        for (int u = 0; u < UF; ++u) v[u] = __ldcg(pm + r + u);
+#pragma unroll
+        for (int u = 0; u < UF; ++u) m += (double)v[u];
+      }
+      for (; r < f.nseg; ++r) m += (double)__ldcg(pm + r);
       f.g_drift[(size_t)s * f.NA + a] = (float)m;
     }
 }
@@ -120,6 +149,10 @@ __global__ void __launch_bounds__(NT + 32, 3) backproject_kernel(
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int s = blockIdx.z % S, ks = blockIdx.z / S;
   const int j0 = blockIdx.x * TILE, i0 = blockIdx.y * TILE;
+#ifdef EI_TRACE
+  const unsigned long long t_start = gtimer3();
+  unsigned long long t_data = 0;
+#endif
   const float ctr = 0.5f * (float)(N - 1), dctr = 0.5f * (float)(ND - 1);
   const size_t rowlen = (size_t)RpG;   // padded G rows: entry e at e + PADG
   const TA *GAs = GA + (size_t)s * NA * rowlen + PADG;
@@ -199,6 +232,9 @@ __global__ void __launch_bounds__(NT + 32, 3) backproject_kernel(
   uint32_t ph = 0;
   for (int c = c_lo; c < c_hi; ++c) {
     mbar_wait(&sm.full[st], ph);
+#ifdef EI_TRACE
+    if (c == c_lo) t_data = gtimer3();
+#endif
     const int na = min(CH, NA3 - c * CH);
 #pragma unroll 2   // two angles in flight per warp (measured: C4 K3 8.94 -> 8.76 ms; x4 8.80)
     for (int al = 0; al < na; ++al) {
@@ -231,6 +267,20 @@ __global__ void __launch_bounds__(NT + 32, 3) backproject_kernel(
     if (++st == NST) { st = 0; ph ^= 1; }
   }
 
+#ifdef EI_TRACE
+  asm volatile("bar.sync 2, %0;\n" ::"n"(NT) : "memory");   // consumers only
+  if (tid == 0) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+    const size_t b = ((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+    if (b < 65536) {
+      g_k3_trace[4 * b] = t_start;
+      g_k3_trace[4 * b + 1] = t_data;
+      g_k3_trace[4 * b + 2] = gtimer3();
+      g_k3_trace[4 * b + 3] = smid | ((unsigned long long)(c_hi - c_lo) << 32);
+    }
+  }
+#endif
   const int i = i0 + row;
   const size_t NN = (size_t)N * N;
   if (KS > 1) {   // angle split: publish partials; ks_reduce_kernel sums them in ks order
@@ -371,3 +421,10 @@ cudaError_t launch_backproject1(const ei_plan &p, float *map, cudaStream_t st, c
 }
 
 }  // namespace ei
+
+#ifdef EI_TRACE
+extern "C" int ei_debug_k3_trace(unsigned long long *host, int n_ctas) {
+  n_ctas = n_ctas < 65536 ? n_ctas : 65536;
+  return cudaMemcpyFromSymbol(host, ei::g_k3_trace, sizeof(unsigned long long) * 4 * n_ctas) == cudaSuccess ? 0 : 5;
+}
+#endif

@@ -153,6 +153,17 @@ __global__ void __launch_bounds__(K2_MAXT + 32, 2) curve_kernel(K2Args g) {
   // PDL: only the producer reads K1's output (the projections, via TMA); the consumers' G and
   // partial writes are read only by this call's K3
   if (wid == nw) {   // ---------------- producer warp ----------------
+    // the measured curves are inputs, not K1's output: the first item's s_exp rows are requested
+    // before the PDL wait, so their HBM latency overlaps K1's tail
+    const bool pre0 = g.vec && i0 < i1;
+    if (pre0 && lane == 0) {
+      const int kb = p0.seg * g.W - J;
+      const int ks = max(0, kb), ke = min(ND, kb + WB);
+      const uint32_t bytes = (uint32_t)(ke - ks) * 4u;
+      mbar_arrive_expect_tx(&full[0], bytes * (uint32_t)g.nrows);   // all rows of the stage
+      for (int r = g.nmap; r < g.nrows; ++r)
+        bulk_g2s(ring + (ks - kb) + r * WB, row_ptr(g, p0, r) + ks, bytes, &full[0]);
+    }
     pdl_wait();   // K1's projections
     Pos q = p0;
     int st = 0;
@@ -168,8 +179,10 @@ __global__ void __launch_bounds__(K2_MAXT + 32, 2) curve_kernel(K2Args g) {
       if (g.vec) {
         if (lane == 0) {
           const uint32_t bytes = (uint32_t)(ke - ks) * 4u;
-          mbar_arrive_expect_tx(&full[st], bytes * (uint32_t)g.nrows);
-          for (int r = 0; r < g.nrows; ++r) bulk_g2s(dst + r * WB, row_ptr(g, q, r) + ks, bytes, &full[st]);
+          const bool pre = pre0 && item == i0;               // s_exp rows already requested
+          if (!pre) mbar_arrive_expect_tx(&full[st], bytes * (uint32_t)g.nrows);
+          const int rend = pre ? g.nmap : g.nrows;
+          for (int r = 0; r < rend; ++r) bulk_g2s(dst + r * WB, row_ptr(g, q, r) + ks, bytes, &full[st]);
         }
       } else {   // unaligned rows: the warp's lanes copy them
         for (int r = 0; r < g.nrows; ++r) {

@@ -284,15 +284,16 @@ __global__ void __launch_bounds__(K2_MAXT + 32, 2) curve_kernel(K2Args g) {
       // per-position constants of the curve (the 4 positions are independent chains: ILP 4)
       float base[J], amp[J], c2[J], W2[J], invW2[J];
       bool mc[J], wc[J], core[J];
+      const int segW = seg * g.W, cw = min(g.W, ND - segW);   // core positions [segW, segW + cw)
+      const float hf = 0.5f * g.inv_du;
 #pragma unroll
       for (int j = 0; j < J; ++j) {
         const int k = k0 + j;
-        const bool ok = k >= 0 && k < ND;
-        core[j] = ok && k >= seg * g.W && k < seg * g.W + g.W;
-        // D P_delta (a2): central inside, one-sided at the two ends
-        const float dP = k == 0 ? (pdv[j + 2] - pdv[j + 1]) * g.inv_du
-                       : k == ND - 1 ? (pdv[j + 1] - pdv[j]) * g.inv_du
-                                     : (pdv[j + 2] - pdv[j]) * (0.5f * g.inv_du);
+        const bool ok = (unsigned)k < (unsigned)ND;
+        core[j] = (unsigned)(k - segW) < (unsigned)cw;
+        // D P_delta (a2): central inside, one-sided at the two ends (selects, no branches)
+        const bool lo = k == 0, hi = k == ND - 1;
+        const float dP = ((hi ? pdv[j + 1] : pdv[j + 2]) - (lo ? pdv[j + 1] : pdv[j])) * ((lo || hi) ? g.inv_du : hf);
         float pm = at(Pm, j);
         mc[j] = (pm > 50.f) || (pm < -50.f);
         pm = fminf(fmaxf(pm, -50.f), 50.f);
@@ -306,76 +307,121 @@ __global__ void __launch_bounds__(K2_MAXT + 32, 2) curve_kernel(K2Args g) {
         amp[j] = ok ? (Mode<MODE>::sampled ? T : T * at(fA, j) * w * rsq(W2[j])) : 0.f;
         c2[j] = -0.5f * LOG2E * invW2[j];   // exp(-u^2 / 2W^2) = 2^(c2 u^2)
         base[j] = (Mode<MODE>::sampled ? 0.f : at(fc, j)) + mo + g.zs * dP;
-        if (core[j]) {
-          mu_cl += mc[j];
-          w2_cl += wc[j];
-        }
+        mu_cl += core[j] & mc[j];
+        w2_cl += core[j] & wc[j];
       }
       const size_t rowb = (size_t)row * g.M * ND + k0;   // s_mod row base (k0)
       float gmm[J], gdd[J], gq[J], cst[J];
 #pragma unroll
       for (int j = 0; j < J; ++j) gmm[j] = gdd[j] = gq[j] = cst[j] = 0.f;
-      // one mask position for the 4 positions: r = s - s_exp; cost += r^2; with rs = r s:
-      //   gmm += rs, gdd += rs u, gq += rs u^2   (g_sigma uses gq - W^2 gmm)
-      auto term = [&](int j, float mpos, int m, float se) {
-        const float du_ = mpos - base[j];
-        float sv, tfp = 0.f, u2 = 0.f;
-        if (Mode<MODE>::sampled) {   // periodic Catmull-Rom through the K knots (R23)
-          const int K = g.K;
-          const float x = du_ * (float)K;
-          const float fl = floorf(x);
-          const float tau = x - fl;
-          int i = (int)fl % K;
-          if (i < 0) i += K;
-          const int q0 = i == 0 ? K - 1 : i - 1, q2 = i + 1 == K ? 0 : i + 1, q3 = q2 + 1 == K ? 0 : q2 + 1;
-          const bool ok = k0 + j >= 0 && k0 + j < ND;
-          const float p0 = ok ? __ldg(fsb + q0 * ND + j) : 0.f, p1 = ok ? __ldg(fsb + i * ND + j) : 0.f,
-                      p2 = ok ? __ldg(fsb + q2 * ND + j) : 0.f, p3 = ok ? __ldg(fsb + q3 * ND + j) : 0.f;
-          const float a1 = p2 - p0, a2 = fmaf(2.f, p0, fmaf(-5.f, p1, fmaf(4.f, p2, -p3)));
-          const float a3 = fmaf(3.f, p1 - p2, p3 - p0);
-          const float f = 0.5f * fmaf(tau, fmaf(tau, fmaf(tau, a3, a2), a1), 2.f * p1);
-          const float fp = 0.5f * (float)K * fmaf(tau, fmaf(3.f * tau, a3, 2.f * a2), a1);
-          sv = amp[j] * f;
-          tfp = amp[j] * fp;
-        } else {
-          u2 = du_ * du_;
-          sv = amp[j] * ex2(c2[j] * u2);
-        }
-        if (!Mode<MODE>::cost) {
-          if (core[j]) g.s_mod[rowb + (size_t)m * ND + j] = sv;
-        } else {
-          const float r = sv - se;
-          cst[j] = fmaf(r, r, cst[j]);
-          const float rsv = r * sv;
-          gmm[j] += rsv;
-          if (Mode<MODE>::sampled) {
-            gdd[j] = fmaf(r, tfp, gdd[j]);   // sum r T f'
-          } else {
-            gdd[j] = fmaf(rsv, du_, gdd[j]);
-            gq[j] = fmaf(rsv, u2, gq[j]);
+      if constexpr (Mode<MODE>::cost && !Mode<MODE>::sampled) {
+        // Gaussian flat, cost path: positions (0, 1) and (2, 3) as packed pairs, so every step of
+        // the term but the two exponentials is one FADD2 / FMUL2 / FFMA2 (same roundings as the
+        // scalar form below):  u = m - base, s = amp 2^(c2 u^2), r = s - s_exp, cost += r^2,
+        //   gmm += r s, gdd += r s u, gq += r s u^2
+        const float2 nb[2] = {make_float2(-base[0], -base[1]), make_float2(-base[2], -base[3])};
+        const float2 am2[2] = {make_float2(amp[0], amp[1]), make_float2(amp[2], amp[3])};
+        const float2 cc2[2] = {make_float2(c2[0], c2[1]), make_float2(c2[2], c2[3])};
+        const float2 m1 = make_float2(-1.f, -1.f);
+        float2 vc[2], vm[2], vd[2], vq[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) vc[h] = vm[h] = vd[h] = vq[h] = make_float2(0.f, 0.f);
+        auto term2 = [&](float mpos, const float4 &se4) {
+          const float2 mp = make_float2(mpos, mpos);
+          const float2 se[2] = {make_float2(se4.x, se4.y), make_float2(se4.z, se4.w)};
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const float2 du = __fadd2_rn(mp, nb[h]);
+            const float2 u2 = __fmul2_rn(du, du);
+            const float2 ar = __fmul2_rn(cc2[h], u2);
+            const float2 sv = __fmul2_rn(am2[h], make_float2(ex2(ar.x), ex2(ar.y)));
+            const float2 r = __ffma2_rn(m1, se[h], sv);
+            vc[h] = __ffma2_rn(r, r, vc[h]);
+            const float2 rsv = __fmul2_rn(r, sv);
+            vm[h] = __fadd2_rn(vm[h], rsv);
+            vd[h] = __ffma2_rn(rsv, du, vd[h]);
+            vq[h] = __ffma2_rn(rsv, u2, vq[h]);
           }
+        };
+#pragma unroll
+        for (int u = 0; u < MPF; ++u) {          // mask positions in registers
+          if (u >= g.M) break;
+          term2(mk[u], r4[(g.nmap + u) * W4 + t]);
         }
-      };
+        for (int m = MPF; m < g.M; ++m) term2(__ldg(g.mask + m), r4[(g.nmap + m) * W4 + t]);
 #pragma unroll
-      for (int u = 0; u < MPF; ++u) {          // mask positions in registers
-        if (u >= g.M) break;
-        const float4 se4 = Mode<MODE>::cost ? r4[(g.nmap + u) * W4 + t] : make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int h = 0; h < 2; ++h) {
+          cst[2 * h] = vc[h].x; cst[2 * h + 1] = vc[h].y;
+          gmm[2 * h] = vm[h].x; gmm[2 * h + 1] = vm[h].y;
+          gdd[2 * h] = vd[h].x; gdd[2 * h + 1] = vd[h].y;
+          gq[2 * h] = vq[h].x; gq[2 * h + 1] = vq[h].y;
+        }
+      } else {
+        // one mask position for the 4 positions: r = s - s_exp; cost += r^2; with rs = r s:
+        //   gmm += rs, gdd += rs u, gq += rs u^2   (g_sigma uses gq - W^2 gmm)
+        auto term = [&](int j, float mpos, int m, float se) {
+          const float du_ = mpos - base[j];
+          float sv, tfp = 0.f, u2 = 0.f;
+          if (Mode<MODE>::sampled) {   // periodic Catmull-Rom through the K knots (R23)
+            const int K = g.K;
+            const float x = du_ * (float)K;
+            const float fl = floorf(x);
+            const float tau = x - fl;
+            int i = (int)fl % K;
+            if (i < 0) i += K;
+            const int q0 = i == 0 ? K - 1 : i - 1, q2 = i + 1 == K ? 0 : i + 1, q3 = q2 + 1 == K ? 0 : q2 + 1;
+            const bool ok = k0 + j >= 0 && k0 + j < ND;
+            const float p0 = ok ? __ldg(fsb + q0 * ND + j) : 0.f, p1 = ok ? __ldg(fsb + i * ND + j) : 0.f,
+                        p2 = ok ? __ldg(fsb + q2 * ND + j) : 0.f, p3 = ok ? __ldg(fsb + q3 * ND + j) : 0.f;
+            const float a1 = p2 - p0, a2 = fmaf(2.f, p0, fmaf(-5.f, p1, fmaf(4.f, p2, -p3)));
+            const float a3 = fmaf(3.f, p1 - p2, p3 - p0);
+            const float f = 0.5f * fmaf(tau, fmaf(tau, fmaf(tau, a3, a2), a1), 2.f * p1);
+            const float fp = 0.5f * (float)K * fmaf(tau, fmaf(3.f * tau, a3, 2.f * a2), a1);
+            sv = amp[j] * f;
+            tfp = amp[j] * fp;
+          } else {
+            u2 = du_ * du_;
+            sv = amp[j] * ex2(c2[j] * u2);
+          }
+          if (!Mode<MODE>::cost) {
+            if (core[j]) g.s_mod[rowb + (size_t)m * ND + j] = sv;
+          } else {
+            const float r = sv - se;
+            cst[j] = fmaf(r, r, cst[j]);
+            const float rsv = r * sv;
+            gmm[j] += rsv;
+            if (Mode<MODE>::sampled) {
+              gdd[j] = fmaf(r, tfp, gdd[j]);   // sum r T f'
+            } else {
+              gdd[j] = fmaf(rsv, du_, gdd[j]);
+              gq[j] = fmaf(rsv, u2, gq[j]);
+            }
+          }
+        };
 #pragma unroll
-        for (int j = 0; j < J; ++j) term(j, mk[u], u, at(se4, j));
-      }
-      for (int m = MPF; m < g.M; ++m) {        // M > MPF
-        const float mp = __ldg(g.mask + m);
-        const float4 se4 = Mode<MODE>::cost ? r4[(g.nmap + m) * W4 + t] : make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int u = 0; u < MPF; ++u) {          // mask positions in registers
+          if (u >= g.M) break;
+          const float4 se4 = Mode<MODE>::cost ? r4[(g.nmap + u) * W4 + t] : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-        for (int j = 0; j < J; ++j) term(j, mp, m, at(se4, j));
+          for (int j = 0; j < J; ++j) term(j, mk[u], u, at(se4, j));
+        }
+        for (int m = MPF; m < g.M; ++m) {        // M > MPF
+          const float mp = __ldg(g.mask + m);
+          const float4 se4 = Mode<MODE>::cost ? r4[(g.nmap + m) * W4 + t] : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+          for (int j = 0; j < J; ++j) term(j, mp, m, at(se4, j));
+        }
       }
       if (Mode<MODE>::cost) {
+        // a non-finite s_exp makes the cost non-finite; only then count the elements (rare)
+        if (!isfinite((cst[0] + cst[1]) + (cst[2] + cst[3])))
+#pragma unroll
+          for (int j = 0; j < J; ++j)
+            if (core[j] && !isfinite(cst[j]))
+              for (int m = 0; m < g.M; ++m) bad += !isfinite(stg[(g.nmap + m) * WB + J * t + j]);
 #pragma unroll
         for (int j = 0; j < J; ++j) {
-          // a non-finite s_exp makes the cost non-finite; only then count the elements (rare)
-          if (core[j] && !isfinite(cst[j]))
-            for (int m = 0; m < g.M; ++m) bad += !isfinite(stg[(g.nmap + m) * WB + J * t + j]);
-          const bool ok = k0 + j >= 0 && k0 + j < ND;
+          const bool ok = (unsigned)(k0 + j) < (unsigned)ND;
           const float gss = fmaf(-W2[j], gmm[j], gq[j]);   // sum r s (u^2 - W^2)
           const float gmj = (mc[j] || !ok) ? 0.f : -2.f * gmm[j];
           const float gsj = (wc[j] || !ok) ? 0.f : gss * invW2[j] * invW2[j];
@@ -384,10 +430,8 @@ __global__ void __launch_bounds__(K2_MAXT + 32, 2) curve_kernel(K2Args g) {
           if (j == 1) { gm4.y = gmj; gs4.y = gsj; gd4.y = gdj; }
           if (j == 2) { gm4.z = gmj; gs4.z = gsj; gd4.z = gdj; }
           if (j == 3) { gm4.w = gmj; gs4.w = gsj; gd4.w = gdj; }
-          if (core[j]) {
-            cost += cst[j];
-            gmo += gdj;
-          }
+          cost += core[j] ? cst[j] : 0.f;
+          gmo += core[j] ? gdj : 0.f;
         }
       }
     }
@@ -396,10 +440,26 @@ __global__ void __launch_bounds__(K2_MAXT + 32, 2) curve_kernel(K2Args g) {
     if (++st == NST) { st = 0; ph ^= 1; }
     if (Mode<MODE>::cost) {
       float4 *x4 = reinterpret_cast<float4 *>(xch + buf * 3 * WB);
-      if (staged) {
-        x4[t] = gd4;
+      // D^T of a2's D (one-sided end rows) is the central formula y[q] = (g'[q-1] - g'[q+1]) / 2du
+      // on a ghost-extended g_Delta: g'[0] = 2 g[0], g'[-1] = -2 g[0], g'[ND-1] = 2 g[ND-1],
+      // g'[ND] = -2 g[ND-1], g' = g elsewhere (K2).  Only threads with positions in
+      // the row publish; the ghosts outside the row are written by the owners of 0 and ND-1.
+      float gx[J];
+      if (any) {
+        const int jl = ND - 1 - k0;                               // position ND-1 in this float4
+        const float gend = (jl >= 0 && jl < J) ? at(gd4, jl) : 0.f;
+#pragma unroll
+        for (int j = 0; j < J; ++j) {
+          const int k = k0 + j;
+          const float v = at(gd4, j);
+          gx[j] = (k == 0 || k == ND - 1) ? 2.f * v : (k == ND ? -2.f * gend : v);
+        }
+        x4[t] = make_float4(gx[0], gx[1], gx[2], gx[3]);
         x4[W4 + t] = gm4;
         if (!Mode<MODE>::h) x4[2 * W4 + t] = gs4;
+        float *xd = xch + buf * 3 * WB - kb;                      // g'_Delta by detector position
+        if (k0 == 0) xd[-1] = -2.f * gd4.x;
+        if (jl == J - 1) xd[ND] = -2.f * gd4.w;
       }
       // cost and dS/dm_o partials: fp32 per thread and per warp, fp64 over items/warps in K3
       const float wc_ = warp_sum(cost);
@@ -411,37 +471,22 @@ __global__ void __launch_bounds__(K2_MAXT + 32, 2) curve_kernel(K2Args g) {
       }
       asm volatile("bar.sync 1, %0;\n" ::"r"(NT) : "memory");   // consumers only
       const int e0 = max(k0, seg * g.W), e1 = min(min(k0 + J, seg * g.W + g.W), ND);
-      if (staged && e0 < e1) {   // core entries imply t <= WB/4 - 2, so x4[t + 1] is staged
-        // neighbours' float4s: g_Delta at k0-4 .. k0+7, g_mu / g_sigma at k0-4 .. k0-1
+      if (staged && e0 < e1) {   // core entries imply any and t <= WB/4 - 2 (x4[t + 1] staged)
+        // neighbours' float4s: g'_Delta at k0-4 .. k0+7, g_mu / g_sigma at k0-4 .. k0-1 (slots of
+        // threads without row positions are stale: only their ghost entries are read)
         const float4 Ld = t > 0 ? x4[t - 1] : make_float4(0.f, 0.f, 0.f, 0.f);
         const float4 Rd = x4[t + 1];
         const float4 Lm = t > 0 ? x4[W4 + t - 1] : make_float4(0.f, 0.f, 0.f, 0.f);
         const float4 Ls = (!Mode<MODE>::h && t > 0) ? x4[2 * W4 + t - 1] : make_float4(0.f, 0.f, 0.f, 0.f);
-        const float dv[J + 3] = {Ld.z, Ld.w, gd4.x, gd4.y, gd4.z, gd4.w, Rd.x};   // D at k0-2 .. k0+4
+        const float dv[J + 3] = {Ld.z, Ld.w, gx[0], gx[1], gx[2], gx[3], Rd.x};   // g' at k0-2 .. k0+4
         const float mv[J + 1] = {Lm.w, gm4.x, gm4.y, gm4.z, gm4.w};              // g_mu at k0-1 .. k0+3
         const float sv[J + 1] = {Ls.w, gs4.x, gs4.y, gs4.z, gs4.w};
-        const float *D = xch + buf * 3 * WB - kb;    // D[k] = g_Delta at detector k (row ends)
         const float zh = 0.5f * g.zs * g.inv_du;
-        // g_delta = zs D^T g_Delta, D^T written out from the rows of D (a2):
-        //   y[q] = [q==0](-g0) + [q==1](g0) + [q==ND-2](-g_{ND-1}) + [q==ND-1](g_{ND-1})
-        //        + 1/2 g_{q-1} [1 <= q-1 <= ND-2] - 1/2 g_{q+1} [1 <= q+1 <= ND-2]   (all / du)
-        auto gdelta = [&](int i) {   // at position q = k0 - 1 + i, i = 0..4
-          const int q = k0 - 1 + i;
-          if (q >= 2 && q <= ND - 3) return zh * (dv[i] - dv[i + 2]);   // interior rows
-          float y = 0.f;
-          if (q == 0) y -= D[0];
-          if (q == 1) y += D[0];
-          if (q == ND - 2) y -= D[ND - 1];
-          if (q == ND - 1) y += D[ND - 1];
-          if (q - 1 >= 1 && q - 1 <= ND - 2) y += 0.5f * dv[i];
-          if (q + 1 >= 1 && q + 1 <= ND - 2) y -= 0.5f * dv[i + 2];
-          return g.zs * g.inv_du * y;
-        };
         const float sc = __ldg(g.k3 + a).w;
         const size_t rb = (size_t)row * g.RpG + g.PADG;
-        float gdl[J + 1];
+        float gdl[J + 1];   // g_delta = zs D^T g_Delta at k0-1 .. k0+3 (k0-1 is used only if >= 0)
 #pragma unroll
-        for (int i = 0; i <= J; ++i) gdl[i] = gdelta(i);
+        for (int i = 0; i <= J; ++i) gdl[i] = zh * (dv[i] - dv[i + 2]);
 #pragma unroll
         for (int j = 0; j < J; ++j) {   // pair entries e = k0 + j: (g[e-1], g[e])
           const int e = k0 + j;

@@ -474,7 +474,7 @@ def run_reference(args, cfg, rank):
     value = 1.0 / (per_slice * cfg.S)
     sample = ("%d timed single-slice fp64 oracle cost+gradient evaluations of %s (one slice = 1/%d "
               "eval)" % (len(times), cfg.name, cfg.S))
-    return {"metric": METRIC, "value": round(value, 6), "unit": UNIT, "n_gpus": 0, "steps": args.steps,
+    return {"metric": METRIC, "value": round(value, 6), "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(per_slice * 1e3 * cfg.S, 3),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "impl": "reference",

@@ -454,11 +454,12 @@ static double wavefront_model(const ei_plan &p, const double *angles, const std:
 //    and the SM's time is the sum of its two CTAs' work.  So the heaviest units run alone on the
 //    SMs that get one CTA, and the rest are paired heaviest with lightest.
 //  * Larger grids: heaviest first (longest-processing-time order), so the light units fill the
-//    tail of the last wave.
+//    tail of the last wave; slice by slice, so the CTAs in flight share one slice's map in L2
+//    (LPT across all 64 slices of C4 raised K1's DRAM traffic from ~18 to ~170 MB per slice).
 static std::vector<int> order_units(const std::vector<int2> &win, int RS, int n_groups, int ntile,
                                     int nch, int S, int RC, int N) {
   const int nu1 = RS * n_groups * ntile;          // per slice: (rs, group, tile)
-  std::vector<std::pair<long long, int>> cost;   // (-cost, unit)
+  std::vector<std::pair<long long, int>> cost;   // (slice, -cost) key, unit
   cost.reserve((size_t)nu1 * S);
   for (int s = 0; s < S; ++s)
     for (int rs = 0; rs < RS; ++rs) {
@@ -469,10 +470,10 @@ static std::vector<int> order_units(const std::vector<int2> &win, int RS, int n_
           long long c = 0;
           for (int ch = 0; r0 + ch * RC < r1; ++ch)
             if (row[ch].y > 0) c += std::min(RC, r1 - (r0 + ch * RC));
-          cost.push_back({-c, t + ntile * (g + n_groups * (rs * S + s))});
+          cost.push_back({(long long)s * (1LL << 40) - c, t + ntile * (g + n_groups * (rs * S + s))});
         }
     }
-  std::stable_sort(cost.begin(), cost.end());    // heaviest first; ties keep (slice, rs, g, t) order
+  std::stable_sort(cost.begin(), cost.end());    // slice-major, heaviest first; ties keep (rs, g, t)
   const int n = (int)cost.size();
   int sms = 148, dev = 0;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);

@@ -40,13 +40,13 @@ EOF
         --log-file $OUT/launches.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline > $OUT/ncu_launch.log 2>&1
       echo "ncu launches rc=$?" | tee -a $OUT/rc.txt ;;
     full)
-      timeout 900 ncu --set full --clock-control none --import-source on \
-        -k regex:"project_kernel|backproject_kernel|curve_kernel" -s 9 -c 3 \
-        -o $OUT/full_c2 python bench.py --steps 3 --warmup 3 --no-cpu-baseline > $OUT/ncu_full_c2.log 2>&1
-      echo "ncu full c2 rc=$?" | tee -a $OUT/rc.txt
-      timeout 900 ncu --set full --clock-control none --import-source on \
-        -k regex:"project_kernel|backproject_kernel|curve_kernel" -s 3 -c 3 \
-        -o $OUT/full_c4s8 python tools/prof_case.py C4 8 2 > $OUT/ncu_full_c4.log 2>&1
-      echo "ncu full c4s8 rc=$?" | tee -a $OUT/rc.txt ;;
+      # one --set full capture per config of the three hot kernels of one bench step (the 4th),
+      # the source of profiles/traffic.json (tools/ncu_traffic.py) and the ncu summaries
+      for c in ${FULL_CFGS:-C2 C3 C5 C4}; do
+        timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
+          -k regex:"project_kernel<\\(int\\)3>|curve_kernel<\\(int\\)1>" -s 9 -c 3 \
+          -o $OUT/full_$c python bench.py --config $c --steps 3 --warmup 3 --no-cpu-baseline > $OUT/ncu_full_$c.log 2>&1
+        echo "ncu full $c rc=$?" | tee -a $OUT/rc.txt
+      done ;;
   esac
 done

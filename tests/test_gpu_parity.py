@@ -300,3 +300,72 @@ def test_angle_shard_partials_sum_to_full(ei, name):
     assert np.all(np.abs(tot_c - c_full) / c_full <= 1e-6)
     for q in range(3):
         assert rel_l2(tot_g[q], g_full[q]) <= 1e-5
+
+
+@pytest.mark.parametrize("n_det,h", [(27, False), (28, False), (27, True), (28, True)])
+def test_detector_end_rows(ei, n_det, h):
+    """K2's one-sided end rows of D (a2) and their transpose, where the
+    rows carry signal: random maps fill the whole grid and the detector is barely wider than it
+    (N_d = 27 / 28 for N = 24: corners project past both ends), unlike the ellipse phantoms whose
+    sinograms vanish at the ends (R9).  N_d = 27 takes K2's lane-copy path, 28 the TMA path.
+    Gates are element-wise (max |gpu - oracle| / max |oracle|), so an error confined to the
+    end rows is not diluted by the L2 norm: s_mod 1e-5 (fp32 exp/rsqrt, ~1e-6 seen), gradient maps
+    1e-4 (fp32 sums of N_theta * M terms), cost 1e-4 (as the north_star gate)."""
+    rng = np.random.default_rng(4242 + n_det)
+    S, N, NA, M = 2, 24, 13, 5
+    ang = np.pi * (np.arange(NA) + 0.3) / NA
+    z, w = 1.0, 0.15
+    flat = np.zeros((S, 3, n_det), np.float32)
+    flat[:, 0] = 1e4 * rng.uniform(0.95, 1.05, (S, n_det))
+    flat[:, 1] = rng.normal(0.0, 0.05, (S, n_det))
+    flat[:, 2] = w
+    mask = ((np.arange(M) - (M - 1) / 2) / M).astype(np.float32)
+    drift = np.cumsum(rng.normal(0.0, 0.003, NA)).astype(np.float32)
+    mu = rng.uniform(0.0, 1.0, (S, N, N))
+    de = rng.uniform(0.0, 1.0, (S, N, N))
+    sg = rng.uniform(0.0, 1.0, (S, N, N))
+    # scale as R16/R17 (oracle projector): max |z D R delta| = 0.3 w, max R sigma = (0.2 w)^2,
+    # max R mu = 0.3
+    for s in range(S):
+        Pd = ora.project(de[s].astype(np.float32), ang, n_det)
+        de[s] *= 0.3 * w / max(np.abs(z * ora.diff_t(r)).max() for r in Pd)
+        sg[s] *= (0.2 * w) ** 2 / ora.project(sg[s].astype(np.float32), ang, n_det).max()
+        mu[s] *= 0.3 / ora.project(mu[s].astype(np.float32), ang, n_det).max()
+    if h:   # the single-map model (NEXT-3): mu = h, delta = gamma h, sigma = 0
+        de, sg = synth.H_GAMMA * mu, np.zeros_like(mu)
+    truth = [x.astype(np.float32) for x in (mu, de, sg)]
+    s_true, _ = ora.forward(ang, *truth, flat, mask, drift, z=z)
+    s_exp = (s_true * (1.0 + 0.01 * rng.standard_normal(s_true.shape))).astype(np.float32)
+    maps = synth.perturbed(tuple(truth), 99)
+    if h:
+        maps = (maps[0], (synth.H_GAMMA * maps[0]).astype(np.float32), np.zeros_like(maps[0]))
+    plan = ei.Plan(S, N, NA, n_det, M, 1.0, 1.0, z, ang)
+    # forward model at the end columns
+    smod = torch.zeros(S, NA, M, n_det, device="cuda")
+    ei.ei_forward(plan, *[dev(m) for m in maps], dev(flat), dev(mask), dev(drift), smod)
+    ref, _ = ora.forward(ang, *maps, flat, mask, drift, z=z)
+    got = smod.cpu().numpy()
+    ends = [0, 1, n_det - 2, n_det - 1]
+    assert np.abs(got[..., ends] - ref[..., ends]).max() / np.abs(ref).max() <= 1e-5
+    # cost and gradient
+    rc, rgm, rgd, rgs, _ = ora.cost_grad(ang, *maps, flat, mask, drift, s_exp, 0.0, z=z)
+    if h:
+        cost = torch.zeros(S, dtype=torch.float64, device="cuda")
+        gh = torch.zeros(S, N, N, device="cuda")
+        st = torch.zeros(4, dtype=torch.int32, device="cuda")
+        ei.ei_cost_grad_h(plan, dev(maps[0]), synth.H_GAMMA, dev(flat), dev(mask), dev(drift),
+                          dev(s_exp), 0.0, cost, gh, None, st)
+        torch.cuda.synchronize()
+        pairs = [(gh.cpu().numpy(), rgm + synth.H_GAMMA * rgd)]   # dS/dh = g_mu + gamma g_delta
+        cost = cost.cpu().numpy()
+    else:
+        ws = ei.Workspace(plan)
+        cost, g, _ = ei.cost_grad(plan, [dev(m) for m in maps], dev(flat), dev(mask), dev(drift),
+                                  dev(s_exp), 0.0, ws)
+        torch.cuda.synchronize()
+        cost = cost.cpu().numpy()
+        pairs = [(x.cpu().numpy(), r) for x, r in zip(g, (rgm, rgd, rgs))]
+    assert np.all(np.abs(cost - rc) / rc <= 1e-4), (cost, rc)
+    for q, (a, b) in enumerate(pairs):
+        err = np.abs(a - b).max() / np.abs(b).max()
+        assert err <= 1e-4, (q, err)

@@ -584,7 +584,13 @@ int plan_curve(ei_plan &p) {
   int nseg = 1;
   const char *mw = getenv("EI_K2_MAXW");   // tuning knob: cap on the segment width
   const int maxw = mw ? std::max(16, atoi(mw)) : 1 << 30;
+  // ring small enough for >= 3-4 CTAs per SM (more independent items in flight per SM; measured
+  // C4 K2 0.596 -> 0.568 ms at W = 384 vs 768, C3 0.061 -> 0.056 ms at W = 256 vs 512), but
+  // segments not narrower than 256 positions (the 8-position halo and per-item costs grow)
+  const char *sk = getenv("EI_K2_SMEM_KB");   // tuning knob
+  const size_t cap = (size_t)(sk ? std::max(16, atoi(sk)) : 60) * 1024;
   while (W_of(nseg) / J + 2 > K2_MAXT || W_of(nseg) > maxw ||
+         (k2_smem(nrows, W_of(nseg) + 2 * J) > cap && W_of(nseg) > 256) ||
          (k2_smem(nrows, W_of(nseg) + 2 * J) > 110 * 1024 && W_of(nseg) > 64))
     ++nseg;
   p.k2.nseg = nseg;

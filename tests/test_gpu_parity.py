@@ -369,3 +369,24 @@ def test_detector_end_rows(ei, n_det, h):
     for q, (a, b) in enumerate(pairs):
         err = np.abs(a - b).max() / np.abs(b).max()
         assert err <= 1e-4, (q, err)
+
+
+def test_k3_angle_split_matches_unsplit(ei, monkeypatch):
+    """K3's angle split (partial gradients summed in split order by ks_reduce_kernel) against one
+    CTA per (tile, slice) (EI_K3_KS=1 at plan creation): the same sums in another order, so equal
+    to fp32 rounding; the cost (fixed-order sums of K2's partials) is bit-identical."""
+    case = _cases.cached_case("R1")
+    cfg = case.cfg
+    out = []
+    for ks in (None, "1"):
+        if ks is None:
+            monkeypatch.delenv("EI_K3_KS", raising=False)
+        else:
+            monkeypatch.setenv("EI_K3_KS", ks)
+        plan = plan_for(ei, cfg)
+        out.append((ei.ei_plan_info(plan)["k3_angle_split"], gpu_cost_grad(ei, plan, case, case.maps(), 1e-2)))
+    (ks_a, (ca, ga, _)), (ks_b, (cb, gb, _)) = out
+    assert ks_a > 1 and ks_b == 1
+    assert np.array_equal(ca, cb)
+    for a, b in zip(ga, gb):
+        assert rel_l2(a, b) <= 1e-6

@@ -26,6 +26,26 @@
 namespace ei {
 namespace {
 
+#ifdef EI_TRACE
+// debug builds only (tools/dbg/step_trace.py): earliest CTA start / latest CTA end of this file's
+// kernels in the last traced call (globaltimer, ns)
+__device__ unsigned long long g_span_bp[2 * 4];
+__device__ __forceinline__ unsigned long long gt_bp() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define SPAN_START_bp() const unsigned long long span_t0_ = gt_bp()
+#define SPAN_END_bp(k)                                   \
+  do {                                                    \
+    atomicMin(&g_span_bp[2 * (k)], span_t0_);            \
+    atomicMax(&g_span_bp[2 * (k) + 1], gt_bp());         \
+  } while (0)
+#else
+#define SPAN_START_bp()
+#define SPAN_END_bp(k)
+#endif
+
 constexpr int TILE = 32;   // pixels per side
 constexpr int CH = 16;     // angles per staged chunk
 constexpr int WL = 48;     // window entries per angle (>= 31*sqrt(2) + 4)
@@ -149,6 +169,7 @@ __global__ void __launch_bounds__(NT + 32, 3) backproject_kernel(
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int s = blockIdx.z % S, ks = blockIdx.z / S;
   const int j0 = blockIdx.x * TILE, i0 = blockIdx.y * TILE;
+SPAN_START_bp();
 #ifdef EI_TRACE
   const unsigned long long t_start = gtimer3();
   unsigned long long t_data = 0;
@@ -228,6 +249,7 @@ __global__ void __launch_bounds__(NT + 32, 3) backproject_kernel(
 #pragma unroll
   for (int q = 0; q < 4; ++q) am[q] = ad[q] = as[q] = make_float2(0.f, 0.f);
 
+  pdl_wait();   // sleep while K2 runs (this CTA may have launched early)
   int st = 0;
   uint32_t ph = 0;
   for (int c = c_lo; c < c_hi; ++c) {
@@ -279,6 +301,7 @@ __global__ void __launch_bounds__(NT + 32, 3) backproject_kernel(
       g_k3_trace[4 * b + 2] = gtimer3();
       g_k3_trace[4 * b + 3] = smid | ((unsigned long long)(c_hi - c_lo) << 32);
     }
+    SPAN_END_bp(0);
   }
 #endif
   const int i = i0 + row;
@@ -335,6 +358,7 @@ __global__ void __launch_bounds__(256) ks_reduce_kernel(const float *__restrict_
                                                         const float *__restrict__ sigma, float lambda,
                                                         float *__restrict__ o0, float *__restrict__ o1,
                                                         float *__restrict__ o2, size_t out_stride) {
+  SPAN_START_bp();
   pdl_wait();
   const size_t NN = (size_t)N * N, total = (size_t)S * NN;
   for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < total; t += (size_t)gridDim.x * blockDim.x) {
@@ -361,6 +385,10 @@ __global__ void __launch_bounds__(256) ks_reduce_kernel(const float *__restrict_
     }
   }
   pdl_trigger();
+#ifdef EI_TRACE
+  __syncthreads();
+  if (threadIdx.x == 0) SPAN_END_bp(1);
+#endif
 }
 
 template <int NMAP>
@@ -426,5 +454,16 @@ cudaError_t launch_backproject1(const ei_plan &p, float *map, cudaStream_t st, c
 extern "C" int ei_debug_k3_trace(unsigned long long *host, int n_ctas) {
   n_ctas = n_ctas < 65536 ? n_ctas : 65536;
   return cudaMemcpyFromSymbol(host, ei::g_k3_trace, sizeof(unsigned long long) * 4 * n_ctas) == cudaSuccess ? 0 : 5;
+}
+#endif
+
+#ifdef EI_TRACE
+extern "C" int ei_debug_span_bp(unsigned long long *host, int reset) {
+  if (reset) {
+    unsigned long long init[8];
+    for (int k = 0; k < 4; ++k) { init[2 * k] = ~0ULL; init[2 * k + 1] = 0ULL; }
+    return cudaMemcpyToSymbol(ei::g_span_bp, init, sizeof(init)) == cudaSuccess ? 0 : 5;
+  }
+  return cudaMemcpyFromSymbol(host, ei::g_span_bp, sizeof(unsigned long long) * 8) == cudaSuccess ? 0 : 5;
 }
 #endif

@@ -42,6 +42,26 @@
 namespace ei {
 namespace {
 
+#ifdef EI_TRACE
+// debug builds only (tools/dbg/step_trace.py): earliest CTA start / latest CTA end of this file's
+// kernels in the last traced call (globaltimer, ns)
+__device__ unsigned long long g_span_curve[2 * 4];
+__device__ __forceinline__ unsigned long long gt_curve() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define SPAN_START_curve() const unsigned long long span_t0_ = gt_curve()
+#define SPAN_END_curve(k)                                   \
+  do {                                                    \
+    atomicMin(&g_span_curve[2 * (k)], span_t0_);            \
+    atomicMax(&g_span_curve[2 * (k) + 1], gt_curve());         \
+  } while (0)
+#else
+#define SPAN_START_curve()
+#define SPAN_END_curve(k)
+#endif
+
 constexpr int J = 4;           // detector positions per consumer thread
 constexpr int K2_MAXT = 256;   // consumer threads per CTA (max)
 constexpr int NST = 3;         // ring stages
@@ -131,6 +151,7 @@ template <int MODE>
 __global__ void __launch_bounds__(K2_MAXT + 32, 2) curve_kernel(K2Args g) {
   extern __shared__ __align__(16) float smem[];   // ring [NST][nrows][WB] + exchange [2][3][WB]
   __shared__ __align__(8) uint64_t full[NST], empty[NST];
+  SPAN_START_curve();
   const int NT = blockDim.x - 32;                  // consumer threads
   const int t = threadIdx.x, lane = t & 31, wid = t >> 5, nw = NT >> 5;
   const int ND = g.ND, WB = g.WB;
@@ -237,6 +258,7 @@ __global__ void __launch_bounds__(K2_MAXT + 32, 2) curve_kernel(K2Args g) {
     fseg = seg;
     const int row = s * g.NA + a;
     const float mo = g.drift ? __ldg(g.drift + a) : 0.f;
+    if (item == i0) pdl_wait();   // sleep while K1 runs (this CTA may have launched early)
     mbar_wait(&full[st], ph);
     const float *stg = ring + st * stage_floats;   // staged rows of this item
     float4 gm4 = make_float4(0.f, 0.f, 0.f, 0.f), gd4 = gm4, gs4 = gm4;
@@ -510,6 +532,10 @@ __global__ void __launch_bounds__(K2_MAXT + 32, 2) curve_kernel(K2Args g) {
     }
   }
   pdl_trigger();
+#ifdef EI_TRACE
+  asm volatile("bar.sync 2, %0;\n" ::"r"(NT) : "memory");   // consumers only
+  if (t == 0) SPAN_END_curve(0);
+#endif
   if (Mode<MODE>::cost) {
     bad = __reduce_add_sync(0xffffffffu, bad);
     mu_cl = __reduce_add_sync(0xffffffffu, mu_cl);
@@ -646,3 +672,14 @@ cudaError_t launch_curve_cost_grad_hs(const ei_plan &p, float gamma, const float
 }
 
 }  // namespace ei
+
+#ifdef EI_TRACE
+extern "C" int ei_debug_span_curve(unsigned long long *host, int reset) {
+  if (reset) {
+    unsigned long long init[8];
+    for (int k = 0; k < 4; ++k) { init[2 * k] = ~0ULL; init[2 * k + 1] = 0ULL; }
+    return cudaMemcpyToSymbol(ei::g_span_curve, init, sizeof(init)) == cudaSuccess ? 0 : 5;
+  }
+  return cudaMemcpyFromSymbol(host, ei::g_span_curve, sizeof(unsigned long long) * 8) == cudaSuccess ? 0 : 5;
+}
+#endif

@@ -17,6 +17,26 @@
 namespace ei {
 namespace {
 
+#ifdef EI_TRACE
+// debug builds only (tools/dbg/step_trace.py): earliest CTA start / latest CTA end of this file's
+// kernels in the last traced call (globaltimer, ns)
+__device__ unsigned long long g_span_pack[2 * 4];
+__device__ __forceinline__ unsigned long long gt_pack() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define SPAN_START_pack() const unsigned long long span_t0_ = gt_pack()
+#define SPAN_END_pack(k)                                   \
+  do {                                                    \
+    atomicMin(&g_span_pack[2 * (k)], span_t0_);            \
+    atomicMax(&g_span_pack[2 * (k) + 1], gt_pack());         \
+  } while (0)
+#else
+#define SPAN_START_pack()
+#define SPAN_END_pack(k)
+#endif
+
 constexpr int T = 16;
 
 template <int NMAP>
@@ -45,6 +65,8 @@ __global__ void __launch_bounds__(256) pack_pairs_kernel(const float *__restrict
                                                          int PAD, int Rp) {
   __shared__ float tile[NMAP][T + 1][T + 2];   // (T+1)^2 with a one-element halo
   __shared__ double red[8];
+  SPAN_START_pack();
+  PDL_TRIGGER_K0();   // K1's CTAs may launch (they wait for this grid before reading its output)
   const int s = blockIdx.z, ta = blockIdx.y, tb = blockIdx.x;
   const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * T + tx;
   const float *src[3] = {in0 + s * in_stride, NMAP == 3 ? in1 + s * in_stride : nullptr,
@@ -114,6 +136,10 @@ __global__ void __launch_bounds__(256) pack_pairs_kernel(const float *__restrict
       part_reg[(size_t)s * gridDim.x * gridDim.y + blockIdx.y * gridDim.x + blockIdx.x] = t;
     }
   }
+#ifdef EI_TRACE
+  __syncthreads();
+  if (tid == 0) SPAN_END_pack(0);
+#endif
 }
 
 // planar sino [S][NMAP][NA][ND] -> pair layout [S][NA][ND+1] (entry e = (g[e-1], g[e]))
@@ -231,3 +257,14 @@ cudaError_t launch_pack_sino(const ei_plan &p, const float *sino, int n_maps, cu
 
 
 }  // namespace ei
+
+#ifdef EI_TRACE
+extern "C" int ei_debug_span_pack(unsigned long long *host, int reset) {
+  if (reset) {
+    unsigned long long init[8];
+    for (int k = 0; k < 4; ++k) { init[2 * k] = ~0ULL; init[2 * k + 1] = 0ULL; }
+    return cudaMemcpyToSymbol(ei::g_span_pack, init, sizeof(init)) == cudaSuccess ? 0 : 5;
+  }
+  return cudaMemcpyFromSymbol(host, ei::g_span_pack, sizeof(unsigned long long) * 8) == cudaSuccess ? 0 : 5;
+}
+#endif

@@ -81,6 +81,26 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 #endif
 
+#ifdef EI_TRACE
+// debug builds only (tools/dbg/step_trace.py): earliest CTA start / latest CTA end of this file's
+// kernels in the last traced call (globaltimer, ns)
+__device__ unsigned long long g_span_proj[2 * 4];
+__device__ __forceinline__ unsigned long long gt_proj() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define SPAN_START_proj() const unsigned long long span_t0_ = gt_proj()
+#define SPAN_END_proj(k)                                   \
+  do {                                                    \
+    atomicMin(&g_span_proj[2 * (k)], span_t0_);            \
+    atomicMax(&g_span_proj[2 * (k) + 1], gt_proj());         \
+  } while (0)
+#else
+#define SPAN_START_proj()
+#define SPAN_END_proj(k)
+#endif
+
 constexpr int NST = 4;          // pipeline stages (shared-memory ring)
 constexpr int MAXCH = 1024;     // window-table entries cached in shared memory per CTA
 constexpr int NCW = NT / 32;    // consumer warps
@@ -116,6 +136,7 @@ __global__ void __launch_bounds__(NT + 32, 2) project_kernel(ProjArgs args) {
   const int un = __ldg(args.unit + blockIdx.x);
   const int tile = un % args.ntile, grp = (un / args.ntile) % args.ngroups, z = un / (args.ntile * args.ngroups);
   const int kt = tile * RT;
+SPAN_START_proj();
 #ifdef EI_TRACE
   const unsigned long long t_start = gtimer();
   __shared__ int s_rows;
@@ -218,6 +239,7 @@ __global__ void __launch_bounds__(NT + 32, 2) project_kernel(ProjArgs args) {
 #pragma unroll
   for (int m = 0; m < 4; ++m) am[m] = ad[m] = as[m] = make_float2(0.f, 0.f);
 
+  pdl_wait();   // sleep (not spin on the ring) while K0 runs: this CTA may have launched early
   int st = 0;
   uint32_t ph = 0;
   for (int c = 0; c < nch; ++c, st = (st + 1 == NST) ? 0 : st + 1, ph ^= (st == 0)) {
@@ -279,6 +301,7 @@ __global__ void __launch_bounds__(NT + 32, 2) project_kernel(ProjArgs args) {
       g_k1_trace[4 * b + 2] = smid;
       g_k1_trace[4 * b + 3] = (unsigned long long)s_rows | ((unsigned long long)un << 32);
     }
+    SPAN_END_proj(0);
   }
 #endif
   if (k >= ND) return;
@@ -591,5 +614,16 @@ cudaError_t launch_project1(const ei_plan &p, float *P, cudaStream_t st, int RS)
 extern "C" int ei_debug_k1_trace(unsigned long long *host, int n_ctas) {
   n_ctas = n_ctas < 65536 ? n_ctas : 65536;
   return cudaMemcpyFromSymbol(host, ei::g_k1_trace, sizeof(unsigned long long) * 4 * n_ctas) == cudaSuccess ? 0 : 5;
+}
+#endif
+
+#ifdef EI_TRACE
+extern "C" int ei_debug_span_proj(unsigned long long *host, int reset) {
+  if (reset) {
+    unsigned long long init[8];
+    for (int k = 0; k < 4; ++k) { init[2 * k] = ~0ULL; init[2 * k + 1] = 0ULL; }
+    return cudaMemcpyToSymbol(ei::g_span_proj, init, sizeof(init)) == cudaSuccess ? 0 : 5;
+  }
+  return cudaMemcpyFromSymbol(host, ei::g_span_proj, sizeof(unsigned long long) * 8) == cudaSuccess ? 0 : 5;
 }
 #endif

@@ -55,5 +55,12 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t by
 // visible).  pdl_trigger() lets the dependent grid's CTAs be scheduled before this grid exits.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+// K0 triggers K1 at its start: K1's CTAs are scheduled once all of K0's CTAs have started and
+// run their prologue while K0 works (whatever they read of K0's output they read after
+// pdl_wait(), which waits for K0's completion): C1 28.8 -> 26.7 us.  The later kernels trigger
+// at the end of their work: an early trigger there let the next single-wave grid (K3 after K2)
+// land on whichever SMs happened to be free while the imbalanced predecessor still ran, and C2
+// lost 3 us (tools/dbg/step_trace.py).
+#define PDL_TRIGGER_K0() pdl_trigger()
 
 }  // namespace ei

@@ -29,6 +29,7 @@ struct ProjPlan {
   int *partner = nullptr;   // device [NA]: the angle theta + pi of a projected angle, or -1
   int n_groups = 0;
   int RC = 0;               // rows per staged chunk
+  int nst = 4;              // K1 ring stages
   int ray_fast = 0;         // number of angle groups using the ray-fastest consumer lane mapping
   int CW = 0;               // window width bound (entries)
   int RS = 1;               // row split of the cost path (partial P summed by K2)

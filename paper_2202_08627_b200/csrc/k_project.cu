@@ -67,6 +67,7 @@ struct ProjArgs {
   const int2 *win;              // [RS][groups][tiles][chunks] {cmin, W} (W = 0: chunk skipped)
   const int *unit;              // CTA -> work unit tile + ntile (group + ngroups (rs S + s)) (plan order)
   int N, NA, ND, S, RS, RC, CW, nch, PAD, Rp, ntile, ngroups;
+  int nst;                      // ring stages (<= NSTMAX)
   float *P;                     // [RS][S][NMAP][NA][ND]
 };
 
@@ -101,7 +102,7 @@ __device__ __forceinline__ unsigned long long gt_proj() {
 #define SPAN_END_proj(k)
 #endif
 
-constexpr int NST = 4;          // pipeline stages (shared-memory ring)
+constexpr int NSTMAX = 4;       // pipeline stages (shared-memory ring): 2 (plan), up to 4 (knob)
 constexpr int MAXCH = 1024;     // window-table entries cached in shared memory per CTA
 constexpr int NCW = NT / 32;    // consumer warps
 
@@ -127,9 +128,10 @@ __global__ void __launch_bounds__(NT + 32, 2) project_kernel(ProjArgs args) {
   constexpr bool A8 = sizeof(TA) == 8;
   const int CWA = A8 ? CW + 2 : CW, CWB = CW + 2;
   extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int NST = args.nst;
   TA *sA = reinterpret_cast<TA *>(smem_raw);                                   // [NST][RC][CWA]
   float2 *sB = reinterpret_cast<float2 *>(sA + NST * RC * CWA);               // [NST][RC][CWB]
-  __shared__ __align__(8) uint64_t full[NST], empty[NST];
+  __shared__ __align__(8) uint64_t full[NSTMAX], empty[NSTMAX];
   __shared__ int2 swin[MAXCH];   // this CTA's window table (host plan), nch <= MAXCH
 
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
@@ -349,8 +351,9 @@ cudaError_t launch(const ei_plan &p, int RS, float *P, cudaStream_t st) {
   a.PAD = p.proj.PAD; a.Rp = p.proj.Rp;
   a.nch = RS == 1 ? p.proj.nch1 : p.proj.nchRS;
   a.P = P;
-  const size_t smem = NMAP == 3 ? (size_t)NST * p.proj.RC * (p.proj.CW * 16 + (p.proj.CW + 2) * 8)
-                                 : (size_t)NST * p.proj.RC * (p.proj.CW + 2) * 8;
+  a.nst = p.proj.nst;
+  const size_t smem = NMAP == 3 ? (size_t)a.nst * p.proj.RC * (p.proj.CW * 16 + (p.proj.CW + 2) * 8)
+                                 : (size_t)a.nst * p.proj.RC * (p.proj.CW + 2) * 8;
   cudaError_t e = cudaFuncSetAttribute((const void *)project_kernel<NMAP>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
@@ -536,19 +539,50 @@ int plan_projector(ei_plan &p, const double *angles, const std::vector<int> &pro
     groups.back().y += 1;
   }
   const size_t per_entry = 24;          // float4 + float2 per staged entry
-  // shared-memory budget per CTA (NST-stage ring): 100 KB keeps two CTAs per SM (tuning knob)
+  // Staging ring: RC rows per chunk, 2 chunks deep, within a shared-memory budget that keeps two
+  // CTAs per SM (104 KB, tuning knob EI_K1_SMEM_KB).  First the row split RS (below) from the
+  // chunk size of a 4-stage ring; then the largest RC that leaves every CTA >= 2 chunks and fits
+  // two stages.  Fewer, larger chunks cost less per-chunk synchronisation than a deeper ring
+  // (measured vs the 4-stage ring: C4 K1 9.16 -> 8.67 ms, C3 0.71 -> 0.62, C5 1.39 -> 1.23,
+  // P1 40.5 -> 39.2 us per evaluation, C2 and C1 unchanged; 3 stages where they fit: P1 40.7).
   const char *env = getenv("EI_K1_SMEM_KB");
-  const size_t budget = (env ? (size_t)atoi(env) : 100) * 1024;
+  const size_t budget = (env ? (size_t)atoi(env) : 104) * 1024;
+  const size_t budget4 = 100 * 1024;
   int RC = 32, nch = 0, CW = 0;
   std::vector<int> rf_flags;
-  for (;;) {
+  for (;;) {   // 4-stage chunk size (sets the row split)
     build_windows(p, angles, groups, order, 1, RC, win1, nch, CW);
-    if ((size_t)NST * RC * (CW + 2) * per_entry <= budget || RC == 1) break;
+    if ((size_t)NSTMAX * RC * (CW + 2) * per_entry <= budget4 || RC == 1) break;
     RC /= 2;
   }
-  if ((size_t)NST * RC * (CW + 2) * per_entry > 200 * 1024) return EI_ERR_SHAPE;
+  const int RC4 = RC;
+  // row split for small problems: aim for >= 2 CTAs per SM
+  const int ntile = (ND + RT - 1) / RT;
+  const long long ctas = (long long)ntile * (long long)groups.size() * p.S;
+  int RS = 1;
+  // largest power of two keeping the grid within one wave of 2 CTAs x 148 SMs (measured best
+  // on C2 with the TMA pipeline: RS = 2)
+  while (RS < 8 && ctas * RS * 2 <= 2 * 148 && N / (RS * 2) >= 2 * RC4) RS *= 2;
+  if (const char *e = getenv("EI_K1_RS")) RS = std::max(1, std::min(8, atoi(e)));   // tuning knob
+  int nst = 2;
+  {
+    int rcmax = 1;
+    while (rcmax * 2 <= std::max(1, (N / RS) / 2) && rcmax < 32) rcmax *= 2;
+    for (int rc = rcmax; rc >= 1; rc /= 2) {
+      int cw = 0, nc = 0;
+      std::vector<int2> w;
+      build_windows(p, angles, groups, order, 1, rc, w, nc, cw);
+      if ((size_t)nst * rc * (cw + 2) * per_entry <= budget || rc == 1) {
+        RC = rc; nch = nc; CW = cw; win1.swap(w);
+        break;
+      }
+    }
+    if (const char *e = getenv("EI_K1_NST")) nst = std::max(2, std::min(NSTMAX, atoi(e)));   // knob
+  }
+  if ((size_t)nst * RC * (CW + 2) * per_entry > 200 * 1024) return EI_ERR_SHAPE;
   if (nch > MAXCH) return EI_ERR_SHAPE;
   p.proj.RC = RC;
+  p.proj.nst = nst;
   p.proj.n_groups = (int)groups.size();
   {   // per angle group, the lane mapping with fewer modelled shared-memory wavefronts, stored in
       // bit 16 of the group's count (tuning knob EI_K1_RAYFAST forces one mapping everywhere)
@@ -572,14 +606,6 @@ int plan_projector(ei_plan &p, const double *angles, const std::vector<int> &pro
               wa_sum / groups.size(), wbest / groups.size(), nrf, (int)groups.size());
   }
   p.proj.nch1 = nch;
-  // row split for small problems: aim for >= 2 CTAs per SM
-  const int ntile = (ND + RT - 1) / RT;
-  const long long ctas = (long long)ntile * groups.size() * p.S;
-  int RS = 1;
-  // largest power of two keeping the grid within one wave of 2 CTAs x 148 SMs (measured best
-  // on C2 with the TMA pipeline: RS = 2)
-  while (RS < 8 && ctas * RS * 2 <= 2 * 148 && N / (RS * 2) >= 2 * RC) RS *= 2;
-  if (const char *e = getenv("EI_K1_RS")) RS = std::max(1, std::min(8, atoi(e)));   // tuning knob
   p.proj.RS = RS;
   int CWrs = CW;
   if (RS > 1) {

@@ -275,7 +275,7 @@ int ei_plan_info(const ei_plan *p, int64_t out[10]) {
   out[2] = p->proj.CW;
   out[3] = p->proj.RS;
   out[4] = d;
-  out[5] = (int64_t)4 * p->proj.RC * (p->proj.CW * 16 + (p->proj.CW + 2) * 8);
+  out[5] = (int64_t)p->proj.nst * p->proj.RC * (p->proj.CW * 16 + (p->proj.CW + 2) * 8);
   out[6] = p->proj.ray_fast;
   out[7] = p->KS;
   out[8] = p->npairs;

@@ -178,9 +178,12 @@ SPAN_START_bp();
   const size_t rowlen = (size_t)RpG;   // padded G rows: entry e at e + PADG
   const TA *GAs = GA + (size_t)s * NA * rowlen + PADG;
   const float2 *GBs = GB ? GB + (size_t)s * NA * rowlen + PADG : nullptr;
-  // angle split (small grids): CTA ks owns chunks [c_lo, c_hi)
-  const int nch_all = (NA3 + CH - 1) / CH;   // chunks over the back-projected angles
-  const int c_lo = (int)(((long long)ks * nch_all) / KS), c_hi = (int)(((long long)(ks + 1) * nch_all) / KS);
+  // angle split (small grids): CTA ks owns angles [a_lo, a_hi) of the back-projected list, an equal
+  // share (not a whole number of chunks: 360 angles in 6 parts are 60 each, staged as 16+16+16+12,
+  // where whole chunks gave 3 or 4 chunks per CTA), in chunks of CH staged angles
+  const int a_lo = (int)(((long long)ks * NA3) / KS), a_hi = (int)(((long long)(ks + 1) * NA3) / KS);
+  const int c_lo = 0, c_hi = (a_hi - a_lo + CH - 1) / CH;
+  const int *alist_k = alist + a_lo;
 
   if (tid == 0) {
     for (int q = 0; q < NST; ++q) {
@@ -204,10 +207,10 @@ SPAN_START_bp();
     uint32_t ph = 0;
     for (int c = c_lo; c < c_hi; ++c) {
       if (c - c_lo >= NST) mbar_wait(&sm.empty[st], ph ^ 1);
-      const int na = min(CH, NA3 - c * CH);
+      const int na = min(CH, a_hi - a_lo - c * CH);
       int ws = 0;
       if (lane < na) {   // per-angle table + window start (first tap entry - 1)
-        const int a = __ldg(alist + c * CH + lane);
+        const int a = __ldg(alist_k + c * CH + lane);
         const float4 g = __ldg(k3 + a);   // cdu, sdu, inv_h, scale
         const float k00 = fmaf(xa, g.x, fmaf(ya, g.y, dctr)), k01 = fmaf(xb, g.x, fmaf(ya, g.y, dctr));
         const float k10 = fmaf(xa, g.x, fmaf(yb, g.y, dctr)), k11 = fmaf(xb, g.x, fmaf(yb, g.y, dctr));
@@ -219,7 +222,7 @@ SPAN_START_bp();
       if (lane == 0) mbar_arrive_expect_tx(&sm.full[st], (uint32_t)na * (bytesA + bytesB));
       __syncwarp();
       if (lane < na) {
-        const size_t row = (size_t)__ldg(alist + c * CH + lane) * rowlen;
+        const size_t row = (size_t)__ldg(alist_k + c * CH + lane) * rowlen;
         // a window entirely off the detector only needs zeros: clamp its copy into the zero pad
         // (a window overlapping [0, ND] is always inside the PADG >= WL padding)
         const int e0 = min(max(ws + 1, -PADG), ND + PADG - WLB), eb = e0 & ~1;
@@ -257,7 +260,7 @@ SPAN_START_bp();
 #ifdef EI_TRACE
     if (c == c_lo) t_data = gtimer3();
 #endif
-    const int na = min(CH, NA3 - c * CH);
+    const int na = min(CH, a_hi - a_lo - c * CH);
 #pragma unroll 2   // two angles in flight per warp (measured: C4 K3 8.94 -> 8.76 ms; x4 8.80)
     for (int al = 0; al < na; ++al) {
       const float4 t = sm.tab[st][al];

@@ -111,7 +111,8 @@ struct ei_plan {
   int32_t *h_status = nullptr;
   cudaStream_t h_copy = nullptr;            // s_exp upload stream (host path)
   cudaStream_t h_work = nullptr;            // host path work stream (graph capture / replay)
-  cudaEvent_t h_ev[3] = {nullptr, nullptr, nullptr};   // small inputs up / s_exp up / caller order
+  cudaEvent_t h_ev[4] = {nullptr, nullptr, nullptr, nullptr};   // small inputs up / s_exp up /
+                                                                // caller order / call done
   cudaGraphExec_t h_exec = nullptr;         // captured host path, replayed for the same arguments
   HostKey h_key{};
   int64_t h_stats[6] = {0, 0, 0, 0, 0, 0};  // launch accounting of one captured call

@@ -608,7 +608,7 @@ int ei_cost_grad_host(ei_plan *p, const float *mu, const float *delta, const flo
   if (!p->h_copy) {   // work + copy streams and events of the host path (created once per plan)
     cudaError_t e = cudaStreamCreateWithFlags(&p->h_copy, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&p->h_work, cudaStreamNonBlocking);
-    for (int k = 0; k < 3 && e == cudaSuccess; ++k) e = cudaEventCreateWithFlags(&p->h_ev[k], cudaEventDisableTiming);
+    for (int k = 0; k < 4 && e == cudaSuccess; ++k) e = cudaEventCreateWithFlags(&p->h_ev[k], cudaEventDisableTiming);
     if (e != cudaSuccess) {
       cudaGetLastError();
       return EI_ERR_RESOURCE;
@@ -657,7 +657,13 @@ int ei_cost_grad_host(ei_plan *p, const float *mu, const float *delta, const flo
     if (p->h_exec) {
       if (cudaGraphLaunch(p->h_exec, p->h_work) != cudaSuccess) return EI_ERR_CUDA;
       for (int i = 0; i < 6; ++i) p->stats[i] += p->h_stats[i];
-      return cudaStreamSynchronize(p->h_work) == cudaSuccess ? EI_OK : EI_ERR_CUDA;
+      // wait by polling an event instead of cudaStreamSynchronize: the call is synchronous and
+      // short (C2: ~0.2 ms), so the driver's blocking wake-up latency would be a visible share
+      if (cudaEventRecord(p->h_ev[3], p->h_work) != cudaSuccess) return EI_ERR_CUDA;
+      cudaError_t q;
+      while ((q = cudaEventQuery(p->h_ev[3])) == cudaErrorNotReady) {
+      }
+      return q == cudaSuccess ? EI_OK : EI_ERR_CUDA;
     }
   }
   int rc = enqueue_host_path(p, mu, delta, sigma, flat, mask, drift, s_exp, lambda, cost, g_mu,

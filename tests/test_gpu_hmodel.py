@@ -172,3 +172,34 @@ def test_status_counters_h_and_sampled(ei):
     assert list(st.cpu().numpy()[:2]) == list(rst)
     assert abs(cost.cpu().numpy()[0] - rc[0]) / rc[0] <= 1e-4
     assert rel_l2(g.cpu().numpy()[0], rg[0]) <= 1e-3
+
+
+@pytest.mark.parametrize("sampled", [False, True])
+def test_h_model_detector_segments(ei, sampled, monkeypatch):
+    """The single-map paths (Gaussian and sampled flat) with several K2 detector segments per row
+    (EI_K2_MAXW at plan creation; RH's 47 detector pixels take the lane-copy path) vs the oracle."""
+    monkeypatch.setenv("EI_K2_MAXW", "16")
+    case, fs, s_exp = _cases.cached_hs_case("RH")
+    cfg = case.cfg
+    plan = plan_for(ei, cfg)
+    assert ei.ei_plan_info(plan)["k2_segments"] > 1
+    h = synth.perturbed((case.h,), cfg.seed + 7)[0]
+    lam = synth.H_LAMBDA
+    if sampled:
+        drift = None if case.drift is None else dev(case.drift)
+        cost = torch.zeros(cfg.S, dtype=torch.float64, device="cuda")
+        g = torch.zeros(cfg.S, cfg.N, cfg.N, device="cuda")
+        st = torch.zeros(4, dtype=torch.int32, device="cuda")
+        ei.ei_cost_grad_hs(plan, dev(h), case.gamma, dev(fs), dev(case.mask), drift, dev(s_exp), lam, cost,
+                           g, None, st)
+        torch.cuda.synchronize()
+        rc, rg, _ = _cases.ora.cost_grad_hs(cfg.angles, h, case.gamma, fs, case.mask, case.drift, s_exp, lam,
+                                            dx=cfg.pixel, du=cfg.det_pitch, z=cfg.z)
+        cost, g = cost.cpu().numpy(), g.cpu().numpy()
+    else:
+        hc = _cases.cached_h_case("RH")
+        cost, g, _, _ = gpu_h(ei, plan, hc, h, lam)
+        rc, rg, _ = _cases.oracle_cost_grad_h(hc, h, lam)
+    assert np.all(np.abs(cost - rc) / rc <= 1e-4), (cost, rc)
+    for s in range(cfg.S):
+        assert rel_l2(g[s], rg[s]) <= 1e-3, (s, rel_l2(g[s], rg[s]))

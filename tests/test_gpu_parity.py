@@ -390,3 +390,30 @@ def test_k3_angle_split_matches_unsplit(ei, monkeypatch):
     assert np.array_equal(ca, cb)
     for a, b in zip(ga, gb):
         assert rel_l2(a, b) <= 1e-6
+
+
+@pytest.mark.parametrize("name,maxw", [("C1", 32), ("R1", 32), ("R1", 48), ("R3", 24)])
+def test_k2_detector_segments(ei, name, maxw, monkeypatch):
+    """K2 with several detector segments per row (each staged with a 4-position halo so D and D^T
+    never cross segments; large configs use 2-7 segments): forced on small cases with
+    EI_K2_MAXW at plan creation — C1 takes the TMA path (N_d % 4 == 0), R1 the lane-copy path,
+    R3 adds mirror pairs and drift.  Same gates as test_cost_grad_parity, and the forward model."""
+    monkeypatch.setenv("EI_K2_MAXW", str(maxw))
+    case = _cases.cached_case(name)
+    cfg = case.cfg
+    plan = plan_for(ei, cfg)
+    assert ei.ei_plan_info(plan)["k2_segments"] > 1
+    maps = eval_points(case)["pert"]
+    cost, g, st = gpu_cost_grad(ei, plan, case, maps, 1e-2)
+    rc, rgm, rgd, rgs, rst = _cases.oracle_cost_grad(case, maps, 1e-2)
+    assert np.all(np.abs(cost - rc) / rc <= 1e-4), (cost, rc)
+    for q, ref in enumerate((rgm, rgd, rgs)):
+        for s in range(cfg.S):
+            assert rel_l2(g[q][s], ref[s]) <= 1e-3, (q, s, rel_l2(g[q][s], ref[s]))
+    smod = torch.zeros(cfg.S, cfg.n_angles, cfg.M, cfg.n_det, device="cuda")
+    drift = None if case.drift is None else dev(case.drift)
+    ei.ei_forward(plan, *[dev(m) for m in maps], dev(case.flat), dev(case.mask), drift, smod)
+    ref, _ = ora.forward(cfg.angles, *maps, case.flat, case.mask, case.drift, dx=cfg.pixel,
+                         du=cfg.det_pitch, z=cfg.z)
+    got = smod.cpu().numpy()
+    assert np.abs(got - ref).max() / np.abs(ref).max() <= 1e-5

@@ -492,40 +492,28 @@ __global__ void __launch_bounds__(K2_MAXT + 32, 2) curve_kernel(K2Args g) {
         g.part_mo[pidx] = wm_;
       }
       asm volatile("bar.sync 1, %0;\n" ::"r"(NT) : "memory");   // consumers only
-      const int e0 = max(k0, seg * g.W), e1 = min(min(k0 + J, seg * g.W + g.W), ND);
-      if (staged && e0 < e1) {   // core entries imply any and t <= WB/4 - 2 (x4[t + 1] staged)
-        // neighbours' float4s: g'_Delta at k0-4 .. k0+7, g_mu / g_sigma at k0-4 .. k0-1 (slots of
-        // threads without row positions are stale: only their ghost entries are read)
-        const float4 Ld = t > 0 ? x4[t - 1] : make_float4(0.f, 0.f, 0.f, 0.f);
-        const float4 Rd = x4[t + 1];
-        const float4 Lm = t > 0 ? x4[W4 + t - 1] : make_float4(0.f, 0.f, 0.f, 0.f);
-        const float4 Ls = (!Mode<MODE>::h && t > 0) ? x4[2 * W4 + t - 1] : make_float4(0.f, 0.f, 0.f, 0.f);
-        const float dv[J + 3] = {Ld.z, Ld.w, gx[0], gx[1], gx[2], gx[3], Rd.x};   // g' at k0-2 .. k0+4
-        const float mv[J + 1] = {Lm.w, gm4.x, gm4.y, gm4.z, gm4.w};              // g_mu at k0-1 .. k0+3
-        const float sv[J + 1] = {Ls.w, gs4.x, gs4.y, gs4.z, gs4.w};
+      // pair entries e = (g[e-1], g[e]) of this segment's core, e in [segW, segW + cw) and the
+      // closing entry N_d after the last segment, lane-contiguous (consecutive lanes write
+      // consecutive entries: fully used 16-B / 8-B store sectors), from the exchange rows:
+      // g_delta[q] = zs D^T g_Delta = (z / 2du) (g'[q-1] - g'[q+1]) on the ghost-extended g'
+      {
+        const int segW = seg * g.W, cw = min(g.W, ND - segW);
+        const float *xd = xch + buf * 3 * WB - kb;   // g'_Delta by detector position
+        const float *xm = xd + WB, *xs = xd + 2 * WB;   // g_mu, g_sigma by detector position
         const float zh = 0.5f * g.zs * g.inv_du;
         const float sc = __ldg(g.k3 + a).w;
         const size_t rb = (size_t)row * g.RpG + g.PADG;
-        float gdl[J + 1];   // g_delta = zs D^T g_Delta at k0-1 .. k0+3 (k0-1 is used only if >= 0)
-#pragma unroll
-        for (int i = 0; i <= J; ++i) gdl[i] = zh * (dv[i] - dv[i + 2]);
-#pragma unroll
-        for (int j = 0; j < J; ++j) {   // pair entries e = k0 + j: (g[e-1], g[e])
-          const int e = k0 + j;
-          if (e < e0 || e >= e1) continue;
-          const float m0 = e >= 1 ? mv[j] : 0.f, m1 = mv[j + 1];
-          const float d0 = e >= 1 ? gdl[j] : 0.f, d1 = gdl[j + 1];
+        const int eend = segW + cw + (segW + cw == ND ? 1 : 0);
+        for (int e = segW + t; e < eend; e += NT) {
+          const bool lo = e >= 1, hi = e < ND;
+          const float m0 = lo ? xm[e - 1] : 0.f, m1 = hi ? xm[e] : 0.f;
+          const float d0 = lo ? zh * (xd[e - 2] - xd[e]) : 0.f, d1 = hi ? zh * (xd[e - 1] - xd[e + 1]) : 0.f;
           if (Mode<MODE>::h) {   // dS/dP_h = g_mu + z gamma D^T g_Delta (eq. 4 chain rule)
             g.GA1[rb + e] = make_float2(sc * (m0 + d0), sc * (m1 + d1));
-            if (e == ND - 1) g.GA1[rb + ND] = make_float2(sc * (m1 + d1), 0.f);
           } else {
-            const float s0 = e >= 1 ? sv[j] : 0.f, s1 = sv[j + 1];
+            const float s0 = lo ? xs[e - 1] : 0.f, s1 = hi ? xs[e] : 0.f;
             g.GA[rb + e] = make_float4(sc * m0, sc * m1, sc * d0, sc * d1);
             g.GB[rb + e] = make_float2(sc * s0, sc * s1);
-            if (e == ND - 1) {   // closing entry e = ND: (g[ND-1], 0)
-              g.GA[rb + ND] = make_float4(sc * m1, 0.f, sc * d1, 0.f);
-              g.GB[rb + ND] = make_float2(sc * s1, 0.f);
-            }
           }
         }
       }

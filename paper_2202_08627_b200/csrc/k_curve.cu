@@ -97,6 +97,7 @@ struct K2Args {
   int WB;                    // staged positions per row: W + 8
   int K;                     // MODES 4, 5: knots of the sampled flat IC (flat = [S][K][ND])
   int vec;                   // 1: rows are 16-B aligned (ND % 4 == 0, aligned arrays) -> TMA
+  int vec_smod;              // forward modes: s_mod rows 16-B aligned (float4 stores)
   float zs, inv_du;          // shift factor: z (three-map model) or z gamma (single-map model)
   float *s_mod;              // forward modes
   float4 *GA;                // MODE 1: pair-layout gradient sinograms (K3 input)
@@ -333,7 +334,7 @@ __global__ void __launch_bounds__(K2_MAXT + 32, 2) curve_kernel(K2Args g) {
         w2_cl += core[j] & wc[j];
       }
       const size_t rowb = (size_t)row * g.M * ND + k0;   // s_mod row base (k0)
-      float gmm[J], gdd[J], gq[J], cst[J];
+      float gmm[J], gdd[J], gq[J], cst[J], smv[J];
 #pragma unroll
       for (int j = 0; j < J; ++j) gmm[j] = gdd[j] = gq[j] = cst[j] = 0.f;
       if constexpr (Mode<MODE>::cost && !Mode<MODE>::sampled) {
@@ -406,7 +407,7 @@ __global__ void __launch_bounds__(K2_MAXT + 32, 2) curve_kernel(K2Args g) {
             sv = amp[j] * ex2(c2[j] * u2);
           }
           if (!Mode<MODE>::cost) {
-            if (core[j]) g.s_mod[rowb + (size_t)m * ND + j] = sv;
+            smv[j] = sv;   // stored per mask position below
           } else {
             const float r = sv - se;
             cst[j] = fmaf(r, r, cst[j]);
@@ -421,17 +422,34 @@ __global__ void __launch_bounds__(K2_MAXT + 32, 2) curve_kernel(K2Args g) {
           }
         };
 #pragma unroll
+        // forward modes: the 4 positions' s_mod of one mask position as one 16-B store when they
+        // are all core positions and the row is 16-B aligned (else element stores)
+        const bool allcore = core[0] && core[1] && core[2] && core[3];
+        auto store = [&](int m) {
+          if (Mode<MODE>::cost) return;
+          float *dst = g.s_mod + rowb + (size_t)m * ND;
+          if (allcore && g.vec_smod) {
+            *reinterpret_cast<float4 *>(dst) = make_float4(smv[0], smv[1], smv[2], smv[3]);
+          } else {
+#pragma unroll
+            for (int j = 0; j < J; ++j)
+              if (core[j]) dst[j] = smv[j];
+          }
+        };
+#pragma unroll
         for (int u = 0; u < MPF; ++u) {          // mask positions in registers
           if (u >= g.M) break;
           const float4 se4 = Mode<MODE>::cost ? r4[(g.nmap + u) * W4 + t] : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
           for (int j = 0; j < J; ++j) term(j, mk[u], u, at(se4, j));
+          store(u);
         }
         for (int m = MPF; m < g.M; ++m) {        // M > MPF
           const float mp = __ldg(g.mask + m);
           const float4 se4 = Mode<MODE>::cost ? r4[(g.nmap + m) * W4 + t] : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
           for (int j = 0; j < J; ++j) term(j, mp, m, at(se4, j));
+          store(m);
         }
       }
       if (Mode<MODE>::cost) {
@@ -563,6 +581,7 @@ cudaError_t launch(const ei_plan &p, const float *flat, const float *mask, const
   g.WB = p.k2.W + 2 * J;
   auto al = [](const void *q) { return ((uintptr_t)q & 15u) == 0; };
   g.vec = (p.ND % 4 == 0) && al(p.P) && al(flat) && (!s_exp || al(s_exp)) ? 1 : 0;
+  g.vec_smod = (p.ND % 4 == 0) && s_mod && al(s_mod) ? 1 : 0;
   g.zs = (float)(p.g.z * (Mode<MODE>::h ? (double)gamma : 1.0));
   g.inv_du = (float)(1.0 / p.g.det_pitch);
   g.s_mod = s_mod;

@@ -68,6 +68,7 @@ struct ProjArgs {
   const int *unit;              // CTA -> work unit tile + ntile (group + ngroups (rs S + s)) (plan order)
   int N, NA, ND, S, RS, RC, CW, nch, PAD, Rp, ntile, ngroups;
   int nst;                      // ring stages (<= NSTMAX)
+  int has_pairs;                // the plan paired mirror angles (else partner[] is all -1)
   float *P;                     // [RS][S][NMAP][NA][ND]
 };
 
@@ -317,7 +318,7 @@ SPAN_START_proj();
     out[(size_t)aidx[m] * ND] = v0;
     // the mirror angle theta + pi samples the same line at the mirrored detector position
     // (R6: detector centred), so its projection is this value: one projection, two rows
-    const int b = __ldg(args.partner + aidx[m]);
+    const int b = args.has_pairs ? __ldg(args.partner + aidx[m]) : -1;   // no load in the tail
     if (b >= 0) outm[(size_t)b * ND] = v0;
     if constexpr (NMAP == 3) {
       const float v1 = (ad[m].x + ad[m].y) * scale[m], v2 = (as[m].x + as[m].y) * scale[m];
@@ -343,6 +344,7 @@ cudaError_t launch(const ei_plan &p, int RS, float *P, cudaStream_t st) {
   a.groups = p.proj.groups;
   a.order = p.proj.order;
   a.partner = p.proj.partner;
+  a.has_pairs = p.npairs > 0 ? 1 : 0;
   a.win = RS == 1 ? p.proj.win1 : p.proj.winRS;
   a.unit = RS == 1 ? p.proj.unit1 : p.proj.unitRS;
   a.ntile = p.proj.n_tiles;

@@ -29,6 +29,8 @@ struct ProjPlan {
   int *partner = nullptr;   // device [NA]: the angle theta + pi of a projected angle, or -1
   int n_groups = 0;
   int RC = 0;               // rows per staged chunk
+  int RT = 64;              // rays per K1 CTA (64, or 32 for small single-wave grids)
+  int k0_early = 0;         // K0 triggers K1's launch at its start (K1 grid smaller than the SMs)
   int nst = 4;              // K1 ring stages
   int ray_fast = 0;         // number of angle groups using the ray-fastest consumer lane mapping
   int CW = 0;               // window width bound (entries)

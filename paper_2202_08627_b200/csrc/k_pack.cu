@@ -62,11 +62,14 @@ __global__ void __launch_bounds__(256) pack_pairs_kernel(const float *__restrict
                                                          double *__restrict__ part_reg,
                                                          int32_t *__restrict__ status,
                                                          SmallCheck chk, int nflat, int M, int NA,
-                                                         int PAD, int Rp) {
+                                                         int PAD, int Rp, int trigger_early) {
   __shared__ float tile[NMAP][T + 1][T + 2];   // (T+1)^2 with a one-element halo
   __shared__ double red[8];
   SPAN_START_pack();
-  PDL_TRIGGER_K0();   // K1's CTAs may launch (they wait for this grid before reading its output)
+  // small K1 grids (fewer CTAs than SMs): let K1's CTAs launch now (they wait for this grid before
+  // reading its output); larger single-wave K1 grids are placed by the plan assuming an empty GPU,
+  // so they launch when this grid completes (plan_projector)
+  if (trigger_early) PDL_TRIGGER_K0();
   const int s = blockIdx.z, ta = blockIdx.y, tb = blockIdx.x;
   const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * T + tx;
   const float *src[3] = {in0 + s * in_stride, NMAP == 3 ? in1 + s * in_stride : nullptr,
@@ -227,7 +230,7 @@ cudaError_t launch_pack3(const ei_plan &p, const float *mu, const float *delta, 
   pack_pairs_kernel<3><<<grid, block, 0, st>>>(mu, delta, sigma, in_stride, p.N, o,
                                                want_reg ? p.part_reg : nullptr, status, chk,
                                                p.S * (chk.nflat_per_slice ? chk.nflat_per_slice : 3 * p.ND),
-                                               p.M, p.NA, p.proj.PAD, p.proj.Rp);
+                                               p.M, p.NA, p.proj.PAD, p.proj.Rp, p.proj.k0_early);
   return cudaGetLastError();
 }
 
@@ -239,7 +242,7 @@ cudaError_t launch_pack1(const ei_plan &p, const float *map, cudaStream_t st, bo
   pack_pairs_kernel<1><<<grid, block, 0, st>>>(map, nullptr, nullptr, (size_t)p.N * p.N, p.N, o,
                                                want_reg ? p.part_reg : nullptr, status, chk,
                                                p.S * (chk.nflat_per_slice ? chk.nflat_per_slice : 3 * p.ND),
-                                               p.M, p.NA, p.proj.PAD, p.proj.Rp);
+                                               p.M, p.NA, p.proj.PAD, p.proj.Rp, p.proj.k0_early);
   return cudaGetLastError();
 }
 

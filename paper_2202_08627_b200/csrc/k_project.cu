@@ -29,8 +29,8 @@ namespace ei {
 namespace {
 
 constexpr int AGB = 16;   // angles per CTA
-constexpr int RT = 64;    // rays per CTA
-constexpr int NT = 256;
+constexpr int RT = 64;    // rays per CTA (RTS = 32 for small single-wave grids, plan_projector)
+constexpr int RTS = 32;
 
 __device__ __forceinline__ void cp_async(void *smem, const void *gmem, int bytes, bool valid) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -105,7 +105,6 @@ __device__ __forceinline__ unsigned long long gt_proj() {
 
 constexpr int NSTMAX = 4;       // pipeline stages (shared-memory ring): 2 (plan), up to 4 (knob)
 constexpr int MAXCH = 1024;     // window-table entries cached in shared memory per CTA
-constexpr int NCW = NT / 32;    // consumer warps
 
 // Warp-specialised pipeline: warp NCW (the producer) streams each row chunk's window of pair
 // entries with 1-D bulk copies (TMA engine) into a NST-deep shared-memory ring, completing on a
@@ -120,8 +119,11 @@ constexpr int NCW = NT / 32;    // consumer warps
 // the same pixels — dense views) or ray fastest (rq = lane & 7, aq = lane >> 3: a quarter warp =
 // 8 adjacent rays of one angle — sparse views with large N, where the 4 angles of a quarter would
 // spread over tens of entries and conflict).
-template <int NMAP>
-__global__ void __launch_bounds__(NT + 32, 2) project_kernel(ProjArgs args) {
+// RTILE rays per CTA: RTILE / 8 consumer warps (NT threads) + the producer warp; 2 CTAs per SM
+// with 64-ray tiles, 4 with 32-ray tiles (same warps per SM, finer units to balance small grids)
+template <int NMAP, int RTILE>
+__global__ void __launch_bounds__(RTILE * 4 + 32, RTILE == 64 ? 2 : 4) project_kernel(ProjArgs args) {
+  constexpr int NT = RTILE * 4, NCW = NT / 32;
   using TA = typename PL<NMAP>::A;
   const int N = args.N, ND = args.ND, RC = args.RC, CW = args.CW;
   // 8-byte-entry planes start their copy at the even entry below the window (16-B aligned
@@ -138,7 +140,7 @@ __global__ void __launch_bounds__(NT + 32, 2) project_kernel(ProjArgs args) {
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int un = __ldg(args.unit + blockIdx.x);
   const int tile = un % args.ntile, grp = (un / args.ntile) % args.ngroups, z = un / (args.ntile * args.ngroups);
-  const int kt = tile * RT;
+  const int kt = tile * RTILE;
 SPAN_START_proj();
 #ifdef EI_TRACE
   const unsigned long long t_start = gtimer();
@@ -356,12 +358,12 @@ cudaError_t launch(const ei_plan &p, int RS, float *P, cudaStream_t st) {
   a.nst = p.proj.nst;
   const size_t smem = NMAP == 3 ? (size_t)a.nst * p.proj.RC * (p.proj.CW * 16 + (p.proj.CW + 2) * 8)
                                  : (size_t)a.nst * p.proj.RC * (p.proj.CW + 2) * 8;
-  cudaError_t e = cudaFuncSetAttribute((const void *)project_kernel<NMAP>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  auto kern = p.proj.RT == RT ? project_kernel<NMAP, RT> : project_kernel<NMAP, RTS>;
+  cudaError_t e = cudaFuncSetAttribute((const void *)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   if (RS != 1 && RS != p.proj.RS) return cudaErrorInvalidValue;   // unit tables exist for these
   dim3 grid(p.proj.n_tiles * p.proj.n_groups * p.S * RS);
-  e = launch_pdl(project_kernel<NMAP>, grid, dim3(NT + 32), smem, st, a);
+  e = launch_pdl(kern, grid, dim3(p.proj.RT * 4 + 32), smem, st, a);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
@@ -381,7 +383,7 @@ static void build_windows(const ei_plan &p, const double *angles, const std::vec
                           int &nch_max, int &wmax) {
   const int N = p.N, ND = p.ND;
   const double dx = p.g.pixel, du = p.g.det_pitch, ctr = 0.5 * (N - 1), dctr = 0.5 * (ND - 1);
-  const int ntile = (ND + RT - 1) / RT;
+  const int rt = p.proj.RT, ntile = (ND + rt - 1) / rt;
   nch_max = 0;
   for (int rs = 0; rs < RS; ++rs) {
     const int r0 = (int)(((long long)rs * N) / RS), r1 = (int)(((long long)(rs + 1) * N) / RS);
@@ -393,7 +395,7 @@ static void build_windows(const ei_plan &p, const double *angles, const std::vec
     const int r0 = (int)(((long long)rs * N) / RS), r1 = (int)(((long long)(rs + 1) * N) / RS);
     for (size_t g = 0; g < groups.size(); ++g) {
       for (int t = 0; t < ntile; ++t) {
-        const int kt = t * RT;
+        const int kt = t * rt;
         int2 *row = &win[((rs * groups.size() + g) * ntile + t) * nch_max];
         for (int c = 0; r0 + c * RC < r1; ++c) {
           const int i0 = r0 + c * RC, i1 = std::min(i0 + RC, r1) - 1;
@@ -403,7 +405,7 @@ static void build_windows(const ei_plan &p, const double *angles, const std::vec
             const double cs = cos(angles[a]), sn = sin(angles[a]);
             const bool rd = fabs(cs) >= fabs(sn);
             const double cd = rd ? cs : sn, so = rd ? sn : cs;
-            for (int kk : {kt, kt + RT - 1})
+            for (int kk : {kt, kt + rt - 1})
               for (int ii : {i0, i1}) {
                 const double xs = (kk - dctr) * du / (cd * dx) - (so / cd) * (ii - ctr) + ctr;
                 lo = std::min(lo, floor(xs));
@@ -485,7 +487,7 @@ static double wavefront_model(const ei_plan &p, const double *angles, const std:
 //    tail of the last wave; slice by slice, so the CTAs in flight share one slice's map in L2
 //    (LPT across all 64 slices of C4 raised K1's DRAM traffic from ~18 to ~170 MB per slice).
 static std::vector<int> order_units(const std::vector<int2> &win, int RS, int n_groups, int ntile,
-                                    int nch, int S, int RC, int N) {
+                                    int nch, int S, int RC, int N, int cps) {
   const int nu1 = RS * n_groups * ntile;          // per slice: (rs, group, tile)
   std::vector<std::pair<long long, int>> cost;   // (slice, -cost) key, unit
   cost.reserve((size_t)nu1 * S);
@@ -507,13 +509,21 @@ static std::vector<int> order_units(const std::vector<int2> &win, int RS, int n_
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaGetLastError();
   std::vector<int> unit(n);
-  if (n > sms && n <= 2 * sms && !getenv("EI_K1_LPT")) {
-    const int npair = n - sms;                    // blocks b < npair share an SM with b + sms
-    int q = 0;
-    for (int b = npair; b < sms; ++b) unit[b] = cost[q++].second;          // alone: heaviest
-    for (int b = 0; b < npair; ++b) {
-      unit[b] = cost[q + b].second;                                         // next heaviest ...
-      unit[b + sms] = cost[n - 1 - b].second;                               // ... with the lightest
+  if (n > sms && n <= cps * sms && !getenv("EI_K1_LPT")) {
+    // one wave: SM m holds blocks m, m + sms, ...; each unit (heaviest first) goes to the SM with
+    // the least work so far among those with a free block
+    std::vector<int> cap(sms, 0), used(sms, 0);
+    std::vector<long long> load(sms, 0);
+    for (int b = 0; b < n; ++b) cap[b % sms] += 1;
+    for (int q = 0; q < n; ++q) {
+      int best = -1;
+      for (int m = 0; m < sms; ++m)
+        if (used[m] < cap[m] && (best < 0 || load[m] < load[best])) best = m;
+      unit[best + used[best] * sms] = cost[q].second;
+      used[best] += 1;
+      long long rows = (-cost[q].first) % (1LL << 40);   // the unit's rows (key = s 2^40 - rows)
+      if (rows < 0) rows += 1LL << 40;
+      load[best] += rows;
     }
   } else {
     for (int b = 0; b < n; ++b) unit[b] = cost[b].second;
@@ -541,31 +551,54 @@ int plan_projector(ei_plan &p, const double *angles, const std::vector<int> &pro
     groups.back().y += 1;
   }
   const size_t per_entry = 24;          // float4 + float2 per staged entry
+  int sms = 148, dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaGetLastError();
   // Staging ring: RC rows per chunk, 2 chunks deep, within a shared-memory budget that keeps two
-  // CTAs per SM (104 KB, tuning knob EI_K1_SMEM_KB).  First the row split RS (below) from the
-  // chunk size of a 4-stage ring; then the largest RC that leaves every CTA >= 2 chunks and fits
-  // two stages.  Fewer, larger chunks cost less per-chunk synchronisation than a deeper ring
-  // (measured vs the 4-stage ring: C4 K1 9.16 -> 8.67 ms, C3 0.71 -> 0.62, C5 1.39 -> 1.23,
-  // P1 40.5 -> 39.2 us per evaluation, C2 and C1 unchanged; 3 stages where they fit: P1 40.7).
+  // (64-ray tiles) or four (32-ray tiles) CTAs per SM (104 / 52 KB, knob EI_K1_SMEM_KB).  First
+  // the row split RS from the chunk size of a 4-stage ring; then the largest RC that leaves every
+  // CTA >= 2 chunks and fits two stages.  Fewer, larger chunks cost less per-chunk
+  // synchronisation than a deeper ring (measured vs the 4-stage ring: C4 K1 9.16 -> 8.67 ms, C3
+  // 0.71 -> 0.62, C5 1.39 -> 1.23, P1 40.5 -> 39.2 us per evaluation; 3 stages where they fit:
+  // P1 40.7).
   const char *env = getenv("EI_K1_SMEM_KB");
-  const size_t budget = (env ? (size_t)atoi(env) : 104) * 1024;
-  const size_t budget4 = 100 * 1024;
-  int RC = 32, nch = 0, CW = 0;
+  int RC = 32, nch = 0, CW = 0, RC4 = 0, RS = 1, cps = 2, ntile = 0;
+  long long ctas = 0;
   std::vector<int> rf_flags;
-  for (;;) {   // 4-stage chunk size (sets the row split)
-    build_windows(p, angles, groups, order, 1, RC, win1, nch, CW);
-    if ((size_t)NSTMAX * RC * (CW + 2) * per_entry <= budget4 || RC == 1) break;
-    RC /= 2;
-  }
-  const int RC4 = RC;
-  // row split for small problems: aim for >= 2 CTAs per SM
-  const int ntile = (ND + RT - 1) / RT;
-  const long long ctas = (long long)ntile * (long long)groups.size() * p.S;
-  int RS = 1;
-  // largest power of two keeping the grid within one wave of 2 CTAs x 148 SMs (measured best
-  // on C2 with the TMA pipeline: RS = 2)
-  while (RS < 8 && ctas * RS * 2 <= 2 * 148 && N / (RS * 2) >= 2 * RC4) RS *= 2;
-  if (const char *e = getenv("EI_K1_RS")) RS = std::max(1, std::min(8, atoi(e)));   // tuning knob
+  size_t budget = 0;
+  auto plan_rs = [&](int rt) {
+    p.proj.RT = rt;
+    cps = rt == RT ? 2 : 4;   // CTAs per SM
+    budget = (env ? (size_t)atoi(env) : (cps == 2 ? 104 : 52)) * 1024;
+    const size_t budget4 = (cps == 2 ? 100 : 50) * 1024;
+    RC = 32;
+    for (;;) {   // 4-stage chunk size (sets the row split)
+      build_windows(p, angles, groups, order, 1, RC, win1, nch, CW);
+      if ((size_t)NSTMAX * RC * (CW + 2) * per_entry <= budget4 || RC == 1) break;
+      RC /= 2;
+    }
+    RC4 = RC;
+    ntile = (ND + rt - 1) / rt;
+    ctas = (long long)ntile * (long long)groups.size() * p.S;
+    // row split for small problems: the largest power of two keeping the grid within one wave
+    // of cps CTAs per SM (measured best on C2 with 64-ray tiles: RS = 2)
+    RS = 1;
+    while (RS < 8 && ctas * RS * 2 <= (long long)cps * sms && N / (RS * 2) >= 2 * RC4) RS *= 2;
+    if (const char *e = getenv("EI_K1_RS")) RS = std::max(1, std::min(8, atoi(e)));   // tuning knob
+  };
+  // Ray tile: 64 rays; 32 when the 64-ray grid is one wave on more CTAs than SMs (C2, P1): twice
+  // the units at four CTAs per SM balance the heavy and light units of the wave better (C2 K1
+  // 39.2 -> 34.8 us; multi-wave grids keep 64: C4 K1 8.65 vs 9.13 ms with 32, C5 1.23 vs 1.49).
+  plan_rs(RT);
+  const long long grid64 = ctas * RS;
+  int rt_use = (grid64 > sms && grid64 <= 2LL * sms) ? RTS : RT;
+  if (const char *e = getenv("EI_K1_RT")) rt_use = atoi(e) == RTS ? RTS : RT;   // tuning knob
+  if (rt_use != RT) plan_rs(rt_use);
+  // K0 triggers K1's launch at its start only for grids smaller than the SMs (C1: 28.8 -> 26.8
+  // us): a larger single-wave grid launched while K0 occupies SMs would not land as the unit
+  // placement below assumes (C2 with 32-ray tiles: 73.4 -> 79.3 us)
+  p.proj.k0_early = ctas * RS <= sms ? 1 : 0;
+  if (const char *e = getenv("EI_K0_EARLY")) p.proj.k0_early = atoi(e) ? 1 : 0;   // tuning knob
   int nst = 2;
   {
     int rcmax = 1;
@@ -622,8 +655,8 @@ int plan_projector(ei_plan &p, const double *angles, const std::vector<int> &pro
   p.proj.Rp = (N + 1 + 2 * p.proj.PAD + 1) & ~1;   // even: 16-B aligned float2 rows
   p.proj.n_tiles = ntile;
   if ((long long)ntile * groups.size() * p.S * RS > 0x7fffffffLL) return EI_ERR_SHAPE;   // 1-D grid
-  unit1 = order_units(win1, 1, (int)groups.size(), ntile, p.proj.nch1, p.S, RC, N);
-  unitRS = RS > 1 ? order_units(winRS, RS, (int)groups.size(), ntile, p.proj.nchRS, p.S, RC, N) : unit1;
+  unit1 = order_units(win1, 1, (int)groups.size(), ntile, p.proj.nch1, p.S, RC, N, cps);
+  unitRS = RS > 1 ? order_units(winRS, RS, (int)groups.size(), ntile, p.proj.nchRS, p.S, RC, N, cps) : unit1;
   for (size_t g = 0; g < groups.size(); ++g) groups[g].y |= rf_flags[g] << 16;   // last: device copy
   return EI_OK;
 }

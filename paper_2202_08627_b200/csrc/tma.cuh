@@ -61,6 +61,10 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 // at the end of their work: an early trigger there let the next single-wave grid (K3 after K2)
 // land on whichever SMs happened to be free while the imbalanced predecessor still ran, and C2
 // lost 3 us (tools/dbg/step_trace.py).
+#ifdef EI_NO_K0_TRIGGER
+#define PDL_TRIGGER_K0()
+#else
 #define PDL_TRIGGER_K0() pdl_trigger()
+#endif
 
 }  // namespace ei

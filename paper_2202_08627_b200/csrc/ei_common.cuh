@@ -97,7 +97,11 @@ struct ei_plan {
   float *part_mo = nullptr;      // [S][NA][nseg][nw] per-warp dS/dm_o partials (K2, NEXT-2)
   double *part_reg = nullptr;    // [S][RB] per-tile sum x^2 partials (K0)
   float *part3 = nullptr;        // [KS][S][3][N][N] K3 angle-split partial gradients
-  int KS = 1;                    // K3 angle split
+  int KS = 1;                    // K3 angle split: most parts of one (slice, tile)
+  int KSk = 1, KSe = 0;          // (slice, tile) pairs v < KSe have KSk + 1 parts, the rest KSk
+  int4 *k3u = nullptr;           // device [n_k3u] K3 units {tile, slice, part, parts} in launch order
+  int n_k3u = 0;                 // (only for split grids with more units than SMs)
+
   // 360-degree scans: angle pairs (theta, theta + pi) sample the same lines (mirrored detector,
   // R6), so K1 projects only the primary angle of each pair and writes both rows, and K3 back-
   // projects only primaries after the gradient rows are folded: G(a) += mirror(G(partner))

@@ -153,7 +153,7 @@ __device__ __forceinline__ void finalize(const FinArgs &f, int s, int tid) {
     }
 }
 
-template <int NMAP>
+template <int NMAP, bool TAB>
 __global__ void __launch_bounds__(NT + 32, 3) backproject_kernel(
     const typename Layout<NMAP>::A *__restrict__ GA, const float2 *__restrict__ GB,
     const float4 *__restrict__ k3, const int *__restrict__ alist, int NA3, int N, int NA, int ND,
@@ -161,14 +161,24 @@ __global__ void __launch_bounds__(NT + 32, 3) backproject_kernel(
     const float *__restrict__ delta, const float *__restrict__ sigma, float lambda,
     float *__restrict__ o0, float *__restrict__ o1, float *__restrict__ o2, size_t out_stride,
     int S, int KS, float *__restrict__ part3, int PADG, int RpG,
-    FinArgs fin) {
+    const int4 *__restrict__ units, FinArgs fin) {
   using TA = typename Layout<NMAP>::A;
   constexpr bool A8 = sizeof(TA) == 8;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   Smem<NMAP> &sm = *reinterpret_cast<Smem<NMAP> *>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const int s = blockIdx.z % S, ks = blockIdx.z / S;
-  const int j0 = blockIdx.x * TILE, i0 = blockIdx.y * TILE;
+  // unit: tile, slice, part ks of the tile's angle split into nks parts.  Grids with more units
+  // than SMs read it from the plan's placement table (parts of unequal size placed heaviest first);
+  // the others decode it from the block index, grid (tiles x, tiles y, KS x S), with no table load
+  // ahead of the first copy
+  int j0, i0, s, ks, nks;
+  if (TAB) {   // (separate instantiation: the untabled kernel keeps its own code schedule)
+    const int4 u = __ldg(units + blockIdx.x);
+    const int ntx = (N + TILE - 1) / TILE;
+    j0 = (u.x % ntx) * TILE; i0 = (u.x / ntx) * TILE; s = u.y; ks = u.z; nks = u.w;
+  } else {
+    j0 = blockIdx.x * TILE; i0 = blockIdx.y * TILE; s = blockIdx.z % S; ks = blockIdx.z / S; nks = KS;
+  }
 SPAN_START_bp();
 #ifdef EI_TRACE
   const unsigned long long t_start = gtimer3();
@@ -181,7 +191,7 @@ SPAN_START_bp();
   // angle split (small grids): CTA ks owns angles [a_lo, a_hi) of the back-projected list, an equal
   // share (not a whole number of chunks: 360 angles in 6 parts are 60 each, staged as 16+16+16+12,
   // where whole chunks gave 3 or 4 chunks per CTA), in chunks of CH staged angles
-  const int a_lo = (int)(((long long)ks * NA3) / KS), a_hi = (int)(((long long)(ks + 1) * NA3) / KS);
+  const int a_lo = (int)(((long long)ks * NA3) / nks), a_hi = (int)(((long long)(ks + 1) * NA3) / nks);
   const int c_lo = 0, c_hi = (a_hi - a_lo + CH - 1) / CH;
   const int *alist_k = alist + a_lo;
 
@@ -238,7 +248,7 @@ SPAN_START_bp();
   // fused K4 (cost path): while the producer fills the ring, CTA (0, 0, s) of angle split 0 sums
   // K2's per-segment partials of slice s in index order (+ lambda * K0's sum x^2 partials) and
   // the per-angle drift gradient
-  if (fin.cost && blockIdx.x == 0 && blockIdx.y == 0 && ks == 0) {
+  if (fin.cost && i0 == 0 && j0 == 0 && ks == 0) {
     pdl_wait();   // K2's partials
     finalize(fin, s, tid);
   }
@@ -297,7 +307,7 @@ SPAN_START_bp();
   if (tid == 0) {
     unsigned smid;
     asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
-    const size_t b = ((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+    const size_t b = ((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;   // linear
     if (b < 65536) {
       g_k3_trace[4 * b] = t_start;
       g_k3_trace[4 * b + 1] = t_data;
@@ -309,7 +319,7 @@ SPAN_START_bp();
 #endif
   const int i = i0 + row;
   const size_t NN = (size_t)N * N;
-  if (KS > 1) {   // angle split: publish partials; ks_reduce_kernel sums them in ks order
+  if (KS > 1) {   // angle split: publish partials; ks_reduce_kernel sums them in part order
     if (i < N) {
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
@@ -355,7 +365,7 @@ SPAN_START_bp();
 // angle split (KS > 1): fixed-order sum of the KS partial gradients + 2 lambda x (eq. 5), one thread
 // per (slice, pixel), launched with PDL right after K3
 template <int NMAP>
-__global__ void __launch_bounds__(256) ks_reduce_kernel(const float *__restrict__ part3, int KS, int S,
+__global__ void __launch_bounds__(256) ks_reduce_kernel(const float *__restrict__ part3, int KSk, int KSe, int S,
                                                         int N, const float *__restrict__ mu,
                                                         const float *__restrict__ delta,
                                                         const float *__restrict__ sigma, float lambda,
@@ -366,6 +376,11 @@ __global__ void __launch_bounds__(256) ks_reduce_kernel(const float *__restrict_
   const size_t NN = (size_t)N * N, total = (size_t)S * NN;
   for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < total; t += (size_t)gridDim.x * blockDim.x) {
     const size_t s = t / NN, p = t - s * NN;
+    int KS = KSk;
+    if (KSe > 0) {   // the first KSe (slice, tile) pairs have one part more
+      const int ntx = (N + TILE - 1) / TILE, tile = (int)(p / N) / TILE * ntx + (int)(p % N) / TILE;
+      KS += (long long)s * ntx * ntx + tile < KSe ? 1 : 0;
+    }
     float v[3] = {0.f, 0.f, 0.f};
     for (int k2 = 0; k2 < KS; ++k2) {
       const float *pp = part3 + ((size_t)(k2 * S + s) * 3) * NN + p;
@@ -413,19 +428,23 @@ cudaError_t launch_bp(const ei_plan &p, const typename Layout<NMAP>::A *GA, cons
     fin.g_drift = fz->g_drift;
   }
   const size_t smem = sizeof(Smem<NMAP>);
-  cudaError_t e = cudaFuncSetAttribute((const void *)backproject_kernel<NMAP>,
+  cudaError_t e = cudaFuncSetAttribute((const void *)backproject_kernel<NMAP, true>,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute((const void *)backproject_kernel<NMAP, false>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  dim3 grid((p.N + TILE - 1) / TILE, (p.N + TILE - 1) / TILE, p.S * p.KS);
-  e = launch_pdl(backproject_kernel<NMAP>, grid, dim3(NT + 32), smem, st, GA, GB, p.tab.k3, p.alist3,
+  const dim3 grid = p.k3u ? dim3(p.n_k3u) : dim3((p.N + TILE - 1) / TILE, (p.N + TILE - 1) / TILE, p.S * p.KS);
+  auto kern = p.k3u ? backproject_kernel<NMAP, true> : backproject_kernel<NMAP, false>;
+  e = launch_pdl(kern, grid, dim3(NT + 32), smem, st, GA, GB, p.tab.k3, p.alist3,
                  p.NA3, p.N, p.NA, p.ND, mu, delta, sigma, lambda, o0, o1, o2, out_stride, p.S, p.KS, p.part3,
-                 p.PADG, p.RpG, fin);
+                 p.PADG, p.RpG, (const int4 *)p.k3u, fin);
   if (e != cudaSuccess) return e;
   if (p.KS > 1) {
     const size_t total = (size_t)p.S * p.N * p.N;
     const int blocks = (int)std::min<size_t>((total + 255) / 256, 148 * 8);
-    e = launch_pdl(ks_reduce_kernel<NMAP>, dim3(blocks), dim3(256), 0, st, (const float *)p.part3, p.KS,
-                   p.S, p.N, mu, delta, sigma, lambda, o0, o1, o2, out_stride);
+    e = launch_pdl(ks_reduce_kernel<NMAP>, dim3(blocks), dim3(256), 0, st, (const float *)p.part3, p.KSk,
+                   p.KSe, p.S, p.N, mu, delta, sigma, lambda, o0, o1, o2, out_stride);
     if (e != cudaSuccess) return e;
   }
   return cudaGetLastError();

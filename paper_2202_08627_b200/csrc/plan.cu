@@ -65,7 +65,7 @@ void free_plan(ei_plan *p) {
     if (ev) cudaEventDestroy(ev);
   void *ptrs[] = {p->tab.k1, p->tab.k3, p->proj.groups, p->proj.order, p->proj.partner, p->alist3,
                   p->pairs, p->proj.win1, p->proj.winRS, p->proj.unit1, p->proj.unitRS, p->MA, p->MAT, p->MB,
-                  p->MBT, p->M1, p->M1T, p->diag, p->part_mo, p->part3, p->P, p->GA, p->GB, p->GA1,
+                  p->MBT, p->M1, p->M1T, p->diag, p->part_mo, p->part3, p->k3u, p->P, p->GA, p->GB, p->GA1,
                   p->part_curve, p->part_reg, p->h_maps, p->h_flat, p->h_mask, p->h_drift,
                   p->h_sexp, p->h_grad, p->h_cost, p->h_status};
   for (void *q : ptrs)
@@ -210,12 +210,53 @@ int ei_plan_create(const ei_geometry *geom, const double *angles, ei_plan **out)
   // K3 angle split for small grids: the largest KS (<= 16, <= angle chunks) keeping the grid within
   // one wave of 3 CTAs per SM; the KS partial gradients are summed by ks_reduce_kernel (measured:
   // C1 KS 1 -> 6-8: 22.5 -> 14.5 us; C2 KS 4-6 best)
+  // The first `extra` (slice, tile) pairs take one part more, so the grid fills the 3 x SMs slots
+  // exactly (C2: 60 tiles in 7 parts and 4 in 6 = 444 CTAs instead of 64 x 6 = 384; the 6-part
+  // units placed heaviest first on the least-loaded SM): C2 K3 33.8 -> 31.8 us.
+  std::vector<int4> k3u;
   {
-    const long long ctas = (long long)ei::bp_tiles(p->N) * p->S;
+    int sms = 148, dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaGetLastError();
+    const int T = ei::bp_tiles(p->N), C = ei::bp_chunks(p->NA3);
+    const long long ctas = (long long)T * p->S, slots = 3LL * sms;
     int KS = 1;
-    while (KS < 16 && KS + 1 <= ei::bp_chunks(p->NA3) && ctas * (KS + 1) <= 3 * 148) ++KS;
-    if (const char *e = getenv("EI_K3_KS")) KS = std::max(1, std::min(16, atoi(e)));   // tuning knob
-    p->KS = KS;
+    while (KS < 16 && KS + 1 <= C && ctas * (KS + 1) <= slots) ++KS;
+    long long extra = (KS < 16 && KS + 1 <= C && ctas * KS < slots) ? std::min(ctas, slots - ctas * KS) : 0;
+    if (const char *e = getenv("EI_K3_KS")) {   // tuning knob: uniform split
+      KS = std::max(1, std::min(16, atoi(e)));
+      extra = 0;
+    }
+    if (ctas * KS + extra <= sms) extra = 0;   // tiny grid: uniform split, block-index decode
+    p->KSk = KS;
+    p->KSe = (int)extra;
+    p->KS = KS + (extra > 0 ? 1 : 0);
+    const long long n = ctas * KS + extra;
+    if (p->KS > 1 && n > sms) {   // placement table: parts heaviest first, least-loaded SM
+      std::vector<int4> u;
+      for (int s = 0; s < p->S; ++s)
+        for (int t = 0; t < T; ++t) {
+          const int np = KS + ((long long)s * T + t < extra ? 1 : 0);
+          for (int q = 0; q < np; ++q) u.push_back(make_int4(t, s, q, np));
+        }
+      std::vector<int> ord(u.size());
+      for (size_t i = 0; i < u.size(); ++i) ord[i] = (int)i;
+      std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return u[a].w < u[b].w; });
+      std::vector<int> cap(sms, 0), used(sms, 0);
+      std::vector<double> load(sms, 0.0);
+      for (size_t b = 0; b < u.size(); ++b) cap[b % sms] += 1;
+      k3u.assign(u.size(), make_int4(0, 0, 0, 1));
+      for (int i : ord) {
+        int best = -1;
+        for (int m = 0; m < sms; ++m)
+          if (used[m] < cap[m] && (best < 0 || load[m] < load[best])) best = m;
+        k3u[best + used[best] * sms] = u[i];
+        used[best] += 1;
+        load[best] += 1.0 / u[i].w;   // the part's share of the angles
+      }
+      p->n_k3u = (int)u.size();
+      A(dalloc(&p->k3u, k3u.size()));
+    }
   }
   if (p->KS > 1) A(dalloc(&p->part3, (size_t)p->KS * S * 3 * p->N * p->N));
   if (e == cudaSuccess) A(cudaMemcpy(p->tab.k1, k1, sizeof(float4) * NA, cudaMemcpyHostToDevice));
@@ -231,6 +272,9 @@ int ei_plan_create(const ei_geometry *geom, const double *angles, ei_plan **out)
   if (e == cudaSuccess && !pairs.empty())
     A(cudaMemcpy(p->pairs, pairs.data(), sizeof(int2) * pairs.size(), cudaMemcpyHostToDevice));
   if (e == cudaSuccess) A(cudaMemset(p->diag, 0, sizeof(int32_t)));
+  if (e == cudaSuccess && p->k3u)
+    A(cudaMemcpy(p->k3u, k3u.data(), sizeof(int4) * k3u.size(), cudaMemcpyHostToDevice));
+
   // the zero padding of the map rows is written once here; K0 only writes the interior
   for (void *q : {(void *)p->MA, (void *)p->MAT})
     if (e == cudaSuccess) A(cudaMemset(q, 0, sizeof(float4) * S * NP));

@@ -613,6 +613,10 @@ int plan_projector(ei_plan &p, const double *angles, const std::vector<int> &pro
       }
     }
     if (const char *e = getenv("EI_K1_NST")) nst = std::max(2, std::min(NSTMAX, atoi(e)));   // knob
+    if (const char *e = getenv("EI_K1_RC")) {   // tuning knob: rows per chunk (any value)
+      RC = std::max(1, atoi(e));
+      build_windows(p, angles, groups, order, 1, RC, win1, nch, CW);
+    }
   }
   if ((size_t)nst * RC * (CW + 2) * per_entry > 200 * 1024) return EI_ERR_SHAPE;
   if (nch > MAXCH) return EI_ERR_SHAPE;

@@ -44,7 +44,7 @@ EOF
       # the source of profiles/traffic.json (tools/ncu_traffic.py) and the ncu summaries
       for c in ${FULL_CFGS:-C2 C3 C5 C4}; do
         timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
-          -k regex:"project_kernel<\\(int\\)3>|curve_kernel<\\(int\\)1>" -s 9 -c 3 \
+          -k regex:"project_kernel<\\(int\\)3|curve_kernel<\\(int\\)1>" -s 9 -c 3 \
           -o $OUT/full_$c python bench.py --config $c --steps 3 --warmup 3 --no-cpu-baseline > $OUT/ncu_full_$c.log 2>&1
         echo "ncu full $c rc=$?" | tee -a $OUT/rc.txt
       done ;;

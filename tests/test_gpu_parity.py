@@ -438,3 +438,48 @@ def test_project_parity_many_slices(ei):
             assert rel_l2(got[s, q], ref) < 2e-5, (s, q)
             refb = ora.backproject(y[s, q].astype(np.float64), cfg.angles, cfg.N, cfg.pixel, cfg.det_pitch)
             assert rel_l2(gbp[s, q], refb) < 2e-5, (s, q)
+
+
+PLAN_MATRIX = [   # (S, N, n_angles, span_deg, n_det, M): ragged geometries that walk the plan's branches
+    (1, 150, 210, 180.0, 229, 3),    # K1 single wave above the SM count -> 32-ray tiles; K3 split with extra parts
+    (3, 96, 120, 360.0, 143, 2),     # mirror pairs, several slices, small K3 split
+    (2, 200, 64, 180.0, 301, 5),     # sparse views: ray-fast groups
+    (5, 40, 33, 360.0, 61, 1),       # odd angle count over 360 (no pairs), M = 1
+    (1, 33, 17, 180.0, 50, 4),       # tiny grid: K0 triggers K1 early
+]
+
+
+@pytest.mark.parametrize("geom", PLAN_MATRIX)
+def test_plan_matrix(ei, geom):
+    """Cost and gradients vs the oracle on geometries chosen to exercise the plan's choices (ray
+    tile width, row split, K3 part counts and placement, mirror pairs, lane mappings, K0's early
+    launch).  Maps are random fields; s_exp is the oracle model at the maps plus 1 % noise."""
+    S, N, NA, span, ND, M = geom
+    cfg = synth.small_config("PM", S=S, N=N, n_angles=NA, span_deg=span, n_det=ND, M=M, K=4, seed=N + NA)
+    rng = np.random.default_rng(N * 7 + NA)
+    ang = cfg.angles
+    mu = (rng.uniform(0.0, 1.0, (S, N, N)) * 0.3 / N).astype(np.float32)
+    de = (rng.uniform(0.0, 1.0, (S, N, N)) * 0.02 / N).astype(np.float32)
+    sg = (rng.uniform(0.0, 1.0, (S, N, N)) * 1e-4 / N).astype(np.float32)
+    flat = np.zeros((S, 3, ND), np.float32)
+    flat[:, 0] = 1e4 * rng.uniform(0.95, 1.05, (S, ND))
+    flat[:, 1] = rng.normal(0.0, 0.05, (S, ND))
+    flat[:, 2] = 0.15
+    mask = ((np.arange(M) - (M - 1) / 2) / max(M, 1)).astype(np.float32)
+    drift = np.cumsum(rng.normal(0.0, 0.002, NA)).astype(np.float32)
+    s_true, _ = ora.forward(ang, mu, de, sg, flat, mask, drift)
+    s_exp = (s_true * (1.0 + 0.01 * rng.standard_normal(s_true.shape))).astype(np.float32)
+    maps = synth.perturbed((mu, de, sg), 5)
+    plan = ei.Plan(S, N, NA, ND, M, 1.0, 1.0, 1.0, ang)
+    ws = ei.Workspace(plan)
+    cost, g, st = ei.cost_grad(plan, [dev(m) for m in maps], dev(flat), dev(mask), dev(drift), dev(s_exp),
+                               1e-2, ws)
+    torch.cuda.synchronize()
+    rc, rgm, rgd, rgs, rst = ora.cost_grad(ang, *maps, flat, mask, drift, s_exp, 1e-2)
+    c = cost.cpu().numpy()
+    assert np.all(np.abs(c - rc) / rc <= 1e-4), (c, rc, ei.ei_plan_info(plan))
+    for q, ref in enumerate((rgm, rgd, rgs)):
+        gq = g[q].cpu().numpy()
+        for s in range(S):
+            assert rel_l2(gq[s], ref[s]) <= 1e-3, (q, s, rel_l2(gq[s], ref[s]), ei.ei_plan_info(plan))
+    assert list(st.cpu().numpy()[:3]) == list(rst)

@@ -586,12 +586,35 @@ int plan_projector(ei_plan &p, const double *angles, const std::vector<int> &pro
     while (RS < 8 && ctas * RS * 2 <= (long long)cps * sms && N / (RS * 2) >= 2 * RC4) RS *= 2;
     if (const char *e = getenv("EI_K1_RS")) RS = std::max(1, std::min(8, atoi(e)));   // tuning knob
   };
-  // Ray tile: 64 rays; 32 when the 64-ray grid is one wave on more CTAs than SMs (C2, P1): twice
+  {   // per angle group, the lane mapping with fewer modelled shared-memory wavefronts, stored in
+      // bit 16 of the group's count (tuning knob EI_K1_RAYFAST forces one mapping everywhere)
+    const char *force = getenv("EI_K1_RAYFAST");
+    rf_flags.assign(groups.size(), 0);
+    double wa_sum = 0.0, wbest = 0.0;
+    int nrf = 0;
+    for (size_t g = 0; g < groups.size(); ++g) {
+      const double wa = wavefront_model(p, angles, groups, order, g, false);
+      const double wr = wavefront_model(p, angles, groups, order, g, true);
+      int rf = wr < 0.9 * wa ? 1 : 0;
+      if (force) rf = atoi(force) ? 1 : 0;
+      wa_sum += wa;
+      wbest += rf ? wr : wa;
+      nrf += rf;
+      rf_flags[g] = rf;   // encoded into the device copy at the end (host code reads counts)
+    }
+    p.proj.ray_fast = nrf;
+    if (getenv("EI_PLAN_VERBOSE"))
+      fprintf(stderr, "libei plan: K1 modelled wavefronts/sample angle-fast %.2f chosen %.2f (%d/%d ray-fast groups)\n",
+              wa_sum / groups.size(), wbest / groups.size(), nrf, (int)groups.size());
+  }  // Ray tile: 64 rays; 32 when the 64-ray grid is one wave on more CTAs than SMs (C2, P1): twice
   // the units at four CTAs per SM balance the heavy and light units of the wave better (C2 K1
   // 39.2 -> 34.8 us; multi-wave grids keep 64: C4 K1 8.65 vs 9.13 ms with 32, C5 1.23 vs 1.49).
   plan_rs(RT);
   const long long grid64 = ctas * RS;
   int rt_use = (grid64 > sms && grid64 <= 2LL * sms) ? RTS : RT;
+  // also for dense views whose 64-ray windows only allow small chunks (C3: K1 0.620 -> 0.603 ms);
+  // not for sparse views, where 32-ray tiles add bank conflicts (C5: 1.23 -> 1.49 ms)
+  if (RC4 <= 4 && 4 * p.proj.ray_fast < (int)groups.size()) rt_use = RTS;
   if (const char *e = getenv("EI_K1_RT")) rt_use = atoi(e) == RTS ? RTS : RT;   // tuning knob
   if (rt_use != RT) plan_rs(rt_use);
   // K0 triggers K1's launch at its start only for grids smaller than the SMs (C1: 28.8 -> 26.8
@@ -623,27 +646,7 @@ int plan_projector(ei_plan &p, const double *angles, const std::vector<int> &pro
   p.proj.RC = RC;
   p.proj.nst = nst;
   p.proj.n_groups = (int)groups.size();
-  {   // per angle group, the lane mapping with fewer modelled shared-memory wavefronts, stored in
-      // bit 16 of the group's count (tuning knob EI_K1_RAYFAST forces one mapping everywhere)
-    const char *force = getenv("EI_K1_RAYFAST");
-    rf_flags.assign(groups.size(), 0);
-    double wa_sum = 0.0, wbest = 0.0;
-    int nrf = 0;
-    for (size_t g = 0; g < groups.size(); ++g) {
-      const double wa = wavefront_model(p, angles, groups, order, g, false);
-      const double wr = wavefront_model(p, angles, groups, order, g, true);
-      int rf = wr < 0.9 * wa ? 1 : 0;
-      if (force) rf = atoi(force) ? 1 : 0;
-      wa_sum += wa;
-      wbest += rf ? wr : wa;
-      nrf += rf;
-      rf_flags[g] = rf;   // encoded into the device copy at the end (host code reads counts)
-    }
-    p.proj.ray_fast = nrf;
-    if (getenv("EI_PLAN_VERBOSE"))
-      fprintf(stderr, "libei plan: K1 modelled wavefronts/sample angle-fast %.2f chosen %.2f (%d/%d ray-fast groups)\n",
-              wa_sum / groups.size(), wbest / groups.size(), nrf, (int)groups.size());
-  }
+
   p.proj.nch1 = nch;
   p.proj.RS = RS;
   int CWrs = CW;

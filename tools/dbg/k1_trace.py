@@ -34,15 +34,21 @@ for _ in range(iters):
     ei.cost_grad(plan, maps, flat, mask, None, s_exp, 1e-2, ws)
 torch.cuda.synchronize()
 info = ei.ei_plan_info(plan)
-ntile = (cfg.n_det + 63) // 64
 ngr = info["k1_groups"]
 RS = info["k1_row_split"]
-n = ntile * ngr * S * RS
-buf = (ctypes.c_ulonglong * (4 * n))()
+cap = 65536
+buf = (ctypes.c_ulonglong * (4 * cap))()
 fn = ei._lib.ei_debug_k1_trace
 fn.argtypes = [ctypes.c_void_p, ctypes.c_int]
-assert fn(ctypes.addressof(buf), n) == 0
-tr = np.frombuffer(buf, dtype=np.uint64).reshape(n, 4).astype(np.int64)
+assert fn(ctypes.addressof(buf), cap) == 0
+tr = np.frombuffer(buf, dtype=np.uint64).reshape(cap, 4).astype(np.int64)
+n = ngr * S * RS * ((cfg.n_det + 31) // 32)          # 32-ray tiles: the most CTAs a plan can have
+tr = tr[:n]
+t_last = tr[:, 1].max()
+tr = tr[(tr[:, 1] > t_last - 10**9) & (tr[:, 0] > 0)]  # records of the last call only
+n = len(tr)
+ntile = n // (ngr * S * RS)
+print("ray tile: %d rays (%d tiles)" % ((cfg.n_det + ntile - 1) // ntile, ntile))
 t0 = tr[:, 0].min()
 st, en, sm = (tr[:, 0] - t0) / 1e3, (tr[:, 1] - t0) / 1e3, tr[:, 2]
 rows, un = tr[:, 3] & 0xffffffff, tr[:, 3] >> 32

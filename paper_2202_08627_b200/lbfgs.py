@@ -99,10 +99,10 @@ def minimize(fg: Callable[[torch.Tensor], Tuple[torch.Tensor, torch.Tensor]], x0
         p = -r
         gp = _sdot(g, p)
         bad = gp >= 0                          # not a descent direction: restart that slice
-        if bool(bad.any()):
-            p = torch.where(_bc(bad, p), -g * _bc(1.0 / _bdot(g, g).sqrt().clamp_min(1e-300), g), p)
-            gp = _sdot(g, p)
-            rho = rho * (~bad).to(rho.dtype)
+        # (masked updates instead of a host-side `if bad.any()`: no device -> host sync)
+        p = torch.where(_bc(bad, p), -g * _bc(1.0 / gnorm, g), p)
+        gp = torch.where(bad, _sdot(g, p), gp)
+        rho = rho * (~bad).to(rho.dtype)
         sd = sd | bad
         # ---- batched backtracking Armijo ----
         step = torch.ones(S, dtype=torch.float64, device=dev)
@@ -125,25 +125,24 @@ def minimize(fg: Callable[[torch.Tensor], Tuple[torch.Tensor, torch.Tensor]], x0
         # no decrease found: restart that slice from steepest descent; if even that fails the
         # slice has converged to working precision
         failed = ~accepted
-        if bool(failed.any()):
-            rho = rho * accepted.to(rho.dtype)
-            has_gamma = has_gamma & accepted
+        rho = rho * accepted.to(rho.dtype)
+        has_gamma = has_gamma & accepted
         s_vec, y_vec = x_new - x, g_new - g
         sy = _sdot(s_vec, y_vec)
         yy = _sdot(y_vec, y_vec)
         curv = sy > 1e-12 * _sdot(s_vec, s_vec).sqrt() * yy.sqrt()
         keep = accepted & curv & ~conv
-        if bool(keep.any()):
-            Sh[head].copy_(s_vec)
-            Yh[head].copy_(y_vec)
-            rho[head] = torch.where(keep, 1.0 / sy.clamp_min(1e-300), torch.zeros_like(sy))
-            head = (head + 1) % m
-            nh = min(nh + 1, m)
-            gb = _bdot(s_vec, y_vec) / _bdot(y_vec, y_vec).clamp_min(1e-300)
-            gg = (sy / yy.clamp_min(1e-300)).unsqueeze(0).expand_as(gb)
-            gb = torch.where(gb > 0, gb, gg)          # block secant not positive: global scalar
-            gamma = torch.where(keep.unsqueeze(0), gb, gamma)
-            has_gamma = has_gamma | keep
+        # the pair is stored for every slice (rho = 0 where it is not kept): no host-side branch
+        Sh[head].copy_(s_vec)
+        Yh[head].copy_(y_vec)
+        rho[head] = torch.where(keep, 1.0 / sy.clamp_min(1e-300), torch.zeros_like(sy))
+        head = (head + 1) % m
+        nh = min(nh + 1, m)
+        gb = _bdot(s_vec, y_vec) / _bdot(y_vec, y_vec).clamp_min(1e-300)
+        gg = (sy / yy.clamp_min(1e-300)).unsqueeze(0).expand_as(gb)
+        gb = torch.where(gb > 0, gb, gg)              # block secant not positive: global scalar
+        gamma = torch.where(keep.unsqueeze(0), gb, gamma)
+        has_gamma = has_gamma | keep
         rel = (f - f_new) / f.abs().clamp_min(1e-300)
         conv = conv | (failed & sd) | (accepted & (rel < rel_tol))
         sd = failed & ~conv

@@ -181,7 +181,7 @@ int ei_plan_read_timing(ei_plan *plan, double ms[6], int *n_evals);
  * out[1] = K1 rows per staged chunk, out[2] = K1 window-width bound (entries), out[3] = K1 row
  * split of the cost path, out[4] = internal window overflows seen so far (must be 0),
  * out[5] = K1 dynamic shared memory per CTA (bytes), out[6] = K1 angle groups using the
- * ray-fastest lane mapping, out[7] = K3 angle split, out[8] = mirror angle pairs (theta,
+ * ray-fastest lane mapping, out[7] = K3 angle split (most parts of one tile), out[8] = mirror angle pairs (theta,
  * theta + pi) of a 360-degree scan projected and back-projected once (env EI_MIRROR=0 at plan
  * creation disables), out[9] = K2 detector segments per row. */
 int ei_plan_info(const ei_plan *plan, int64_t out[10]);

@@ -701,8 +701,10 @@ int ei_cost_grad_host(ei_plan *p, const float *mu, const float *delta, const flo
     if (p->h_exec) {
       if (cudaGraphLaunch(p->h_exec, p->h_work) != cudaSuccess) return EI_ERR_CUDA;
       for (int i = 0; i < 6; ++i) p->stats[i] += p->h_stats[i];
-      // wait by polling an event instead of cudaStreamSynchronize: the call is synchronous and
-      // short (C2: ~0.2 ms), so the driver's blocking wake-up latency would be a visible share
+      // EI_HOST_SPIN=1 polls an event instead of cudaStreamSynchronize (no measurable difference
+      // on the box, where host scheduling noise dominates the 0.2-0.4 ms call)
+      const char *spin = getenv("EI_HOST_SPIN");
+      if (!(spin && atoi(spin) != 0)) return cudaStreamSynchronize(p->h_work) == cudaSuccess ? EI_OK : EI_ERR_CUDA;
       if (cudaEventRecord(p->h_ev[3], p->h_work) != cudaSuccess) return EI_ERR_CUDA;
       cudaError_t q;
       while ((q = cudaEventQuery(p->h_ev[3])) == cudaErrorNotReady) {

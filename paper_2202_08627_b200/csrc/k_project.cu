@@ -4,16 +4,19 @@
 // swapped (H2); x*(k, i) = (k-(Nd-1)/2)*ic - tn*(i-(N-1)/2) + (N-1)/2, taps (floor x*, +1).
 //
 // B200 design (DESIGN.md §5 K1):
-//  * a CTA owns AGB = 16 consecutive same-dominance angles x RT = 64 adjacent rays; it walks the
-//    rows in chunks of RC rows, staging with cp.async only the window of PAIR entries (K0 layout:
-//    entry e = (x[e-1], x[e]) of all maps) that its 1024 rays touch in those rows (double-
-//    buffered); the window width bound CW is computed exactly on the host (plan) so every index
-//    stays inside the staged window without per-sample checks;
-//  * a warp = 4 adjacent angles x 8 adjacent rays: near the centre of the map the 4 angles
-//    sample the same pixels, so lanes share shared-memory words (broadcast);
+//  * a CTA owns AGB = 16 consecutive same-dominance angles x RTILE = 64 adjacent rays (32 at four
+//    CTAs per SM for single-wave grids and dense wide-window views, plan_projector); it walks the
+//    rows in chunks of RC rows; a producer warp streams, with 1-D bulk copies (TMA engine), only
+//    the window of PAIR entries (K0 layout: entry e = (x[e-1], x[e]) of all maps) that the CTA's
+//    rays touch in those rows into a 2-3 stage mbarrier ring; the window bound CW is computed
+//    exactly on the host (plan) so every index stays inside the staged window without per-sample
+//    checks;
+//  * a warp = 4 adjacent angles x 8 adjacent rays (angle fastest) or 8 rays x 4 angles (ray
+//    fastest, sparse views), chosen per angle group from a bank-conflict model;
 //  * one tap pair of all three maps = one LDS.128 + one LDS.64; weights (1-w, w) as a float2 and
 //    three FFMA2 per sample (acc.x: left taps, acc.y: right taps);
-//  * small problems split the rows over RS CTAs (partial P summed in fixed order by K2).
+//  * small problems split the rows over RS CTAs (partial P summed in fixed order by K2); the
+//    CTAs run work units from a plan table (heaviest first, placed per SM for single waves).
 #include <math.h>
 
 #include <stdio.h>

@@ -37,6 +37,9 @@ fn = ei._lib.ei_debug_k3_trace
 fn.argtypes = [ctypes.c_void_p, ctypes.c_int]
 assert fn(ctypes.addressof(buf), n) == 0
 tr = np.frombuffer(buf, dtype=np.uint64).reshape(n, 4).astype(np.int64)
+# n is an upper bound (split grids give only some tiles KS parts): keep the records written
+tr = tr[tr[:, 2] > 0]
+n = len(tr)
 t0 = tr[:, 0].min()
 st, da, en = (tr[:, 0] - t0) / 1e3, (tr[:, 1] - t0) / 1e3, (tr[:, 2] - t0) / 1e3
 sm, nch = tr[:, 3] & 0xffffffff, tr[:, 3] >> 32

@@ -123,6 +123,13 @@ struct ei_plan {
   HostKey h_key{};
   int64_t h_stats[6] = {0, 0, 0, 0, 0, 0};  // launch accounting of one captured call
   bool h_graph_failed = false;
+  // stacks: the host path runs in chunks of slices (sub-plans of h_Sc and of the last chunk's
+  // slice count) so uploads, evaluation and downloads of different chunks overlap
+  std::vector<double> angles;               // host copy (sub-plan creation)
+  int h_nchunk = 0, h_Sc = 0;               // 0: not decided yet, 1: one piece
+  ei_plan *h_sub[2] = {nullptr, nullptr};
+  cudaStream_t h_down = nullptr;            // download stream (chunked host path)
+  cudaEvent_t h_cev[17] = {};               // per chunk: uploaded, evaluated; + downloads done
   // launch accounting
   mutable int64_t stats[6] = {0, 0, 0, 0, 0, 0};
   // optional per-kernel timing of ei_cost_grad: 7 events per recorded evaluation

@@ -230,7 +230,8 @@ cudaError_t launch_pack3(const ei_plan &p, const float *mu, const float *delta, 
   pack_pairs_kernel<3><<<grid, block, 0, st>>>(mu, delta, sigma, in_stride, p.N, o,
                                                want_reg ? p.part_reg : nullptr, status, chk,
                                                p.S * (chk.nflat_per_slice ? chk.nflat_per_slice : 3 * p.ND),
-                                               p.M, p.NA, p.proj.PAD, p.proj.Rp, p.proj.k0_early);
+                                               chk.mask ? p.M : 0, p.NA, p.proj.PAD, p.proj.Rp,
+                                               p.proj.k0_early);
   return cudaGetLastError();
 }
 
@@ -242,7 +243,8 @@ cudaError_t launch_pack1(const ei_plan &p, const float *map, cudaStream_t st, bo
   pack_pairs_kernel<1><<<grid, block, 0, st>>>(map, nullptr, nullptr, (size_t)p.N * p.N, p.N, o,
                                                want_reg ? p.part_reg : nullptr, status, chk,
                                                p.S * (chk.nflat_per_slice ? chk.nflat_per_slice : 3 * p.ND),
-                                               p.M, p.NA, p.proj.PAD, p.proj.Rp, p.proj.k0_early);
+                                               chk.mask ? p.M : 0, p.NA, p.proj.PAD, p.proj.Rp,
+                                               p.proj.k0_early);
   return cudaGetLastError();
 }
 

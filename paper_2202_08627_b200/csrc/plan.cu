@@ -56,7 +56,11 @@ void free_plan(ei_plan *p) {
   if (!p) return;
   free_timing(p);
   if (p->h_exec) cudaGraphExecDestroy(p->h_exec);
-  for (cudaStream_t q : {p->h_copy, p->h_work})
+  for (ei_plan *q : p->h_sub)
+    if (q) free_plan(q);
+  for (cudaEvent_t ev : p->h_cev)
+    if (ev) cudaEventDestroy(ev);
+  for (cudaStream_t q : {p->h_copy, p->h_work, p->h_down})
     if (q) {
       cudaStreamSynchronize(q);
       cudaStreamDestroy(q);
@@ -113,6 +117,7 @@ int ei_plan_create(const ei_geometry *geom, const double *angles, ei_plan **out)
   p->NA = geom->n_angles;
   p->ND = geom->n_det;
   p->M = geom->n_mask;
+  p->angles.assign(angles, angles + geom->n_angles);
   const double dx = geom->pixel, du = geom->det_pitch;
 
   // a0: per-angle tables in fp64 -> fp32 (reading R5: row-dominant iff
@@ -438,7 +443,8 @@ namespace {
 int cost_grad_impl(const ei_plan *p, const float *mu, const float *delta, const float *sigma,
                    const float *flat, const float *mask, const float *drift, const float *s_exp,
                    float lambda, double *cost, float *g_mu, float *g_delta, float *g_sigma,
-                   float *g_drift, int32_t *status, void *stream, cudaEvent_t sexp_ready = nullptr) {
+                   float *g_drift, int32_t *status, void *stream, cudaEvent_t sexp_ready = nullptr,
+                   bool check_shared = true) {
   if (!p || !mu || !delta || !sigma || !flat || !mask || !s_exp || !cost || !g_mu || !g_delta ||
       !g_sigma || !status)
     return EI_ERR_NULL;
@@ -447,7 +453,8 @@ int cost_grad_impl(const ei_plan *p, const float *mu, const float *delta, const 
   cudaEvent_t *ev = (p->tev && p->tn < p->tcap) ? p->tev + 7 * p->tn++ : nullptr;
   auto mark = [&](int k) { if (ev) cudaEventRecord(ev[k], st); };
   const size_t NN = (size_t)p->N * p->N;
-  ei::SmallCheck chk{flat, mask, drift};
+  // mask / drift are shared by the slices: a chunked call scans them once
+  ei::SmallCheck chk{flat, check_shared ? mask : nullptr, check_shared ? drift : nullptr};
   mark(0);
   cudaError_t e = ei::launch_pack3(*p, mu, delta, sigma, NN, lambda > 0.f, status, chk, st);  // K0
   mark(1);
@@ -576,6 +583,96 @@ int ei_cost_grad_hs(const ei_plan *p, const float *h, float gamma, const float *
 }
 
 namespace {
+// Chunked host path for stacks (decided on the first host call): K chunks of Sc slices, each
+// evaluated by a sub-plan of the same geometry, so chunk c's upload (h_copy), chunk c-1's
+// evaluation (st) and chunk c-2's download (h_down) overlap.  Only when the sub-plans compute
+// exactly what the whole plan computes: no K3 angle split and the same K1 row split (every other
+// planning choice leaves each slice's arithmetic unchanged), so the results are bit-identical.
+// Env EI_HOST_CHUNKS=K sets the count (1 disables; default 8 for >= 16 slices, 4 for >= 8).
+void setup_chunks(ei_plan *p) {
+  p->h_nchunk = 1;
+  const char *env = getenv("EI_HOST_CHUNKS");
+  int want = env ? atoi(env) : (p->S >= 16 ? 8 : (p->S >= 8 ? 4 : 1));
+  want = std::min(std::min(want, p->S), 8);
+  if (want <= 1 || p->KS != 1) return;
+  const int Sc = (p->S + want - 1) / want, n = (p->S + Sc - 1) / Sc, Sl = p->S - (n - 1) * Sc;
+  if (n <= 1) return;
+  ei_geometry g = p->g;
+  ei_plan *sub[2] = {nullptr, nullptr};
+  bool ok = true;
+  for (int k = 0; k < 2 && ok; ++k) {
+    if (k == 1 && Sl == Sc) break;
+    g.n_slices = k == 0 ? Sc : Sl;
+    ok = ei_plan_create(&g, p->angles.data(), &sub[k]) == EI_OK && sub[k]->KS == 1 &&
+         sub[k]->proj.RS == p->proj.RS && sub[k]->k2.nseg == p->k2.nseg;
+  }
+  cudaError_t e = cudaSuccess;
+  if (ok) e = cudaStreamCreateWithFlags(&p->h_down, cudaStreamNonBlocking);
+  for (int k = 0; k < 2 * n + 1 && ok && e == cudaSuccess; ++k)
+    e = cudaEventCreateWithFlags(&p->h_cev[k], cudaEventDisableTiming);
+  if (!ok || e != cudaSuccess) {
+    cudaGetLastError();
+    for (ei_plan *q : sub)
+      if (q) free_plan(q);
+    return;   // one piece
+  }
+  p->h_sub[0] = sub[0];
+  p->h_sub[1] = sub[1];
+  p->h_Sc = Sc;
+  p->h_nchunk = n;
+}
+
+int enqueue_host_chunked(ei_plan *p, const float *mu, const float *delta, const float *sigma,
+                         const float *flat, const float *mask, const float *drift, const float *s_exp,
+                         float lambda, double *cost, float *g_mu, float *g_delta, float *g_sigma,
+                         int32_t *status, cudaStream_t st) {
+  const size_t S = p->S, NN = (size_t)p->N * p->N, ND = p->ND, NA = p->NA, M = p->M;
+  const int n = p->h_nchunk;
+  cudaError_t e = cudaSuccess;
+  auto A = [&](cudaError_t r) { if (e == cudaSuccess) e = r; };
+  const cudaMemcpyKind H2D = cudaMemcpyHostToDevice, D2H = cudaMemcpyDeviceToHost;
+  A(cudaMemcpyAsync(p->h_mask, mask, sizeof(float) * M, H2D, st));
+  if (drift) A(cudaMemcpyAsync(p->h_drift, drift, sizeof(float) * NA, H2D, st));
+  A(cudaMemsetAsync(p->h_status, 0, sizeof(int32_t) * 4, st));
+  A(cudaEventRecord(p->h_ev[0], st));
+  A(cudaStreamWaitEvent(p->h_copy, p->h_ev[0], 0));
+  A(cudaStreamWaitEvent(p->h_down, p->h_ev[0], 0));
+  if (e != cudaSuccess) return EI_ERR_CUDA;
+  float *dm[3] = {p->h_maps, p->h_maps + S * NN, p->h_maps + 2 * S * NN};
+  float *dg[3] = {p->h_grad, p->h_grad + S * NN, p->h_grad + 2 * S * NN};
+  const float *hm[3] = {mu, delta, sigma};
+  float *hg[3] = {g_mu, g_delta, g_sigma};
+  for (int c = 0; c < n; ++c) {
+    const size_t s0 = (size_t)c * p->h_Sc, sc = std::min((size_t)p->h_Sc, S - s0);
+    ei_plan *q = sc == (size_t)p->h_Sc ? p->h_sub[0] : p->h_sub[1];
+    for (int k = 0; k < 3; ++k)
+      A(cudaMemcpyAsync(dm[k] + s0 * NN, hm[k] + s0 * NN, sizeof(float) * sc * NN, H2D, p->h_copy));
+    A(cudaMemcpyAsync(p->h_flat + s0 * 3 * ND, flat + s0 * 3 * ND, sizeof(float) * sc * 3 * ND, H2D, p->h_copy));
+    const size_t se = NA * M * ND;
+    A(cudaMemcpyAsync(p->h_sexp + s0 * se, s_exp + s0 * se, sizeof(float) * sc * se, H2D, p->h_copy));
+    A(cudaEventRecord(p->h_cev[2 * c], p->h_copy));
+    A(cudaStreamWaitEvent(st, p->h_cev[2 * c], 0));
+    if (e != cudaSuccess) return EI_ERR_CUDA;
+    int64_t s_before[6];
+    for (int i = 0; i < 6; ++i) s_before[i] = q->stats[i];
+    int rc = cost_grad_impl(q, dm[0] + s0 * NN, dm[1] + s0 * NN, dm[2] + s0 * NN, p->h_flat + s0 * 3 * ND,
+                            p->h_mask, drift ? p->h_drift : nullptr, p->h_sexp + s0 * se, lambda,
+                            p->h_cost + s0, dg[0] + s0 * NN, dg[1] + s0 * NN, dg[2] + s0 * NN, nullptr,
+                            p->h_status, st, nullptr, c == 0);
+    for (int i = 0; i < 6; ++i) p->stats[i] += q->stats[i] - s_before[i];
+    if (rc) return rc;
+    A(cudaEventRecord(p->h_cev[2 * c + 1], st));
+    A(cudaStreamWaitEvent(p->h_down, p->h_cev[2 * c + 1], 0));
+    A(cudaMemcpyAsync(cost + s0, p->h_cost + s0, sizeof(double) * sc, D2H, p->h_down));
+    for (int k = 0; k < 3; ++k)
+      A(cudaMemcpyAsync(hg[k] + s0 * NN, dg[k] + s0 * NN, sizeof(float) * sc * NN, D2H, p->h_down));
+  }
+  A(cudaMemcpyAsync(status, p->h_status, sizeof(int32_t) * 4, D2H, st));
+  A(cudaEventRecord(p->h_cev[2 * n], p->h_down));
+  A(cudaStreamWaitEvent(st, p->h_cev[2 * n], 0));
+  return e == cudaSuccess ? EI_OK : EI_ERR_CUDA;
+}
+
 // the host path's device work (uploads, K0..K3, downloads) enqueued on st (+ the copy stream)
 int enqueue_host_path(ei_plan *p, const float *mu, const float *delta, const float *sigma,
                       const float *flat, const float *mask, const float *drift, const float *s_exp,
@@ -583,6 +680,9 @@ int enqueue_host_path(ei_plan *p, const float *mu, const float *delta, const flo
                       int32_t *status, cudaStream_t st) {
   const size_t S = p->S, NN = (size_t)p->N * p->N, ND = p->ND, NA = p->NA, M = p->M;
   const size_t nsexp = S * NA * M * ND;
+  if (p->h_nchunk > 1)
+    return enqueue_host_chunked(p, mu, delta, sigma, flat, mask, drift, s_exp, lambda, cost, g_mu,
+                                g_delta, g_sigma, status, st);
   cudaError_t e = cudaSuccess;
   auto A = [&](cudaError_t r) { if (e == cudaSuccess) e = r; };
   const cudaMemcpyKind H2D = cudaMemcpyHostToDevice, D2H = cudaMemcpyDeviceToHost;
@@ -658,6 +758,7 @@ int ei_cost_grad_host(ei_plan *p, const float *mu, const float *delta, const flo
       return EI_ERR_RESOURCE;
     }
   }
+  if (p->h_nchunk == 0) setup_chunks(p);
   cudaStream_t st = (cudaStream_t)stream;
   // The whole call (12 copies, a memset, 4-5 kernels) is captured once into a CUDA graph on the
   // plan's work stream and replayed while the arguments stay the same: one launch instead of ~20

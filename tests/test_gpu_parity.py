@@ -483,3 +483,48 @@ def test_plan_matrix(ei, geom):
         for s in range(S):
             assert rel_l2(gq[s], ref[s]) <= 1e-3, (q, s, rel_l2(gq[s], ref[s]), ei.ei_plan_info(plan))
     assert list(st.cpu().numpy()[:3]) == list(rst)
+
+
+@pytest.mark.parametrize("chunks,n_pieces", [("3", 3), ("2", 2), ("1", 1)])
+def test_host_path_chunked_stack(ei, chunks, n_pieces, monkeypatch):
+    """Stacks: ei_cost_grad_host evaluates chunks of slices (sub-plans of the same geometry) so
+    the uploads, evaluations and downloads of different chunks overlap.  Bit-identical to the
+    device entry point on the same inputs (23 slices of C2's geometry in chunks of 8, 8, 7 or 12,
+    11: no K3 angle split, same K1 row split), status counts equal (the shared mask/drift scanned once), one K1 launch per
+    chunk; a non-finite s_exp element in slice 9 shows up in that slice's cost only."""
+    monkeypatch.setenv("EI_HOST_CHUNKS", chunks)
+    cfg = synth.with_slices(synth.CONFIGS["C2"], 23)
+    S, N = cfg.S, cfg.N
+    rng = np.random.default_rng(5)
+    sl, _ = synth.draw_slice(cfg, 0)
+    maps = [np.ascontiguousarray((np.broadcast_to(m * sc, (S, N, N)) *
+                                  (1 + 0.1 * rng.standard_normal((S, N, N)))).astype(np.float32))
+            for m, sc in ((sl.mu, 1.0), (sl.delta, 1.0), (sl.sigma, 1.0))]
+    flat = np.ascontiguousarray(np.broadcast_to(sl.flat, (S, 3, cfg.n_det))).astype(np.float32)
+    mask = cfg.mask.astype(np.float32)
+    drift = (0.002 * rng.standard_normal(cfg.n_angles)).astype(np.float32)
+    s_exp = (rng.random((S, cfg.n_angles, cfg.M, cfg.n_det)) * 2e4).astype(np.float32)
+    s_exp[9, 3, 1, 7] = np.nan
+    plan = plan_for(ei, cfg)
+    ws = ei.Workspace(plan)
+    cost_d, g_d, st_d = ei.cost_grad(plan, [dev(m) for m in maps], dev(flat), dev(mask), dev(drift),
+                                     dev(s_exp), 1e-2, ws)
+    torch.cuda.synchronize()
+    cost_d, g_d, st_d = cost_d.cpu().numpy(), [g.cpu().numpy() for g in g_d], st_d.cpu().numpy()
+
+    def pinned(a):
+        return torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
+
+    h_in = [pinned(m) for m in maps] + [pinned(flat), pinned(mask), pinned(drift), pinned(s_exp)]
+    for rep in range(2):   # the first call sets up the chunks (and captures the graph), then replay
+        cost = pinned(np.zeros(S))
+        gh = [pinned(np.zeros((S, N, N), np.float32)) for _ in range(3)]
+        st = pinned(np.zeros(4, np.int32))
+        s0 = ei.ei_plan_stats(plan)
+        ei.ei_cost_grad_host(plan, *h_in[:7], 1e-2, cost, *gh, st)
+        s1 = ei.ei_plan_stats(plan)
+        assert s1[0] - s0[0] == n_pieces, (s0, s1)
+        assert np.array_equal(cost, cost_d, equal_nan=True)
+        assert np.isnan(cost[9]) and np.all(np.isfinite(np.delete(cost, 9)))
+        assert all(np.array_equal(a, b, equal_nan=True) for a, b in zip(gh, g_d))
+        assert np.array_equal(st, st_d) and st[0] == 1

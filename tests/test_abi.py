@@ -94,3 +94,17 @@ def test_null_arguments_extended_entry_points(ei):
                                None) == 1
     lib.ei_plan_info.argtypes = [vp, vp]
     assert lib.ei_plan_info(None, None) == 1
+
+
+def test_binding_fails_loudly_without_library(tmp_path):
+    """No CPU fallback: the binding raises at import when libei.so is absent."""
+    import shutil
+    import subprocess
+    import sys
+    src = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_2202_08627_b200")
+    pkg = tmp_path / "nolib_pkg"
+    pkg.mkdir()
+    (pkg / "__init__.py").write_text("")
+    shutil.copy(os.path.join(src, "ei.py"), pkg / "ei.py")
+    r = subprocess.run([sys.executable, "-c", "import nolib_pkg.ei"], cwd=tmp_path, capture_output=True, text=True)
+    assert r.returncode != 0 and "ImportError" in r.stderr and "no CPU fallback" in r.stderr

@@ -88,6 +88,36 @@ def kernel_bytes(cfg, rsu, mirror_pairs=0):
             "K2_curve": float(S * NA * ND * (12 + 4 * M + 12) + S * ND * 12)}
 
 
+def kernel_bytes_h(cfg, rsu, mirror_pairs=0):
+    """The same for the single-map model (NEXT-3): K1/K3 gather 2 taps x 1 fp32 map (8 B) per
+    ray-sample update; K2 streams P_h (4 B) + s_exp (4M B) in and the G_h pair (8 B) out per
+    (s, theta, t), flat (12 B) per (s, t)."""
+    S, NA, ND, M = cfg.S, cfg.n_angles, cfg.n_det, cfg.M
+    share = (NA - mirror_pairs) / NA
+    return {"K1_project": 8.0 * rsu * S * share,
+            "K3_backproject": 8.0 * rsu * S * share,
+            "K2_curve": float(S * NA * ND * (4 + 4 * M + 8) + S * ND * 12)}
+
+
+def kernel_table(kb, kern_ms, n_rec, ms_step, sm_mhz, hbm_peak):
+    """Per-kernel time, share of the step and roofline fraction (K1/K3 against the shared-memory
+    data-pipe peak, K2 against HBM), and the dominant kernel."""
+    per_kernel_ms = {k: v / max(n_rec, 1) for k, v in kern_ms.items()}
+    l1_peak = 128.0 * 148 * sm_mhz * 1e6 / 1e9                       # GB/s, DESIGN.md §6
+    kernels = {}
+    for k in ("K1_project", "K2_curve", "K3_backproject"):
+        bound = "hbm" if k == "K2_curve" else "l1"
+        peak = hbm_peak if bound == "hbm" else l1_peak
+        ach = kb[k] / (per_kernel_ms[k] * 1e-3) / 1e9 if per_kernel_ms[k] > 0 else 0.0
+        kernels[k] = {"ms": round(per_kernel_ms[k], 5), "share": round(per_kernel_ms[k] / ms_step, 4),
+                      "bound": bound, "achieved": round(ach, 1), "peak": round(peak, 1), "unit": "GB/s",
+                      "frac": round(ach / peak, 4), "bytes_per_launch": kb[k]}
+    kernels["K0_pack"] = {"ms": round(per_kernel_ms["K0_pack"], 5),
+                          "share": round(per_kernel_ms["K0_pack"] / ms_step, 4)}
+    dom = max(("K1_project", "K2_curve", "K3_backproject"), key=lambda k: per_kernel_ms[k])
+    return kernels, dom
+
+
 # ---------------------------------------------------------------------------------------
 # clocks sampler (nvidia-smi during the timed region)
 # ---------------------------------------------------------------------------------------
@@ -303,21 +333,8 @@ def run_gpu(args, cfg, rank, world, local_rank):
     ms_step = ms / K
     rsu = ray_sample_updates(cfg)
     kb = kernel_bytes(cfg, rsu, plan_info.get("mirror_pairs", 0))
-    per_kernel_ms = {k: v / max(n_rec, 1) for k, v in kern_ms.items()}
-    dom = max(("K1_project", "K2_curve", "K3_backproject"), key=lambda k: per_kernel_ms[k])
     sm_mhz = clocks.get("sm_mhz") or peaks.get("sm_max_mhz", 1965.0)
-    l1_peak = 128.0 * 148 * sm_mhz * 1e6 / 1e9                       # GB/s, DESIGN.md §6
-    hbm_peak = peaks.get("hbm_gbs", 6650.0)
-    kernels = {}
-    for k in ("K1_project", "K2_curve", "K3_backproject"):
-        bound = "hbm" if k == "K2_curve" else "l1"
-        peak = hbm_peak if bound == "hbm" else l1_peak
-        ach = kb[k] / (per_kernel_ms[k] * 1e-3) / 1e9 if per_kernel_ms[k] > 0 else 0.0
-        kernels[k] = {"ms": round(per_kernel_ms[k], 5), "share": round(per_kernel_ms[k] / ms_step, 4),
-                      "bound": bound, "achieved": round(ach, 1), "peak": round(peak, 1), "unit": "GB/s",
-                      "frac": round(ach / peak, 4), "bytes_per_launch": kb[k]}
-    for k in ("K0_pack",):
-        kernels[k] = {"ms": round(per_kernel_ms[k], 5), "share": round(per_kernel_ms[k] / ms_step, 4)}
+    kernels, dom = kernel_table(kb, kern_ms, n_rec, ms_step, sm_mhz, peaks.get("hbm_gbs", 6650.0))
     d = kernels[dom]
     roofline = {"kernel": dom, "bound": d["bound"], "achieved": d["achieved"], "peak": d["peak"],
                 "unit": "GB/s", "frac": d["frac"], "traffic": load_traffic(cfg.name, dom)[0],
@@ -576,6 +593,18 @@ def run_gpu_h(args, cfg):
     sampler.stop()
     clocks = sampler.summary(t0, t1)
     rsu = ray_sample_updates(cfg)
+    peaks = load_peaks()
+    sm_mhz = clocks.get("sm_mhz") or peaks.get("sm_max_mhz", 1965.0)
+    kb = kernel_bytes_h(cfg, rsu, ei.ei_plan_info(plan).get("mirror_pairs", 0))
+    kernels, dom = kernel_table(kb, kern_ms, n_rec, ms_step, sm_mhz, peaks.get("hbm_gbs", 6650.0))
+    d = kernels[dom]
+    traffic, tsrc = load_traffic(cfg.name, dom)
+    roofline = {"kernel": dom, "bound": d["bound"], "achieved": d["achieved"], "peak": d["peak"],
+                "unit": "GB/s", "frac": d["frac"], "traffic": traffic,
+                "traffic_unit": "dram bytes per launch", "traffic_source": tsrc,
+                "peak_source": ("derived: 128 B/clk/SM x 148 SMs x median SM clock under load "
+                                "(%.0f MHz)" % sm_mhz) if d["bound"] == "l1" else
+                               "measured hbm_gbs (MEASURED_PEAKS.json)"}
     line = {
         "metric": "cost+gradient evals/sec (single-map model, eq. 4)", "value": round(1000.0 / ms_step, 3),
         "unit": UNIT, "n_gpus": 1, "steps": K, "warmup": args.warmup, "ms_per_step": round(ms_step, 5),
@@ -585,7 +614,7 @@ def run_gpu_h(args, cfg):
                    "mask_position": float(case.mask[0]),
                    "l2": "flushed before every timed step (256 MiB write, untimed)", "parallelism": "1 GPU"},
         "ray_sample_updates_per_s": round(2 * rsu * cfg.S / (ms_step * 1e-3), 1),
-        "kernels_ms": {k: round(v / max(n_rec, 1), 5) for k, v in kern_ms.items() if v > 0},
+        "roofline": roofline, "kernels": kernels,
         "gpu_launches": int(s1[5] - s0[5]), "clocks": clocks, "status": st.cpu().numpy().tolist(),
         "paper_context": PAPER_CONTEXT, "input_gen_s": round(t_gen, 2),
     }

@@ -21,7 +21,9 @@ for c in ["C1", "C2", "C3", "C4", "C5"]:
         k["K1_project"]["frac"], k["K2_curve"]["frac"], k["K3_backproject"]["frac"],
         d["cpu_baseline"]["value"], d["cpu_baseline"]["cores"]))
 p1 = line("P1")
-rows.append("| P1 (single-map model, paper geometry) | %.1f µs | %.0f | %.2f T | — | — | %.3g (%d) |" % (
-    p1["ms_per_step"] * 1000, p1["value"], p1["ray_sample_updates_per_s"] / 1e12, p1["cpu_baseline"]["value"],
+k = p1.get("kernels")   # the single-map line has no host-buffer (e2e) leg
+fr = "%.2f / %.2f / %.2f" % tuple(k[n]["frac"] for n in ("K1_project", "K2_curve", "K3_backproject")) if k else "—"
+rows.append("| P1 (single-map model, paper geometry) | %.1f µs | %.0f | %.2f T | — | %s | %.3g (%d) |" % (
+    p1["ms_per_step"] * 1000, p1["value"], p1["ray_sample_updates_per_s"] / 1e12, fr, p1["cpu_baseline"]["value"],
     p1["cpu_baseline"]["cores"]))
 print("\n".join(rows))

@@ -485,15 +485,20 @@ def test_plan_matrix(ei, geom):
     assert list(st.cpu().numpy()[:3]) == list(rst)
 
 
+@pytest.mark.parametrize("span", [180.0, 360.0])
 @pytest.mark.parametrize("chunks,n_pieces", [("3", 3), ("2", 2), ("1", 1)])
-def test_host_path_chunked_stack(ei, chunks, n_pieces, monkeypatch):
+def test_host_path_chunked_stack(ei, chunks, n_pieces, span, monkeypatch):
     """Stacks: ei_cost_grad_host evaluates chunks of slices (sub-plans of the same geometry) so
     the uploads, evaluations and downloads of different chunks overlap.  Bit-identical to the
     device entry point on the same inputs (23 slices of C2's geometry in chunks of 8, 8, 7 or 12,
     11: no K3 angle split, same K1 row split), status counts equal (the shared mask/drift scanned once), one K1 launch per
-    chunk; a non-finite s_exp element in slice 9 shows up in that slice's cost only."""
+    chunk; a non-finite s_exp element in slice 9 shows up in that slice's cost only.  The 360-degree
+    variant (240 angles: 120 mirror pairs, folded before K3) runs the same checks."""
     monkeypatch.setenv("EI_HOST_CHUNKS", chunks)
     cfg = synth.with_slices(synth.CONFIGS["C2"], 23)
+    if span == 360.0:
+        import dataclasses
+        cfg = dataclasses.replace(cfg, span_deg=360.0, n_angles=240)
     S, N = cfg.S, cfg.N
     rng = np.random.default_rng(5)
     sl, _ = synth.draw_slice(cfg, 0)
@@ -506,6 +511,7 @@ def test_host_path_chunked_stack(ei, chunks, n_pieces, monkeypatch):
     s_exp = (rng.random((S, cfg.n_angles, cfg.M, cfg.n_det)) * 2e4).astype(np.float32)
     s_exp[9, 3, 1, 7] = np.nan
     plan = plan_for(ei, cfg)
+    assert ei.ei_plan_info(plan)["mirror_pairs"] == (120 if span == 360.0 else 0)
     ws = ei.Workspace(plan)
     cost_d, g_d, st_d = ei.cost_grad(plan, [dev(m) for m in maps], dev(flat), dev(mask), dev(drift),
                                      dev(s_exp), 1e-2, ws)

@@ -1,10 +1,12 @@
 #!/usr/bin/env python
 """Benchmark of the EI cost+gradient hot path (one `ei_cost_grad` = one step).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4] [--impl ours|reference]
 
-Workload: BASELINE.json configs[1] (C2: 256x256 slice, 360 angles, 384 detector pixels, M=7)
-by default; --config C1..C5 selects another (C4 = 64-slice stack).  Inputs are synthetic
+Workload: BASELINE.json configs[3] (C4: a stack of 64 slices of 512x512, 720 angles over 180 deg,
+768 detector pixels, M=7, per-angle mask drift) by default -- the largest configuration that
+fits one GPU (991 MB of measured curves, 65.4 G ray-sample updates per evaluation); --config
+C1..C5 selects another (C2 is the small latency-bound slice, C1 the oracle-sized case).  Inputs are synthetic
 (paper_2202_08627_b200.synth), resident in HBM before the timed region; L2 is flushed
 (256 MiB write, untimed) before every timed step.  Each step is timed with CUDA events on
 the launching stream; per-kernel times come from events the library records around its own
@@ -55,6 +57,25 @@ def load_peaks():
         return {}
 
 
+ONCHIP_PEAKS = os.path.join("profiles", "r02", "peaks.json")
+
+
+def onchip_peak(sm_mhz):
+    """K1/K3 roofline peak: the shared-memory (LDS.128) bandwidth MEASURED on a B200 of this pool
+    by tools/microbench.cu (tools/measure_peaks.py -> profiles/r02/peaks.json, with the SM clock
+    seen during that measurement), scaled to this run's median SM clock.  Falls back to the
+    guide's unit count (128 B/clk/SM x 148 SMs x clock) only if the file is missing."""
+    try:
+        d = json.load(open(os.path.join(ROOT, ONCHIP_PEAKS)))
+        mhz0 = (d.get("clocks") or {}).get("sm_mhz") or sm_mhz
+        peak = d["smem_lds128_gbs"] * sm_mhz / mhz0
+        return peak, ("measured: LDS.128 %.0f GB/s at %.0f MHz (%s), x %.0f/%.0f MHz this run"
+                      % (d["smem_lds128_gbs"], mhz0, ONCHIP_PEAKS, sm_mhz, mhz0))
+    except Exception:
+        return (128.0 * 148 * sm_mhz * 1e6 / 1e9,
+                "derived (no measured file): 128 B/clk/SM x 148 SMs x %.0f MHz" % sm_mhz)
+
+
 # ---------------------------------------------------------------------------------------
 # algorithmic counts (DESIGN.md §6)
 # ---------------------------------------------------------------------------------------
@@ -103,7 +124,7 @@ def kernel_table(kb, kern_ms, n_rec, ms_step, sm_mhz, hbm_peak):
     """Per-kernel time, share of the step and roofline fraction (K1/K3 against the shared-memory
     data-pipe peak, K2 against HBM), and the dominant kernel."""
     per_kernel_ms = {k: v / max(n_rec, 1) for k, v in kern_ms.items()}
-    l1_peak = 128.0 * 148 * sm_mhz * 1e6 / 1e9                       # GB/s, DESIGN.md §6
+    l1_peak, _ = onchip_peak(sm_mhz)                                  # GB/s, DESIGN.md §6
     kernels = {}
     for k in ("K1_project", "K2_curve", "K3_backproject"):
         bound = "hbm" if k == "K2_curve" else "l1"
@@ -339,8 +360,7 @@ def run_gpu(args, cfg, rank, world, local_rank):
     roofline = {"kernel": dom, "bound": d["bound"], "achieved": d["achieved"], "peak": d["peak"],
                 "unit": "GB/s", "frac": d["frac"], "traffic": load_traffic(cfg.name, dom)[0],
                 "traffic_unit": "dram bytes per launch", "traffic_source": load_traffic(cfg.name, dom)[1],
-                "peak_source": ("derived: 128 B/clk/SM x 148 SMs x median SM clock under load "
-                                "(%.0f MHz)" % sm_mhz) if d["bound"] == "l1" else
+                "peak_source": onchip_peak(sm_mhz)[1] if d["bound"] == "l1" else
                                "measured hbm_gbs (MEASURED_PEAKS.json)"}
     value = world * 1000.0 / ms_step
     line = {
@@ -351,7 +371,13 @@ def run_gpu(args, cfg, rank, world, local_rank):
                    "lambda": lam, "eval_point": "x_pert (R21)",
                    "l2": "flushed before every timed step (256 MiB write, untimed)",
                    "parallelism": "slice-parallel replicas" if world > 1 else "1 GPU"},
+        # SURVEY §8(d) counts every angle's samples ("effective"); with mirror pairs (360-degree
+        # scans) K1/K3 execute only the primaries' samples ("executed")
         "ray_sample_updates_per_s": round(world * 6 * rsu * cfg.S / (ms_step * 1e-3), 1),
+        "ray_sample_updates_per_s_kind": "effective (every angle counted)" if plan_info.get("mirror_pairs", 0)
+                                         else "executed (= effective: no mirror pairs)",
+        "ray_sample_updates_per_s_executed": round(world * 6 * rsu * cfg.S * (cfg.n_angles - plan_info.get(
+            "mirror_pairs", 0)) / cfg.n_angles / (ms_step * 1e-3), 1),
         "slice_evals_per_s": round(world * cfg.S * 1000.0 / ms_step, 3),
         "ray_sample_updates_per_eval": 6 * rsu * cfg.S,
         "roofline": roofline, "kernels": kernels,
@@ -602,8 +628,7 @@ def run_gpu_h(args, cfg):
     roofline = {"kernel": dom, "bound": d["bound"], "achieved": d["achieved"], "peak": d["peak"],
                 "unit": "GB/s", "frac": d["frac"], "traffic": traffic,
                 "traffic_unit": "dram bytes per launch", "traffic_source": tsrc,
-                "peak_source": ("derived: 128 B/clk/SM x 148 SMs x median SM clock under load "
-                                "(%.0f MHz)" % sm_mhz) if d["bound"] == "l1" else
+                "peak_source": onchip_peak(sm_mhz)[1] if d["bound"] == "l1" else
                                "measured hbm_gbs (MEASURED_PEAKS.json)"}
     line = {
         "metric": "cost+gradient evals/sec (single-map model, eq. 4)", "value": round(1000.0 / ms_step, 3),
@@ -639,7 +664,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="C2", choices=sorted(synth.CONFIGS) + sorted(synth.H_CONFIGS),
+    ap.add_argument("--config", default="C4", choices=sorted(synth.CONFIGS) + sorted(synth.H_CONFIGS),
                     help="C1-C5: three-map model (BASELINE.json configs); P1: the paper's single-map "
                          "model on its own scan geometry (context line)")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])

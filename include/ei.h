@@ -152,8 +152,10 @@ int ei_cost_grad_hs(const ei_plan *plan, const float *h, float gamma, const floa
  * queued on `stream` and runs on the plan's own streams: the maps/flat/mask/drift upload first,
  * the s_exp upload (the bulk of the bytes) on a copy stream overlapping K0/K1 (K2 waits for it).
  * With pinned host memory the whole call is captured once into a CUDA graph and replayed while
- * the 13 pointers and lambda stay the same (one launch instead of ~20 API calls; env
- * EI_HOST_GRAPH=0 disables; pageable memory falls back to direct calls).  Stacks (>= 8 slices)
+ * the 13 pointers and lambda stay the same and every host buffer is still page-locked (checked
+ * with cudaPointerGetAttributes on each call; one launch instead of ~20 API calls; env
+ * EI_HOST_GRAPH=0 disables; pageable memory, or arguments whose capture failed, take direct
+ * calls).  Stacks (>= 8 slices)
  * run in chunks of slices (up to 8; env EI_HOST_CHUNKS=K, 1 disables), each evaluated by an
  * internal sub-plan of the same geometry, so chunk c's upload, chunk c-1's evaluation and the
  * downloads of earlier chunks overlap (C4: 34.5 -> 25.7 ms per call); chunking is used only when
@@ -183,7 +185,9 @@ int ei_plan_read_timing(ei_plan *plan, double ms[6], int *n_evals);
 
 /* Launch-plan diagnostics (synchronous: reads a device counter).  out[0] = K1 angle groups,
  * out[1] = K1 rows per staged chunk, out[2] = K1 window-width bound (entries), out[3] = K1 row
- * split of the cost path, out[4] = internal window overflows seen so far (must be 0),
+ * split of the cost path, out[4] = staged-window overflows seen so far (must be 0: K1 checks the
+ * first and last row of every staged chunk, where its taps are extreme; -DEI_CHECK builds also
+ * check every K3 tap),
  * out[5] = K1 dynamic shared memory per CTA (bytes), out[6] = K1 angle groups using the
  * ray-fastest lane mapping, out[7] = K3 angle split (most parts of one tile), out[8] = mirror angle pairs (theta,
  * theta + pi) of a 360-degree scan projected and back-projected once (env EI_MIRROR=0 at plan

@@ -93,7 +93,7 @@ struct ei_plan {
   float2 *GB = nullptr;       // [S][NA][RpG]
   float2 *GA1 = nullptr;      // [S][NA][RpG]  single-map pairs (ei_backproject n_maps=1)
   int PADG = 0, RpG = 0;
-  float *part_curve = nullptr;   // [S][NA][nseg][nw] per-warp cost partials (K2)
+  double *part_curve = nullptr;  // [S][NA][nseg][nw] per-warp cost partials (K2, fp64)
   float *part_mo = nullptr;      // [S][NA][nseg][nw] per-warp dS/dm_o partials (K2, NEXT-2)
   double *part_reg = nullptr;    // [S][RB] per-tile sum x^2 partials (K0)
   float *part3 = nullptr;        // [KS][S][3][N][N] K3 angle-split partial gradients
@@ -122,7 +122,8 @@ struct ei_plan {
   cudaGraphExec_t h_exec = nullptr;         // captured host path, replayed for the same arguments
   HostKey h_key{};
   int64_t h_stats[6] = {0, 0, 0, 0, 0, 0};  // launch accounting of one captured call
-  bool h_graph_failed = false;
+  HostKey h_fail_key{};         // arguments whose graph capture failed (direct path for them)
+  bool h_graph_failed = false;  // h_fail_key is set
   // stacks: the host path runs in chunks of slices (sub-plans of h_Sc and of the last chunk's
   // slice count) so uploads, evaluation and downloads of different chunks overlap
   std::vector<double> angles;               // host copy (sub-plan creation)

@@ -53,17 +53,6 @@ constexpr int NT = 256;     // consumer threads (+ one producer warp)
 constexpr int NST = 3;      // ring stages
 constexpr int WLB = WL + 2; // 8-byte-entry rows: 16-B aligned copy start needs one spare entry
 
-__device__ __forceinline__ void cp_async(void *smem, const void *gmem, int bytes, bool valid) {
-  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  if (bytes == 16)
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(valid ? 16 : 0));
-  else
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(valid ? 8 : 0));
-}
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
-
 template <int NMAP>
 struct Layout;
 template <>
@@ -99,12 +88,14 @@ __device__ __forceinline__ unsigned long long gtimer3() {
 #endif
 
 struct FinArgs {
-  const float *part_cost, *part_mo;   // K2 per-warp partials [S][NA][nseg * nw]
+  const double *part_cost;            // K2 per-warp partials [S][NA][nseg * nw]
+  const float *part_mo;
   const double *part_reg;
   int per_slice, nseg, NA, RB;   // per_slice = NA * nseg * nw, nseg here = nseg * nw
   double lambda;
   double *cost;                  // NULL: no finalize (ei_backproject)
   float *g_drift;                // [S][NA] or NULL
+  int *diag;                     // -DEI_CHECK builds: staged-window overflows (ei_plan_info out[4])
 };
 
 // consumer threads only (named barrier 1, NT threads); fixed order: per-thread strided fp64 sums,
@@ -115,16 +106,16 @@ __device__ __forceinline__ void finalize(const FinArgs &f, int s, int tid) {
   // in the same strided order as a plain loop: q = tid, tid + NT, ...
   constexpr int UF = 8;
   double c = 0.0, rg = 0.0;
-  const float *pc = f.part_cost + (size_t)s * f.per_slice;
+  const double *pc = f.part_cost + (size_t)s * f.per_slice;
   int q = tid;
   for (; q + (UF - 1) * NT < f.per_slice; q += UF * NT) {
-    float v[UF];
+    double v[UF];
 #pragma unroll
     for (int u = 0; u < UF; ++u) v[u] = __ldcg(pc + q + u * NT);
 #pragma unroll
-    for (int u = 0; u < UF; ++u) c += (double)v[u];
+    for (int u = 0; u < UF; ++u) c += v[u];
   }
-  for (; q < f.per_slice; q += NT) c += (double)__ldcg(pc + q);
+  for (; q < f.per_slice; q += NT) c += __ldcg(pc + q);
   if (f.lambda > 0.0)
     for (int b = tid; b < f.RB; b += NT) rg += __ldcg(f.part_reg + (size_t)s * f.RB + b);
   double v = c + f.lambda * rg;
@@ -287,6 +278,10 @@ SPAN_START_bp();
         // tent weights of the pair (k0, k0+1); G was pre-scaled by dx/|c_dom| in K2, so each
         // weight is one saturating FMA: max(0, 1 - |k - k*|/h) with |k - k*|/h <= 1/h
         const float2 wt = make_float2(__saturatef(fmaf(-fr, t.z, 1.f)), __saturatef(fmaf(fr, t.z, t.w)));
+#ifdef EI_CHECK
+        // debug build: the pair (k0, k0+1) lies inside the staged window of WL entries
+        if (k0 < 0 || k0 + 1 >= WL) atomicAdd(fin.diag, 1);
+#endif
         const TA ga = arow[k0];
         if constexpr (NMAP == 3) {
           am[q] = __ffma2_rn(wt, make_float2(ga.x, ga.y), am[q]);
@@ -415,6 +410,7 @@ cudaError_t launch_bp(const ei_plan &p, const typename Layout<NMAP>::A *GA, cons
                       float *o0, float *o1, float *o2, size_t out_stride, const Finalize *fz,
                       cudaStream_t st) {
   FinArgs fin{};
+  fin.diag = p.diag;
   if (fz) {
     fin.part_cost = p.part_curve;
     fin.part_mo = p.part_mo;

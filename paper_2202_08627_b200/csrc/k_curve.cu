@@ -28,8 +28,8 @@
 //  * per item one consumer barrier: the g values go to a double-buffered shared row, each thread
 //    reads its neighbours' float4s for D^T and writes its 4 gradient entries directly in K3's PAIR
 //    layout (entry e = (g[e-1], g[e]) of every map, pre-multiplied by the Joseph weight);
-//  * cost and drift-gradient partials: fp32 per thread and per warp (shuffle) -> one partial per
-//    (item, warp); K3 sums them in fp64 in index order (fused finalize, K4).
+//  * cost partials: fp32 per thread, fp64 per warp (shuffle) -> one partial per (item, warp);
+//    drift-gradient partials fp32 per warp; K3 sums both in fp64 in index order (fused K4).
 // Deterministic: no float atomics, fixed reduction order, results independent of the grid size.
 #include <stdint.h>
 #include <stdlib.h>
@@ -105,7 +105,8 @@ struct K2Args {
   float2 *GA1;               // MODES 2, 4: pair-layout gradient sinogram of h
   int PADG, RpG;
   const float4 *k3;          // per-angle table, .w = Joseph weight dx/|c_dom|
-  float *part_cost, *part_mo;    // [S * NA * nseg * nw] per-warp partials
+  double *part_cost;         // [S * NA * nseg * nw] per-warp cost partials (fp64)
+  float *part_mo;            // [S * NA * nseg * nw] per-warp drift-gradient partials
   int32_t *status;
   int items;                 // S * NA * nseg
 };
@@ -133,6 +134,10 @@ struct Pos {
 };
 
 __device__ __forceinline__ float warp_sum(float v) {
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+  return v;
+}
+__device__ __forceinline__ double warp_sum(double v) {
   for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
   return v;
 }
@@ -501,8 +506,11 @@ __global__ void __launch_bounds__(K2_MAXT + 32, 2) curve_kernel(K2Args g) {
         if (k0 == 0) xd[-1] = -2.f * gd4.x;
         if (jl == J - 1) xd[ND] = -2.f * gd4.w;
       }
-      // cost and dS/dm_o partials: fp32 per thread and per warp, fp64 over items/warps in K3
-      const float wc_ = warp_sum(cost);
+      // cost partials: fp32 over one thread's 4 positions x M mask positions, fp64 from the warp
+      // sum on (so the evaluated cost resolves relative changes far below fp32's 6e-8 x the
+      // number of terms: an optimizer's line search compares costs); dS/dm_o partials fp32 per
+      // warp; both summed in fp64 over items/warps by K3's finalize
+      const double wc_ = warp_sum((double)cost);
       const float wm_ = warp_sum(gmo);
       if (lane == 0) {   // per-warp partials, (s, a, seg, warp) order
         const int pidx = ((s * g.NA + a) * g.nseg + seg) * nw + wid;

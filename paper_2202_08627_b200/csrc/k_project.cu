@@ -35,17 +35,6 @@ constexpr int AGB = 16;   // angles per CTA
 constexpr int RT = 64;    // rays per CTA (RTS = 32 for small single-wave grids, plan_projector)
 constexpr int RTS = 32;
 
-__device__ __forceinline__ void cp_async(void *smem, const void *gmem, int bytes, bool valid) {
-  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  if (bytes == 16)
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(valid ? 16 : 0));
-  else
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(s), "l"(gmem), "r"(valid ? 8 : 0));
-}
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
-
 template <int NMAP>
 struct PL;
 
@@ -73,6 +62,7 @@ struct ProjArgs {
   int nst;                      // ring stages (<= NSTMAX)
   int has_pairs;                // the plan paired mirror angles (else partner[] is all -1)
   float *P;                     // [RS][S][NMAP][NA][ND]
+  int *diag;                    // window overflows (ei_plan_info out[4]; must stay 0)
 };
 
 #ifdef EI_TRACE
@@ -261,6 +251,20 @@ SPAN_START_proj();
       all &= (wlo[m] <= i0 && whi[m] >= i1);
     }
     if (wn.y > 0 && any) {
+      // staged-window check (the counter behind ei_plan_info out[4]): x* is linear in the row
+      // and fmaf / floor are monotone, so every row's tap of a slot lies in the staged entries
+      // [wn.x, wn.x + wn.y) iff the chunk's first and last rows' taps do
+      {
+        const float ya = (float)i0 - ctr, yb = (float)i1 - ctr;
+        bool bad = false;
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+          const int ja = __float2int_rd(fmaf(-tn[m], ya, alpha[m]));
+          const int jb = __float2int_rd(fmaf(-tn[m], yb, alpha[m]));
+          bad |= min(ja, jb) < wn.x || max(ja, jb) >= wn.x + wn.y;
+        }
+        if (bad) atomicAdd(args.diag, 1);
+      }
       const int bofs = (wn.x + 1) & 1;
       const TA *arow = sA + st * RC * CWA - wn.x + (A8 ? bofs : 0);
       const float2 *brow = sB + st * RC * CWB - wn.x + bofs;
@@ -358,6 +362,7 @@ cudaError_t launch(const ei_plan &p, int RS, float *P, cudaStream_t st) {
   a.PAD = p.proj.PAD; a.Rp = p.proj.Rp;
   a.nch = RS == 1 ? p.proj.nch1 : p.proj.nchRS;
   a.P = P;
+  a.diag = p.diag;
   a.nst = p.proj.nst;
   const size_t smem = NMAP == 3 ? (size_t)a.nst * p.proj.RC * (p.proj.CW * 16 + (p.proj.CW + 2) * 8)
                                  : (size_t)a.nst * p.proj.RC * (p.proj.CW + 2) * 8;

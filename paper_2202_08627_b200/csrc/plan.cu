@@ -767,7 +767,21 @@ int ei_cost_grad_host(ei_plan *p, const float *mu, const float *delta, const flo
   // buffers (not capturable), the timing mode and EI_HOST_GRAPH=0 take the direct path.
   const HostKey key{mu, delta, sigma, flat, mask, drift, s_exp, lambda, cost, g_mu, g_delta, g_sigma, status};
   const char *genv = getenv("EI_HOST_GRAPH");
-  const bool use_graph = !p->tev && !(genv && atoi(genv) == 0) && !p->h_graph_failed;
+  // The graph replays DMAs from these exact host addresses, so it is used only while every host
+  // buffer is page-locked right now (checked on every call: a freed pinned buffer whose address
+  // comes back as pageable memory must not be replayed), and a failed capture disables it only
+  // for the arguments that failed
+  bool pinned = true;
+  for (const void *h : {(const void *)mu, (const void *)delta, (const void *)sigma, (const void *)flat,
+                        (const void *)mask, (const void *)drift, (const void *)s_exp, (const void *)cost,
+                        (const void *)g_mu, (const void *)g_delta, (const void *)g_sigma, (const void *)status}) {
+    if (!h) continue;
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, h) != cudaSuccess || at.type != cudaMemoryTypeHost) pinned = false;
+  }
+  cudaGetLastError();
+  const bool use_graph = !p->tev && !(genv && atoi(genv) == 0) && pinned &&
+                         !(p->h_graph_failed && p->h_fail_key == key);
   if (use_graph) {
     cudaError_t e = cudaEventRecord(p->h_ev[2], st);
     if (e == cudaSuccess) e = cudaStreamWaitEvent(p->h_work, p->h_ev[2], 0);
@@ -794,7 +808,8 @@ int ei_cost_grad_host(ei_plan *p, const float *mu, const float *delta, const flo
         p->h_key = key;
       } else {
         p->h_exec = nullptr;
-        p->h_graph_failed = true;   // e.g. pageable host memory: direct path from now on
+        p->h_graph_failed = true;   // direct path for these arguments
+        p->h_fail_key = key;
       }
       if (graph) cudaGraphDestroy(graph);
       cudaGetLastError();

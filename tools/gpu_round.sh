@@ -1,10 +1,11 @@
 #!/bin/bash
 # One GPU-box pass: parity tests, smoke, bench lines for every config, ncu launch list of the
 # default bench command and one `--set full` capture of K1/K3/K2.  Usage (under gpurun):
-#   bash tools/gpu_round.sh TAG [what...]     what ⊂ {tests smoke bench ncu full}
+#   bash tools/gpu_round.sh TAG [what...]     what ⊂ {tests smoke bench ref ncu full peaks}
 set -u
 TAG=${1:-run}; shift || true
 WHAT=${*:-tests smoke bench ncu full}
+BENCH_CFGS=${BENCH_CFGS:-C4 C2 C1 C3 C5 P1}
 OUT=gpurun_out/$TAG
 mkdir -p $OUT
 python -c "import __graft_entry__ as g; g.build()" > $OUT/build.log 2>&1 || { echo build failed; tail $OUT/build.log; exit 1; }
@@ -19,7 +20,7 @@ for w in $WHAT; do
       timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $OUT/smoke.log 2>&1; echo "smoke rc=$?" | tee -a $OUT/rc.txt
       tail -1 $OUT/smoke.log ;;
     bench)
-      for c in C2 C1 C3 C5 C4 P1; do
+      for c in $BENCH_CFGS; do
         timeout 600 python bench.py --config $c > $OUT/bench_$c.json 2> $OUT/bench_$c.err; echo "bench $c rc=$?" | tee -a $OUT/rc.txt
         python - $OUT/bench_$c.json <<'EOF'
 import json, sys
@@ -35,6 +36,9 @@ EOF
     ref)
       timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > $OUT/bench_ref.json 2> $OUT/bench_ref.err; echo "ref rc=$?" | tee -a $OUT/rc.txt
       tail -c 600 $OUT/bench_ref.json ;;
+    peaks)
+      timeout 600 python tools/measure_peaks.py $OUT/peaks.json > $OUT/peaks.log 2>&1; echo "peaks rc=$?" | tee -a $OUT/rc.txt
+      tail -c 400 $OUT/peaks.json ;;
     ncu)
       timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
         --log-file $OUT/launches.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline > $OUT/ncu_launch.log 2>&1

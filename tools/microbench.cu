@@ -1,6 +1,10 @@
-// tools/microbench.cu — measures the on-chip roofline denominators used in DESIGN.md §6 on
-// the B200 box: L2 read bandwidth (L2-resident buffer), shared-memory LDS.128 bandwidth, and
-// HBM read bandwidth (buffer >> L2).  Prints one JSON line.  Not part of libei.
+// tools/microbench.cu — measures the on-chip roofline denominators used by bench.py for K1/K3
+// on the B200 box: shared-memory LDS.128 and LDS.64 bandwidth (conflict-free,
+// every lane a distinct address), L2 read bandwidth (L2-resident 48 MB buffer) and HBM read
+// bandwidth (4 GiB buffer >> L2).  Each figure is the best of 5 timed launches of ~0.1-1 s
+// (CUDA events).  Prints one JSON line; tools/measure_peaks.py runs it under an nvidia-smi
+// clock sampler and writes profiles/r02/peaks.json.  Not part of libei.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/microbench tools/microbench.cu
 #include <cstdio>
 #include <cuda_runtime.h>
 
@@ -14,50 +18,84 @@ __global__ void read_kernel(const float4* __restrict__ p, size_t n, int passes, 
   if (acc.x + acc.y + acc.z + acc.w == 1234.5f) out[0] = acc.x;
 }
 
+// T = float4 (LDS.128) or float2 (LDS.64): lane l of a warp reads element (base + l) — a quarter
+// (LDS.128) or half (LDS.64) warp covers 128 contiguous bytes, one wavefront each
+template <typename T>
 __global__ void smem_kernel(int iters, float* out) {
-  __shared__ float4 buf[2048];
-  for (int i = threadIdx.x; i < 2048; i += blockDim.x) buf[i] = make_float4(i, i, i, i);
+  __shared__ T buf[2048];
+  float* f = reinterpret_cast<float*>(buf);
+  for (int i = threadIdx.x; i < 2048 * (int)(sizeof(T) / 4); i += blockDim.x) f[i] = (float)i;
   __syncthreads();
-  float4 acc = make_float4(0, 0, 0, 0);
+  T acc;
+  float* a = reinterpret_cast<float*>(&acc);
+  for (int q = 0; q < (int)(sizeof(T) / 4); ++q) a[q] = 0.f;
   int idx = threadIdx.x;
   for (int it = 0; it < iters; ++it) {
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
-      float4 v = buf[(idx + u * 256) & 2047];
-      acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+      T v = buf[(idx + u * 256) & 2047];
+      const float* b = reinterpret_cast<const float*>(&v);
+#pragma unroll
+      for (int q = 0; q < (int)(sizeof(T) / 4); ++q) a[q] += b[q];
     }
     idx += 32;
   }
-  if (acc.x + acc.y + acc.z + acc.w == 1234.5f) out[0] = acc.x;
+  float s = 0.f;
+  for (int q = 0; q < (int)(sizeof(T) / 4); ++q) s += a[q];
+  if (s == 1234.5f) out[0] = s;
+}
+
+template <typename F>
+static double best_ms(F launch, int reps = 5) {
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  launch();   // warm-up
+  double best = 1e30;
+  for (int r = 0; r < reps; ++r) {
+    float ms;
+    cudaEventRecord(a);
+    launch();
+    cudaEventRecord(b);
+    cudaEventSynchronize(b);
+    cudaEventElapsedTime(&ms, a, b);
+    if (ms < best) best = ms;
+  }
+  return best;
 }
 
 int main() {
-  int dev = 0; cudaDeviceProp prop; cudaGetDeviceProperties(&prop, dev);
-  int clk_khz = 0; cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, dev);
-  float* out; cudaMalloc(&out, 4);
-  cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
-  float ms;
-  // L2: 48 MB resident buffer, read many passes
-  size_t n2 = 48ull << 20; float4* p2; cudaMalloc(&p2, n2); cudaMemset(p2, 0, n2);
-  int grid = prop.multiProcessorCount * 8;
-  read_kernel<<<grid, 256>>>(p2, n2 / 16, 2, out);
-  cudaEventRecord(a); read_kernel<<<grid, 256>>>(p2, n2 / 16, 40, out); cudaEventRecord(b);
-  cudaEventSynchronize(b); cudaEventElapsedTime(&ms, a, b);
-  double l2 = 40.0 * n2 / (ms * 1e-3) / 1e9;
-  // HBM: 4 GB buffer, one pass
-  size_t nh = 4ull << 30; float4* ph; cudaMalloc(&ph, nh); cudaMemset(ph, 0, nh);
-  read_kernel<<<grid, 256>>>(ph, nh / 16, 1, out);
-  cudaEventRecord(a); read_kernel<<<grid, 256>>>(ph, nh / 16, 2, out); cudaEventRecord(b);
-  cudaEventSynchronize(b); cudaEventElapsedTime(&ms, a, b);
-  double hbm = 2.0 * nh / (ms * 1e-3) / 1e9;
-  // SMEM: LDS.128, conflict-free, 8 blocks x 256 threads per SM
-  int iters = 20000;
-  smem_kernel<<<prop.multiProcessorCount * 4, 256>>>(10, out);
-  cudaEventRecord(a); smem_kernel<<<prop.multiProcessorCount * 4, 256>>>(iters, out); cudaEventRecord(b);
-  cudaEventSynchronize(b); cudaEventElapsedTime(&ms, a, b);
-  double sm_bytes = (double)prop.multiProcessorCount * 4 * 256 * iters * 8 * 16;
-  double smem = sm_bytes / (ms * 1e-3) / 1e9;
-  printf("{\"l2_read_gbs\": %.1f, \"hbm_read_gbs\": %.1f, \"smem_lds128_gbs\": %.1f, \"sms\": %d, \"clock_khz_attr\": %d}\n",
-         l2, hbm, smem, prop.multiProcessorCount, clk_khz);
-  return 0;
+  int dev = 0;
+  cudaDeviceProp prop;
+  cudaGetDeviceProperties(&prop, dev);
+  const int sms = prop.multiProcessorCount;
+  float* out;
+  cudaMalloc(&out, 4);
+  // L2: 48 MB resident buffer (fits either die's half of the 126 MB L2), 40 passes per launch
+  const size_t n2 = 48ull << 20;
+  float4* p2;
+  cudaMalloc(&p2, n2);
+  cudaMemset(p2, 0, n2);
+  const int grid = sms * 8;
+  double ms = best_ms([&] { read_kernel<<<grid, 256>>>(p2, n2 / 16, 40, out); });
+  const double l2 = 40.0 * n2 / (ms * 1e-3) / 1e9;
+  // HBM: 4 GiB buffer, 8 passes per launch
+  const size_t nh = 4ull << 30;
+  float4* ph;
+  cudaMalloc(&ph, nh);
+  cudaMemset(ph, 0, nh);
+  ms = best_ms([&] { read_kernel<<<grid, 256>>>(ph, nh / 16, 8, out); });
+  const double hbm = 8.0 * nh / (ms * 1e-3) / 1e9;
+  // SMEM: 4 CTAs x 256 threads per SM, 8 loads per iteration
+  const int iters = 20000;
+  const double nload = (double)sms * 4 * 256 * iters * 8;
+  ms = best_ms([&] { smem_kernel<float4><<<sms * 4, 256>>>(iters, out); });
+  const double lds128 = nload * 16 / (ms * 1e-3) / 1e9;
+  ms = best_ms([&] { smem_kernel<float2><<<sms * 4, 256>>>(iters, out); });
+  const double lds64 = nload * 8 / (ms * 1e-3) / 1e9;
+  const cudaError_t e = cudaDeviceSynchronize();
+  printf("{\"l2_read_gbs\": %.1f, \"hbm_read_gbs\": %.1f, \"smem_lds128_gbs\": %.1f, "
+         "\"smem_lds64_gbs\": %.1f, \"sms\": %d, \"cuda\": \"%s\"}\n",
+         l2, hbm, lds128, lds64, sms, cudaGetErrorString(e));
+  return e == cudaSuccess ? 0 : 1;
 }

@@ -67,7 +67,7 @@ def onchip_peak(sm_mhz):
     guide's unit count (128 B/clk/SM x 148 SMs x clock) only if the file is missing."""
     try:
         d = json.load(open(os.path.join(ROOT, ONCHIP_PEAKS)))
-        mhz0 = (d.get("clocks") or {}).get("sm_mhz") or sm_mhz
+        mhz0 = d.get("sm_mhz") or sm_mhz          # SM clock inside the microbenchmark kernel
         peak = d["smem_lds128_gbs"] * sm_mhz / mhz0
         return peak, ("measured: LDS.128 %.0f GB/s at %.0f MHz (%s), x %.0f/%.0f MHz this run"
                       % (d["smem_lds128_gbs"], mhz0, ONCHIP_PEAKS, sm_mhz, mhz0))

@@ -154,3 +154,41 @@ class AngleShardEval:
                              stream)
         all_reduce_sum_(ws.g, ws.cost)
         return ws.cost, ws.g, ws.status
+
+
+# ---------------------------------------------------------------------------------------------
+# Joint drift estimation over a slice-sharded stack (R25): the
+# mask drift m_o(theta) is shared by every slice of a stack, so the stack is ONE
+# optimisation problem — its cost is the sum of all slices' costs and dS/dm_o the sum of all
+# slices' per-slice drift gradients.  With the slices sharded over ranks these two sums are the
+# exchange (N_theta + 1 fp64 values per evaluation), and the optimizer's dot products over the
+# sharded map blocks are summed over ranks too, so every rank takes identical steps.
+# ---------------------------------------------------------------------------------------------
+def drift_allreduce(cost_local: torch.Tensor, g_drift_local: torch.Tensor):
+    """(stack cost [1] fp64, stack drift gradient [N_theta] fp64) on every rank, from this rank's
+    per-slice costs [S_r] and per-slice drift gradients [S_r][N_theta] (fixed-order local sums in
+    fp64, then one all-reduce of N_theta + 1 values)."""
+    buf = torch.cat([cost_local.double().sum().reshape(1), g_drift_local.double().sum(0)])
+    all_reduce_sum_(buf)
+    return buf[:1], buf[1:]
+
+
+class ShardedDot:
+    """dot_reduce hook for lbfgs.minimize: rows of the [B, S] per-block dot-product matrix that
+    belong to blocks sharded over ranks (the maps of this rank's slices) are summed across ranks;
+    replicated blocks (the drift) are already complete on every rank."""
+
+    def __init__(self, sharded):
+        self.sharded = list(bool(b) for b in sharded)
+
+    def __call__(self, bd: torch.Tensor) -> torch.Tensor:
+        if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+            return bd
+        idx = [i for i, s in enumerate(self.sharded) if s]
+        part = bd[idx].contiguous()
+        dev = _device()
+        t = part.to(dev)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        out = bd.clone()
+        out[idx] = t.to(bd.device)
+        return out

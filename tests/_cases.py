@@ -93,3 +93,56 @@ def cached_hs_case(name: str, n_knots: int = 33):
     rng = np.random.default_rng(c.seed + 32)
     s_exp = rng.poisson(np.maximum(smod, 0.0)).astype(np.float32)
     return base, fs, s_exp
+
+
+def oracle_objective(case: synth.Case, lam: float = 0.0):
+    """fg(x) over x = [3, S, N, N] (CPU fp64 tensors) with the fp64 oracle's cost and gradient:
+    the same objective the product path evaluates on the GPU (lbfgs.ei_objective)."""
+    import torch
+    cfg = case.cfg
+
+    def fg(x):
+        m = x.numpy()
+        c, gm, gd, gs, _ = ora.cost_grad(cfg.angles, m[0], m[1], m[2], case.flat, case.mask, case.drift,
+                                         case.s_exp, lam, dx=cfg.pixel, du=cfg.det_pitch, z=cfg.z)
+        return torch.from_numpy(c), torch.from_numpy(np.stack([gm, gd, gs]))
+    return fg
+
+
+def oracle_objective_drift(case: synth.Case, lam: float = 0.0, slices=None):
+    """fg over the blocks [mu, delta, sigma, m_o] of a stack treated as ONE problem (joint drift
+    estimation, R25): mu/delta/sigma [1, S, N, N], m_o [1, N_theta]; cost = sum over slices,
+    dS/dm_o = sum over slices of the oracle's per-slice drift gradient.  `slices`: evaluate only
+    these slices of the case (one rank's shard)."""
+    import torch
+    cfg = case.cfg
+    sl = list(range(cfg.S)) if slices is None else list(slices)
+
+    def fg(x):
+        mu, de, sg, mo = (b.numpy() for b in x)
+        full = [np.zeros((cfg.S,) + mu.shape[2:], np.float64) for _ in range(3)]
+        for q, b in enumerate((mu, de, sg)):
+            full[q][sl] = b[0]
+        c, gm, gd, gs, _, gdr = ora.cost_grad(cfg.angles, *full, case.flat, case.mask,
+                                              mo[0].astype(np.float32), case.s_exp, lam, dx=cfg.pixel,
+                                              du=cfg.det_pitch, z=cfg.z, slices=sl, want_drift=True)
+        return (torch.tensor([c.sum()], dtype=torch.float64),
+                [torch.from_numpy(gm)[None], torch.from_numpy(gd)[None], torch.from_numpy(gs)[None],
+                 torch.from_numpy(gdr.sum(0))[None]])
+    return fg
+
+
+def rms_of_range(x, truth, border: int = 2) -> float:
+    """SPEC.md:562 (acceptance 9): RMS error excluding a `border`-pixel frame, as a fraction of the
+    phantom's dynamic range."""
+    d = (np.asarray(x, np.float64) - truth)[..., border:-border, border:-border]
+    return float(np.sqrt((d ** 2).mean()) / (truth.max() - truth.min()))
+
+
+def drift_rms(est, truth) -> float:
+    """drift error RMS up to a global constant, relative to the drift's own RMS about
+    its mean."""
+    d = np.asarray(est, np.float64) - truth
+    d = d - d.mean()
+    t = truth - truth.mean()
+    return float(np.sqrt((d ** 2).mean()) / np.sqrt((t ** 2).mean()))

@@ -140,3 +140,60 @@ def test_angle_sharded_sum_equals_full_world2():
     for rank, cost, g in res:
         np.testing.assert_allclose(cost, rc, rtol=1e-12)
         assert np.linalg.norm(g - ref) / np.linalg.norm(ref) < 1e-12
+
+
+def _drift_worker(rank, world, port, q, iters):
+    """Joint map + drift estimation of one stack sharded by slices (rank r owns slice r): the
+    oracle's cost and drift gradient of the rank's slice, summed over ranks (dist.drift_allreduce),
+    and the optimizer's dot products over the sharded map blocks summed too (dist.ShardedDot)."""
+    import numpy as np
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world), LOCAL_RANK=str(rank))
+    edist.init("gloo")
+    try:
+        import _cases
+        from paper_2202_08627_b200 import lbfgs
+        import test_recon_oracle as tro
+        case = tro.drift_case(noise=False)
+        cfg = case.cfg
+        first, count = edist.shard(cfg.S, rank, world)
+        local = _cases.oracle_objective_drift(case, 0.0, slices=range(first, first + count))
+
+        def fg(x):
+            c, g = local(x)
+            ct, gdr = edist.drift_allreduce(c, g[3])
+            return ct, g[:3] + [gdr.reshape(1, -1)]
+        x0 = ([torch.zeros(1, count, cfg.N, cfg.N, dtype=torch.float64) for _ in range(3)] +
+              [torch.zeros(1, cfg.n_angles, dtype=torch.float64)])
+        res = lbfgs.minimize(fg, x0, max_iter=iters, dot_reduce=edist.ShardedDot([1, 1, 1, 0]))
+        q.put((rank, float(res.cost[0]), res.x[3][0].numpy(), res.x[0][0].numpy(), res.n_iter))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_joint_drift_world2():
+    import numpy as np
+    import _cases
+    from paper_2202_08627_b200 import lbfgs
+    import test_recon_oracle as tro
+    iters = 25
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_drift_worker, args=(r, world, port, q, iters)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=300) for _ in range(world)], key=lambda r: r[0])
+    for p in procs:
+        p.join(60)
+        assert p.exitcode == 0
+    case = tro.drift_case(noise=False)
+    ref = lbfgs.minimize(_cases.oracle_objective_drift(case, 0.0), tro.drift_x0(case.cfg), max_iter=iters)
+    # every rank took the same steps: identical drift and stack cost on both ranks
+    assert res[0][1] == res[1][1] and np.array_equal(res[0][2], res[1][2])
+    # and the same steps as the unsharded optimisation (up to the order of the fp64 sums)
+    assert abs(res[0][1] - float(ref.cost[0])) <= 1e-6 * float(ref.cost[0])
+    mo = ref.x[3][0].numpy()
+    assert np.linalg.norm(res[0][2] - mo) <= 1e-4 * np.linalg.norm(mo)
+    maps = np.concatenate([res[0][3], res[1][3]])
+    assert np.linalg.norm(maps - ref.x[0][0].numpy()) <= 1e-4 * np.linalg.norm(maps)

@@ -281,11 +281,13 @@ def run_gpu(args, cfg, rank, world, local_rank):
         dist.barrier()
     torch.cuda.synchronize()
     t0 = time.time()
+    torch.cuda.nvtx.range_push("timed")                           # ncu --nvtx-include "timed/"
     for i in range(K):
         flush.fill_(1.0)                                          # untimed L2 flush
         ev[i][0].record(stream)
         step()
         ev[i][1].record(stream)
+    torch.cuda.nvtx.range_pop()
     torch.cuda.synchronize()
     t1 = time.time()
     if world > 1:

@@ -180,7 +180,7 @@ def _as_blocks(x0) -> Tuple[Blocks, bool]:
 def minimize(fg: Callable, x0: Union[torch.Tensor, Sequence[torch.Tensor]], max_iter: int = 200,
              m: int = 10, rel_tol: float = 1e-9, c1: float = 1e-4, c2: float = 0.9, max_ls: int = 25,
              target: Optional[Union[float, Sequence[float]]] = None,
-             callback: Optional[Callable[[int, torch.Tensor, Blocks], None]] = None,
+             callback: Optional[Callable[[int, torch.Tensor, object], None]] = None,
              dot_reduce: Optional[Callable[[torch.Tensor], torch.Tensor]] = None) -> Result:
     """Minimise S independent problems.  x0: a tensor [B, S, ...] (B blocks of one shape) or a list
     of block tensors [S, ...] of any shapes; fg(x) -> (cost [S] fp64, gradient with x's structure).
@@ -282,7 +282,7 @@ def minimize(fg: Callable, x0: Union[torch.Tensor, Sequence[torch.Tensor]], max_
         f = torch.from_numpy(fh.copy()).to(dev)
         history.append(f.clone())
         if callback is not None:
-            callback(it, f, x)
+            callback(it, f, pack(x))
     for s in range(S):
         if not done[s]:
             reason[s] = "max_iter"

@@ -40,15 +40,19 @@ EOF
       timeout 600 python tools/measure_peaks.py $OUT/peaks.json > $OUT/peaks.log 2>&1; echo "peaks rc=$?" | tee -a $OUT/rc.txt
       tail -c 400 $OUT/peaks.json ;;
     ncu)
-      timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
+      # the launch list of the default bench command's timed steps (NVTX range "timed" in bench.py)
+      timeout 900 python bench.py --steps 3 --warmup 3 --no-cpu-baseline > $OUT/plain_launch.log 2>&1 &&
+      timeout 900 ncu --nvtx --nvtx-include "timed/" --metrics gpu__time_duration.sum --clock-control none --csv \
         --log-file $OUT/launches.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline > $OUT/ncu_launch.log 2>&1
       echo "ncu launches rc=$?" | tee -a $OUT/rc.txt ;;
     full)
       # one --set full capture per config of the three hot kernels of one bench step (the 4th),
       # the source of profiles/traffic.json (tools/ncu_traffic.py) and the ncu summaries
       for c in ${FULL_CFGS:-C2 C3 C5 C4}; do
-        timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
-          -k regex:"project_kernel<\\(int\\)3|curve_kernel<\\(int\\)1>" -s 9 -c 3 \
+        timeout 900 python bench.py --config $c --steps 3 --warmup 3 --no-cpu-baseline > $OUT/plain_full_$c.log 2>&1 &&
+        timeout 900 ncu --set full --metrics lts__t_bytes.sum,l1tex__t_bytes.sum --clock-control none \
+          --import-source on --kernel-name-base demangled --nvtx --nvtx-include "timed/" \
+          -k regex:"project_kernel<\\(int\\)3|curve_kernel<\\(int\\)1>" -c 3 \
           -o $OUT/full_$c python bench.py --config $c --steps 3 --warmup 3 --no-cpu-baseline > $OUT/ncu_full_$c.log 2>&1
         echo "ncu full $c rc=$?" | tee -a $OUT/rc.txt
       done ;;

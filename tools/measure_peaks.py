@@ -29,12 +29,13 @@ def main(out):
     d = json.loads(r.stdout.strip().splitlines()[-1])
     clocks = sampler.summary(t0, t1)
     d["clocks"] = clocks
-    # the SM clock under the SMEM kernel, from its own clock64() span (the nvidia-smi samples also
-    # see the idle gaps between the short launches)
-    d["sm_mhz"] = d["sm_mhz_in_kernel_smem"]
+    # the SM clock: nvidia-smi's median during the run (the kernels' own clock64 spans are kept as
+    # a cross-check; they undercount when a launch's blocks do not all start at once)
+    d["sm_mhz"] = clocks.get("sm_mhz") or 1965.0
+    for k in ("smem_lds128", "smem_lds64", "l2_read"):
+        d[k + "_bytes_per_clk_per_sm"] = round(d[k + "_gbs"] * 1e9 / (d["sm_mhz"] * 1e6) / d["sms"], 2)
     d["nominal_smem_gbs_at_clock"] = round(128.0 * d["sms"] * d["sm_mhz"] * 1e6 / 1e9, 1)
-    d["how"] = ("tools/microbench.cu: best of 5 CUDA-event-timed launches each (bytes per SM clock from "
-                "the kernel's own clock64 span); LDS.128 / LDS.64 "
+    d["how"] = ("tools/microbench.cu: best of 5 CUDA-event-timed launches each; LDS.128 / LDS.64 "
                 "conflict-free (4 CTAs x 256 threads per SM), L2 read of a 48 MB resident buffer "
                 "(__ldcg, 40 passes), HBM read of 4 GiB (8 passes); clocks sampled by nvidia-smi "
                 "during the run")

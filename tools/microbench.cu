@@ -117,9 +117,9 @@ int main() {
   const double lds64_bpc = nload * 8 / sms / mean_cycles(cyc, sms * 4);
   const cudaError_t e = cudaDeviceSynchronize();
   printf("{\"l2_read_gbs\": %.1f, \"hbm_read_gbs\": %.1f, \"smem_lds128_gbs\": %.1f, "
-         "\"smem_lds64_gbs\": %.1f, \"smem_lds128_bytes_per_sm_clk\": %.2f, "
-         "\"smem_lds64_bytes_per_sm_clk\": %.2f, \"sm_mhz_in_kernel_smem\": %.1f, "
-         "\"sm_mhz_in_kernel_l2\": %.1f, \"sms\": %d, \"cuda\": \"%s\"}\n",
+         "\"smem_lds64_gbs\": %.1f, \"blockspan_lds128_bytes_per_sm_clk\": %.2f, "
+         "\"blockspan_lds64_bytes_per_sm_clk\": %.2f, \"blockspan_mhz_smem\": %.1f, "
+         "\"blockspan_mhz_l2\": %.1f, \"sms\": %d, \"cuda\": \"%s\"}\n",
          l2, hbm, lds128, lds64, lds128_bpc, lds64_bpc, smem_mhz, l2_mhz, sms, cudaGetErrorString(e));
   return e == cudaSuccess ? 0 : 1;
 }

@@ -12,7 +12,8 @@ KEYS = ["gpu__time_duration.sum", "sm__throughput.avg.pct_of_peak_sustained_elap
         "smsp__sass_inst_executed_op_shared_ld.sum", "smsp__inst_executed.sum",
         "sm__inst_executed.sum.per_cycle_active", "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
         "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active",
-        "sm__warps_active.avg.pct_of_peak_sustained_active", "lts__t_bytes.sum", "dram__bytes_read.sum",
+        "sm__warps_active.avg.pct_of_peak_sustained_active", "lts__t_bytes.sum", "l1tex__t_bytes.sum",
+        "dram__bytes_read.sum",
         "dram__bytes_write.sum", "launch__registers_per_thread", "sm__cycles_elapsed.avg"]
 
 

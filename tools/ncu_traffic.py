@@ -30,9 +30,11 @@ def main(rep, cfg, cmd):
         b = 0.0
         for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
             b += float(r[h.index(m)]) * SCALE[units[h.index(m)]]
+        def metric(m):
+            return float(r[h.index(m)]) * SCALE[units[h.index(m)]] if m in h and r[h.index(m)] else None
         got[key] = {"dram_bytes_per_launch": b,
-                    "lts_bytes_per_launch": float(r[h.index("lts__t_bytes.sum")]) * SCALE[units[h.index("lts__t_bytes.sum")]]
-                    if "lts__t_bytes.sum" in h else None,
+                    "lts_bytes_per_launch": metric("lts__t_bytes.sum"),
+                    "l1tex_bytes_per_launch": metric("l1tex__t_bytes.sum"),
                     "duration_us_cold": float(r[h.index("gpu__time_duration.sum")]) *
                     (1e-3 if units[h.index("gpu__time_duration.sum")] == "ns" else
                      1e3 if units[h.index("gpu__time_duration.sum")] == "ms" else 1.0)}

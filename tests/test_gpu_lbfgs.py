@@ -1,7 +1,20 @@
-"""NEXT-1 on the GPU: the host L-BFGS loop over ei_cost_grad reconstructs the three maps of the
-C1 geometry from noise-free oracle curves (exact-fit experiment, S:304-305 analogue): the cost
-falls by >= 1e6 and mu, delta are recovered to a few percent (sigma, the weakest channel, to
-< 30 %) starting from x0 = 0 (BASELINE.json configs[0]: "the start estimate is all-zero maps")."""
+"""NEXT-1 / NEXT-2 on the GPU: the host L-BFGS loop (strong Wolfe, lbfgs.py) over the C ABI.
+
+* C1 noise-free from x0 = 0 (BASELINE.json configs[0]): the loop CONVERGES (stops on its own rule,
+  not on max_iter) and every map is within 2 % RMS of its dynamic range, 2-pixel border excluded
+  (SPEC.md:284, :562 acceptance 9); the cost sequence is monotone;
+* C1 Poisson data with the discrepancy-principle stop (cost <= sum of the measured counts): stops
+  early, mu and delta within a few percent of their range;
+* the minimum the GPU loop reaches equals the minimum SciPy's L-BFGS-B (the paper's optimizer,
+  PAPER.md:81) reaches on the fp64 ORACLE's cost, within 1e-6 relative, on the strongly
+  regularised (strictly convex, well-conditioned) C1 problem;
+* joint estimation of the maps and the mask drift m_o(theta) of a 4-slice stack of the C4 geometry
+  (720 angles, drift random walk; eq. 4): drift within 5 % RMS up to a constant
+  (SPEC.md:285), from the noise-free and from Poisson data;
+* the paper's single-map model on its own scan geometry P1 (noise-free): converges, h within 2 %.
+Inputs from synth + the oracle only."""
+import dataclasses
+
 import numpy as np
 import pytest
 
@@ -12,43 +25,100 @@ from paper_2202_08627_b200 import synth  # noqa: E402
 import _cases  # noqa: E402
 
 
-def test_lbfgs_reconstructs_c1_noise_free():
+@pytest.fixture(scope="module")
+def mods():
     assert torch.cuda.is_available()
     from paper_2202_08627_b200 import build
     build.build()
     from paper_2202_08627_b200 import ei, lbfgs
+    return ei, lbfgs
+
+
+def d(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def plan_for(ei, cfg):
+    return ei.Plan(cfg.S, cfg.N, cfg.n_angles, cfg.n_det, cfg.M, cfg.pixel, cfg.det_pitch, cfg.z, cfg.angles)
+
+
+def test_lbfgs_c1_noise_free_converges(mods):
+    ei, lbfgs = mods
     cfg = synth.CONFIGS["C1"]
     case = _cases.oracle_case(cfg, noise=False)
-    d = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
-    plan = ei.Plan(cfg.S, cfg.N, cfg.n_angles, cfg.n_det, cfg.M, cfg.pixel, cfg.det_pitch, cfg.z, cfg.angles)
-    fg = lbfgs.ei_objective(plan, d(case.flat), d(case.mask), None, d(case.s_exp), 0.0)
-    x0 = torch.zeros(3, 1, cfg.N, cfg.N, device="cuda")
-    res = lbfgs.minimize(fg, x0, max_iter=400, rel_tol=1e-12)
-    c0, c = float(res.history[0][0]), float(res.cost[0])
-    assert c <= 1e-6 * c0, (c0, c)
+    fg = lbfgs.ei_objective(ei.Plan(1, cfg.N, cfg.n_angles, cfg.n_det, cfg.M, cfg.pixel, cfg.det_pitch,
+                                    cfg.z, cfg.angles), d(case.flat), d(case.mask), None, d(case.s_exp), 0.0)
+    res = lbfgs.minimize(fg, torch.zeros(3, 1, cfg.N, cfg.N, device="cuda"), max_iter=6000)
+    assert bool(res.converged.all()) and res.reason[0] in ("rel_tol", "precision"), res.reason
     for h0, h1 in zip(res.history, res.history[1:]):
         assert float(h1[0]) <= float(h0[0])
     got = res.x.cpu().numpy()[:, 0]
-    truth = np.stack(case.maps())[:, 0]
-    err = [np.linalg.norm(got[q] - truth[q]) / np.linalg.norm(truth[q]) for q in range(3)]
-    assert err[0] < 0.05 and err[1] < 0.05 and err[2] < 0.3, err
+    for q, t in enumerate(case.maps()):
+        e = _cases.rms_of_range(got[q], t[0].astype(np.float64))
+        assert e < 0.02, (q, e)
 
 
-def test_lbfgs_single_map_model_p1_noise_free():
+def test_lbfgs_c1_poisson_discrepancy(mods):
+    ei, lbfgs = mods
+    case = _cases.cached_case("C1")
+    cfg = case.cfg
+    fg = lbfgs.ei_objective(plan_for(ei, cfg), d(case.flat), d(case.mask), None, d(case.s_exp), 0.0)
+    target = float(case.s_exp.astype(np.float64).sum())
+    res = lbfgs.minimize(fg, torch.zeros(3, 1, cfg.N, cfg.N, device="cuda"), max_iter=300, target=target)
+    assert res.reason == ["target"] and res.iters[0] < 60, (res.reason, res.iters)
+    got = res.x.cpu().numpy()[:, 0]
+    e = [_cases.rms_of_range(got[q], case.maps()[q][0].astype(np.float64)) for q in range(3)]
+    assert e[0] < 0.05 and e[1] < 0.06, e
+
+
+def test_lbfgs_matches_scipy_on_oracle(mods):
+    import scipy.optimize as so
+    from threadpoolctl import threadpool_limits
+    ei, lbfgs = mods
+    case = _cases.cached_case("C1")
+    cfg = case.cfg
+    lam = 1e10           # strictly convex, well-conditioned: one minimum for both optimizers
+    ofg = _cases.oracle_objective(case, lam)
+    N = cfg.N
+
+    def f_np(v):
+        c, g = ofg(torch.from_numpy(v.reshape(3, 1, N, N)))
+        return float(c[0]), g.numpy().ravel()
+    with threadpool_limits(limits=1, user_api="blas"):
+        ref = so.minimize(f_np, np.zeros(3 * N * N), jac=True, method="L-BFGS-B",
+                          options=dict(maxiter=3000, ftol=1e-13, gtol=1e-12, maxcor=10))
+    assert ref.success, ref.message
+    fg = lbfgs.ei_objective(plan_for(ei, cfg), d(case.flat), d(case.mask), None, d(case.s_exp), lam)
+    res = lbfgs.minimize(fg, torch.zeros(3, 1, N, N, device="cuda"), max_iter=3000)
+    assert bool(res.converged.all()), res.reason
+    assert abs(float(res.cost[0]) - ref.fun) <= 1e-6 * ref.fun, (float(res.cost[0]), ref.fun)
+
+
+@pytest.mark.parametrize("noise", [False, True])
+def test_joint_drift_c4_geometry(mods, noise):
+    ei, lbfgs = mods
+    cfg = dataclasses.replace(synth.CONFIGS["C4"], S=4)
+    case = _cases.oracle_case(cfg, noise=noise)
+    fg = lbfgs.ei_objective_drift(plan_for(ei, cfg), d(case.flat), d(case.mask), d(case.s_exp), 0.0, check=False)
+    x0 = ([torch.zeros(1, cfg.S, cfg.N, cfg.N, device="cuda") for _ in range(3)] +
+          [torch.zeros(1, cfg.n_angles, device="cuda")])
+    target = float(case.s_exp.astype(np.float64).sum()) if noise else None
+    res = lbfgs.minimize(fg, x0, max_iter=150, target=target)
+    e = _cases.drift_rms(res.x[3][0].cpu().numpy(), case.drift.astype(np.float64))
+    assert e < (0.05 if noise else 1e-3), e
+    if noise:
+        assert res.reason == ["target"], res.reason
+
+
+def test_lbfgs_single_map_model_p1_noise_free(mods):
     """NEXT-1 with the paper's single-map model (eq. 4) on its own scan geometry P1: from h = 0 and
-    noise-free oracle curves, L-BFGS over ei_cost_grad_h lowers the cost by >= 1e6 and recovers h
-    to < 5 % relative L2."""
-    assert torch.cuda.is_available()
-    from paper_2202_08627_b200 import build
-    build.build()
-    from paper_2202_08627_b200 import ei, lbfgs
+    noise-free oracle curves, L-BFGS over ei_cost_grad_h converges and recovers h to < 2 % RMS of
+    its range (2-pixel border excluded)."""
+    ei, lbfgs = mods
     case = _cases.oracle_h_case(synth.H_CONFIGS["P1"], noise=False)
     cfg = case.cfg
-    d = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
-    plan = ei.Plan(cfg.S, cfg.N, cfg.n_angles, cfg.n_det, cfg.M, cfg.pixel, cfg.det_pitch, cfg.z, cfg.angles)
-    fg = lbfgs.ei_objective_h(plan, case.gamma, d(case.flat), d(case.mask), None, d(case.s_exp), 0.0)
-    res = lbfgs.minimize(fg, torch.zeros(1, 1, cfg.N, cfg.N, device="cuda"), max_iter=400, rel_tol=1e-12)
-    c0, c = float(res.history[0][0]), float(res.cost[0])
-    assert c <= 1e-6 * c0, (c0, c)
-    err = np.linalg.norm(res.x.cpu().numpy()[0, 0] - case.h[0]) / np.linalg.norm(case.h[0])
-    assert err < 0.05, err
+    fg = lbfgs.ei_objective_h(plan_for(ei, cfg), case.gamma, d(case.flat), d(case.mask), None, d(case.s_exp), 0.0)
+    res = lbfgs.minimize(fg, torch.zeros(1, 1, cfg.N, cfg.N, device="cuda"), max_iter=3000)
+    assert bool(res.converged.all()), res.reason
+    e = _cases.rms_of_range(res.x.cpu().numpy()[0, 0], case.h[0].astype(np.float64))
+    assert e < 0.02, e

@@ -86,12 +86,15 @@ struct ei_plan {
   float2 *M1 = nullptr, *M1T = nullptr;   // [S][N][Rp] single map (ei_project n_maps=1)
   float *P = nullptr;         // [RS][S][3][NA][ND] (partial) projections
   int32_t *diag = nullptr;    // device counter of internal window overflows (must stay 0)
-  // gradient sinograms in the PAIR layout read by K3: entry e = (g[e-1], g[e]), e = 0..ND
-  // (zero outside the detector), stored at e + PADG in rows of RpG entries (zero padding both
-  // sides, written once at plan creation): GA = (mu0, mu1, delta0, delta1), GB = (sigma0, sigma1)
+  // gradient sinograms read by K3, stored at entry e + PADG in rows of RpG entries (RpG a multiple
+  // of 4; zero padding both sides, written once at plan creation), zero outside the detector:
+  //  * three maps, TRIPLE layout, e = -1..ND: GA = (m[e-1], m[e], s[e-1], s[e]),
+  //    GB = (d[e-1], d[e], m[e+1], d[e+1]), GC = s[e+1]  (m, d, s: mu, delta, sigma gradients)
+  //  * single map, PAIR layout, e = 0..ND: GA1 = (g[e-1], g[e])
   float4 *GA = nullptr;       // [S][NA][RpG]
-  float2 *GB = nullptr;       // [S][NA][RpG]
-  float2 *GA1 = nullptr;      // [S][NA][RpG]  single-map pairs (ei_backproject n_maps=1)
+  float4 *GB = nullptr;       // [S][NA][RpG]
+  float *GC = nullptr;        // [S][NA][RpG]
+  float2 *GA1 = nullptr;      // [S][NA][RpG]
   int PADG = 0, RpG = 0;
   double *part_curve = nullptr;  // [S][NA][nseg][nw] per-warp cost partials (K2, fp64)
   float *part_mo = nullptr;      // [S][NA][nseg][nw] per-warp dS/dm_o partials (K2, NEXT-2)

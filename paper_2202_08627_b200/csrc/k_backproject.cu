@@ -4,19 +4,27 @@
 // k* = (x_j cos + y_i sin)/du + (Nd-1)/2 and h = |c_dom| dx/du <= 1, so only the detector pair
 // (floor(k*), floor(k*)+1) contributes (du >= dx is enforced by the plan).
 //
-// B200 design:
-//  * gradient sinograms arrive in a PAIR layout written by K2: entry e of a row holds
-//    (g[e-1], g[e]) for every map, so one tap pair of all three maps is one LDS.128 + one LDS.64
-//    (A = (mu0, mu1, delta0, delta1), B = (sigma0, sigma1)); row length Nd+1 (e = 0..Nd).
-//  * a CTA owns a 32x32 pixel tile (256 consumer threads x 4 pixels) and walks the angles in
-//    chunks of 16; a producer warp stages, per angle, only the 48-entry detector window the tile
-//    projects onto, with 1-D bulk copies (TMA engine) into a 3-stage shared-memory ring that
-//    completes on full/empty mbarriers (G rows are zero-padded, so every window is one
-//    in-bounds copy); consumer warps never meet a CTA-wide barrier in the loop;
-//  * a warp covers an 8x4 pixel sub-tile, whose taps fall on ~10 consecutive window entries:
-//    lanes share (broadcast) most loads, ~3 shared-memory wavefronts per 32 pixel-angles;
-//  * the pair products accumulate with FFMA2 (__ffma2_rn: two fp32 FMAs per instruction on
-//    sm_100a): acc.x collects the left taps, acc.y the right taps, summed once at the end.
+// B200 design — three-map model (backproject3_kernel), bound by the shared-memory data pipe:
+//  * gradient sinograms arrive in a TRIPLE layout written by K2: entry e of a row holds the three
+//    detector values e-1, e, e+1 of every map in three planes, A = (m[e-1], m[e], s[e-1], s[e]),
+//    B = (d[e-1], d[e], m[e+1], d[e+1]), C = s[e+1] (m, d, s = the mu, delta, sigma gradients
+//    pre-scaled by the Joseph weight), e = -1..Nd, zero outside the detector;
+//  * a thread owns horizontally adjacent PIXEL PAIRS: their k* differ by |c'| = |cos| dx/du <= 1,
+//    so the pair's four taps lie in three consecutive detector positions and one entry serves both
+//    pixels — 36 B (LDS.128 + LDS.128 + LDS.32) per pixel pair instead of 24 B per pixel (the pair
+//    layout's LDS.128 + LDS.64), i.e. 4.5 instead of >= 6 shared-memory wavefronts per 32 pixels;
+//    the lower pixel (smaller k*) takes the tent weights of its two taps, the upper one three tent
+//    weights over the entry's three positions (max(0, 1 - |k - k*|/h), identical values);
+//  * which pixel of a pair is lower depends on the sign of cos(theta) only: the plan lists the
+//    back-projected angles cos >= 0 first, and the per-pixel partial sums of the first class are
+//    folded into totals at the (warp-uniform) class change;
+//  * a CTA owns a 32x32 pixel tile (256 consumer threads x 2 pairs; a quarter warp = 4 pair columns
+//    x 2 rows, whose entries span <= 8 consecutive entries: no bank conflicts) and walks the angles
+//    in chunks of 16; a producer warp stages, per angle, the 48-entry detector window of the tile
+//    (1-D bulk copies, TMA engine) into a 2-stage mbarrier ring;
+//  * FFMA2 (two fp32 FMAs per instruction on sm_100a) on the taps held in aligned register pairs.
+// Single-map model (backproject1_kernel): the PAIR layout (g[e-1], g[e]) per entry, one LDS.64 per
+// pixel, a 3-stage ring, warp = 8x4 pixel sub-tile with 4 pixels per thread.
 // Nothing is scattered: deterministic.  The cost path adds 2*lambda*x (eq. 5).
 #include <algorithm>
 
@@ -53,28 +61,29 @@ constexpr int NT = 256;     // consumer threads (+ one producer warp)
 constexpr int NST = 3;      // ring stages
 constexpr int WLB = WL + 2; // 8-byte-entry rows: 16-B aligned copy start needs one spare entry
 
-template <int NMAP>
-struct Layout;
-template <>
-struct Layout<3> {   // A = (mu0, mu1, delta0, delta1), B = (sigma0, sigma1)
-  using A = float4;
-  static constexpr bool hasB = true;
-};
-template <>
-struct Layout<1> {   // A = (g0, g1)
-  using A = float2;
-  static constexpr bool hasB = false;
-};
-
-// staged windows: separate planes (16-B and 8-B element strides keep the LDS.128 / LDS.64 of a
-// quarter/half warp on distinct banks; an interleaved 32-B entry stride measured 1.5x slower)
-template <int NMAP>
-struct Smem {
-  typename Layout<NMAP>::A a[NST][CH][sizeof(typename Layout<NMAP>::A) == 8 ? WLB : WL];
-  float2 b[NST][CH][Layout<NMAP>::hasB ? WLB : 2];
+// single-map staged windows (pair layout, 8-B entries)
+struct Smem1 {
+  float2 a[NST][CH][WLB];
   float4 tab[NST][CH];
   int ws[NST][CH];
   uint64_t full[NST], empty[NST];
+};
+
+// three-map staged windows (triple layout): planes of 16-B, 16-B and 4-B entries (separate planes
+// keep each LDS on distinct banks), all starting at the same entry e0, a multiple of 4 (16-B aligned
+// C-plane copies), so one index addresses all three; e0 <= floor(min k*) + 1 - 0 and the window
+// holds WL3 = 52 >= 45 + 4 entries
+constexpr int NST3 = 2;
+constexpr int WL3 = 52;
+struct Smem3 {
+  float4 a[NST3][CH][WL3];   // (m[e-1], m[e], s[e-1], s[e])
+  float4 b[NST3][CH][WL3];   // (d[e-1], d[e], m[e+1], d[e+1])
+  float c[NST3][CH][WL3];    // s[e+1]
+  float4 t1[NST3][CH];       // c', s', 1/h, 1 - 1/h
+  float4 t2[NST3][CH];       // (Nd-1)/2 + 1 - e0 + min(c', 0), |c'|, 1 - 2/h, 1 + 1/h
+  int nb[NST3];              // first angle of the chunk with cos < 0 (CH if none)
+  float tot[12][NT];        // per consumer thread: totals of finished angle classes (pair, L/R, map)
+  uint64_t full[NST3], empty[NST3];
 };
 
 #ifdef EI_TRACE
@@ -144,19 +153,16 @@ __device__ __forceinline__ void finalize(const FinArgs &f, int s, int tid) {
     }
 }
 
-template <int NMAP, bool TAB>
-__global__ void __launch_bounds__(NT + 32, 3) backproject_kernel(
-    const typename Layout<NMAP>::A *__restrict__ GA, const float2 *__restrict__ GB,
-    const float4 *__restrict__ k3, const int *__restrict__ alist, int NA3, int N, int NA, int ND,
-    const float *__restrict__ mu,
-    const float *__restrict__ delta, const float *__restrict__ sigma, float lambda,
-    float *__restrict__ o0, float *__restrict__ o1, float *__restrict__ o2, size_t out_stride,
+// single-map model (NEXT-3): pair layout (g[e-1], g[e]) per entry
+template <bool TAB>
+__global__ void __launch_bounds__(NT + 32, 3) backproject1_kernel(
+    const float2 *__restrict__ GA, const float4 *__restrict__ k3, const int *__restrict__ alist,
+    int NA3, int N, int NA, int ND, const float *__restrict__ mu, float lambda,
+    float *__restrict__ o0, size_t out_stride,
     int S, int KS, float *__restrict__ part3, int PADG, int RpG,
     const int4 *__restrict__ units, FinArgs fin) {
-  using TA = typename Layout<NMAP>::A;
-  constexpr bool A8 = sizeof(TA) == 8;
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  Smem<NMAP> &sm = *reinterpret_cast<Smem<NMAP> *>(smem_raw);
+  Smem1 &sm = *reinterpret_cast<Smem1 *>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   // unit: tile, slice, part ks of the tile's angle split into nks parts.  Grids with more units
   // than SMs read it from the plan's placement table (parts of unequal size placed heaviest first);
@@ -177,8 +183,7 @@ SPAN_START_bp();
 #endif
   const float ctr = 0.5f * (float)(N - 1), dctr = 0.5f * (float)(ND - 1);
   const size_t rowlen = (size_t)RpG;   // padded G rows: entry e at e + PADG
-  const TA *GAs = GA + (size_t)s * NA * rowlen + PADG;
-  const float2 *GBs = GB ? GB + (size_t)s * NA * rowlen + PADG : nullptr;
+  const float2 *GAs = GA + (size_t)s * NA * rowlen + PADG;
   // angle split (small grids): CTA ks owns angles [a_lo, a_hi) of the back-projected list, an equal
   // share (not a whole number of chunks: 360 angles in 6 parts are 60 each, staged as 16+16+16+12,
   // where whole chunks gave 3 or 4 chunks per CTA), in chunks of CH staged angles
@@ -202,8 +207,7 @@ SPAN_START_bp();
     // tile corners (full 32x32 tile, even past the map edge, so every lane indexes the window)
     const float xa = (float)j0 - ctr, xb = xa + (float)(TILE - 1);
     const float ya = (float)i0 - ctr, yb = ya + (float)(TILE - 1);
-    const uint32_t bytesA = A8 ? (uint32_t)WLB * 8 : (uint32_t)WL * 16;
-    const uint32_t bytesB = NMAP == 3 ? (uint32_t)WLB * 8 : 0u;
+    const uint32_t bytesA = (uint32_t)WLB * 8;
     int st = 0;
     uint32_t ph = 0;
     for (int c = c_lo; c < c_hi; ++c) {
@@ -220,15 +224,14 @@ SPAN_START_bp();
         sm.ws[st][lane] = ws;
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive_expect_tx(&sm.full[st], (uint32_t)na * (bytesA + bytesB));
+      if (lane == 0) mbar_arrive_expect_tx(&sm.full[st], (uint32_t)na * bytesA);
       __syncwarp();
       if (lane < na) {
         const size_t row = (size_t)__ldg(alist_k + c * CH + lane) * rowlen;
         // a window entirely off the detector only needs zeros: clamp its copy into the zero pad
         // (a window overlapping [0, ND] is always inside the PADG >= WL padding)
         const int e0 = min(max(ws + 1, -PADG), ND + PADG - WLB), eb = e0 & ~1;
-        bulk_g2s(&sm.a[st][lane][0], GAs + row + (A8 ? eb : e0), bytesA, &sm.full[st]);
-        if (NMAP == 3) bulk_g2s(&sm.b[st][lane][0], GBs + row + eb, bytesB, &sm.full[st]);
+        bulk_g2s(&sm.a[st][lane][0], GAs + row + eb, bytesA, &sm.full[st]);
       }
       if (++st == NST) { st = 0; ph ^= 1; }
     }
@@ -249,9 +252,9 @@ SPAN_START_bp();
 #pragma unroll
   for (int q = 0; q < 4; ++q) xq[q] = (float)(j0 + lx + 8 * q) - ctr;
 
-  float2 am[4], ad[4], as[4];
+  float2 am[4];
 #pragma unroll
-  for (int q = 0; q < 4; ++q) am[q] = ad[q] = as[q] = make_float2(0.f, 0.f);
+  for (int q = 0; q < 4; ++q) am[q] = make_float2(0.f, 0.f);
 
   pdl_wait();   // sleep while K2 runs (this CTA may have launched early)
   int st = 0;
@@ -268,8 +271,7 @@ SPAN_START_bp();
       const int ws = sm.ws[st][al];
       const int bofs = (ws + 1) & 1;
       const float base = fmaf(yi, t.y, dctr - (float)ws);
-      const TA *arow = &sm.a[st][al][A8 ? bofs : 0];
-      const float2 *brow = &sm.b[st][Layout<NMAP>::hasB ? al : 0][bofs];
+      const float2 *arow = &sm.a[st][al][bofs];
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const float kst = fmaf(xq[q], t.x, base);   // window-local k*, > 0
@@ -282,14 +284,7 @@ SPAN_START_bp();
         // debug build: the pair (k0, k0+1) lies inside the staged window of WL entries
         if (k0 < 0 || k0 + 1 >= WL) atomicAdd(fin.diag, 1);
 #endif
-        const TA ga = arow[k0];
-        if constexpr (NMAP == 3) {
-          am[q] = __ffma2_rn(wt, make_float2(ga.x, ga.y), am[q]);
-          ad[q] = __ffma2_rn(wt, make_float2(ga.z, ga.w), ad[q]);
-          as[q] = __ffma2_rn(wt, brow[k0], as[q]);
-        } else {
-          am[q] = __ffma2_rn(wt, ga, am[q]);
-        }
+        am[q] = __ffma2_rn(wt, arow[k0], am[q]);
       }
     }
     __syncwarp();
@@ -320,12 +315,7 @@ SPAN_START_bp();
       for (int q = 0; q < 4; ++q) {
         const int j = j0 + lx + 8 * q;
         if (j >= N) continue;
-        float *pp = part3 + ((size_t)(ks * S + s) * 3) * NN + (size_t)i * N + j;
-        pp[0] = am[q].x + am[q].y;
-        if constexpr (NMAP == 3) {
-          pp[NN] = ad[q].x + ad[q].y;
-          pp[2 * NN] = as[q].x + as[q].y;
-        }
+        part3[((size_t)(ks * S + s) * 3) * NN + (size_t)i * N + j] = am[q].x + am[q].y;
       }
     }
     return;
@@ -338,23 +328,218 @@ SPAN_START_bp();
     const size_t p = (size_t)i * N + j;
     const size_t oo = (size_t)s * out_stride + p;
     float vm = am[q].x + am[q].y;
-    if constexpr (NMAP == 3) {
-      float vd = ad[q].x + ad[q].y, vs = as[q].x + as[q].y;
-      if (mu) {   // cost path: + 2 lambda x (eq. 5); maps have slice stride N*N
-        const size_t ip = (size_t)s * NN + p;
-        const float l2 = 2.f * lambda;
-        vm = fmaf(l2, __ldg(mu + ip), vm);
-        vd = fmaf(l2, __ldg(delta + ip), vd);
-        vs = fmaf(l2, __ldg(sigma + ip), vs);
-      }
-      o0[oo] = vm;
-      o1[oo] = vd;
-      o2[oo] = vs;
-    } else {
-      if (mu) vm = fmaf(2.f * lambda, __ldg(mu + (size_t)s * NN + p), vm);   // single-map cost path
-      o0[oo] = vm;
-    }
+    if (mu) vm = fmaf(2.f * lambda, __ldg(mu + (size_t)s * NN + p), vm);   // cost path: + 2 lambda h
+    o0[oo] = vm;
   }
+}
+
+// three-map model: triple layout, pixel pairs (see the file header)
+template <bool TAB>
+__global__ void __launch_bounds__(NT + 32, 3) backproject3_kernel(
+    const float4 *__restrict__ GA, const float4 *__restrict__ GB, const float *__restrict__ GC,
+    const float4 *__restrict__ k3, const int *__restrict__ alist, int NA3, int N, int NA, int ND,
+    const float *__restrict__ mu, const float *__restrict__ delta, const float *__restrict__ sigma,
+    float lambda, float *__restrict__ o0, float *__restrict__ o1, float *__restrict__ o2,
+    size_t out_stride, int S, int KS, float *__restrict__ part3, int PADG, int RpG,
+    const int4 *__restrict__ units, FinArgs fin) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  Smem3 &sm = *reinterpret_cast<Smem3 *>(smem_raw);
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  int j0, i0, s, ks, nks;   // unit decode as in backproject1_kernel
+  if (TAB) {
+    const int4 u = __ldg(units + blockIdx.x);
+    const int ntx = (N + TILE - 1) / TILE;
+    j0 = (u.x % ntx) * TILE; i0 = (u.x / ntx) * TILE; s = u.y; ks = u.z; nks = u.w;
+  } else {
+    j0 = blockIdx.x * TILE; i0 = blockIdx.y * TILE; s = blockIdx.z % S; ks = blockIdx.z / S; nks = KS;
+  }
+SPAN_START_bp();
+  const float ctr = 0.5f * (float)(N - 1), dctr = 0.5f * (float)(ND - 1);
+  const size_t rowlen = (size_t)RpG, soff = (size_t)s * NA * rowlen + PADG;
+  const int a_lo = (int)(((long long)ks * NA3) / nks), a_hi = (int)(((long long)(ks + 1) * NA3) / nks);
+  const int c_hi = (a_hi - a_lo + CH - 1) / CH;
+  const int *alist_k = alist + a_lo;
+
+  if (tid == 0) {
+    for (int q = 0; q < NST3; ++q) {
+      mbar_init(&sm.full[q], 1);
+      mbar_init(&sm.empty[q], NT / 32);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+
+  if (w == NT / 32) {   // ---------------- producer warp ----------------
+    pdl_wait();   // K2's gradient sinograms
+    const float xa = (float)j0 - ctr, xb = xa + (float)(TILE - 1);
+    const float ya = (float)i0 - ctr, yb = ya + (float)(TILE - 1);
+    constexpr uint32_t bytesAB = (uint32_t)WL3 * 16, bytesC = (uint32_t)WL3 * 4;
+    int st = 0;
+    uint32_t ph = 0;
+    for (int c = 0; c < c_hi; ++c) {
+      if (c >= NST3) mbar_wait(&sm.empty[st], ph ^ 1);
+      const int na = min(CH, a_hi - a_lo - c * CH);
+      int e0 = 0;
+      if (lane < na) {   // per-angle tables + window start
+        const int a = __ldg(alist_k + c * CH + lane);
+        const float4 g = __ldg(k3 + a);   // c', s', 1/h, Joseph weight
+        const float k00 = fmaf(xa, g.x, fmaf(ya, g.y, dctr)), k01 = fmaf(xb, g.x, fmaf(ya, g.y, dctr));
+        const float k10 = fmaf(xa, g.x, fmaf(yb, g.y, dctr)), k11 = fmaf(xb, g.x, fmaf(yb, g.y, dctr));
+        // first entry the tile needs (floor of the smallest k*, + 1), one of slack, rounded down
+        // to a multiple of 4; a window entirely off the detector only needs zeros: clamp its copy
+        // into the zero pad (a window overlapping [-1, ND] is never clamped: PADG >= WL3 + 8)
+        const int ws = (int)floorf(fminf(fminf(k00, k01), fminf(k10, k11))) - 1;
+        e0 = min(max((ws + 1) & ~3, -PADG + 4), (RpG - PADG - WL3 - 4) & ~3);
+        sm.t1[st][lane] = make_float4(g.x, g.y, g.z, 1.f - g.z);
+        sm.t2[st][lane] = make_float4(dctr + 1.f - (float)e0 + fminf(g.x, 0.f), fabsf(g.x), 1.f - 2.f * g.z, 1.f + g.z);
+      }
+      {   // first angle of the chunk with cos < 0 (the list has cos >= 0 first), na if none
+        const unsigned neg = __ballot_sync(0xffffffffu, lane < na && sm.t1[st][lane].x < 0.f);
+        if (lane == 0) sm.nb[st] = neg ? __ffs(neg) - 1 : na;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive_expect_tx(&sm.full[st], (uint32_t)na * (2u * bytesAB + bytesC));
+      __syncwarp();
+      if (lane < na) {
+        const size_t row = soff + (size_t)__ldg(alist_k + c * CH + lane) * rowlen + e0;
+        bulk_g2s(&sm.a[st][lane][0], GA + row, bytesAB, &sm.full[st]);
+        bulk_g2s(&sm.b[st][lane][0], GB + row, bytesAB, &sm.full[st]);
+        bulk_g2s(&sm.c[st][lane][0], GC + row, bytesC, &sm.full[st]);
+      }
+      if (++st == NST3) { st = 0; ph ^= 1; }
+    }
+    return;
+  }
+
+  // ---------------- consumer warps ----------------
+  if (fin.cost && i0 == 0 && j0 == 0 && ks == 0) {   // fused K4 (see backproject1_kernel)
+    pdl_wait();
+    finalize(fin, s, tid);
+  }
+  // warp w covers a 16 x 8 pixel block (2 x 4 blocks per tile); lane = (pair column pc, row r):
+  // a quarter warp is 4 pair columns x 2 rows; pair p of a thread sits 8 pixels right of pair 0
+  const int wx = w & 1, wy = w >> 1, pc = lane & 3, r = lane >> 2;
+  const int row = 8 * wy + r, jl = j0 + 16 * wx + 2 * pc;      // left pixel of pair 0
+  const float yi = (float)(i0 + row) - ctr;
+  const float xl0 = (float)jl - ctr, xl1 = xl0 + 8.f;
+  // partial sums of the current class: lower pixel (2 taps: float2 per map), upper pixel (3 taps:
+  // float2 + float per map); totals of finished classes per (pair, left/right, map)
+  float2 lm0 = make_float2(0.f, 0.f), ld0 = lm0, ls0 = lm0, hm0 = lm0, hd0 = lm0, hs0 = lm0;
+  float2 lm1 = lm0, ld1 = lm0, ls1 = lm0, hm1 = lm0, hd1 = lm0, hs1 = lm0;
+  float hm30 = 0.f, hd30 = 0.f, hs30 = 0.f, hm31 = 0.f, hd31 = 0.f, hs31 = 0.f;
+  // totals of finished classes in shared memory (this thread's column; touched once per class):
+  // tot[(2 p + side) 3 + map][tid], side 0 = left pixel
+#pragma unroll
+  for (int m = 0; m < 12; ++m) sm.tot[m][tid] = 0.f;
+  int cls = 0;   // 0: cos >= 0, lower pixel = left; 1: cos < 0, lower pixel = right
+  auto flush = [&]() {   // fold the class's partial sums into the per-pixel totals, restart
+    const float L[2][3] = {{lm0.x + lm0.y, ld0.x + ld0.y, ls0.x + ls0.y},
+                           {lm1.x + lm1.y, ld1.x + ld1.y, ls1.x + ls1.y}};
+    const float H[2][3] = {{hm0.x + hm0.y + hm30, hd0.x + hd0.y + hd30, hs0.x + hs0.y + hs30},
+                           {hm1.x + hm1.y + hm31, hd1.x + hd1.y + hd31, hs1.x + hs1.y + hs31}};
+#pragma unroll
+    for (int p = 0; p < 2; ++p)
+#pragma unroll
+      for (int m = 0; m < 3; ++m) {
+        sm.tot[(2 * p) * 3 + m][tid] += cls ? H[p][m] : L[p][m];
+        sm.tot[(2 * p + 1) * 3 + m][tid] += cls ? L[p][m] : H[p][m];
+      }
+    lm0 = ld0 = ls0 = hm0 = hd0 = hs0 = lm1 = ld1 = ls1 = hm1 = hd1 = hs1 = make_float2(0.f, 0.f);
+    hm30 = hd30 = hs30 = hm31 = hd31 = hs31 = 0.f;
+  };
+
+  pdl_wait();   // sleep while K2 runs (this CTA may have launched early)
+  int st = 0;
+  uint32_t ph = 0;
+  for (int c = 0; c < c_hi; ++c) {
+    mbar_wait(&sm.full[st], ph);
+    const int na = min(CH, a_hi - a_lo - c * CH);
+    // the chunk's angles of the current class, then (at most once per CTA) the class change
+    // and the rest: the plan lists cos >= 0 first, so the change is one index per chunk
+    const int nb = cls ? na : min(na, sm.nb[st]);
+    auto angle = [&](int al) {
+      const float4 t1 = sm.t1[st][al], t2 = sm.t2[st][al];
+      const float4 *ar = &sm.a[st][al][0], *br = &sm.b[st][al][0];
+      const float *cr = &sm.c[st][al][0];
+      const float base = fmaf(yi, t1.y, t2.x);   // staged index of the lower pixel's entry, - x term
+      auto pair = [&](float xl, float2 &lm, float2 &ld, float2 &ls, float2 &hm, float2 &hd, float2 &hs,
+                      float &hm3, float &hd3, float &hs3) {
+        const float kst = fmaf(xl, t1.x, base);   // lower pixel's k* + 1 - e0 (> 0)
+        const int k0 = __float2int_rd(kst);
+        const float fr = kst - (float)k0;
+        // lower pixel: taps k0, k0+1; upper pixel (k* + |c'|, |c'| <= 1): taps k0, k0+1, k0+2 with
+        // the tent max(0, 1 - |k - k*|/h) at distances f1, |f1 - 1|, 2 - f1
+        const float2 wl = make_float2(__saturatef(fmaf(-fr, t1.z, 1.f)), __saturatef(fmaf(fr, t1.z, t1.w)));
+        const float f1 = fr + t2.y;
+        const float2 u01 = make_float2(__saturatef(fmaf(-f1, t1.z, 1.f)),
+                                       fminf(__saturatef(fmaf(f1, t1.z, t1.w)), __saturatef(fmaf(-f1, t1.z, t2.w))));
+        const float u2 = __saturatef(fmaf(f1, t1.z, t2.z));
+#ifdef EI_CHECK
+        if (k0 < 0 || k0 >= WL3) atomicAdd(fin.diag, 1);   // debug build: inside the staged window
+#endif
+        const float4 A = ar[k0], B = br[k0];
+        const float C = cr[k0];
+        lm = __ffma2_rn(wl, make_float2(A.x, A.y), lm);
+        ls = __ffma2_rn(wl, make_float2(A.z, A.w), ls);
+        ld = __ffma2_rn(wl, make_float2(B.x, B.y), ld);
+        hm = __ffma2_rn(u01, make_float2(A.x, A.y), hm);
+        hs = __ffma2_rn(u01, make_float2(A.z, A.w), hs);
+        hd = __ffma2_rn(u01, make_float2(B.x, B.y), hd);
+        hm3 = fmaf(u2, B.z, hm3);
+        hd3 = fmaf(u2, B.w, hd3);
+        hs3 = fmaf(u2, C, hs3);
+      };
+      pair(xl0, lm0, ld0, ls0, hm0, hd0, hs0, hm30, hd30, hs30);
+      pair(xl1, lm1, ld1, ls1, hm1, hd1, hs1, hm31, hd31, hs31);
+    };
+#pragma unroll 1
+    for (int al = 0; al < nb; ++al) angle(al);
+    if (nb < na) {   // the class changes inside this chunk (warp-uniform)
+      flush();
+      cls = 1;
+#pragma unroll 1
+      for (int al = nb; al < na; ++al) angle(al);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&sm.empty[st]);
+    if (++st == NST3) { st = 0; ph ^= 1; }
+  }
+  flush();
+#ifdef EI_TRACE
+  asm volatile("bar.sync 2, %0;\n" ::"n"(NT) : "memory");   // consumers only
+  if (tid == 0) SPAN_END_bp(0);
+#endif
+  const int i = i0 + row;
+  if (i >= N) return;
+  const size_t NN = (size_t)N * N;
+#pragma unroll
+  for (int p = 0; p < 2; ++p)
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int j = jl + 8 * p + q;
+      if (j >= N) continue;
+      const size_t px = (size_t)i * N + j;
+      float v0 = sm.tot[(2 * p + q) * 3][tid], v1 = sm.tot[(2 * p + q) * 3 + 1][tid],
+            v2 = sm.tot[(2 * p + q) * 3 + 2][tid];
+      if (KS > 1) {   // angle split: publish partials; ks_reduce_kernel sums them in part order
+        float *pp = part3 + ((size_t)(ks * S + s) * 3) * NN + px;
+        pp[0] = v0;
+        pp[NN] = v1;
+        pp[2 * NN] = v2;
+        continue;
+      }
+      if (mu) {   // cost path: + 2 lambda x (eq. 5); maps have slice stride N*N
+        const size_t ip = (size_t)s * NN + px;
+        const float l2 = 2.f * lambda;
+        v0 = fmaf(l2, __ldg(mu + ip), v0);
+        v1 = fmaf(l2, __ldg(delta + ip), v1);
+        v2 = fmaf(l2, __ldg(sigma + ip), v2);
+      }
+      const size_t oo = (size_t)s * out_stride + px;
+      o0[oo] = v0;
+      o1[oo] = v1;
+      o2[oo] = v2;
+    }
 }
 
 // angle split (KS > 1): fixed-order sum of the KS partial gradients + 2 lambda x (eq. 5), one thread
@@ -404,11 +589,7 @@ __global__ void __launch_bounds__(256) ks_reduce_kernel(const float *__restrict_
 #endif
 }
 
-template <int NMAP>
-cudaError_t launch_bp(const ei_plan &p, const typename Layout<NMAP>::A *GA, const float2 *GB,
-                      const float *mu, const float *delta, const float *sigma, float lambda,
-                      float *o0, float *o1, float *o2, size_t out_stride, const Finalize *fz,
-                      cudaStream_t st) {
+FinArgs fin_args(const ei_plan &p, float lambda, const Finalize *fz) {
   FinArgs fin{};
   fin.diag = p.diag;
   if (fz) {
@@ -423,48 +604,69 @@ cudaError_t launch_bp(const ei_plan &p, const typename Layout<NMAP>::A *GA, cons
     fin.cost = fz->cost;
     fin.g_drift = fz->g_drift;
   }
-  const size_t smem = sizeof(Smem<NMAP>);
-  cudaError_t e = cudaFuncSetAttribute((const void *)backproject_kernel<NMAP, true>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  return fin;
+}
+
+template <class K>
+cudaError_t set_smem(K kt, K kf, size_t smem) {
+  cudaError_t e = cudaFuncSetAttribute((const void *)kt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e == cudaSuccess)
-    e = cudaFuncSetAttribute((const void *)backproject_kernel<NMAP, false>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  const dim3 grid = p.k3u ? dim3(p.n_k3u) : dim3((p.N + TILE - 1) / TILE, (p.N + TILE - 1) / TILE, p.S * p.KS);
-  auto kern = p.k3u ? backproject_kernel<NMAP, true> : backproject_kernel<NMAP, false>;
-  e = launch_pdl(kern, grid, dim3(NT + 32), smem, st, GA, GB, p.tab.k3, p.alist3,
-                 p.NA3, p.N, p.NA, p.ND, mu, delta, sigma, lambda, o0, o1, o2, out_stride, p.S, p.KS, p.part3,
-                 p.PADG, p.RpG, (const int4 *)p.k3u, fin);
-  if (e != cudaSuccess) return e;
-  if (p.KS > 1) {
-    const size_t total = (size_t)p.S * p.N * p.N;
-    const int blocks = (int)std::min<size_t>((total + 255) / 256, 148 * 8);
-    e = launch_pdl(ks_reduce_kernel<NMAP>, dim3(blocks), dim3(256), 0, st, (const float *)p.part3, p.KSk,
-                   p.KSe, p.S, p.N, mu, delta, sigma, lambda, o0, o1, o2, out_stride);
-    if (e != cudaSuccess) return e;
-  }
-  return cudaGetLastError();
+    e = cudaFuncSetAttribute((const void *)kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  return e;
+}
+
+dim3 bp_grid(const ei_plan &p) {
+  return p.k3u ? dim3(p.n_k3u) : dim3((p.N + TILE - 1) / TILE, (p.N + TILE - 1) / TILE, p.S * p.KS);
+}
+
+template <int NMAP>
+cudaError_t launch_ks_reduce(const ei_plan &p, const float *mu, const float *delta, const float *sigma,
+                             float lambda, float *o0, float *o1, float *o2, size_t out_stride,
+                             cudaStream_t st) {
+  if (p.KS <= 1) return cudaSuccess;
+  const size_t total = (size_t)p.S * p.N * p.N;
+  const int blocks = (int)std::min<size_t>((total + 255) / 256, 148 * 8);
+  return launch_pdl(ks_reduce_kernel<NMAP>, dim3(blocks), dim3(256), 0, st, (const float *)p.part3, p.KSk,
+                    p.KSe, p.S, p.N, mu, delta, sigma, lambda, o0, o1, o2, out_stride);
 }
 
 }  // namespace
 
-int bp_pad() { return 64; }   // G row padding (entries) >= window width WL + slack, even
-int bp_tiles(int N) { return ((N + TILE - 1) / TILE) * ((N + TILE - 1) / TILE); }
-int bp_chunks(int NA) { return (NA + CH - 1) / CH; }
-
 cudaError_t launch_backproject3(const ei_plan &p, const float *mu, const float *delta,
                                 const float *sigma, float lambda, float *g_mu, float *g_delta,
-                                float *g_sigma, size_t out_stride, const Finalize *fin,
+                                float *g_sigma, size_t out_stride, const Finalize *fz,
                                 cudaStream_t st) {
-  return launch_bp<3>(p, p.GA, p.GB, mu, delta, sigma, lambda, g_mu, g_delta, g_sigma, out_stride, fin,
-                      st);
+  const FinArgs fin = fin_args(p, lambda, fz);
+  cudaError_t e = set_smem(backproject3_kernel<true>, backproject3_kernel<false>, sizeof(Smem3));
+  if (e != cudaSuccess) return e;
+  auto kern = p.k3u ? backproject3_kernel<true> : backproject3_kernel<false>;
+  e = launch_pdl(kern, bp_grid(p), dim3(NT + 32), sizeof(Smem3), st, (const float4 *)p.GA,
+                 (const float4 *)p.GB, (const float *)p.GC, p.tab.k3, p.alist3, p.NA3, p.N, p.NA, p.ND, mu,
+                 delta, sigma, lambda, g_mu, g_delta, g_sigma, out_stride, p.S, p.KS, p.part3, p.PADG,
+                 p.RpG, (const int4 *)p.k3u, fin);
+  if (e == cudaSuccess)
+    e = launch_ks_reduce<3>(p, mu, delta, sigma, lambda, g_mu, g_delta, g_sigma, out_stride, st);
+  return e == cudaSuccess ? cudaGetLastError() : e;
 }
 
 cudaError_t launch_backproject1(const ei_plan &p, float *map, cudaStream_t st, const float *h,
-                                float lambda, const Finalize *fin) {
-  return launch_bp<1>(p, p.GA1, nullptr, h, nullptr, nullptr, lambda, map, nullptr, nullptr,
-                      (size_t)p.N * p.N, fin, st);
+                                float lambda, const Finalize *fz) {
+  const FinArgs fin = fin_args(p, lambda, fz);
+  cudaError_t e = set_smem(backproject1_kernel<true>, backproject1_kernel<false>, sizeof(Smem1));
+  if (e != cudaSuccess) return e;
+  const size_t os = (size_t)p.N * p.N;
+  auto kern = p.k3u ? backproject1_kernel<true> : backproject1_kernel<false>;
+  e = launch_pdl(kern, bp_grid(p), dim3(NT + 32), sizeof(Smem1), st, (const float2 *)p.GA1, p.tab.k3,
+                 p.alist3, p.NA3, p.N, p.NA, p.ND, h, lambda, map, os, p.S, p.KS, p.part3, p.PADG, p.RpG,
+                 (const int4 *)p.k3u, fin);
+  if (e == cudaSuccess)
+    e = launch_ks_reduce<1>(p, h, nullptr, nullptr, lambda, map, nullptr, nullptr, os, st);
+  return e == cudaSuccess ? cudaGetLastError() : e;
 }
+
+int bp_pad() { return 64; }   // G row padding (entries) >= window width WL3 + 12, multiple of 4
+int bp_tiles(int N) { return ((N + TILE - 1) / TILE) * ((N + TILE - 1) / TILE); }
+int bp_chunks(int NA) { return (NA + CH - 1) / CH; }
 
 }  // namespace ei
 

@@ -100,8 +100,8 @@ struct K2Args {
   int vec_smod;              // forward modes: s_mod rows 16-B aligned (float4 stores)
   float zs, inv_du;          // shift factor: z (three-map model) or z gamma (single-map model)
   float *s_mod;              // forward modes
-  float4 *GA;                // MODE 1: pair-layout gradient sinograms (K3 input)
-  float2 *GB;
+  float4 *GA, *GB;           // MODE 1: triple-layout gradient sinograms (K3 input)
+  float *GC;
   float2 *GA1;               // MODES 2, 4: pair-layout gradient sinogram of h
   int PADG, RpG;
   const float4 *k3;          // per-angle table, .w = Joseph weight dx/|c_dom|
@@ -518,10 +518,13 @@ __global__ void __launch_bounds__(K2_MAXT + 32, 2) curve_kernel(K2Args g) {
         g.part_mo[pidx] = wm_;
       }
       asm volatile("bar.sync 1, %0;\n" ::"r"(NT) : "memory");   // consumers only
-      // pair entries e = (g[e-1], g[e]) of this segment's core, e in [segW, segW + cw) and the
-      // closing entry N_d after the last segment, lane-contiguous (consecutive lanes write
-      // consecutive entries: fully used 16-B / 8-B store sectors), from the exchange rows:
-      // g_delta[q] = zs D^T g_Delta = (z / 2du) (g'[q-1] - g'[q+1]) on the ghost-extended g'
+      // K3's input entries of this segment's core, lane-contiguous (consecutive lanes write
+      // consecutive entries: fully used store sectors), from the exchange rows, pre-multiplied by
+      // the Joseph weight; g_delta[q] = zs D^T g_Delta = (z / 2du) (g'[q-1] - g'[q+1]) on the
+      // ghost-extended g'.  Single map: PAIR entries e = (g[e-1], g[e]), e in [segW, segW + cw) and
+      // the closing entry N_d after the last segment.  Three maps: TRIPLE entries e = positions
+      // e-1, e, e+1 of every map (k_backproject.cu), e in [segW, segW + cw), plus e = -1 before the
+      // first and e = N_d after the last segment
       {
         const int segW = seg * g.W, cw = min(g.W, ND - segW);
         const float *xd = xch + buf * 3 * WB - kb;   // g'_Delta by detector position
@@ -530,16 +533,22 @@ __global__ void __launch_bounds__(K2_MAXT + 32, 2) curve_kernel(K2Args g) {
         const float sc = __ldg(g.k3 + a).w;
         const size_t rb = (size_t)row * g.RpG + g.PADG;
         const int eend = segW + cw + (segW + cw == ND ? 1 : 0);
-        for (int e = segW + t; e < eend; e += NT) {
-          const bool lo = e >= 1, hi = e < ND;
-          const float m0 = lo ? xm[e - 1] : 0.f, m1 = hi ? xm[e] : 0.f;
-          const float d0 = lo ? zh * (xd[e - 2] - xd[e]) : 0.f, d1 = hi ? zh * (xd[e - 1] - xd[e + 1]) : 0.f;
-          if (Mode<MODE>::h) {   // dS/dP_h = g_mu + z gamma D^T g_Delta (eq. 4 chain rule)
+        if (Mode<MODE>::h) {   // dS/dP_h = g_mu + z gamma D^T g_Delta (eq. 4 chain rule)
+          for (int e = segW + t; e < eend; e += NT) {
+            const bool lo = e >= 1, hi = e < ND;
+            const float m0 = lo ? xm[e - 1] : 0.f, m1 = hi ? xm[e] : 0.f;
+            const float d0 = lo ? zh * (xd[e - 2] - xd[e]) : 0.f, d1 = hi ? zh * (xd[e - 1] - xd[e + 1]) : 0.f;
             g.GA1[rb + e] = make_float2(sc * (m0 + d0), sc * (m1 + d1));
-          } else {
-            const float s0 = lo ? xs[e - 1] : 0.f, s1 = hi ? xs[e] : 0.f;
-            g.GA[rb + e] = make_float4(sc * m0, sc * m1, sc * d0, sc * d1);
-            g.GB[rb + e] = make_float2(sc * s0, sc * s1);
+          }
+        } else {
+          auto in = [&](int q) { return (unsigned)q < (unsigned)ND; };
+          auto M = [&](int q) { return in(q) ? sc * xm[q] : 0.f; };
+          auto Sg = [&](int q) { return in(q) ? sc * xs[q] : 0.f; };
+          auto Dl = [&](int q) { return in(q) ? sc * zh * (xd[q - 1] - xd[q + 1]) : 0.f; };
+          for (int e = segW - (segW == 0 ? 1 : 0) + t; e < eend; e += NT) {
+            g.GA[rb + e] = make_float4(M(e - 1), M(e), Sg(e - 1), Sg(e));
+            g.GB[rb + e] = make_float4(Dl(e - 1), Dl(e), M(e + 1), Dl(e + 1));
+            g.GC[rb + e] = Sg(e + 1);
           }
         }
       }
@@ -595,6 +604,7 @@ cudaError_t launch(const ei_plan &p, const float *flat, const float *mask, const
   g.s_mod = s_mod;
   g.GA = p.GA;
   g.GB = p.GB;
+  g.GC = p.GC;
   g.GA1 = p.GA1;
   g.PADG = p.PADG;
   g.RpG = p.RpG;

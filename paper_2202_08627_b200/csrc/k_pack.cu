@@ -147,26 +147,31 @@ __global__ void __launch_bounds__(256) pack_pairs_kernel(const float *__restrict
 
 // planar sino [S][NMAP][NA][ND] -> pair layout [S][NA][ND+1] (entry e = (g[e-1], g[e]))
 // (each value pre-multiplied by the angle's Joseph weight dx/|c_dom|, as K2 does)
+// ei_backproject's input sinograms -> K3's layout, pre-multiplied by the Joseph weight: three
+// maps the TRIPLE layout (entries e = -1..ND: positions e-1, e, e+1 of every map, see
+// ei_common.cuh), one map the PAIR layout (entries e = 0..ND: (g[e-1], g[e])).  One thread per
+// (slice, angle, entry).
 template <int NMAP>
 __global__ void pack_sino_kernel(const float *__restrict__ in, int NA, int ND, int S,
-                                 float4 *__restrict__ GA, float2 *__restrict__ GB,
-                                 float2 *__restrict__ GA1, const float4 *__restrict__ k3, int PADG,
-                                 int RpG) {
-  const size_t plane = (size_t)NA * ND, rl = (size_t)ND + 1;
+                                 float4 *__restrict__ GA, float4 *__restrict__ GB,
+                                 float *__restrict__ GC, float2 *__restrict__ GA1,
+                                 const float4 *__restrict__ k3, int PADG, int RpG) {
+  const size_t plane = (size_t)NA * ND, rl = (size_t)ND + 2;   // entries -1..ND
   const size_t total = (size_t)S * NA * rl;
   for (size_t t = blockIdx.x * (size_t)blockDim.x + threadIdx.x; t < total;
        t += (size_t)gridDim.x * blockDim.x) {
     const size_t sa = t / rl;
-    const int e = (int)(t - sa * rl);
+    const int e = (int)(t - sa * rl) - 1;
     const size_t o = sa * (size_t)RpG + PADG + e;
     const size_t s = sa / NA, a = sa - s * NA;
     const float *b = in + s * NMAP * plane + a * ND;
     const float sc = __ldg(k3 + a).w;
     auto at = [&](int m, int k) { return (k >= 0 && k < ND) ? sc * __ldg(b + m * plane + k) : 0.f; };
     if (NMAP == 3) {
-      GA[o] = make_float4(at(0, e - 1), at(0, e), at(1, e - 1), at(1, e));
-      GB[o] = make_float2(at(2, e - 1), at(2, e));
-    } else {
+      GA[o] = make_float4(at(0, e - 1), at(0, e), at(2, e - 1), at(2, e));
+      GB[o] = make_float4(at(1, e - 1), at(1, e), at(0, e + 1), at(1, e + 1));
+      GC[o] = at(2, e + 1);
+    } else if (e >= 0) {
       GA1[o] = make_float2(at(0, e - 1), at(0, e));
     }
   }
@@ -175,31 +180,35 @@ __global__ void pack_sino_kernel(const float *__restrict__ in, int NA, int ND, i
 
 // Mirror-pair fold (360-degree scans): the angle theta + pi sees the same lines as theta with the
 // detector mirrored, k -> ND-1-k (R6), so R^T g = sum over primaries of R_theta^T (g_theta +
-// mirror(g_{theta+pi})).  In the pair layout (entry e = (g[e-1], g[e])) the mirrored row's entry e
-// is the partner's entry ND-e with its two taps swapped.  In place on the primary rows; one thread
-// per (slice, pair, entry).
+// mirror(g_{theta+pi})).  In place on the primary rows (a); the partner's (b) value at position k
+// is the centre of its entry k: g_b(k) = m: GA.y, d: GB.y, s: GA.w (three maps).  Three maps,
+// entry e (positions e-1, e, e+1) gains g_b at ND-e, ND-1-e, ND-2-e; one map, entry e (positions
+// e-1, e) gains the partner's entry ND-e with its two taps swapped.  Partner entries outside -1..ND lie in the zero
+// padding.  One thread per (slice, pair, entry).
 template <int NMAP>
 __global__ void __launch_bounds__(256) fold_kernel(const int2 *__restrict__ pairs, int npairs, int NA,
                                                    int ND, int S, float4 *__restrict__ GA,
-                                                   float2 *__restrict__ GB, float2 *__restrict__ GA1,
-                                                   int PADG, int RpG) {
+                                                   float4 *__restrict__ GB, float *__restrict__ GC,
+                                                   float2 *__restrict__ GA1, int PADG, int RpG) {
   pdl_wait();   // K2's (or pack_sino's) gradient rows
-  const long long rl = ND + 1, total = (long long)S * npairs * rl;
+  const long long rl = ND + 2, total = (long long)S * npairs * rl;
   for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < total;
        t += (long long)gridDim.x * blockDim.x) {
-    const int e = (int)(t % rl);
+    const int e = (int)(t % rl) - 1;
     const long long sp = t / rl;
     const int q = (int)(sp % npairs), s = (int)(sp / npairs);
     const int2 ab = __ldg(pairs + q);
     const size_t oa = ((size_t)s * NA + ab.x) * RpG + PADG + e;
-    const size_t ob = ((size_t)s * NA + ab.y) * RpG + PADG + (ND - e);
+    const size_t ob = ((size_t)s * NA + ab.y) * RpG + PADG;   // partner row, entry 0
     if (NMAP == 3) {
-      const float4 x = GA[oa], y = GA[ob];
-      GA[oa] = make_float4(x.x + y.y, x.y + y.x, x.z + y.w, x.w + y.z);
-      const float2 u = GB[oa], v = GB[ob];
-      GB[oa] = make_float2(u.x + v.y, u.y + v.x);
-    } else {
-      const float2 u = GA1[oa], v = GA1[ob];
+      const float4 b0 = GA[ob + ND - e], b1 = GA[ob + ND - 1 - e], b2 = GA[ob + ND - 2 - e];
+      const float4 c0 = GB[ob + ND - e], c1 = GB[ob + ND - 1 - e], c2 = GB[ob + ND - 2 - e];
+      const float4 x = GA[oa], y = GB[oa];
+      GA[oa] = make_float4(x.x + b0.y, x.y + b1.y, x.z + b0.w, x.w + b1.w);
+      GB[oa] = make_float4(y.x + c0.y, y.y + c1.y, y.z + b2.y, y.w + c2.y);
+      GC[oa] += b2.w;
+    } else if (e >= 0) {   // partner entry ND-e = (g_b(ND-e-1), g_b(ND-e)), taps swapped
+      const float2 u = GA1[oa], v = GA1[ob + ND - e];
       GA1[oa] = make_float2(u.x + v.y, u.y + v.x);
     }
   }
@@ -210,13 +219,14 @@ __global__ void __launch_bounds__(256) fold_kernel(const int2 *__restrict__ pair
 
 cudaError_t launch_fold(const ei_plan &p, int n_maps, cudaStream_t st) {
   if (p.npairs == 0) return cudaSuccess;
-  const long long total = (long long)p.S * p.npairs * (p.ND + 1);
+  const long long total = (long long)p.S * p.npairs * (p.ND + 2);
   const int blocks = (int)std::min<long long>((total + 255) / 256, 148 * 8);
   if (n_maps == 3)
     return launch_pdl(fold_kernel<3>, dim3(blocks), dim3(256), 0, st, (const int2 *)p.pairs, p.npairs,
-                      p.NA, p.ND, p.S, p.GA, p.GB, (float2 *)nullptr, p.PADG, p.RpG);
+                      p.NA, p.ND, p.S, p.GA, p.GB, p.GC, (float2 *)nullptr, p.PADG, p.RpG);
   return launch_pdl(fold_kernel<1>, dim3(blocks), dim3(256), 0, st, (const int2 *)p.pairs, p.npairs,
-                    p.NA, p.ND, p.S, (float4 *)nullptr, (float2 *)nullptr, p.GA1, p.PADG, p.RpG);
+                    p.NA, p.ND, p.S, (float4 *)nullptr, (float4 *)nullptr, (float *)nullptr, p.GA1, p.PADG,
+                    p.RpG);
 }
 
 int reg_blocks(int N) { return ((N + 1 + T - 1) / T) * ((N + 1 + T - 1) / T); }
@@ -249,14 +259,14 @@ cudaError_t launch_pack1(const ei_plan &p, const float *map, cudaStream_t st, bo
 }
 
 cudaError_t launch_pack_sino(const ei_plan &p, const float *sino, int n_maps, cudaStream_t st) {
-  const size_t total = (size_t)p.S * p.NA * (p.ND + 1);
+  const size_t total = (size_t)p.S * p.NA * (p.ND + 2);
   const int blocks = (int)((total + 255) / 256 < 148 * 16 ? (total + 255) / 256 : 148 * 16);
   if (n_maps == 3)
-    pack_sino_kernel<3><<<blocks, 256, 0, st>>>(sino, p.NA, p.ND, p.S, p.GA, p.GB, nullptr, p.tab.k3,
-                                                p.PADG, p.RpG);
+    pack_sino_kernel<3><<<blocks, 256, 0, st>>>(sino, p.NA, p.ND, p.S, p.GA, p.GB, p.GC, nullptr,
+                                                p.tab.k3, p.PADG, p.RpG);
   else
-    pack_sino_kernel<1><<<blocks, 256, 0, st>>>(sino, p.NA, p.ND, p.S, nullptr, nullptr, p.GA1, p.tab.k3,
-                                                p.PADG, p.RpG);
+    pack_sino_kernel<1><<<blocks, 256, 0, st>>>(sino, p.NA, p.ND, p.S, nullptr, nullptr, nullptr, p.GA1,
+                                                p.tab.k3, p.PADG, p.RpG);
   return cudaGetLastError();
 }
 

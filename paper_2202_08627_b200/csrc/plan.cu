@@ -69,7 +69,7 @@ void free_plan(ei_plan *p) {
     if (ev) cudaEventDestroy(ev);
   void *ptrs[] = {p->tab.k1, p->tab.k3, p->proj.groups, p->proj.order, p->proj.partner, p->alist3,
                   p->pairs, p->proj.win1, p->proj.winRS, p->proj.unit1, p->proj.unitRS, p->MA, p->MAT, p->MB,
-                  p->MBT, p->M1, p->M1T, p->diag, p->part_mo, p->part3, p->k3u, p->P, p->GA, p->GB, p->GA1,
+                  p->MBT, p->M1, p->M1T, p->diag, p->part_mo, p->part3, p->k3u, p->P, p->GA, p->GB, p->GC, p->GA1,
                   p->part_curve, p->part_reg, p->h_maps, p->h_flat, p->h_mask, p->h_drift,
                   p->h_sexp, p->h_grad, p->h_cost, p->h_status};
   for (void *q : ptrs)
@@ -203,11 +203,12 @@ int ei_plan_create(const ei_geometry *geom, const double *angles, ei_plan **out)
   A(dalloc(&p->M1T, S * NP));
   A(dalloc(&p->diag, 1));
   p->PADG = ei::bp_pad();
-  p->RpG = (p->ND + 1 + 2 * p->PADG + 1) & ~1;
+  p->RpG = (p->ND + 2 + 2 * p->PADG + 3) & ~3;   // multiple of 4: 16-B aligned C-plane rows
   const size_t SINO1 = (size_t)p->NA * p->RpG;
   A(dalloc(&p->P, (size_t)p->proj.RS * S * 3 * SINO));
   A(dalloc(&p->GA, S * SINO1));
   A(dalloc(&p->GB, S * SINO1));
+  A(dalloc(&p->GC, S * SINO1));
   A(dalloc(&p->GA1, S * SINO1));
   A(dalloc(&p->part_curve, S * NA * p->k2.nseg * p->k2.nw));
   A(dalloc(&p->part_mo, S * NA * p->k2.nseg * p->k2.nw));
@@ -272,8 +273,12 @@ int ei_plan_create(const ei_geometry *geom, const double *angles, ei_plan **out)
     A(cudaMemcpy(p->proj.order, order.data(), sizeof(int) * order.size(), cudaMemcpyHostToDevice));
   if (e == cudaSuccess)
     A(cudaMemcpy(p->proj.partner, partner.data(), sizeof(int) * NA, cudaMemcpyHostToDevice));
-  if (e == cudaSuccess)
-    A(cudaMemcpy(p->alist3, prim.data(), sizeof(int) * prim.size(), cudaMemcpyHostToDevice));
+  {   // K3's angle list: cos >= 0 first (the pixel-pair roles of the three-map adjoint flip with
+      // the sign of cos, k_backproject.cu), each class in angle-index order
+    std::vector<int> al(prim);
+    std::stable_sort(al.begin(), al.end(), [&](int x, int y) { return (cos(angles[x]) < 0) < (cos(angles[y]) < 0); });
+    if (e == cudaSuccess) A(cudaMemcpy(p->alist3, al.data(), sizeof(int) * al.size(), cudaMemcpyHostToDevice));
+  }
   if (e == cudaSuccess && !pairs.empty())
     A(cudaMemcpy(p->pairs, pairs.data(), sizeof(int2) * pairs.size(), cudaMemcpyHostToDevice));
   if (e == cudaSuccess) A(cudaMemset(p->diag, 0, sizeof(int32_t)));
@@ -286,7 +291,8 @@ int ei_plan_create(const ei_geometry *geom, const double *angles, ei_plan **out)
   for (void *q : {(void *)p->MB, (void *)p->MBT, (void *)p->M1, (void *)p->M1T})
     if (e == cudaSuccess) A(cudaMemset(q, 0, sizeof(float2) * S * NP));
   if (e == cudaSuccess) A(cudaMemset(p->GA, 0, sizeof(float4) * S * SINO1));   // zero padding
-  if (e == cudaSuccess) A(cudaMemset(p->GB, 0, sizeof(float2) * S * SINO1));
+  if (e == cudaSuccess) A(cudaMemset(p->GB, 0, sizeof(float4) * S * SINO1));
+  if (e == cudaSuccess) A(cudaMemset(p->GC, 0, sizeof(float) * S * SINO1));
   if (e == cudaSuccess) A(cudaMemset(p->GA1, 0, sizeof(float2) * S * SINO1));
   if (e == cudaSuccess)
     A(cudaMemcpy(p->proj.win1, win1.data(), sizeof(int2) * win1.size(), cudaMemcpyHostToDevice));

@@ -19,7 +19,8 @@ optimizer parameters):
     bracketing + Alg. 3.6 zoom, safeguarded cubic interpolation; c1 = 1e-4, c2 = 0.9, first
     trial step 1), so every stored pair has <s, y> > 0;
   * a problem stops when (a) its relative cost decrease over an accepted step is below rel_tol
-    ("rel_tol"), (b) its cost reaches `target` (a discrepancy-principle stop for
+    ("rel_tol"; a step along an L-BFGS direction that falls below it first drops the
+    history, and the decision is taken on the following steepest-descent step), (b) its cost reaches `target` (a discrepancy-principle stop for
     noisy data, e.g. Morozov's S <= tau * sum s_exp for Poisson counts: "target"), (c) the line
     search finds no decrease even along steepest descent ("precision": the cost is at the
     resolution of the fp32 model), or (d) max_iter ("max_iter", converged = False).
@@ -235,7 +236,7 @@ def minimize(fg: Callable, x0: Union[torch.Tensor, Sequence[torch.Tensor]], max_
             r = [rb + sb * _bc(a_k - b_k, rb) for rb, sb in zip(r, Sh[k])]
         p = [-rb for rb in r]
         d0 = _sdot_r(g, p)
-        sd_dir = [-gb * _bc(1.0 / gnorm[b], gb) for b, gb in enumerate(g)]
+        sd_dir = [-gb * _bc(scal[b], gb) for b, gb in enumerate(g)]   # scaled steepest descent
         bad = d0 >= 0                          # not a descent direction: steepest descent
         p = _where(bad, sd_dir, p)
         d0 = torch.where(bad, _sdot_r(g, p), d0)
@@ -250,6 +251,13 @@ def minimize(fg: Callable, x0: Union[torch.Tensor, Sequence[torch.Tensor]], max_
         failed = active & ~ok
         for s in np.nonzero(failed & sd_now)[0]:
             done[s], reason[s] = True, "precision"
+        # an accepted step below rel_tol along an L-BFGS direction may be a poor direction (a stale
+        # or noisy curvature history) rather than convergence: drop the history and take the rel_tol
+        # decision on the next, steepest-descent step
+        rel = (fh - f_new) / np.maximum(np.abs(fh), 1e-300)
+        acc = ok & active
+        hit = acc & ((f_new <= tgt) if tgt is not None else np.zeros(S, bool))
+        stall = acc & ~hit & (rel < rel_tol) & ~sd_now
         okt = torch.from_numpy(ok & active).to(dev)
         s_vec = [xn - xb for xn, xb in zip(x_new, x)]
         y_vec = [gn - gb for gn, gb in zip(g_new, g)]
@@ -261,22 +269,21 @@ def minimize(fg: Callable, x0: Union[torch.Tensor, Sequence[torch.Tensor]], max_
         rho.append(torch.where(keep, 1.0 / sy.clamp_min(1e-300), torch.zeros_like(sy)))
         if len(Sh) > m:
             Sh.pop(0), Yh.pop(0), rho.pop(0)
-        reset = torch.from_numpy(failed).to(dev)        # drop the history of problems that failed
+        reset = torch.from_numpy(failed | stall).to(dev)   # drop the history: failed or stalled
         rho = [rk * (~reset).to(rk.dtype) for rk in rho]
         gb_ = _bdot_r(s_vec, y_vec) / _bdot_r(y_vec, y_vec).clamp_min(1e-300)
         gg = (sy / yy.clamp_min(1e-300)).unsqueeze(0).expand_as(gb_)
         gb_ = torch.where(gb_ > 0, gb_, gg)             # block secant not positive: global scalar
         gamma = torch.where(keep.unsqueeze(0), gb_, gamma)
-        has_gamma = (has_gamma & ~reset) | keep
-        rel = (fh - f_new) / np.maximum(np.abs(fh), 1e-300)
-        acc = ok & active
+        has_gamma = has_gamma | keep    # a reset keeps the block scaling: the restart direction is
+        # -gamma_b g_b, not a unit step (which overshoots badly scaled blocks by orders of magnitude)
         iters[acc] += 1
         for s in np.nonzero(acc)[0]:
-            if tgt is not None and f_new[s] <= tgt[s]:
+            if hit[s]:
                 done[s], reason[s] = True, "target"
-            elif rel[s] < rel_tol:
+            elif rel[s] < rel_tol and not stall[s]:
                 done[s], reason[s] = True, "rel_tol"
-        sd = failed & ~done
+        sd = (failed | stall) & ~done
         x, g = x_new, g_new
         fh = np.where(acc, f_new, fh)
         f = torch.from_numpy(fh.copy()).to(dev)

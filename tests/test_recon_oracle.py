@@ -1,9 +1,9 @@
 """NEXT-1 / NEXT-2 on the CPU: the host L-BFGS loop (paper_2202_08627_b200/lbfgs.py) driven by the
 fp64 ORACLE's cost and gradient — the same objective the GPU path evaluates.
 
-* cross-check against SciPy's L-BFGS-B (the optimizer the paper used) on a strongly
-  regularised, hence well-conditioned and strictly convex, small instance: both reach the same
-  minimum (final costs within 1e-6 relative);
+* cross-check against SciPy's L-BFGS-B (the optimizer the paper used) on the C1
+  problem made strongly regularised, hence well-conditioned and strictly convex: both reach the
+  same minimum (final costs within 1e-6 relative; measured 6e-11);
 * noise-free C1 from x0 = 0 (BASELINE.json configs[0]): RMS error < 2 % of each map's dynamic
   range, 2-pixel border excluded (SPEC.md:284, :562 acceptance 9);
 * Poisson C1 with the discrepancy-principle stop (cost <= sum of the measured counts, the
@@ -21,11 +21,12 @@ import _cases
 
 
 def test_scipy_lbfgsb_same_minimum():
+    """C1 (BASELINE.json configs[0], Poisson data) with lambda = 1e10: the regulariser dominates
+    the data term's curvature, so the minimum is unique and both optimizers reach it."""
     import scipy.optimize as so
-    cfg = synth.small_config("SC", S=1, N=24, n_angles=34, span_deg=180.0, n_det=36, M=5, K=6,
-                             drift_sd=0.0, w_jit=0.0, texture=0.0, seed=1234)
-    case = _cases.oracle_case(cfg)
-    lam = 1e10          # dominates the data term's curvature: a unique, well-conditioned minimum
+    case = _cases.cached_case("C1")
+    cfg = case.cfg
+    lam = 1e10
     fg = _cases.oracle_objective(case, lam)
     N = cfg.N
 

@@ -52,7 +52,7 @@ EOF
         timeout 900 python bench.py --config $c --steps 3 --warmup 3 --no-cpu-baseline > $OUT/plain_full_$c.log 2>&1 &&
         timeout 900 ncu --set full --metrics lts__t_bytes.sum,l1tex__t_bytes.sum --clock-control none \
           --import-source on --kernel-name-base demangled --nvtx --nvtx-include "timed/" \
-          -k regex:"project_kernel<\\(int\\)3|curve_kernel<\\(int\\)1>" -c 3 \
+          -k regex:"project_kernel<\\(int\\)3|curve_kernel<\\(int\\)1>|backproject3_kernel" -c 3 \
           -o $OUT/full_$c python bench.py --config $c --steps 3 --warmup 3 --no-cpu-baseline > $OUT/ncu_full_$c.log 2>&1
         echo "ncu full $c rc=$?" | tee -a $OUT/rc.txt
       done ;;

@@ -7,7 +7,8 @@ import csv
 import sys
 from collections import OrderedDict
 
-OURS = ("pack_pairs_kernel", "check_small_kernel", "backproject_kernel", "project_kernel", "curve_kernel",
+OURS = ("pack_pairs_kernel", "check_small_kernel", "backproject3_kernel", "backproject1_kernel",
+        "backproject_kernel", "project_kernel", "curve_kernel",
         "pack_sino_kernel", "ks_reduce_kernel", "fold_kernel")   # backproject before project: substring match
 
 

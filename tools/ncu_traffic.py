@@ -12,7 +12,8 @@ import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-NAMES = (("backproject_kernel<3", "K3_backproject"), ("project_kernel<3", "K1_project"),
+NAMES = (("backproject3_kernel", "K3_backproject"), ("backproject_kernel<3", "K3_backproject"),
+         ("project_kernel<3", "K1_project"),
          ("curve_kernel<1>", "K2_curve"), ("pack_pairs_kernel<3>", "K0_pack"))   # K1/K3 have 2 template args
 SCALE = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 

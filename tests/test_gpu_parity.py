@@ -85,7 +85,9 @@ def test_backproject_parity(ei, name):
         for q in range(3):
             ref = ora.backproject(y[s, q].astype(np.float64), cfg.angles, cfg.N, cfg.pixel, cfg.det_pitch)
             assert rel_l2(got[s, q], ref) < 2e-5, (s, q)
-        assert np.array_equal(got1[s, 0], got[s, 2])
+        # the single-map adjoint (pair layout) and the three-map one (triple layout, pixel pairs)
+        # compute the same operator with different fp32 roundings
+        assert rel_l2(got1[s, 0], got[s, 2]) < 1e-6
 
 
 @pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4", "C5", "R1", "R2"])

@@ -27,7 +27,7 @@ import json, sys
 try:
     d = json.loads(open(sys.argv[1]).read().strip().splitlines()[-1])
     k = d.get("kernels", {})   # P1's line has no per-kernel split
-    print(d["config"]["workload"][:3], "ms/step %.4f" % d["ms_per_step"], "e2e %.1f" % d["e2e"]["value"],
+    print(d["config"]["workload"][:3], "ms/step %.4f" % d["ms_per_step"], "e2e %.1f" % (d.get("e2e") or {}).get("value", 0.0),
           " ".join("%s %.4fms %.3f" % (n, v["ms"], v.get("frac", 0)) for n, v in k.items()))
 except Exception as e:
     print("parse fail", e)

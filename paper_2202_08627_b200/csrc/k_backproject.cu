@@ -260,7 +260,7 @@ SPAN_START_bp();
   int st = 0;
   uint32_t ph = 0;
   for (int c = c_lo; c < c_hi; ++c) {
-    mbar_wait(&sm.full[st], ph);
+    mbar_wait_full(&sm.full[st], ph);
 #ifdef EI_TRACE
     if (c == c_lo) t_data = gtimer3();
 #endif
@@ -452,7 +452,7 @@ SPAN_START_bp();
   int st = 0;
   uint32_t ph = 0;
   for (int c = 0; c < c_hi; ++c) {
-    mbar_wait(&sm.full[st], ph);
+    mbar_wait_full(&sm.full[st], ph);
     const int na = min(CH, a_hi - a_lo - c * CH);
     // the chunk's angles of the current class, then (at most once per CTA) the class change
     // and the rest: the plan lists cos >= 0 first, so the change is one index per chunk

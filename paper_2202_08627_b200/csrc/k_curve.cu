@@ -265,7 +265,7 @@ __global__ void __launch_bounds__(K2_MAXT + 32, 2) curve_kernel(K2Args g) {
     const int row = s * g.NA + a;
     const float mo = g.drift ? __ldg(g.drift + a) : 0.f;
     if (item == i0) pdl_wait();   // sleep while K1 runs (this CTA may have launched early)
-    mbar_wait(&full[st], ph);
+    mbar_wait_full(&full[st], ph);
     const float *stg = ring + st * stage_floats;   // staged rows of this item
     float4 gm4 = make_float4(0.f, 0.f, 0.f, 0.f), gd4 = gm4, gs4 = gm4;
     float cost = 0.f, gmo = 0.f;

@@ -172,7 +172,7 @@ SPAN_START_proj();
       int st = 0;
       uint32_t ph = 0;
       for (int c = 0; c < nch; ++c) {
-        if (c >= NST) mbar_wait(&empty[st], ph ^ 1);
+        if (c >= NST) mbar_wait_sleep(&empty[st], ph ^ 1);
         const int2 wn = swin[c];
         const int i0 = r0 + c * RC, rc = min(RC, r1 - i0);
         const int e0 = wn.x + 1;                       // first staged entry
@@ -241,7 +241,7 @@ SPAN_START_proj();
   int st = 0;
   uint32_t ph = 0;
   for (int c = 0; c < nch; ++c, st = (st + 1 == NST) ? 0 : st + 1, ph ^= (st == 0)) {
-    mbar_wait(&full[st], ph);
+    mbar_wait_full(&full[st], ph);
     const int2 wn = swin[c];
     const int i0 = r0 + c * RC, rc = min(RC, r1 - i0), i1 = i0 + rc - 1;
     bool any = false, all = true;

@@ -1,15 +1,16 @@
 """Regenerate DESIGN.md §9's status table from committed bench lines:
-    python tools/status_table.py v6"""
+    python tools/status_table.py v12 [r02]"""
 import json
 import os
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-tag = sys.argv[1] if len(sys.argv) > 1 else "v6"
+tag = sys.argv[1] if len(sys.argv) > 1 else "v12"
+rnd = sys.argv[2] if len(sys.argv) > 2 else "r02"
 
 
 def line(c):
-    return json.loads(open(os.path.join(ROOT, "profiles", "r01", "bench_%s_%s.json" % (c, tag))).read().splitlines()[-1])
+    return json.loads(open(os.path.join(ROOT, "profiles", rnd, "bench_%s_%s.json" % (c, tag))).read().splitlines()[-1])
 
 
 rows = []

@@ -28,16 +28,19 @@ struct ProjPlan {
   int *order = nullptr;     // device: sorted position -> angle index (row-dominant first)
   int *partner = nullptr;   // device [NA]: the angle theta + pi of a projected angle, or -1
   int n_groups = 0;
-  int RC = 0;               // rows per staged chunk
   int RT = 64;              // rays per K1 CTA (64, or 32 for small single-wave grids)
   int k0_early = 0;         // K0 triggers K1's launch at its start (K1 grid smaller than the SMs)
   int nst = 4;              // K1 ring stages
+  int E = 0;                // K1 ring-stage capacity (entries; rows x stride of a chunk <= E)
   int ray_fast = 0;         // number of angle groups using the ray-fastest consumer lane mapping
-  int CW = 0;               // window width bound (entries)
+  int rcmax = 0;            // most rows of a chunk (diagnostics)
+  int wmax = 0;             // widest chunk window (entries)
   int RS = 1;               // row split of the cost path (partial P summed by K2)
-  int2 *win1 = nullptr;     // device window table for RS = 1  [groups][tiles][nch1]
-  int2 *winRS = nullptr;    // device window table for RS      [RS][groups][tiles][nchRS]
-  int nch1 = 0, nchRS = 0;
+  int4 *chunks1 = nullptr;  // device chunk tables {first entry - 1, W, first row, rows}, RS = 1,
+  int *coff1 = nullptr;     //   CSR offsets per unit (group, tile)
+  int4 *chunksRS = nullptr; // the same for the row-split cost path, units (rs, group, tile)
+  int *coffRS = nullptr;
+  int nchmax1 = 0, nchmaxRS = 0;   // most chunks of one unit
   int n_tiles = 0;          // ray tiles per angle group
   int *unit1 = nullptr;     // device: CTA -> work unit (tile, group, slice) for RS = 1 (launch order)
   int *unitRS = nullptr;    // device: the same for the row-split cost path
@@ -162,8 +165,10 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
 }
 
 int plan_projector(ei_plan &p, const double *angles, const std::vector<int> &proj_angles,
-                   std::vector<int2> &groups, std::vector<int> &order, std::vector<int2> &win1,
-                   std::vector<int2> &winRS, std::vector<int> &unit1, std::vector<int> &unitRS);
+                   std::vector<int2> &groups, std::vector<int> &order, std::vector<int4> &chunks1,
+                   std::vector<int> &coff1, std::vector<int4> &chunksRS, std::vector<int> &coffRS,
+                   std::vector<int> &unit1, std::vector<int> &unitRS);
+size_t k1_smem(int nst, int E, int nchmax, int nmap);   // K1 dynamic shared memory (bytes)
 // fold of mirror-pair gradient rows (k_pack.cu): G(primary) += mirror(G(mirror)), pair layout
 cudaError_t launch_fold(const ei_plan &p, int n_maps, cudaStream_t st);
 // K0 (k_pack.cu)

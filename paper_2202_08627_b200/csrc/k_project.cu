@@ -6,11 +6,12 @@
 // B200 design (DESIGN.md §5 K1):
 //  * a CTA owns AGB = 16 consecutive same-dominance angles x RTILE = 64 adjacent rays (32 at four
 //    CTAs per SM for single-wave grids and dense wide-window views, plan_projector); it walks the
-//    rows in chunks of RC rows; a producer warp streams, with 1-D bulk copies (TMA engine), only
-//    the window of PAIR entries (K0 layout: entry e = (x[e-1], x[e]) of all maps) that the CTA's
-//    rays touch in those rows into a 2-3 stage mbarrier ring; the window bound CW is computed
-//    exactly on the host (plan) so every index stays inside the staged window without per-sample
-//    checks;
+//    rows in CHUNKS of as many rows as fit a ring stage of E entries (the window of a chunk widens
+//    with its rows; narrow where the CTA's rays converge, so chunks there hold more rows); a
+//    producer warp streams, with 1-D bulk copies (TMA engine), only the window of PAIR entries (K0
+//    layout: entry e = (x[e-1], x[e]) of all maps) that the CTA's rays touch in those rows into a
+//    2-3 stage mbarrier ring; every chunk's window is computed exactly on the host (plan) so every
+//    index stays inside the staged window without per-sample checks;
 //  * a warp = 4 adjacent angles x 8 adjacent rays (angle fastest) or 8 rays x 4 angles (ray
 //    fastest, sparse views), chosen per angle group from a bank-conflict model;
 //  * one tap pair of all three maps = one LDS.128 + one LDS.64; weights (1-w, w) as a float2 and
@@ -29,6 +30,13 @@
 #include "tma.cuh"
 
 namespace ei {
+
+// dynamic shared memory of K1: the ring (A plane: 16-B entries for three maps, 8-B for one; B
+// plane: 8-B entries, three maps only) and the unit's chunk table
+size_t k1_smem(int nst, int E, int nchmax, int nmap) {
+  return (size_t)nst * E * (nmap == 3 ? 24 : 8) + (size_t)nchmax * sizeof(int4);
+}
+
 namespace {
 
 constexpr int AGB = 16;   // angles per CTA
@@ -56,9 +64,10 @@ struct ProjArgs {
   const int2 *groups;           // {first sorted position, count}
   const int *order;             // sorted position -> angle index
   const int *partner;           // angle -> its mirror angle theta + pi, or -1
-  const int2 *win;              // [RS][groups][tiles][chunks] {cmin, W} (W = 0: chunk skipped)
+  const int4 *chunks;           // {cmin, W, first row, rows} per chunk (plan), CSR over units:
+  const int *coff;              // [RS][groups][tiles] + 1 offsets into chunks
   const int *unit;              // CTA -> work unit tile + ntile (group + ngroups (rs S + s)) (plan order)
-  int N, NA, ND, S, RS, RC, CW, nch, PAD, Rp, ntile, ngroups;
+  int N, NA, ND, S, RS, E, nchmax, PAD, Rp, ntile, ngroups;   // E: ring-stage entries
   int nst;                      // ring stages (<= NSTMAX)
   int has_pairs;                // the plan paired mirror angles (else partner[] is all -1)
   float *P;                     // [RS][S][NMAP][NA][ND]
@@ -97,14 +106,15 @@ __device__ __forceinline__ unsigned long long gt_proj() {
 #endif
 
 constexpr int NSTMAX = 4;       // pipeline stages (shared-memory ring): 2 (plan), up to 4 (knob)
-constexpr int MAXCH = 1024;     // window-table entries cached in shared memory per CTA
 
 // Warp-specialised pipeline: warp NCW (the producer) streams each row chunk's window of pair
 // entries with 1-D bulk copies (TMA engine) into a NST-deep shared-memory ring, completing on a
 // per-stage "full" mbarrier (transaction bytes); the NCW consumer warps wait on "full", compute,
 // and release the stage on its "empty" mbarrier.  No CTA-wide barrier inside the loop.
-// Map rows are zero-padded by PAD >= CW entries on both sides, so every window is one in-bounds
-// contiguous copy per row and plane.
+// Map rows are zero-padded by PAD >= the widest window on both sides, so every window is one
+// in-bounds contiguous copy per row and plane.  A chunk's rows are staged at a stride of
+// (W + 3) & ~1 entries (even: 8-byte-entry rows stay 16-B aligned; >= W + 2: their copy starts at
+// the even entry below the window), rows x stride <= E.
 // Consumer lane -> (angle aq of the group's current angle quad, ray rq of the warp's 8 rays);
 // slot m adds 4m to the angle.  Two mappings, chosen per angle group from a bank-conflict model
 // of the geometry (plan_projector): angle fastest (aq = lane & 3, rq = lane >> 2: a quarter warp = 4
@@ -118,17 +128,14 @@ template <int NMAP, int RTILE>
 __global__ void __launch_bounds__(RTILE * 4 + 32, RTILE == 64 ? 2 : 4) project_kernel(ProjArgs args) {
   constexpr int NT = RTILE * 4, NCW = NT / 32;
   using TA = typename PL<NMAP>::A;
-  const int N = args.N, ND = args.ND, RC = args.RC, CW = args.CW;
-  // 8-byte-entry planes start their copy at the even entry below the window (16-B aligned
-  // bulk copies) and need 2 spare entries per row; CW is even (host), so rows stay 16-B aligned
+  const int N = args.N, ND = args.ND, E = args.E;
   constexpr bool A8 = sizeof(TA) == 8;
-  const int CWA = A8 ? CW + 2 : CW, CWB = CW + 2;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int NST = args.nst;
-  TA *sA = reinterpret_cast<TA *>(smem_raw);                                   // [NST][RC][CWA]
-  float2 *sB = reinterpret_cast<float2 *>(sA + NST * RC * CWA);               // [NST][RC][CWB]
+  TA *sA = reinterpret_cast<TA *>(smem_raw);                                   // [NST][E]
+  float2 *sB = reinterpret_cast<float2 *>(sA + NST * E);                     // [NST][E]
+  int4 *swin = reinterpret_cast<int4 *>(sB + (NMAP == 3 ? NST * E : 0));     // this unit's chunks
   __shared__ __align__(8) uint64_t full[NSTMAX], empty[NSTMAX];
-  __shared__ int2 swin[MAXCH];   // this CTA's window table (host plan), nch <= MAXCH
 
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int un = __ldg(args.unit + blockIdx.x);
@@ -150,9 +157,9 @@ SPAN_START_proj();
   const size_t Rp = (size_t)args.Rp;
   const TA *gA = reinterpret_cast<const TA *>(rowdom ? args.MA : args.MAT) + (size_t)s * N * Rp + args.PAD;
   const float2 *gB = NMAP == 3 ? (rowdom ? args.MB : args.MBT) + (size_t)s * N * Rp + args.PAD : nullptr;
-  const int r0 = (int)(((long long)rs * N) / args.RS), r1 = (int)(((long long)(rs + 1) * N) / args.RS);
-  const int nch = (r1 - r0 + RC - 1) / RC;
-  const int2 *wtab = args.win + (((size_t)rs * args.ngroups + grp) * args.ntile + tile) * args.nch;
+  const int ui = ((int)rs * args.ngroups + grp) * args.ntile + tile;
+  const int cbeg = __ldg(args.coff + ui), nch = __ldg(args.coff + ui + 1) - cbeg;
+  const int4 *wtab = args.chunks + cbeg;
 
   for (int c = tid; c < nch; c += NT + 32) swin[c] = __ldg(wtab + c);
   if (tid == 0) {
@@ -173,20 +180,18 @@ SPAN_START_proj();
       uint32_t ph = 0;
       for (int c = 0; c < nch; ++c) {
         if (c >= NST) mbar_wait_sleep(&empty[st], ph ^ 1);
-        const int2 wn = swin[c];
-        const int i0 = r0 + c * RC, rc = min(RC, r1 - i0);
+        const int4 wn = swin[c];
+        const int i0 = wn.z, rc = wn.w, stride = (wn.y + 3) & ~1;
         const int e0 = wn.x + 1;                       // first staged entry
         const int eb = e0 & ~1, bofs = e0 - eb;        // B plane: 16-B aligned start
         const uint32_t bytes8 = (uint32_t)(((wn.y + bofs) * 8 + 15) & ~15);
         const uint32_t bytesA = A8 ? bytes8 : (uint32_t)wn.y * (uint32_t)sizeof(TA);
         const uint32_t bytesB = NMAP == 3 ? bytes8 : 0u;
-        mbar_arrive_expect_tx(&full[st], wn.y > 0 ? (uint32_t)rc * (bytesA + bytesB) : 0u);
-        if (wn.y > 0) {
-          for (int r = 0; r < rc; ++r) {
-            const size_t row = (size_t)(i0 + r) * Rp;
-            bulk_g2s(sA + (st * RC + r) * CWA, gA + row + (A8 ? eb : e0), bytesA, &full[st]);
-            if (NMAP == 3) bulk_g2s(sB + (st * RC + r) * CWB, gB + row + eb, bytesB, &full[st]);
-          }
+        mbar_arrive_expect_tx(&full[st], (uint32_t)rc * (bytesA + bytesB));
+        for (int r = 0; r < rc; ++r) {
+          const size_t row = (size_t)(i0 + r) * Rp;
+          bulk_g2s(sA + st * E + r * stride, gA + row + (A8 ? eb : e0), bytesA, &full[st]);
+          if (NMAP == 3) bulk_g2s(sB + st * E + r * stride, gB + row + eb, bytesB, &full[st]);
         }
         if (++st == NST) { st = 0; ph ^= 1; }
       }
@@ -242,15 +247,15 @@ SPAN_START_proj();
   uint32_t ph = 0;
   for (int c = 0; c < nch; ++c, st = (st + 1 == NST) ? 0 : st + 1, ph ^= (st == 0)) {
     mbar_wait_full(&full[st], ph);
-    const int2 wn = swin[c];
-    const int i0 = r0 + c * RC, rc = min(RC, r1 - i0), i1 = i0 + rc - 1;
+    const int4 wn = swin[c];
+    const int i0 = wn.z, rc = wn.w, i1 = i0 + rc - 1, stride = (wn.y + 3) & ~1;
     bool any = false, all = true;
 #pragma unroll
     for (int m = 0; m < 4; ++m) {
       any |= (whi[m] >= i0 && wlo[m] <= i1);
       all &= (wlo[m] <= i0 && whi[m] >= i1);
     }
-    if (wn.y > 0 && any) {
+    if (any) {
       // staged-window check (the counter behind ei_plan_info out[4]): x* is linear in the row
       // and fmaf / floor are monotone, so every row's tap of a slot lies in the staged entries
       // [wn.x, wn.x + wn.y) iff the chunk's first and last rows' taps do
@@ -266,8 +271,8 @@ SPAN_START_proj();
         if (bad) atomicAdd(args.diag, 1);
       }
       const int bofs = (wn.x + 1) & 1;
-      const TA *arow = sA + st * RC * CWA - wn.x + (A8 ? bofs : 0);
-      const float2 *brow = sB + st * RC * CWB - wn.x + bofs;
+      const TA *arow = sA + st * E - wn.x + (A8 ? bofs : 0);
+      const float2 *brow = sB + st * E - wn.x + bofs;
       float yi = (float)i0 - ctr;
       auto body = [&](bool masked, int i) {
 #pragma unroll
@@ -288,9 +293,9 @@ SPAN_START_proj();
         }
       };
       if (all) {
-        for (int r = 0; r < rc; ++r, yi += 1.f, arow += CWA, brow += CWB) body(false, 0);
+        for (int r = 0; r < rc; ++r, yi += 1.f, arow += stride, brow += stride) body(false, 0);
       } else {
-        for (int r = 0; r < rc; ++r, yi += 1.f, arow += CWA, brow += CWB) body(true, i0 + r);
+        for (int r = 0; r < rc; ++r, yi += 1.f, arow += stride, brow += stride) body(true, i0 + r);
       }
 #ifdef EI_TRACE
       my_rows += rc;
@@ -354,18 +359,18 @@ cudaError_t launch(const ei_plan &p, int RS, float *P, cudaStream_t st) {
   a.order = p.proj.order;
   a.partner = p.proj.partner;
   a.has_pairs = p.npairs > 0 ? 1 : 0;
-  a.win = RS == 1 ? p.proj.win1 : p.proj.winRS;
+  a.chunks = RS == 1 ? p.proj.chunks1 : p.proj.chunksRS;
+  a.coff = RS == 1 ? p.proj.coff1 : p.proj.coffRS;
   a.unit = RS == 1 ? p.proj.unit1 : p.proj.unitRS;
   a.ntile = p.proj.n_tiles;
   a.ngroups = p.proj.n_groups;
-  a.N = p.N; a.NA = p.NA; a.ND = p.ND; a.S = p.S; a.RS = RS; a.RC = p.proj.RC; a.CW = p.proj.CW;
+  a.N = p.N; a.NA = p.NA; a.ND = p.ND; a.S = p.S; a.RS = RS; a.E = p.proj.E;
   a.PAD = p.proj.PAD; a.Rp = p.proj.Rp;
-  a.nch = RS == 1 ? p.proj.nch1 : p.proj.nchRS;
+  a.nchmax = RS == 1 ? p.proj.nchmax1 : p.proj.nchmaxRS;
   a.P = P;
   a.diag = p.diag;
   a.nst = p.proj.nst;
-  const size_t smem = NMAP == 3 ? (size_t)a.nst * p.proj.RC * (p.proj.CW * 16 + (p.proj.CW + 2) * 8)
-                                 : (size_t)a.nst * p.proj.RC * (p.proj.CW + 2) * 8;
+  const size_t smem = k1_smem(a.nst, a.E, a.nchmax, NMAP);
   auto kern = p.proj.RT == RT ? project_kernel<NMAP, RT> : project_kernel<NMAP, RTS>;
   cudaError_t e = cudaFuncSetAttribute((const void *)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
@@ -380,55 +385,88 @@ cudaError_t launch(const ei_plan &p, int RS, float *P, cudaStream_t st) {
 
 // Host planning for K1 (called once by ei_plan_create):
 //  * groups: runs of <= AGB angularly adjacent angles of one dominance class;
-//  * window table: for every (row split, group, ray tile, row chunk) the first staged pair entry
-//    and the window width, from the fp64 positions of the extreme rays at the chunk's first and
-//    last rows (x* is linear in ray and row), widened by one entry on each side so fp32 rounding
-//    in the kernel can never leave the window; chunks whose window misses the map get W = 0;
-//  * RC (rows per chunk) as large as fits two CTAs per SM, CW = max window width, and the row
-//    split RS of the cost path for problems with fewer than ~2 CTAs per SM.
-static void build_windows(const ei_plan &p, const double *angles, const std::vector<int2> &groups,
-                          const std::vector<int> &order, int RS, int RC, std::vector<int2> &win,
-                          int &nch_max, int &wmax) {
+//  * chunk table: for every (row split, group, ray tile) the rows are cut greedily into chunks of
+//    as many rows as fit one ring stage of E entries at a stride of (W + 3) & ~1 per row (<= RCMAX
+//    rows), where W is the width of the chunk's window of pair entries: from the fp64 positions of
+//    the extreme rays at every row (x* is linear in ray and row), widened by one entry on each side
+//    so fp32 rounding in the kernel can never leave the window; rows whose window misses the map
+//    contribute nothing and get no chunk.  Stored {first entry - 1, W, first row, rows} in CSR form
+//    (offsets per unit);
+//  * the ring stage size E from the shared-memory budget, and the row split RS of the cost path for
+//    problems with fewer than ~2 CTAs per SM.
+struct Chunks {
+  std::vector<int4> c;      // all chunks, unit by unit
+  std::vector<int> off;     // [RS][groups][tiles] + 1
+  int nchmax = 0, wmax = 1, rcmax = 0;
+  long long rows(size_t u) const {   // rows staged by unit u (its cost)
+    long long r = 0;
+    for (int q = off[u]; q < off[u + 1]; ++q) r += c[q].w;
+    return r;
+  }
+};
+
+static bool build_chunks(const ei_plan &p, const double *angles, const std::vector<int2> &groups,
+                         const std::vector<int> &order, int RS, int E, int RCMAX, Chunks &ch) {
   const int N = p.N, ND = p.ND;
   const double dx = p.g.pixel, du = p.g.det_pitch, ctr = 0.5 * (N - 1), dctr = 0.5 * (ND - 1);
   const int rt = p.proj.RT, ntile = (ND + rt - 1) / rt;
-  nch_max = 0;
-  for (int rs = 0; rs < RS; ++rs) {
-    const int r0 = (int)(((long long)rs * N) / RS), r1 = (int)(((long long)(rs + 1) * N) / RS);
-    nch_max = std::max(nch_max, (r1 - r0 + RC - 1) / RC);
-  }
-  win.assign((size_t)RS * groups.size() * ntile * nch_max, make_int2(0, 0));
-  wmax = 1;
+  ch = Chunks();
+  ch.off.push_back(0);
+  std::vector<double> lo(N), hi(N);
   for (int rs = 0; rs < RS; ++rs) {
     const int r0 = (int)(((long long)rs * N) / RS), r1 = (int)(((long long)(rs + 1) * N) / RS);
     for (size_t g = 0; g < groups.size(); ++g) {
       for (int t = 0; t < ntile; ++t) {
         const int kt = t * rt;
-        int2 *row = &win[((rs * groups.size() + g) * ntile + t) * nch_max];
-        for (int c = 0; r0 + c * RC < r1; ++c) {
-          const int i0 = r0 + c * RC, i1 = std::min(i0 + RC, r1) - 1;
-          double lo = 1e300, hi = -1e300;
-          for (int q = 0; q < groups[g].y; ++q) {
-            const int a = order[groups[g].x + q];
-            const double cs = cos(angles[a]), sn = sin(angles[a]);
-            const bool rd = fabs(cs) >= fabs(sn);
-            const double cd = rd ? cs : sn, so = rd ? sn : cs;
-            for (int kk : {kt, kt + rt - 1})
-              for (int ii : {i0, i1}) {
-                const double xs = (kk - dctr) * du / (cd * dx) - (so / cd) * (ii - ctr) + ctr;
-                lo = std::min(lo, floor(xs));
-                hi = std::max(hi, floor(xs));
-              }
-          }
-          // taps j0 in [lo-1, hi+1] (one entry of rounding slack each side)
-          if (hi + 1 < -1 || lo - 1 > N - 1) continue;     // misses the map: W = 0
-          const int W = (int)(hi - lo) + 3;
-          row[c] = make_int2((int)lo - 1, W);
-          wmax = std::max(wmax, W);
+        // per-row extreme floor(x*) over the group's angles and the tile's extreme rays
+        for (int i = r0; i < r1; ++i) {
+          lo[i] = 1e300;
+          hi[i] = -1e300;
         }
+        for (int q = 0; q < groups[g].y; ++q) {
+          const int a = order[groups[g].x + q];
+          const double cs = cos(angles[a]), sn = sin(angles[a]);
+          const bool rd = fabs(cs) >= fabs(sn);
+          const double cd = rd ? cs : sn, so = rd ? sn : cs;
+          for (int kk : {kt, kt + rt - 1}) {
+            const double a0 = (kk - dctr) * du / (cd * dx) + ctr, b0 = so / cd;
+            for (int i = r0; i < r1; ++i) {
+              const double xs = floor(a0 - b0 * (i - ctr));
+              lo[i] = std::min(lo[i], xs);
+              hi[i] = std::max(hi[i], xs);
+            }
+          }
+        }
+        int i = r0;
+        while (i < r1) {
+          if (hi[i] + 1 < -1 || lo[i] - 1 > N - 1) { ++i; continue; }   // taps [lo-1, hi+1] miss the map
+          double clo = lo[i], chi = hi[i];
+          int rc = 1;
+          const int W1 = (int)(chi - clo) + 3;
+          if ((((W1 + 3) & ~1)) > E) return false;                      // one row must fit a stage
+          while (i + rc < r1 && rc < RCMAX) {
+            const int j = i + rc;
+            if (hi[j] + 1 < -1 || lo[j] - 1 > N - 1) break;
+            const double nlo = std::min(clo, lo[j]), nhi = std::max(chi, hi[j]);
+            const int W = (int)(nhi - nlo) + 3;
+            if ((long long)(rc + 1) * ((W + 3) & ~1) > E) break;
+            clo = nlo;
+            chi = nhi;
+            ++rc;
+          }
+          const int W = (int)(chi - clo) + 3;
+          ch.c.push_back(make_int4((int)clo - 1, W, i, rc));
+          ch.wmax = std::max(ch.wmax, W);
+          ch.rcmax = std::max(ch.rcmax, rc);
+          i += rc;
+        }
+        const int n = (int)ch.c.size() - ch.off.back();
+        ch.nchmax = std::max(ch.nchmax, n);
+        ch.off.push_back((int)ch.c.size());
       }
     }
   }
+  return true;
 }
 
 // Shared-memory wavefront model of the consumer gathers for one lane mapping (see the kernel):
@@ -494,23 +532,17 @@ static double wavefront_model(const ei_plan &p, const double *angles, const std:
 //  * Larger grids: heaviest first (longest-processing-time order), so the light units fill the
 //    tail of the last wave; slice by slice, so the CTAs in flight share one slice's map in L2
 //    (LPT across all 64 slices of C4 raised K1's DRAM traffic from ~18 to ~170 MB per slice).
-static std::vector<int> order_units(const std::vector<int2> &win, int RS, int n_groups, int ntile,
-                                    int nch, int S, int RC, int N, int cps) {
+static std::vector<int> order_units(const Chunks &ch, int RS, int n_groups, int ntile, int S, int cps) {
   const int nu1 = RS * n_groups * ntile;          // per slice: (rs, group, tile)
   std::vector<std::pair<long long, int>> cost;   // (slice, -cost) key, unit
   cost.reserve((size_t)nu1 * S);
   for (int s = 0; s < S; ++s)
-    for (int rs = 0; rs < RS; ++rs) {
-      const int r0 = (int)(((long long)rs * N) / RS), r1 = (int)(((long long)(rs + 1) * N) / RS);
+    for (int rs = 0; rs < RS; ++rs)
       for (int g = 0; g < n_groups; ++g)
         for (int t = 0; t < ntile; ++t) {
-          const int2 *row = &win[(((size_t)rs * n_groups + g) * ntile + t) * nch];
-          long long c = 0;
-          for (int ch = 0; r0 + ch * RC < r1; ++ch)
-            if (row[ch].y > 0) c += std::min(RC, r1 - (r0 + ch * RC));
+          const long long c = ch.rows(((size_t)rs * n_groups + g) * ntile + t);
           cost.push_back({(long long)s * (1LL << 40) - c, t + ntile * (g + n_groups * (rs * S + s))});
         }
-    }
   std::stable_sort(cost.begin(), cost.end());    // slice-major, heaviest first; ties keep (rs, g, t)
   const int n = (int)cost.size();
   int sms = 148, dev = 0;
@@ -540,8 +572,9 @@ static std::vector<int> order_units(const std::vector<int2> &win, int RS, int n_
 }
 
 int plan_projector(ei_plan &p, const double *angles, const std::vector<int> &proj_angles,
-                   std::vector<int2> &groups, std::vector<int> &order, std::vector<int2> &win1,
-                   std::vector<int2> &winRS, std::vector<int> &unit1, std::vector<int> &unitRS) {
+                   std::vector<int2> &groups, std::vector<int> &order, std::vector<int4> &chunks1,
+                   std::vector<int> &coff1, std::vector<int4> &chunksRS, std::vector<int> &coffRS,
+                   std::vector<int> &unit1, std::vector<int> &unitRS) {
   const int N = p.N, ND = p.ND;
   const int NA = (int)proj_angles.size();   // the angles K1 projects (mirror pairs: primaries)
   // groups = runs of angularly adjacent angles (sorted by angle mod 2 pi) of one dominance class
@@ -562,30 +595,33 @@ int plan_projector(ei_plan &p, const double *angles, const std::vector<int> &pro
   int sms = 148, dev = 0;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   cudaGetLastError();
-  // Staging ring: RC rows per chunk, 2 chunks deep, within a shared-memory budget that keeps two
-  // (64-ray tiles) or four (32-ray tiles) CTAs per SM (104 / 52 KB, knob EI_K1_SMEM_KB).  First
-  // the row split RS from the chunk size of a 4-stage ring; then the largest RC that leaves every
-  // CTA >= 2 chunks and fits two stages.  Fewer, larger chunks cost less per-chunk
-  // synchronisation than a deeper ring (measured vs the 4-stage ring: C4 K1 9.16 -> 8.67 ms, C3
-  // 0.71 -> 0.62, C5 1.39 -> 1.23, P1 40.5 -> 39.2 us per evaluation; 3 stages where they fit:
-  // P1 40.7).
+  // Staging ring: 2 stages of E entries, within a shared-memory budget that keeps two (64-ray
+  // tiles) or four (32-ray tiles) CTAs per SM (104 / 50 KB, knob EI_K1_SMEM_KB), filled by chunks
+  // of as many rows as fit a stage (<= RCMAX, which leaves every CTA >= 2 chunks).  First the row
+  // split RS from the rows per chunk a 4-stage ring would allow; fewer, larger chunks cost less
+  // per-chunk synchronisation than a deeper ring (measured vs the 4-stage ring: C4 K1 9.16 -> 8.67
+  // ms, C3 0.71 -> 0.62, C5 1.39 -> 1.23, P1 40.5 -> 39.2 us per evaluation; 3 stages where they
+  // fit: P1 40.7), and chunks sized by their own window rather than the widest one hold more rows
+  // where the rays converge.
   const char *env = getenv("EI_K1_SMEM_KB");
-  int RC = 32, nch = 0, CW = 0, RC4 = 0, RS = 1, cps = 2, ntile = 0;
+  Chunks ch1, chRS;
+  int RC4 = 0, RS = 1, cps = 2, ntile = 0;
   long long ctas = 0;
   std::vector<int> rf_flags;
   size_t budget = 0;
   auto plan_rs = [&](int rt) {
     p.proj.RT = rt;
     cps = rt == RT ? 2 : 4;   // CTAs per SM
-    budget = (env ? (size_t)atoi(env) : (cps == 2 ? 104 : 52)) * 1024;
+    budget = (env ? (size_t)atoi(env) : (cps == 2 ? 104 : 50)) * 1024;
     const size_t budget4 = (cps == 2 ? 100 : 50) * 1024;
-    RC = 32;
-    for (;;) {   // 4-stage chunk size (sets the row split)
-      build_windows(p, angles, groups, order, 1, RC, win1, nch, CW);
-      if ((size_t)NSTMAX * RC * (CW + 2) * per_entry <= budget4 || RC == 1) break;
-      RC /= 2;
+    int rc = 32;
+    for (;;) {   // rows per chunk of a 4-stage ring at the widest window (sets the row split)
+      Chunks t;
+      build_chunks(p, angles, groups, order, 1, 1 << 30, rc, t);
+      if ((size_t)NSTMAX * rc * (t.wmax + 2) * per_entry <= budget4 || rc == 1) break;
+      rc /= 2;
     }
-    RC4 = RC;
+    RC4 = rc;
     ntile = (ND + rt - 1) / rt;
     ctas = (long long)ntile * (long long)groups.size() * p.S;
     // row split for small problems: the largest power of two keeping the grid within one wave
@@ -631,49 +667,51 @@ int plan_projector(ei_plan &p, const double *angles, const std::vector<int> &pro
   p.proj.k0_early = ctas * RS <= sms ? 1 : 0;
   if (const char *e = getenv("EI_K0_EARLY")) p.proj.k0_early = atoi(e) ? 1 : 0;   // tuning knob
   int nst = 2;
-  {
-    int rcmax = 1;
-    while (rcmax * 2 <= std::max(1, (N / RS) / 2) && rcmax < 32) rcmax *= 2;
-    for (int rc = rcmax; rc >= 1; rc /= 2) {
-      int cw = 0, nc = 0;
-      std::vector<int2> w;
-      build_windows(p, angles, groups, order, 1, rc, w, nc, cw);
-      if ((size_t)nst * rc * (cw + 2) * per_entry <= budget || rc == 1) {
-        RC = rc; nch = nc; CW = cw; win1.swap(w);
-        break;
-      }
-    }
-    // 32-ray tiles: a third stage where it fits the 4-CTA budget (C2 72.0 -> 71.6 us, P1 39.2 -> 38.9)
-    if (p.proj.RT == RTS && (size_t)3 * RC * (CW + 2) * per_entry <= budget) nst = 3;
-    if (const char *e = getenv("EI_K1_NST")) nst = std::max(2, std::min(NSTMAX, atoi(e)));   // knob
-    if (const char *e = getenv("EI_K1_RC")) {   // tuning knob: rows per chunk (any value)
-      RC = std::max(1, atoi(e));
-      build_windows(p, angles, groups, order, 1, RC, win1, nch, CW);
-    }
+  int RCMAX = 1;
+  while (RCMAX * 2 <= std::max(1, (N / RS) / 2) && RCMAX < 32) RCMAX *= 2;
+  if (const char *e = getenv("EI_K1_RC")) RCMAX = std::max(1, atoi(e));   // tuning knob: rows per chunk cap
+  auto stage_entries = [&](int n) { return (int)(budget / ((size_t)n * per_entry)) & ~1; };
+  if (!build_chunks(p, angles, groups, order, 1, stage_entries(nst), RCMAX, ch1)) return EI_ERR_SHAPE;
+  // 32-ray tiles: a third stage where it fits the 4-CTA budget (C2 72.0 -> 71.6 us, P1 39.2 -> 38.9)
+  if (p.proj.RT == RTS && (size_t)3 * ch1.rcmax * (ch1.wmax + 2) * per_entry <= budget) nst = 3;
+  if (const char *e = getenv("EI_K1_NST")) nst = std::max(2, std::min(NSTMAX, atoi(e)));   // knob
+  const int E = stage_entries(nst);
+  if (!build_chunks(p, angles, groups, order, 1, E, RCMAX, ch1)) return EI_ERR_SHAPE;
+  if (RS > 1) {
+    if (!build_chunks(p, angles, groups, order, RS, E, RCMAX, chRS)) return EI_ERR_SHAPE;
+  } else {
+    chRS = ch1;
   }
-  if ((size_t)nst * RC * (CW + 2) * per_entry > 200 * 1024) return EI_ERR_SHAPE;
-  if (nch > MAXCH) return EI_ERR_SHAPE;
-  p.proj.RC = RC;
+  if (k1_smem(nst, E, std::max(ch1.nchmax, chRS.nchmax), 3) > 220 * 1024) return EI_ERR_SHAPE;
+  if (getenv("EI_PLAN_VERBOSE"))
+    fprintf(stderr, "libei plan: K1 RT %d RS %d nst %d E %d: %zu chunks, <= %d per unit, %.2f rows avg, <= %d rows, "
+            "widest window %d\n", p.proj.RT, RS, nst, E, ch1.c.size(), ch1.nchmax,
+            ch1.c.empty() ? 0.0 : (double)[&] { long long r = 0; for (auto &q : ch1.c) r += q.w; return r; }() / ch1.c.size(),
+            ch1.rcmax, ch1.wmax);
+  p.proj.E = E;
   p.proj.nst = nst;
   p.proj.n_groups = (int)groups.size();
-
-  p.proj.nch1 = nch;
   p.proj.RS = RS;
-  int CWrs = CW;
-  if (RS > 1) {
-    build_windows(p, angles, groups, order, RS, RC, winRS, p.proj.nchRS, CWrs);
-  } else {
-    winRS.clear();
-    p.proj.nchRS = nch;
-  }
-  p.proj.CW = (std::max(CW, CWrs) + 1) & ~1;   // even (16-B aligned 8-byte-entry rows)
+  p.proj.nchmax1 = ch1.nchmax;
+  p.proj.nchmaxRS = chRS.nchmax;
+  p.proj.rcmax = std::max(ch1.rcmax, chRS.rcmax);
+  p.proj.wmax = std::max(ch1.wmax, chRS.wmax);
   // zero padding of the pair-layout map rows so every staged window is one in-bounds copy
-  p.proj.PAD = p.proj.CW + 2;   // even
+  p.proj.PAD = ((p.proj.wmax + 1) & ~1) + 2;   // even
   p.proj.Rp = (N + 1 + 2 * p.proj.PAD + 1) & ~1;   // even: 16-B aligned float2 rows
   p.proj.n_tiles = ntile;
   if ((long long)ntile * groups.size() * p.S * RS > 0x7fffffffLL) return EI_ERR_SHAPE;   // 1-D grid
-  unit1 = order_units(win1, 1, (int)groups.size(), ntile, p.proj.nch1, p.S, RC, N, cps);
-  unitRS = RS > 1 ? order_units(winRS, RS, (int)groups.size(), ntile, p.proj.nchRS, p.S, RC, N, cps) : unit1;
+  unit1 = order_units(ch1, 1, (int)groups.size(), ntile, p.S, cps);
+  unitRS = RS > 1 ? order_units(chRS, RS, (int)groups.size(), ntile, p.S, cps) : unit1;
+  chunks1.swap(ch1.c);
+  coff1.swap(ch1.off);
+  if (RS > 1) {
+    chunksRS.swap(chRS.c);
+    coffRS.swap(chRS.off);
+  } else {
+    chunksRS.clear();
+    coffRS.clear();
+  }
   for (size_t g = 0; g < groups.size(); ++g) groups[g].y |= rf_flags[g] << 16;   // last: device copy
   return EI_OK;
 }

@@ -68,7 +68,7 @@ void free_plan(ei_plan *p) {
   for (cudaEvent_t ev : p->h_ev)
     if (ev) cudaEventDestroy(ev);
   void *ptrs[] = {p->tab.k1, p->tab.k3, p->proj.groups, p->proj.order, p->proj.partner, p->alist3,
-                  p->pairs, p->proj.win1, p->proj.winRS, p->proj.unit1, p->proj.unitRS, p->MA, p->MAT, p->MB,
+                  p->pairs, p->proj.chunks1, p->proj.coff1, p->proj.chunksRS, p->proj.coffRS, p->proj.unit1, p->proj.unitRS, p->MA, p->MAT, p->MB,
                   p->MBT, p->M1, p->M1T, p->diag, p->part_mo, p->part3, p->k3u, p->P, p->GA, p->GB, p->GC, p->GA1,
                   p->part_curve, p->part_reg, p->h_maps, p->h_flat, p->h_mask, p->h_drift,
                   p->h_sexp, p->h_grad, p->h_cost, p->h_status};
@@ -169,9 +169,10 @@ int ei_plan_create(const ei_geometry *geom, const double *angles, ei_plan **out)
   }
   p->npairs = (int)pairs.size();
   p->NA3 = (int)prim.size();
-  std::vector<int2> groups, win1, winRS;
-  std::vector<int> order, unit1, unitRS;
-  rc = ei::plan_projector(*p, angles, prim, groups, order, win1, winRS, unit1, unitRS);
+  std::vector<int2> groups;
+  std::vector<int4> chunks1, chunksRS;
+  std::vector<int> order, unit1, unitRS, coff1, coffRS;
+  rc = ei::plan_projector(*p, angles, prim, groups, order, chunks1, coff1, chunksRS, coffRS, unit1, unitRS);
   if (!rc) rc = ei::plan_curve(*p);
   if (rc) {
     delete[] k1;
@@ -191,8 +192,12 @@ int ei_plan_create(const ei_geometry *geom, const double *angles, ei_plan **out)
   A(dalloc(&p->proj.partner, NA));
   A(dalloc(&p->alist3, prim.size()));
   if (!pairs.empty()) A(dalloc(&p->pairs, pairs.size()));
-  A(dalloc(&p->proj.win1, win1.size()));
-  if (!winRS.empty()) A(dalloc(&p->proj.winRS, winRS.size()));
+  A(dalloc(&p->proj.chunks1, std::max<size_t>(1, chunks1.size())));
+  A(dalloc(&p->proj.coff1, coff1.size()));
+  if (!coffRS.empty()) {
+    A(dalloc(&p->proj.chunksRS, std::max<size_t>(1, chunksRS.size())));
+    A(dalloc(&p->proj.coffRS, coffRS.size()));
+  }
   A(dalloc(&p->proj.unit1, unit1.size()));
   A(dalloc(&p->proj.unitRS, unitRS.size()));
   A(dalloc(&p->MA, S * NP));
@@ -294,10 +299,14 @@ int ei_plan_create(const ei_geometry *geom, const double *angles, ei_plan **out)
   if (e == cudaSuccess) A(cudaMemset(p->GB, 0, sizeof(float4) * S * SINO1));
   if (e == cudaSuccess) A(cudaMemset(p->GC, 0, sizeof(float) * S * SINO1));
   if (e == cudaSuccess) A(cudaMemset(p->GA1, 0, sizeof(float2) * S * SINO1));
-  if (e == cudaSuccess)
-    A(cudaMemcpy(p->proj.win1, win1.data(), sizeof(int2) * win1.size(), cudaMemcpyHostToDevice));
-  if (e == cudaSuccess && !winRS.empty())
-    A(cudaMemcpy(p->proj.winRS, winRS.data(), sizeof(int2) * winRS.size(), cudaMemcpyHostToDevice));
+  if (e == cudaSuccess && !chunks1.empty())
+    A(cudaMemcpy(p->proj.chunks1, chunks1.data(), sizeof(int4) * chunks1.size(), cudaMemcpyHostToDevice));
+  if (e == cudaSuccess) A(cudaMemcpy(p->proj.coff1, coff1.data(), sizeof(int) * coff1.size(), cudaMemcpyHostToDevice));
+  if (e == cudaSuccess && !coffRS.empty()) {
+    if (!chunksRS.empty())
+      A(cudaMemcpy(p->proj.chunksRS, chunksRS.data(), sizeof(int4) * chunksRS.size(), cudaMemcpyHostToDevice));
+    A(cudaMemcpy(p->proj.coffRS, coffRS.data(), sizeof(int) * coffRS.size(), cudaMemcpyHostToDevice));
+  }
   if (e == cudaSuccess)
     A(cudaMemcpy(p->proj.unit1, unit1.data(), sizeof(int) * unit1.size(), cudaMemcpyHostToDevice));
   if (e == cudaSuccess)
@@ -326,11 +335,11 @@ int ei_plan_info(const ei_plan *p, int64_t out[10]) {
   int32_t d = 0;
   if (cudaMemcpy(&d, p->diag, sizeof(d), cudaMemcpyDeviceToHost) != cudaSuccess) return EI_ERR_CUDA;
   out[0] = p->proj.n_groups;
-  out[1] = p->proj.RC;
-  out[2] = p->proj.CW;
+  out[1] = p->proj.rcmax;
+  out[2] = p->proj.wmax;
   out[3] = p->proj.RS;
   out[4] = d;
-  out[5] = (int64_t)p->proj.nst * p->proj.RC * (p->proj.CW * 16 + (p->proj.CW + 2) * 8);
+  out[5] = (int64_t)ei::k1_smem(p->proj.nst, p->proj.E, std::max(p->proj.nchmax1, p->proj.nchmaxRS), 3);
   out[6] = p->proj.ray_fast;
   out[7] = p->KS;
   out[8] = p->npairs;

@@ -41,8 +41,6 @@ struct ProjPlan {
   int4 *chunksRS = nullptr; // the same for the row-split cost path, units (rs, group, tile)
   int *coffRS = nullptr;
   int nchmax1 = 0, nchmaxRS = 0;   // most chunks of one unit
-  int *counter = nullptr;   // device: the persistent K1's next work unit (reset by K0)
-  int ctas = 0;             // persistent K1 grid (CTAs per SM x SMs)
   int n_tiles = 0;          // ray tiles per angle group
   int *unit1 = nullptr;     // device: CTA -> work unit (tile, group, slice) for RS = 1 (launch order)
   int *unitRS = nullptr;    // device: the same for the row-split cost path
@@ -170,7 +168,7 @@ int plan_projector(ei_plan &p, const double *angles, const std::vector<int> &pro
                    std::vector<int2> &groups, std::vector<int> &order, std::vector<int4> &chunks1,
                    std::vector<int> &coff1, std::vector<int4> &chunksRS, std::vector<int> &coffRS,
                    std::vector<int> &unit1, std::vector<int> &unitRS);
-size_t k1_smem(int nst, int E, int nmap);   // K1 dynamic shared memory (bytes)
+size_t k1_smem(int nst, int E, int nchmax, int nmap);   // K1 dynamic shared memory (bytes)
 // fold of mirror-pair gradient rows (k_pack.cu): G(primary) += mirror(G(mirror)), pair layout
 cudaError_t launch_fold(const ei_plan &p, int n_maps, cudaStream_t st);
 // K0 (k_pack.cu)

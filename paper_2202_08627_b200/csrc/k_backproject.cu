@@ -354,10 +354,6 @@ __global__ void __launch_bounds__(NT + 32, 3) backproject3_kernel(
     j0 = blockIdx.x * TILE; i0 = blockIdx.y * TILE; s = blockIdx.z % S; ks = blockIdx.z / S; nks = KS;
   }
 SPAN_START_bp();
-#ifdef EI_TRACE
-  const unsigned long long t_start = gtimer3();
-  unsigned long long t_data = 0;
-#endif
   const float ctr = 0.5f * (float)(N - 1), dctr = 0.5f * (float)(ND - 1);
   const size_t rowlen = (size_t)RpG, soff = (size_t)s * NA * rowlen + PADG;
   const int a_lo = (int)(((long long)ks * NA3) / nks), a_hi = (int)(((long long)(ks + 1) * NA3) / nks);
@@ -457,9 +453,6 @@ SPAN_START_bp();
   uint32_t ph = 0;
   for (int c = 0; c < c_hi; ++c) {
     mbar_wait_full(&sm.full[st], ph);
-#ifdef EI_TRACE
-    if (c == 0) t_data = gtimer3();
-#endif
     const int na = min(CH, a_hi - a_lo - c * CH);
     // the chunk's angles of the current class, then (at most once per CTA) the class change
     // and the rest: the plan lists cos >= 0 first, so the change is one index per chunk
@@ -514,18 +507,7 @@ SPAN_START_bp();
   flush();
 #ifdef EI_TRACE
   asm volatile("bar.sync 2, %0;\n" ::"n"(NT) : "memory");   // consumers only
-  if (tid == 0) {
-    unsigned smid;
-    asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
-    const size_t b = ((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;   // linear
-    if (b < 65536) {
-      g_k3_trace[4 * b] = t_start;
-      g_k3_trace[4 * b + 1] = t_data;
-      g_k3_trace[4 * b + 2] = gtimer3();
-      g_k3_trace[4 * b + 3] = smid | ((unsigned long long)c_hi << 32);
-    }
-    SPAN_END_bp(0);
-  }
+  if (tid == 0) SPAN_END_bp(0);
 #endif
   const int i = i0 + row;
   if (i >= N) return;

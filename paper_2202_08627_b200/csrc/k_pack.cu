@@ -62,8 +62,7 @@ __global__ void __launch_bounds__(256) pack_pairs_kernel(const float *__restrict
                                                          double *__restrict__ part_reg,
                                                          int32_t *__restrict__ status,
                                                          SmallCheck chk, int nflat, int M, int NA,
-                                                         int PAD, int Rp, int trigger_early,
-                                                         int *__restrict__ k1_counter) {
+                                                         int PAD, int Rp, int trigger_early) {
   __shared__ float tile[NMAP][T + 1][T + 2];   // (T+1)^2 with a one-element halo
   __shared__ double red[8];
   SPAN_START_pack();
@@ -73,9 +72,6 @@ __global__ void __launch_bounds__(256) pack_pairs_kernel(const float *__restrict
   if (trigger_early) PDL_TRIGGER_K0();
   const int s = blockIdx.z, ta = blockIdx.y, tb = blockIdx.x;
   const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * T + tx;
-  // the persistent K1 that follows takes its work units from this counter (it reads it only after
-  // waiting for this grid's completion)
-  if (k1_counter && (s | ta | tb | tid) == 0) *k1_counter = 0;
   const float *src[3] = {in0 + s * in_stride, NMAP == 3 ? in1 + s * in_stride : nullptr,
                          NMAP == 3 ? in2 + s * in_stride : nullptr};
   double sq = 0.0;
@@ -245,7 +241,7 @@ cudaError_t launch_pack3(const ei_plan &p, const float *mu, const float *delta, 
                                                want_reg ? p.part_reg : nullptr, status, chk,
                                                p.S * (chk.nflat_per_slice ? chk.nflat_per_slice : 3 * p.ND),
                                                chk.mask ? p.M : 0, p.NA, p.proj.PAD, p.proj.Rp,
-                                               p.proj.k0_early, p.proj.counter);
+                                               p.proj.k0_early);
   return cudaGetLastError();
 }
 
@@ -258,7 +254,7 @@ cudaError_t launch_pack1(const ei_plan &p, const float *map, cudaStream_t st, bo
                                                want_reg ? p.part_reg : nullptr, status, chk,
                                                p.S * (chk.nflat_per_slice ? chk.nflat_per_slice : 3 * p.ND),
                                                chk.mask ? p.M : 0, p.NA, p.proj.PAD, p.proj.Rp,
-                                               p.proj.k0_early, p.proj.counter);
+                                               p.proj.k0_early);
   return cudaGetLastError();
 }
 

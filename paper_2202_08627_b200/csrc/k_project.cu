@@ -32,8 +32,10 @@
 namespace ei {
 
 // dynamic shared memory of K1: the ring (A plane: 16-B entries for three maps, 8-B for one; B
-// plane: 8-B entries, three maps only)
-size_t k1_smem(int nst, int E, int nmap) { return (size_t)nst * E * (nmap == 3 ? 24 : 8); }
+// plane: 8-B entries, three maps only) and the unit's chunk table
+size_t k1_smem(int nst, int E, int nchmax, int nmap) {
+  return (size_t)nst * E * (nmap == 3 ? 24 : 8) + (size_t)nchmax * sizeof(int4);
+}
 
 namespace {
 
@@ -64,10 +66,8 @@ struct ProjArgs {
   const int *partner;           // angle -> its mirror angle theta + pi, or -1
   const int4 *chunks;           // {cmin, W, first row, rows} per chunk (plan), CSR over units:
   const int *coff;              // [RS][groups][tiles] + 1 offsets into chunks
-  const int *unit;              // work units tile + ntile (group + ngroups (rs S + s)) in plan order
-  int *counter;                 // next unit to take (reset to 0 by K0 before every K1 launch)
-  int nunits;
-  int N, NA, ND, S, RS, E, PAD, Rp, ntile, ngroups;   // E: ring-stage entries
+  const int *unit;              // CTA -> work unit tile + ntile (group + ngroups (rs S + s)) (plan order)
+  int N, NA, ND, S, RS, E, nchmax, PAD, Rp, ntile, ngroups;   // E: ring-stage entries
   int nst;                      // ring stages (<= NSTMAX)
   int has_pairs;                // the plan paired mirror angles (else partner[] is all -1)
   float *P;                     // [RS][S][NMAP][NA][ND]
@@ -134,22 +134,34 @@ __global__ void __launch_bounds__(RTILE * 4 + 32, RTILE == 64 ? 2 : 4) project_k
   const int NST = args.nst;
   TA *sA = reinterpret_cast<TA *>(smem_raw);                                   // [NST][E]
   float2 *sB = reinterpret_cast<float2 *>(sA + NST * E);                     // [NST][E]
+  int4 *swin = reinterpret_cast<int4 *>(sB + (NMAP == 3 ? NST * E : 0));     // this unit's chunks
   __shared__ __align__(8) uint64_t full[NSTMAX], empty[NSTMAX];
-  // per stage: the staged chunk {first entry - 1, W, first row, rows} and {work unit, flags}
-  __shared__ int4 mchunk[NSTMAX];
-  __shared__ int2 munit[NSTMAX];
-  constexpr int FIRST = 1, LAST = 2, END = 4;
 
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int un = __ldg(args.unit + blockIdx.x);
+  const int tile = un % args.ntile, grp = (un / args.ntile) % args.ngroups, z = un / (args.ntile * args.ngroups);
+  const int kt = tile * RTILE;
 SPAN_START_proj();
 #ifdef EI_TRACE
   const unsigned long long t_start = gtimer();
-  int my_rows = 0, my_units = 0;
-  __shared__ int s_rows, s_units;
-  if (tid == 0) s_rows = s_units = 0;
+  __shared__ int s_rows;
+  if (tid == 0) s_rows = 0;
+  int my_rows = 0;
 #endif
+  const int2 gr = args.groups[grp];
+  const int2 gi = make_int2(gr.x, gr.y & 0xffff);   // {first sorted position, count}
+  const bool ray_fast = (gr.y >> 16) != 0;          // lane mapping of this group (plan)
+  const int s = z % args.S, rs = z / args.S;
   const float ctr = 0.5f * (float)(N - 1), dctr = 0.5f * (float)(ND - 1);
+  const bool rowdom = __ldg(args.k1 + args.order[gi.x]).w != 0.f;
   const size_t Rp = (size_t)args.Rp;
+  const TA *gA = reinterpret_cast<const TA *>(rowdom ? args.MA : args.MAT) + (size_t)s * N * Rp + args.PAD;
+  const float2 *gB = NMAP == 3 ? (rowdom ? args.MB : args.MBT) + (size_t)s * N * Rp + args.PAD : nullptr;
+  const int ui = ((int)rs * args.ngroups + grp) * args.ntile + tile;
+  const int cbeg = __ldg(args.coff + ui), nch = __ldg(args.coff + ui + 1) - cbeg;
+  const int4 *wtab = args.chunks + cbeg;
+
+  for (int c = tid; c < nch; c += NT + 32) swin[c] = __ldg(wtab + c);
   if (tid == 0) {
     for (int q = 0; q < NST; ++q) {
       mbar_init(&full[q], 1);
@@ -159,135 +171,83 @@ SPAN_START_proj();
   }
   __syncthreads();
 
-  // PDL: only the producer reads K0's output (the packed maps, via TMA) and the work counter K0
-  // resets; the consumers' P writes are read only by this call's K2
+  // PDL: only the producer reads K0's output (the packed maps, via TMA); the consumers' prologue
+  // (tables, row ranges) overlaps K0's tail and their P writes are read only by this call's K2
   if (w == NCW) {   // ---------------- producer warp ----------------
-    pdl_wait();   // K0's packed maps (and the reset work counter)
+    pdl_wait();   // K0's packed maps
     if (lane == 0) {
-      int st = 0, staged = 0;
+      int st = 0;
       uint32_t ph = 0;
-      auto next_stage = [&]() {
-        if (staged++ >= NST) mbar_wait_sleep(&empty[st], ph ^ 1);
-      };
-      for (;;) {
-        // persistent CTAs take the work units (tile, group, row split, slice) in plan order from a
-        // global counter: the order is the plan's (heaviest first, slice by slice), the
-        // assignment to CTAs dynamic, and the ring keeps streaming across units
-        const int q = atomicAdd(args.counter, 1);
-        if (q >= args.nunits) break;
-        const int un = __ldg(args.unit + q);
-        const int tile = un % args.ntile, grp = (un / args.ntile) % args.ngroups, z = un / (args.ntile * args.ngroups);
-        const int s = z % args.S, rs = z / args.S;
-        const int gx = __ldg(&args.groups[grp].x);
-        const bool rowdom = __ldg(args.k1 + __ldg(args.order + gx)).w != 0.f;
-        const TA *gA = reinterpret_cast<const TA *>(rowdom ? args.MA : args.MAT) + (size_t)s * N * Rp + args.PAD;
-        const float2 *gB = NMAP == 3 ? (rowdom ? args.MB : args.MBT) + (size_t)s * N * Rp + args.PAD : nullptr;
-        const int ui = (rs * args.ngroups + grp) * args.ntile + tile;
-        const int cbeg = __ldg(args.coff + ui), nch = __ldg(args.coff + ui + 1) - cbeg;
-        if (nch == 0) {   // no row of this unit reaches the map: P = 0, one empty stage says so
-          next_stage();
-          mchunk[st] = make_int4(0, 0, 0, 0);
-          munit[st] = make_int2(un, FIRST | LAST);
-          mbar_arrive_expect_tx(&full[st], 0u);
-          if (++st == NST) { st = 0; ph ^= 1; }
-          continue;
+      for (int c = 0; c < nch; ++c) {
+        if (c >= NST) mbar_wait_sleep(&empty[st], ph ^ 1);
+        const int4 wn = swin[c];
+        const int i0 = wn.z, rc = wn.w, stride = (wn.y + 3) & ~1;
+        const int e0 = wn.x + 1;                       // first staged entry
+        const int eb = e0 & ~1, bofs = e0 - eb;        // B plane: 16-B aligned start
+        const uint32_t bytes8 = (uint32_t)(((wn.y + bofs) * 8 + 15) & ~15);
+        const uint32_t bytesA = A8 ? bytes8 : (uint32_t)wn.y * (uint32_t)sizeof(TA);
+        const uint32_t bytesB = NMAP == 3 ? bytes8 : 0u;
+        mbar_arrive_expect_tx(&full[st], (uint32_t)rc * (bytesA + bytesB));
+        for (int r = 0; r < rc; ++r) {
+          const size_t row = (size_t)(i0 + r) * Rp;
+          bulk_g2s(sA + st * E + r * stride, gA + row + (A8 ? eb : e0), bytesA, &full[st]);
+          if (NMAP == 3) bulk_g2s(sB + st * E + r * stride, gB + row + eb, bytesB, &full[st]);
         }
-        for (int c = 0; c < nch; ++c) {
-          next_stage();
-          const int4 wn = __ldg(args.chunks + cbeg + c);
-          const int i0 = wn.z, rc = wn.w, stride = (wn.y + 3) & ~1;
-          const int e0 = wn.x + 1;                       // first staged entry
-          const int eb = e0 & ~1, bofs = e0 - eb;        // B plane: 16-B aligned start
-          const uint32_t bytes8 = (uint32_t)(((wn.y + bofs) * 8 + 15) & ~15);
-          const uint32_t bytesA = A8 ? bytes8 : (uint32_t)wn.y * (uint32_t)sizeof(TA);
-          const uint32_t bytesB = NMAP == 3 ? bytes8 : 0u;
-          mchunk[st] = wn;
-          munit[st] = make_int2(un, (c == 0 ? FIRST : 0) | (c == nch - 1 ? LAST : 0));
-          mbar_arrive_expect_tx(&full[st], (uint32_t)rc * (bytesA + bytesB));   // (release: the meta)
-          for (int r = 0; r < rc; ++r) {
-            const size_t row = (size_t)(i0 + r) * Rp;
-            bulk_g2s(sA + st * E + r * stride, gA + row + (A8 ? eb : e0), bytesA, &full[st]);
-            if (NMAP == 3) bulk_g2s(sB + st * E + r * stride, gB + row + eb, bytesB, &full[st]);
-          }
-          if (++st == NST) { st = 0; ph ^= 1; }
-        }
+        if (++st == NST) { st = 0; ph ^= 1; }
       }
-      next_stage();   // end of work
-      munit[st] = make_int2(0, END);
-      mbar_arrive_expect_tx(&full[st], 0u);
     }
     return;
   }
 
   // ---------------- consumer warps ----------------
-  // per unit (set up when its first chunk arrives): lane -> (angle slot, ray); the slots' angle
-  // parameters and warp-uniform row ranges; accumulators
-  int k = 0, s = 0, rs = 0;
+  const int aq = ray_fast ? lane >> 3 : lane & 3;
+  const int k = kt + w * 8 + (ray_fast ? lane & 7 : lane >> 2);
+  const float kc = (float)k - dctr;
   float alpha[4], tn[4], scale[4];
-  int aidx[4], wlo[4], whi[4];
-  float2 am[4], ad[4], as[4];
+  int aidx[4];
 #pragma unroll
   for (int m = 0; m < 4; ++m) {
-    alpha[m] = tn[m] = scale[m] = 0.f;
-    aidx[m] = -1;
-    wlo[m] = 0x7fffffff;
-    whi[m] = -0x7fffffff;
+    const int al = min(aq + 4 * m, gi.y - 1);
+    const int a = args.order[gi.x + al];
+    aidx[m] = (aq + 4 * m < gi.y) ? a : -1;
+    const float4 t = __ldg(args.k1 + a);
+    alpha[m] = fmaf(kc, t.x, ctr);   // x* = alpha - tn * (i - ctr)
+    tn[m] = t.y;
+    scale[m] = t.z;
   }
+  // warp-uniform row range per slot: rows where at least one lane's ray has a tap inside the
+  // map (x* in (-1, N), linear in the row); rows outside it contribute exactly 0
+  int wlo[4], whi[4];
+#pragma unroll
+  for (int m = 0; m < 4; ++m) {
+    int lo = 0x7fffffff, hi = -0x7fffffff;
+    if (aidx[m] >= 0 && k < ND) {
+      // x* varies by less than 1/4 entry over the map (e.g. exactly 90 deg, where tn ~ 6e-17 and
+      // the row bounds below would overflow int): the ray keeps all rows or none (conservatively
+      // wide: rows outside the map read the zero padding inside the staged window)
+      if (fabsf(tn[m]) * (float)N < 0.25f) {
+        if (alpha[m] > -1.25f && alpha[m] < (float)N + 0.25f) { lo = 0; hi = N - 1; }
+      } else {
+        float y0 = (alpha[m] + 1.f) / tn[m], y1 = (alpha[m] - (float)N) / tn[m];
+        if (y0 > y1) { const float t = y0; y0 = y1; y1 = t; }
+        lo = max(0, (int)floorf(y0 + ctr) - 1);
+        hi = min(N - 1, (int)ceilf(y1 + ctr) + 1);
+      }
+    }
+    wlo[m] = __reduce_min_sync(0xffffffffu, lo);
+    whi[m] = __reduce_max_sync(0xffffffffu, hi);
+  }
+
+  float2 am[4], ad[4], as[4];
+#pragma unroll
+  for (int m = 0; m < 4; ++m) am[m] = ad[m] = as[m] = make_float2(0.f, 0.f);
+
   pdl_wait();   // sleep (not spin on the ring) while K0 runs: this CTA may have launched early
   int st = 0;
   uint32_t ph = 0;
-  for (;; st = (st + 1 == NST) ? 0 : st + 1, ph ^= (st == 0)) {
+  for (int c = 0; c < nch; ++c, st = (st + 1 == NST) ? 0 : st + 1, ph ^= (st == 0)) {
     mbar_wait_full(&full[st], ph);
-    const int2 mu = munit[st];
-    if (mu.y & END) break;
-    if (mu.y & FIRST) {   // a new work unit
-      const int un = mu.x;
-      const int tile = un % args.ntile, grp = (un / args.ntile) % args.ngroups, z = un / (args.ntile * args.ngroups);
-      s = z % args.S;
-      rs = z / args.S;
-      const int2 gr = __ldg(args.groups + grp);
-      const int2 gi = make_int2(gr.x, gr.y & 0xffff);   // {first sorted position, count}
-      const bool ray_fast = (gr.y >> 16) != 0;          // lane mapping of this group (plan)
-      const int aq = ray_fast ? lane >> 3 : lane & 3;
-      k = tile * RTILE + w * 8 + (ray_fast ? lane & 7 : lane >> 2);
-      const float kc = (float)k - dctr;
-#pragma unroll
-      for (int m = 0; m < 4; ++m) {
-        const int al = min(aq + 4 * m, gi.y - 1);
-        const int a = __ldg(args.order + gi.x + al);
-        aidx[m] = (aq + 4 * m < gi.y) ? a : -1;
-        const float4 t = __ldg(args.k1 + a);
-        alpha[m] = fmaf(kc, t.x, ctr);   // x* = alpha - tn * (i - ctr)
-        tn[m] = t.y;
-        scale[m] = t.z;
-      }
-      // warp-uniform row range per slot: rows where at least one lane's ray has a tap inside the
-      // map (x* in (-1, N), linear in the row); rows outside it contribute exactly 0
-#pragma unroll
-      for (int m = 0; m < 4; ++m) {
-        int lo = 0x7fffffff, hi = -0x7fffffff;
-        if (aidx[m] >= 0 && k < ND) {
-          // x* varies by less than 1/4 entry over the map (e.g. exactly 90 deg, where tn ~ 6e-17
-          // and the row bounds below would overflow int): the ray keeps all rows or none
-          // (conservatively wide: rows outside the map read the zero padding inside the window)
-          if (fabsf(tn[m]) * (float)N < 0.25f) {
-            if (alpha[m] > -1.25f && alpha[m] < (float)N + 0.25f) { lo = 0; hi = N - 1; }
-          } else {
-            float y0 = (alpha[m] + 1.f) / tn[m], y1 = (alpha[m] - (float)N) / tn[m];
-            if (y0 > y1) { const float t = y0; y0 = y1; y1 = t; }
-            lo = max(0, (int)floorf(y0 + ctr) - 1);
-            hi = min(N - 1, (int)ceilf(y1 + ctr) + 1);
-          }
-        }
-        wlo[m] = __reduce_min_sync(0xffffffffu, lo);
-        whi[m] = __reduce_max_sync(0xffffffffu, hi);
-        am[m] = ad[m] = as[m] = make_float2(0.f, 0.f);
-      }
-#ifdef EI_TRACE
-      ++my_units;
-#endif
-    }
-    const int4 wn = mchunk[st];
+    const int4 wn = swin[c];
     const int i0 = wn.z, rc = wn.w, i1 = i0 + rc - 1, stride = (wn.y + 3) & ~1;
     bool any = false, all = true;
 #pragma unroll
@@ -295,7 +255,7 @@ SPAN_START_proj();
       any |= (whi[m] >= i0 && wlo[m] <= i1);
       all &= (wlo[m] <= i0 && whi[m] >= i1);
     }
-    if (rc > 0 && any) {
+    if (any) {
       // staged-window check (the counter behind ei_plan_info out[4]): x* is linear in the row
       // and fmaf / floor are monotone, so every row's tap of a slot lies in the staged entries
       // [wn.x, wn.x + wn.y) iff the chunk's first and last rows' taps do
@@ -343,37 +303,10 @@ SPAN_START_proj();
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[st]);
-    if ((mu.y & LAST) && k < ND) {   // the unit's projections
-      const size_t plane = (size_t)args.NA * ND;
-      float *out = args.P + ((size_t)rs * args.S + s) * NMAP * plane + k;
-      float *outm = out + (ND - 1 - 2 * k);   // mirrored detector position ND-1-k
-#pragma unroll
-      for (int m = 0; m < 4; ++m) {
-        if (aidx[m] < 0) continue;
-        const float v0 = (am[m].x + am[m].y) * scale[m];
-        out[(size_t)aidx[m] * ND] = v0;
-        // the mirror angle theta + pi samples the same line at the mirrored detector position
-        // (R6: detector centred), so its projection is this value: one projection, two rows
-        const int b = args.has_pairs ? __ldg(args.partner + aidx[m]) : -1;   // no load in the tail
-        if (b >= 0) outm[(size_t)b * ND] = v0;
-        if constexpr (NMAP == 3) {
-          const float v1 = (ad[m].x + ad[m].y) * scale[m], v2 = (as[m].x + as[m].y) * scale[m];
-          out[plane + (size_t)aidx[m] * ND] = v1;
-          out[2 * plane + (size_t)aidx[m] * ND] = v2;
-          if (b >= 0) {
-            outm[plane + (size_t)b * ND] = v1;
-            outm[2 * plane + (size_t)b * ND] = v2;
-          }
-        }
-      }
-    }
   }
   pdl_trigger();
 #ifdef EI_TRACE
-  if (lane == 0) {
-    atomicMax(&s_rows, my_rows);
-    atomicMax(&s_units, my_units);
-  }
+  if (lane == 0) atomicMax(&s_rows, my_rows);
   asm volatile("bar.sync 1, %0;\n" ::"r"(NT) : "memory");   // consumers only
   if (tid == 0) {
     unsigned smid;
@@ -383,11 +316,34 @@ SPAN_START_proj();
       g_k1_trace[4 * b] = t_start;
       g_k1_trace[4 * b + 1] = gtimer();
       g_k1_trace[4 * b + 2] = smid;
-      g_k1_trace[4 * b + 3] = (unsigned long long)s_rows | ((unsigned long long)s_units << 32);
+      g_k1_trace[4 * b + 3] = (unsigned long long)s_rows | ((unsigned long long)un << 32);
     }
     SPAN_END_proj(0);
   }
 #endif
+  if (k >= ND) return;
+  const size_t plane = (size_t)args.NA * ND;
+  float *out = args.P + ((size_t)rs * args.S + s) * NMAP * plane + k;
+  float *outm = out + (ND - 1 - 2 * k);   // mirrored detector position ND-1-k
+#pragma unroll
+  for (int m = 0; m < 4; ++m) {
+    if (aidx[m] < 0) continue;
+    const float v0 = (am[m].x + am[m].y) * scale[m];
+    out[(size_t)aidx[m] * ND] = v0;
+    // the mirror angle theta + pi samples the same line at the mirrored detector position
+    // (R6: detector centred), so its projection is this value: one projection, two rows
+    const int b = args.has_pairs ? __ldg(args.partner + aidx[m]) : -1;   // no load in the tail
+    if (b >= 0) outm[(size_t)b * ND] = v0;
+    if constexpr (NMAP == 3) {
+      const float v1 = (ad[m].x + ad[m].y) * scale[m], v2 = (as[m].x + as[m].y) * scale[m];
+      out[plane + (size_t)aidx[m] * ND] = v1;
+      out[2 * plane + (size_t)aidx[m] * ND] = v2;
+      if (b >= 0) {
+        outm[plane + (size_t)b * ND] = v1;
+        outm[2 * plane + (size_t)b * ND] = v2;
+      }
+    }
+  }
 }
 
 template <int NMAP>
@@ -410,18 +366,16 @@ cudaError_t launch(const ei_plan &p, int RS, float *P, cudaStream_t st) {
   a.ngroups = p.proj.n_groups;
   a.N = p.N; a.NA = p.NA; a.ND = p.ND; a.S = p.S; a.RS = RS; a.E = p.proj.E;
   a.PAD = p.proj.PAD; a.Rp = p.proj.Rp;
+  a.nchmax = RS == 1 ? p.proj.nchmax1 : p.proj.nchmaxRS;
   a.P = P;
   a.diag = p.diag;
   a.nst = p.proj.nst;
-  a.counter = p.proj.counter;
-  a.nunits = p.proj.n_tiles * p.proj.n_groups * p.S * RS;
-  const size_t smem = k1_smem(a.nst, a.E, NMAP);
+  const size_t smem = k1_smem(a.nst, a.E, a.nchmax, NMAP);
   auto kern = p.proj.RT == RT ? project_kernel<NMAP, RT> : project_kernel<NMAP, RTS>;
   cudaError_t e = cudaFuncSetAttribute((const void *)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   if (RS != 1 && RS != p.proj.RS) return cudaErrorInvalidValue;   // unit tables exist for these
-  // persistent grid: the CTAs per SM the ring allows (plan) on every SM, or one per unit
-  dim3 grid(std::min(a.nunits, p.proj.ctas));
+  dim3 grid(p.proj.n_tiles * p.proj.n_groups * p.S * RS);
   e = launch_pdl(kern, grid, dim3(p.proj.RT * 4 + 32), smem, st, a);
   if (e != cudaSuccess) return e;
   return cudaGetLastError();
@@ -590,12 +544,30 @@ static std::vector<int> order_units(const Chunks &ch, int RS, int n_groups, int 
           cost.push_back({(long long)s * (1LL << 40) - c, t + ntile * (g + n_groups * (rs * S + s))});
         }
   std::stable_sort(cost.begin(), cost.end());    // slice-major, heaviest first; ties keep (rs, g, t)
-  // the persistent K1's CTAs take units from a counter in this order: heaviest first (longest-
-  // processing-time, the light units fill the tail), slice by slice (the CTAs in flight share one
-  // slice's maps in L2: LPT across all 64 slices of C4 raised K1's DRAM traffic ~10x)
-  (void)cps;
-  std::vector<int> unit(cost.size());
-  for (size_t b = 0; b < cost.size(); ++b) unit[b] = cost[b].second;
+  const int n = (int)cost.size();
+  int sms = 148, dev = 0;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaGetLastError();
+  std::vector<int> unit(n);
+  if (n > sms && n <= cps * sms && !getenv("EI_K1_LPT")) {
+    // one wave: SM m holds blocks m, m + sms, ...; each unit (heaviest first) goes to the SM with
+    // the least work so far among those with a free block
+    std::vector<int> cap(sms, 0), used(sms, 0);
+    std::vector<long long> load(sms, 0);
+    for (int b = 0; b < n; ++b) cap[b % sms] += 1;
+    for (int q = 0; q < n; ++q) {
+      int best = -1;
+      for (int m = 0; m < sms; ++m)
+        if (used[m] < cap[m] && (best < 0 || load[m] < load[best])) best = m;
+      unit[best + used[best] * sms] = cost[q].second;
+      used[best] += 1;
+      long long rows = (-cost[q].first) % (1LL << 40);   // the unit's rows (key = s 2^40 - rows)
+      if (rows < 0) rows += 1LL << 40;
+      load[best] += rows;
+    }
+  } else {
+    for (int b = 0; b < n; ++b) unit[b] = cost[b].second;
+  }
   return unit;
 }
 
@@ -710,8 +682,7 @@ int plan_projector(ei_plan &p, const double *angles, const std::vector<int> &pro
   } else {
     chRS = ch1;
   }
-  if (k1_smem(nst, E, 3) > 220 * 1024) return EI_ERR_SHAPE;
-  p.proj.ctas = cps * sms;   // persistent K1 grid
+  if (k1_smem(nst, E, std::max(ch1.nchmax, chRS.nchmax), 3) > 220 * 1024) return EI_ERR_SHAPE;
   if (getenv("EI_PLAN_VERBOSE"))
     fprintf(stderr, "libei plan: K1 RT %d RS %d nst %d E %d: %zu chunks, <= %d per unit, %.2f rows avg, <= %d rows, "
             "widest window %d\n", p.proj.RT, RS, nst, E, ch1.c.size(), ch1.nchmax,

@@ -68,7 +68,7 @@ void free_plan(ei_plan *p) {
   for (cudaEvent_t ev : p->h_ev)
     if (ev) cudaEventDestroy(ev);
   void *ptrs[] = {p->tab.k1, p->tab.k3, p->proj.groups, p->proj.order, p->proj.partner, p->alist3,
-                  p->pairs, p->proj.counter, p->proj.chunks1, p->proj.coff1, p->proj.chunksRS, p->proj.coffRS, p->proj.unit1, p->proj.unitRS, p->MA, p->MAT, p->MB,
+                  p->pairs, p->proj.chunks1, p->proj.coff1, p->proj.chunksRS, p->proj.coffRS, p->proj.unit1, p->proj.unitRS, p->MA, p->MAT, p->MB,
                   p->MBT, p->M1, p->M1T, p->diag, p->part_mo, p->part3, p->k3u, p->P, p->GA, p->GB, p->GC, p->GA1,
                   p->part_curve, p->part_reg, p->h_maps, p->h_flat, p->h_mask, p->h_drift,
                   p->h_sexp, p->h_grad, p->h_cost, p->h_status};
@@ -207,7 +207,6 @@ int ei_plan_create(const ei_geometry *geom, const double *angles, ei_plan **out)
   A(dalloc(&p->M1, S * NP));
   A(dalloc(&p->M1T, S * NP));
   A(dalloc(&p->diag, 1));
-  A(dalloc(&p->proj.counter, 1));
   p->PADG = ei::bp_pad();
   p->RpG = (p->ND + 2 + 2 * p->PADG + 3) & ~3;   // multiple of 4: 16-B aligned C-plane rows
   const size_t SINO1 = (size_t)p->NA * p->RpG;
@@ -288,7 +287,6 @@ int ei_plan_create(const ei_geometry *geom, const double *angles, ei_plan **out)
   if (e == cudaSuccess && !pairs.empty())
     A(cudaMemcpy(p->pairs, pairs.data(), sizeof(int2) * pairs.size(), cudaMemcpyHostToDevice));
   if (e == cudaSuccess) A(cudaMemset(p->diag, 0, sizeof(int32_t)));
-  if (e == cudaSuccess) A(cudaMemset(p->proj.counter, 0, sizeof(int)));
   if (e == cudaSuccess && p->k3u)
     A(cudaMemcpy(p->k3u, k3u.data(), sizeof(int4) * k3u.size(), cudaMemcpyHostToDevice));
 
@@ -341,7 +339,7 @@ int ei_plan_info(const ei_plan *p, int64_t out[10]) {
   out[2] = p->proj.wmax;
   out[3] = p->proj.RS;
   out[4] = d;
-  out[5] = (int64_t)ei::k1_smem(p->proj.nst, p->proj.E, 3);
+  out[5] = (int64_t)ei::k1_smem(p->proj.nst, p->proj.E, std::max(p->proj.nchmax1, p->proj.nchmaxRS), 3);
   out[6] = p->proj.ray_fast;
   out[7] = p->KS;
   out[8] = p->npairs;

@@ -29,16 +29,17 @@ def main(out):
     d = json.loads(r.stdout.strip().splitlines()[-1])
     clocks = sampler.summary(t0, t1)
     d["clocks"] = clocks
-    # the SM clock: nvidia-smi's median during the run (the kernels' own clock64 spans are kept as
-    # a cross-check; they undercount when a launch's blocks do not all start at once)
-    d["sm_mhz"] = clocks.get("sm_mhz") or 1965.0
+    # the SM clock: measured under load by a clock64 spin kernel (cycles / event time); nvidia-smi's
+    # samples also see the idle gaps between the short launches, and the block-span figures
+    # undercount when a launch's blocks do not all start at once (both kept as cross-checks)
+    d["sm_mhz"] = d.get("sm_mhz_spin") or clocks.get("sm_mhz") or 1965.0
     for k in ("smem_lds128", "smem_lds64", "l2_read"):
         d[k + "_bytes_per_clk_per_sm"] = round(d[k + "_gbs"] * 1e9 / (d["sm_mhz"] * 1e6) / d["sms"], 2)
     d["nominal_smem_gbs_at_clock"] = round(128.0 * d["sms"] * d["sm_mhz"] * 1e6 / 1e9, 1)
     d["how"] = ("tools/microbench.cu: best of 5 CUDA-event-timed launches each; LDS.128 / LDS.64 "
                 "conflict-free (4 CTAs x 256 threads per SM), L2 read of a 48 MB resident buffer "
-                "(__ldcg, 40 passes), HBM read of 4 GiB (8 passes); clocks sampled by nvidia-smi "
-                "during the run")
+                "(__ldcg, 40 passes), HBM read of 4 GiB (8 passes); SM clock from a "
+                "clock64 spin kernel; nvidia-smi clocks sampled during the run")
     d["when"] = time.strftime("%Y-%m-%dT%H:%M:%SZ", time.gmtime())
     os.makedirs(os.path.dirname(os.path.abspath(out)), exist_ok=True)
     json.dump(d, open(out, "w"), indent=1)

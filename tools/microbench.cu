@@ -60,6 +60,15 @@ static double mean_cycles(const long long* d, int n) {
   return s / n;
 }
 
+// SM clock under load: every block spins for a fixed number of its SM's clock64 cycles; the event
+// time of the launch gives the clock rate (the spin keeps the SMs busy, so DVFS sees load)
+__global__ void clock_kernel(long long cycles, float* out) {
+  const long long t0 = clock64();
+  long long t = t0;
+  while (t - t0 < cycles) t = clock64();
+  if (t == 42) out[0] = 1.f;
+}
+
 template <typename F>
 static double best_ms(F launch, int reps = 5) {
   cudaEvent_t a, b;
@@ -115,11 +124,15 @@ int main() {
   ms = best_ms([&] { smem_kernel<float2><<<sms * 4, 256>>>(iters, out, cyc); });
   const double lds64 = nload * 8 / (ms * 1e-3) / 1e9;
   const double lds64_bpc = nload * 8 / sms / mean_cycles(cyc, sms * 4);
+  // SM clock under load (right after the shared-memory runs): cycles / time of a spin launch
+  const long long spin = 400000000LL;
+  ms = best_ms([&] { clock_kernel<<<sms * 4, 32>>>(spin, out); }, 3);
+  const double spin_mhz = (double)spin / (ms * 1e3);
   const cudaError_t e = cudaDeviceSynchronize();
   printf("{\"l2_read_gbs\": %.1f, \"hbm_read_gbs\": %.1f, \"smem_lds128_gbs\": %.1f, "
          "\"smem_lds64_gbs\": %.1f, \"blockspan_lds128_bytes_per_sm_clk\": %.2f, "
          "\"blockspan_lds64_bytes_per_sm_clk\": %.2f, \"blockspan_mhz_smem\": %.1f, "
-         "\"blockspan_mhz_l2\": %.1f, \"sms\": %d, \"cuda\": \"%s\"}\n",
-         l2, hbm, lds128, lds64, lds128_bpc, lds64_bpc, smem_mhz, l2_mhz, sms, cudaGetErrorString(e));
+         "\"blockspan_mhz_l2\": %.1f, \"sm_mhz_spin\": %.1f, \"sms\": %d, \"cuda\": \"%s\"}\n",
+         l2, hbm, lds128, lds64, lds128_bpc, lds64_bpc, smem_mhz, l2_mhz, spin_mhz, sms, cudaGetErrorString(e));
   return e == cudaSuccess ? 0 : 1;
 }

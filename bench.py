@@ -120,9 +120,12 @@ def kernel_bytes_h(cfg, rsu, mirror_pairs=0):
             "K2_curve": float(S * NA * ND * (4 + 4 * M + 8) + S * ND * 12)}
 
 
-def kernel_table(kb, kern_ms, n_rec, ms_step, sm_mhz, hbm_peak):
+def kernel_table(kb, kern_ms, n_rec, ms_step, sm_mhz, hbm_peak, cfg_name=None):
     """Per-kernel time, share of the step and roofline fraction (K1/K3 against the shared-memory
-    data-pipe peak, K2 against HBM), and the dominant kernel."""
+    data-pipe peak, K2 against HBM), and the dominant kernel.  Beside the algorithmic fraction, the
+    DRAM bytes the committed ncu capture of this config measured per launch (profiles/traffic.json)
+    over the same CUDA-event time: `dram_frac` is the kernel's HBM utilisation on its actual bytes
+    (K2 writes K3's 36-B triple layout where SURVEY's algorithmic count has 12 B of gradient)."""
     per_kernel_ms = {k: v / max(n_rec, 1) for k, v in kern_ms.items()}
     l1_peak, _ = onchip_peak(sm_mhz)                                  # GB/s, DESIGN.md §6
     kernels = {}
@@ -133,6 +136,11 @@ def kernel_table(kb, kern_ms, n_rec, ms_step, sm_mhz, hbm_peak):
         kernels[k] = {"ms": round(per_kernel_ms[k], 5), "share": round(per_kernel_ms[k] / ms_step, 4),
                       "bound": bound, "achieved": round(ach, 1), "peak": round(peak, 1), "unit": "GB/s",
                       "frac": round(ach / peak, 4), "bytes_per_launch": kb[k]}
+        dram, _ = load_traffic(cfg_name, k) if cfg_name else (None, None)
+        if dram and per_kernel_ms[k] > 0:
+            dgbs = dram / (per_kernel_ms[k] * 1e-3) / 1e9
+            kernels[k].update({"dram_bytes_per_launch": dram, "dram_gbs": round(dgbs, 1),
+                               "dram_frac": round(dgbs / hbm_peak, 4)})
     kernels["K0_pack"] = {"ms": round(per_kernel_ms["K0_pack"], 5),
                           "share": round(per_kernel_ms["K0_pack"] / ms_step, 4)}
     dom = max(("K1_project", "K2_curve", "K3_backproject"), key=lambda k: per_kernel_ms[k])
@@ -357,7 +365,7 @@ def run_gpu(args, cfg, rank, world, local_rank):
     rsu = ray_sample_updates(cfg)
     kb = kernel_bytes(cfg, rsu, plan_info.get("mirror_pairs", 0))
     sm_mhz = clocks.get("sm_mhz") or peaks.get("sm_max_mhz", 1965.0)
-    kernels, dom = kernel_table(kb, kern_ms, n_rec, ms_step, sm_mhz, peaks.get("hbm_gbs", 6650.0))
+    kernels, dom = kernel_table(kb, kern_ms, n_rec, ms_step, sm_mhz, peaks.get("hbm_gbs", 6650.0), cfg.name)
     d = kernels[dom]
     roofline = {"kernel": dom, "bound": d["bound"], "achieved": d["achieved"], "peak": d["peak"],
                 "unit": "GB/s", "frac": d["frac"], "traffic": load_traffic(cfg.name, dom)[0],
@@ -624,7 +632,7 @@ def run_gpu_h(args, cfg):
     peaks = load_peaks()
     sm_mhz = clocks.get("sm_mhz") or peaks.get("sm_max_mhz", 1965.0)
     kb = kernel_bytes_h(cfg, rsu, ei.ei_plan_info(plan).get("mirror_pairs", 0))
-    kernels, dom = kernel_table(kb, kern_ms, n_rec, ms_step, sm_mhz, peaks.get("hbm_gbs", 6650.0))
+    kernels, dom = kernel_table(kb, kern_ms, n_rec, ms_step, sm_mhz, peaks.get("hbm_gbs", 6650.0), cfg.name)
     d = kernels[dom]
     traffic, tsrc = load_traffic(cfg.name, dom)
     roofline = {"kernel": dom, "bound": d["bound"], "achieved": d["achieved"], "peak": d["peak"],

@@ -357,7 +357,17 @@ SPAN_START_bp();
   const float ctr = 0.5f * (float)(N - 1), dctr = 0.5f * (float)(ND - 1);
   const size_t rowlen = (size_t)RpG, soff = (size_t)s * NA * rowlen + PADG;
   const int a_lo = (int)(((long long)ks * NA3) / nks), a_hi = (int)(((long long)(ks + 1) * NA3) / nks);
-  const int c_hi = (a_hi - a_lo + CH - 1) / CH;
+#ifndef EI_K3_CH0
+#define EI_K3_CH0 8
+#endif
+  // chunk c holds angles [c0(c), c0(c) + na(c)): a first chunk of CH0 = 8 <= CH angles lets the
+  // consumers start before a whole chunk has landed (C4 K3 8.13 -> 8.07 ms, C1 15.0 -> 13.7 us;
+  // 4 angles: the same on C4, slower on C1; compile-time switch EI_K3_CH0)
+  constexpr int CH0 = EI_K3_CH0;
+  const int nang = a_hi - a_lo;
+  const int c_hi = nang <= CH0 ? 1 : 1 + (nang - CH0 + CH - 1) / CH;
+  auto c0 = [&](int c) { return c == 0 ? 0 : CH0 + (c - 1) * CH; };
+  auto nac = [&](int c) { return min(c == 0 ? CH0 : CH, nang - c0(c)); };
   const int *alist_k = alist + a_lo;
 
   if (tid == 0) {
@@ -378,10 +388,10 @@ SPAN_START_bp();
     uint32_t ph = 0;
     for (int c = 0; c < c_hi; ++c) {
       if (c >= NST3) mbar_wait(&sm.empty[st], ph ^ 1);
-      const int na = min(CH, a_hi - a_lo - c * CH);
+      const int na = nac(c);
       int e0 = 0;
       if (lane < na) {   // per-angle tables + window start
-        const int a = __ldg(alist_k + c * CH + lane);
+        const int a = __ldg(alist_k + c0(c) + lane);
         const float4 g = __ldg(k3 + a);   // c', s', 1/h, Joseph weight
         const float k00 = fmaf(xa, g.x, fmaf(ya, g.y, dctr)), k01 = fmaf(xb, g.x, fmaf(ya, g.y, dctr));
         const float k10 = fmaf(xa, g.x, fmaf(yb, g.y, dctr)), k11 = fmaf(xb, g.x, fmaf(yb, g.y, dctr));
@@ -401,7 +411,7 @@ SPAN_START_bp();
       if (lane == 0) mbar_arrive_expect_tx(&sm.full[st], (uint32_t)na * (2u * bytesAB + bytesC));
       __syncwarp();
       if (lane < na) {
-        const size_t row = soff + (size_t)__ldg(alist_k + c * CH + lane) * rowlen + e0;
+        const size_t row = soff + (size_t)__ldg(alist_k + c0(c) + lane) * rowlen + e0;
         bulk_g2s(&sm.a[st][lane][0], GA + row, bytesAB, &sm.full[st]);
         bulk_g2s(&sm.b[st][lane][0], GB + row, bytesAB, &sm.full[st]);
         bulk_g2s(&sm.c[st][lane][0], GC + row, bytesC, &sm.full[st]);
@@ -453,7 +463,7 @@ SPAN_START_bp();
   uint32_t ph = 0;
   for (int c = 0; c < c_hi; ++c) {
     mbar_wait_full(&sm.full[st], ph);
-    const int na = min(CH, a_hi - a_lo - c * CH);
+    const int na = nac(c);
     // the chunk's angles of the current class, then (at most once per CTA) the class change
     // and the rest: the plan lists cos >= 0 first, so the change is one index per chunk
     const int nb = cls ? na : min(na, sm.nb[st]);

@@ -73,14 +73,21 @@ struct Smem1 {
 // keep each LDS on distinct banks), all starting at the same entry e0, a multiple of 4 (16-B aligned
 // C-plane copies), so one index addresses all three; e0 <= floor(min k*) + 1 - 0 and the window
 // holds WL3 = 52 >= 45 + 4 entries
-constexpr int NST3 = 2;
+#ifndef EI_K3_NST3
+#define EI_K3_NST3 2
+#endif
+#ifndef EI_K3_CH3
+#define EI_K3_CH3 16
+#endif
+constexpr int NST3 = EI_K3_NST3;   // ring stages (compile-time switches for A/B runs)
+constexpr int CH3 = EI_K3_CH3;     // angles per staged chunk
 constexpr int WL3 = 52;
 struct Smem3 {
-  float4 a[NST3][CH][WL3];   // (m[e-1], m[e], s[e-1], s[e])
-  float4 b[NST3][CH][WL3];   // (d[e-1], d[e], m[e+1], d[e+1])
-  float c[NST3][CH][WL3];    // s[e+1]
-  float4 t1[NST3][CH];       // c', s', 1/h, 1 - 1/h
-  float4 t2[NST3][CH];       // (Nd-1)/2 + 1 - e0 + min(c', 0), |c'|, 1 - 2/h, 1 + 1/h
+  float4 a[NST3][CH3][WL3];   // (m[e-1], m[e], s[e-1], s[e])
+  float4 b[NST3][CH3][WL3];   // (d[e-1], d[e], m[e+1], d[e+1])
+  float c[NST3][CH3][WL3];    // s[e+1]
+  float4 t1[NST3][CH3];       // c', s', 1/h, 1 - 1/h
+  float4 t2[NST3][CH3];       // (Nd-1)/2 + 1 - e0 + min(c', 0), |c'|, 1 - 2/h, 1 + 1/h
   int nb[NST3];              // first angle of the chunk with cos < 0 (CH if none)
   float tot[12][NT];        // per consumer thread: totals of finished angle classes (pair, L/R, map)
   uint64_t full[NST3], empty[NST3];
@@ -365,9 +372,9 @@ SPAN_START_bp();
   // 4 angles: the same on C4, slower on C1; compile-time switch EI_K3_CH0)
   constexpr int CH0 = EI_K3_CH0;
   const int nang = a_hi - a_lo;
-  const int c_hi = nang <= CH0 ? 1 : 1 + (nang - CH0 + CH - 1) / CH;
-  auto c0 = [&](int c) { return c == 0 ? 0 : CH0 + (c - 1) * CH; };
-  auto nac = [&](int c) { return min(c == 0 ? CH0 : CH, nang - c0(c)); };
+  const int c_hi = nang <= CH0 ? 1 : 1 + (nang - CH0 + CH3 - 1) / CH3;
+  auto c0 = [&](int c) { return c == 0 ? 0 : CH0 + (c - 1) * CH3; };
+  auto nac = [&](int c) { return min(c == 0 ? CH0 : CH3, nang - c0(c)); };
   const int *alist_k = alist + a_lo;
 
   if (tid == 0) {

@@ -237,6 +237,35 @@ def test_project_parity_both_lane_mappings(ei, name, ray_fast, monkeypatch):
             assert rel_l2(got[s, q], ref) < 2e-5, (s, q)
 
 
+@pytest.mark.parametrize("name", ["C2", "R1", "C5"])
+def test_k1_chunking_does_not_change_projections(ei, name, monkeypatch):
+    """K1 cuts each unit's rows into chunks of as many rows as fit a ring stage at the chunk's own
+    window width; every ray still sums its rows one by one in row order, so the projections are
+    bit-identical whatever the chunk sizes (capped at 1, 3 and 7 rows here), and match the oracle."""
+    cfg = synth.CONFIGS[name] if name in synth.CONFIGS else _cases.cached_case(name).cfg
+    S = min(cfg.S, 2)
+    maps = synth.uniform((S, 3, cfg.N, cfg.N), 31)
+    outs, rows = [], []
+    for rc in (None, "1", "3", "7"):
+        if rc is None:
+            monkeypatch.delenv("EI_K1_RC", raising=False)
+        else:
+            monkeypatch.setenv("EI_K1_RC", rc)
+        plan = plan_for(ei, cfg, S)
+        sino = torch.zeros(S, 3, cfg.n_angles, cfg.n_det, device="cuda")
+        ei.ei_project(plan, dev(maps), 3, sino)
+        torch.cuda.synchronize()
+        info = ei.ei_plan_info(plan)
+        assert info["window_overflows"] == 0
+        rows.append(info["k1_rows_per_chunk"])
+        outs.append(sino.cpu().numpy())
+    assert rows[1] == 1 and rows[2] <= 3 and rows[3] <= 7
+    for o in outs[1:]:
+        assert np.array_equal(o, outs[0])
+    ref = ora.project(maps[0, 0].astype(np.float64), cfg.angles, cfg.n_det, cfg.pixel, cfg.det_pitch)
+    assert rel_l2(outs[0][0, 0], ref) < 2e-5
+
+
 @pytest.mark.parametrize("mirror", ["1", "0"])
 def test_mirror_pairs_360(ei, mirror, monkeypatch):
     """360-degree scans: (theta, theta + pi) sample the same lines with the detector mirrored (R6),

@@ -377,10 +377,9 @@ def run_gpu(args, cfg, rank, world, local_rank):
         "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": K,
         "warmup": args.warmup, "ms_per_step": round(ms_step, 5), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": "%s: %s" % (cfg.name, describe(cfg)), "slices_per_gpu": cfg.S,
-                   "lambda": lam, "eval_point": "x_pert (R21)",
-                   "l2": "flushed before every timed step (256 MiB write, untimed)",
-                   "parallelism": "slice-parallel replicas" if world > 1 else "1 GPU"},
+        "config": bench_config(cfg, lam),
+        "l2": "flushed before every timed step (256 MiB write, untimed)",
+        "parallelism": "slice-parallel replicas" if world > 1 else "1 GPU",
         # SURVEY §8(d) counts every angle's samples ("effective"); with mirror pairs (360-degree
         # scans) K1/K3 execute only the primaries' samples ("executed")
         "ray_sample_updates_per_s": round(world * 6 * rsu * cfg.S / (ms_step * 1e-3), 1),
@@ -458,15 +457,22 @@ def run_gpu_angles(args, cfg, rank, world, local_rank):
         "metric": METRIC, "value": round(1000.0 / ms_step, 3), "unit": UNIT, "n_gpus": world, "steps": K,
         "warmup": args.warmup, "ms_per_step": round(ms_step, 5), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": "%s: %s" % (cfg.name, describe(cfg)), "slices_per_gpu": cfg.S,
-                   "lambda": lam, "eval_point": "x_pert (R21)", "parallelism": "angle-sharded x%d, NCCL "
-                   "all-reduce of gradient + cost per evaluation" % world,
-                   "l2": "flushed before every timed step (256 MiB write, untimed)"},
+        "config": bench_config(cfg, lam),
+        "parallelism": "angle-sharded x%d, NCCL all-reduce of gradient + cost per evaluation" % world,
+        "l2": "flushed before every timed step (256 MiB write, untimed)",
         "ray_sample_updates_per_s": round(6 * rsu * cfg.S / (ms_step * 1e-3), 1),
         "angles_rank0": int(len(sh.idx)), "gpu_launches": int(s1[5] - s0[5]),
         "clocks": sampler.summary(t0, t1), "plan": ei.ei_plan_info(sh.plan),
         "e2e": None,
     }
+
+
+def bench_config(cfg, lam):
+    """The workload identity, the same dict on the GPU arm and the reference arm (both evaluate
+    the x_pert point of the same seeded case); how a run was executed (parallelism, L2 policy)
+    sits in top-level keys."""
+    return {"workload": "%s: %s" % (cfg.name, describe(cfg)), "slices_per_gpu": cfg.S,
+            "lambda": lam, "eval_point": "x_pert (R21)"}
 
 
 def describe(cfg):
@@ -533,7 +539,7 @@ def run_reference(args, cfg, rank):
             "warmup": args.warmup, "ms_per_step": round(per_slice * 1e3 * cfg.S, 3),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "impl": "reference",
-            "config": {"workload": "%s: %s" % (cfg.name, describe(cfg)), "lambda": args.lam},
+            "config": bench_config(cfg, args.lam), "parallelism": "1 process, oracle threads on host cores",
             "cpu_baseline": {"value": round(value, 6), "unit": UNIT, "cores": ora.num_threads(),
                              "kind": "oracle", "sample": sample},
             "e2e": {"value": round(value, 6), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}

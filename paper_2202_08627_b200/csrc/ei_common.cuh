@@ -29,6 +29,7 @@ struct ProjPlan {
   int *partner = nullptr;   // device [NA]: the angle theta + pi of a projected angle, or -1
   int n_groups = 0;
   int RT = 64;              // rays per K1 CTA (64, or 32 for small single-wave grids)
+  int nsl = 4;              // angle slots per K1 thread (angles per CTA = 4 nsl)
   int k0_early = 0;         // K0 triggers K1's launch at its start (K1 grid smaller than the SMs)
   int nst = 4;              // K1 ring stages
   int E = 0;                // K1 ring-stage capacity (entries; rows x stride of a chunk <= E)

@@ -13,7 +13,8 @@
 //    2-3 stage mbarrier ring; every chunk's window is computed exactly on the host (plan) so every
 //    index stays inside the staged window without per-sample checks;
 //  * a warp = 4 adjacent angles x 8 adjacent rays (angle fastest) or 8 rays x 4 angles (ray
-//    fastest, sparse views), chosen per angle group from a bank-conflict model;
+//    fastest, sparse views), chosen per angle group from a bank-conflict model; each thread
+//    carries NSL = 4 angle slots (2 for grids far below one wave: 8-angle CTAs);
 //  * one tap pair of all three maps = one LDS.128 + one LDS.64; weights (1-w, w) as a float2 and
 //    three FFMA2 per sample (acc.x: left taps, acc.y: right taps);
 //  * small problems split the rows over RS CTAs (partial P summed in fixed order by K2); the
@@ -39,7 +40,7 @@ size_t k1_smem(int nst, int E, int nchmax, int nmap) {
 
 namespace {
 
-constexpr int AGB = 16;   // angles per CTA
+constexpr int AGB = 16;   // angles per CTA (4 x NSL: 8 with two slots, small grids, plan_projector)
 constexpr int RT = 64;    // rays per CTA (RTS = 32 for small single-wave grids, plan_projector)
 constexpr int RTS = 32;
 
@@ -124,7 +125,7 @@ constexpr int NSTMAX = 4;       // pipeline stages (shared-memory ring): 2 (plan
 // spread over tens of entries and conflict).
 // RTILE rays per CTA: RTILE / 8 consumer warps (NT threads) + the producer warp; 2 CTAs per SM
 // with 64-ray tiles, 4 with 32-ray tiles (same warps per SM, finer units to balance small grids)
-template <int NMAP, int RTILE>
+template <int NMAP, int RTILE, int NSL>
 __global__ void __launch_bounds__(RTILE * 4 + 32, RTILE == 64 ? 2 : 4) project_kernel(ProjArgs args) {
   constexpr int NT = RTILE * 4, NCW = NT / 32;
   using TA = typename PL<NMAP>::A;
@@ -203,10 +204,10 @@ SPAN_START_proj();
   const int aq = ray_fast ? lane >> 3 : lane & 3;
   const int k = kt + w * 8 + (ray_fast ? lane & 7 : lane >> 2);
   const float kc = (float)k - dctr;
-  float alpha[4], tn[4], scale[4];
-  int aidx[4];
+  float alpha[NSL], tn[NSL], scale[NSL];
+  int aidx[NSL];
 #pragma unroll
-  for (int m = 0; m < 4; ++m) {
+  for (int m = 0; m < NSL; ++m) {
     const int al = min(aq + 4 * m, gi.y - 1);
     const int a = args.order[gi.x + al];
     aidx[m] = (aq + 4 * m < gi.y) ? a : -1;
@@ -217,9 +218,9 @@ SPAN_START_proj();
   }
   // warp-uniform row range per slot: rows where at least one lane's ray has a tap inside the
   // map (x* in (-1, N), linear in the row); rows outside it contribute exactly 0
-  int wlo[4], whi[4];
+  int wlo[NSL], whi[NSL];
 #pragma unroll
-  for (int m = 0; m < 4; ++m) {
+  for (int m = 0; m < NSL; ++m) {
     int lo = 0x7fffffff, hi = -0x7fffffff;
     if (aidx[m] >= 0 && k < ND) {
       // x* varies by less than 1/4 entry over the map (e.g. exactly 90 deg, where tn ~ 6e-17 and
@@ -238,9 +239,9 @@ SPAN_START_proj();
     whi[m] = __reduce_max_sync(0xffffffffu, hi);
   }
 
-  float2 am[4], ad[4], as[4];
+  float2 am[NSL], ad[NSL], as[NSL];
 #pragma unroll
-  for (int m = 0; m < 4; ++m) am[m] = ad[m] = as[m] = make_float2(0.f, 0.f);
+  for (int m = 0; m < NSL; ++m) am[m] = ad[m] = as[m] = make_float2(0.f, 0.f);
 
   pdl_wait();   // sleep (not spin on the ring) while K0 runs: this CTA may have launched early
   int st = 0;
@@ -251,7 +252,7 @@ SPAN_START_proj();
     const int i0 = wn.z, rc = wn.w, i1 = i0 + rc - 1, stride = (wn.y + 3) & ~1;
     bool any = false, all = true;
 #pragma unroll
-    for (int m = 0; m < 4; ++m) {
+    for (int m = 0; m < NSL; ++m) {
       any |= (whi[m] >= i0 && wlo[m] <= i1);
       all &= (wlo[m] <= i0 && whi[m] >= i1);
     }
@@ -263,7 +264,7 @@ SPAN_START_proj();
         const float ya = (float)i0 - ctr, yb = (float)i1 - ctr;
         bool bad = false;
 #pragma unroll
-        for (int m = 0; m < 4; ++m) {
+        for (int m = 0; m < NSL; ++m) {
           const int ja = __float2int_rd(fmaf(-tn[m], ya, alpha[m]));
           const int jb = __float2int_rd(fmaf(-tn[m], yb, alpha[m]));
           bad |= min(ja, jb) < wn.x || max(ja, jb) >= wn.x + wn.y;
@@ -276,7 +277,7 @@ SPAN_START_proj();
       float yi = (float)i0 - ctr;
       auto body = [&](bool masked, int i) {
 #pragma unroll
-        for (int m = 0; m < 4; ++m) {
+        for (int m = 0; m < NSL; ++m) {
           const float xs = fmaf(-tn[m], yi, alpha[m]);
           const int j0 = __float2int_rd(xs);
           const float fr = xs - (float)j0;
@@ -326,7 +327,7 @@ SPAN_START_proj();
   float *out = args.P + ((size_t)rs * args.S + s) * NMAP * plane + k;
   float *outm = out + (ND - 1 - 2 * k);   // mirrored detector position ND-1-k
 #pragma unroll
-  for (int m = 0; m < 4; ++m) {
+  for (int m = 0; m < NSL; ++m) {
     if (aidx[m] < 0) continue;
     const float v0 = (am[m].x + am[m].y) * scale[m];
     out[(size_t)aidx[m] * ND] = v0;
@@ -371,7 +372,8 @@ cudaError_t launch(const ei_plan &p, int RS, float *P, cudaStream_t st) {
   a.diag = p.diag;
   a.nst = p.proj.nst;
   const size_t smem = k1_smem(a.nst, a.E, a.nchmax, NMAP);
-  auto kern = p.proj.RT == RT ? project_kernel<NMAP, RT> : project_kernel<NMAP, RTS>;
+  auto kern = p.proj.nsl == 2 ? (p.proj.RT == RT ? project_kernel<NMAP, RT, 2> : project_kernel<NMAP, RTS, 2>)
+                                : (p.proj.RT == RT ? project_kernel<NMAP, RT, 4> : project_kernel<NMAP, RTS, 4>);
   cudaError_t e = cudaFuncSetAttribute((const void *)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   if (RS != 1 && RS != p.proj.RS) return cudaErrorInvalidValue;   // unit tables exist for these
@@ -484,7 +486,7 @@ static double wavefront_model(const ei_plan &p, const double *angles, const std:
   const int tstep = std::max(1, (ND / 64) / 6);
   for (int kt = 0; kt + 64 <= ND; kt += 64 * tstep)
       for (int w = 0; w < 8; ++w)
-        for (int m = 0; m < 4; ++m)
+        for (int m = 0; m < p.proj.nsl; ++m)
           for (int i : rows) {
             long long e[32];
             for (int lane = 0; lane < 32; ++lane) {
@@ -582,11 +584,22 @@ int plan_projector(ei_plan &p, const double *angles, const std::vector<int> &pro
   auto wrap = [](double t) { t = fmod(t, 2 * M_PI); return t < 0 ? t + 2 * M_PI : t; };
   std::stable_sort(idx.begin(), idx.end(), [&](int x, int y) { return wrap(angles[x]) < wrap(angles[y]); });
   auto rowdom = [&](int a) { return fabs(cos(angles[a])) >= fabs(sin(angles[a])); };
+  // Angles per CTA: 16 (4 slots per thread), or 8 (2 slots) when the 16-angle grid of 64-ray
+  // tiles would leave more than half the SMs idle: twice the units, each half as long (C1 K1 11.9
+  // -> 10.6 us, step 27.9 -> 26.8; P1 unchanged; on C2's single wave of 138 x 4 units the 8-angle
+  // units lose more in per-unit staging than they gain in balance, K1 33.1 -> 37.2 us, so C2
+  // keeps 16; tools/dbg/sweep_nsl.sh; knob EI_K1_NSL)
+  int sms0 = 148, dev0 = 0;
+  if (cudaGetDevice(&dev0) == cudaSuccess) cudaDeviceGetAttribute(&sms0, cudaDevAttrMultiProcessorCount, dev0);
+  cudaGetLastError();
+  p.proj.nsl = 2LL * ((ND + RT - 1) / RT) * ((NA + AGB - 1) / AGB) * p.S <= sms0 ? 2 : 4;
+  if (const char *e = getenv("EI_K1_NSL")) p.proj.nsl = atoi(e) == 2 ? 2 : 4;   // tuning knob
+  const int agb = 4 * p.proj.nsl;
   order.clear();
   groups.clear();
   for (int q = 0; q < NA; ++q) {
     const int a = idx[q];
-    if (groups.empty() || groups.back().y == AGB || rowdom(a) != rowdom(order.back()))
+    if (groups.empty() || groups.back().y == agb || rowdom(a) != rowdom(order.back()))
       groups.push_back(make_int2((int)order.size(), 0));
     order.push_back(a);
     groups.back().y += 1;
@@ -684,8 +697,8 @@ int plan_projector(ei_plan &p, const double *angles, const std::vector<int> &pro
   }
   if (k1_smem(nst, E, std::max(ch1.nchmax, chRS.nchmax), 3) > 220 * 1024) return EI_ERR_SHAPE;
   if (getenv("EI_PLAN_VERBOSE"))
-    fprintf(stderr, "libei plan: K1 RT %d RS %d nst %d E %d: %zu chunks, <= %d per unit, %.2f rows avg, <= %d rows, "
-            "widest window %d\n", p.proj.RT, RS, nst, E, ch1.c.size(), ch1.nchmax,
+    fprintf(stderr, "libei plan: K1 RT %d angles %d RS %d nst %d E %d: %zu chunks, <= %d per unit, %.2f rows avg, <= %d rows, "
+            "widest window %d\n", p.proj.RT, 4 * p.proj.nsl, RS, nst, E, ch1.c.size(), ch1.nchmax,
             ch1.c.empty() ? 0.0 : (double)[&] { long long r = 0; for (auto &q : ch1.c) r += q.w; return r; }() / ch1.c.size(),
             ch1.rcmax, ch1.wmax);
   p.proj.E = E;

@@ -266,6 +266,33 @@ def test_k1_chunking_does_not_change_projections(ei, name, monkeypatch):
     assert rel_l2(outs[0][0, 0], ref) < 2e-5
 
 
+@pytest.mark.parametrize("name", ["C1", "C2", "R1"])
+@pytest.mark.parametrize("n_maps", [3, 1])
+def test_k1_angles_per_cta_do_not_change_projections(ei, name, n_maps, monkeypatch):
+    """K1 CTAs of 16 angles (4 slots per thread) or 8 (2 slots, the plan's choice for grids far
+    below one wave): each ray's samples are summed in the same row order either way, so the
+    projections are bit-identical, for the three-map and the single-map kernels, and match the
+    oracle."""
+    cfg = synth.CONFIGS[name] if name in synth.CONFIGS else _cases.cached_case(name).cfg
+    S = min(cfg.S, 2)
+    maps = synth.uniform((S, n_maps, cfg.N, cfg.N), 37)
+    outs, groups = [], []
+    for nsl in ("4", "2"):
+        monkeypatch.setenv("EI_K1_NSL", nsl)
+        plan = plan_for(ei, cfg, S)
+        sino = torch.zeros(S, n_maps, cfg.n_angles, cfg.n_det, device="cuda")
+        ei.ei_project(plan, dev(maps), n_maps, sino)
+        torch.cuda.synchronize()
+        info = ei.ei_plan_info(plan)
+        assert info["window_overflows"] == 0
+        groups.append(info["k1_groups"])
+        outs.append(sino.cpu().numpy())
+    assert groups[1] >= 2 * groups[0] - 2          # 8-angle groups (dominance runs split both)
+    assert np.array_equal(outs[0], outs[1])
+    ref = ora.project(maps[0, 0].astype(np.float64), cfg.angles, cfg.n_det, cfg.pixel, cfg.det_pitch)
+    assert rel_l2(outs[1][0, 0], ref) < 2e-5
+
+
 @pytest.mark.parametrize("mirror", ["1", "0"])
 def test_mirror_pairs_360(ei, mirror, monkeypatch):
     """360-degree scans: (theta, theta + pi) sample the same lines with the detector mirrored (R6),

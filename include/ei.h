@@ -156,9 +156,10 @@ int ei_cost_grad_hs(const ei_plan *plan, const float *h, float gamma, const floa
  * with cudaPointerGetAttributes on each call; one launch instead of ~20 API calls; env
  * EI_HOST_GRAPH=0 disables; pageable memory, or arguments whose capture failed, take direct
  * calls).  Stacks (>= 8 slices)
- * run in chunks of slices (up to 8; env EI_HOST_CHUNKS=K, 1 disables), each evaluated by an
- * internal sub-plan of the same geometry, so chunk c's upload, chunk c-1's evaluation and the
- * downloads of earlier chunks overlap (C4: 34.5 -> 25.7 ms per call); chunking is used only when
+ * run in chunks of slices (4 / 8 / 16 chunks from 8 / 16 / 32 slices; env EI_HOST_CHUNKS=K, up to
+ * 32, 1 disables), each evaluated by an internal sub-plan of the same geometry, so chunk c's
+ * upload, chunk c-1's evaluation and the downloads of earlier chunks overlap (C4: 34.5 ms in one
+ * piece, 25.1 ms in 8 chunks, 23.7 ms in 16); chunking is used only when
  * the sub-plans compute bit-identical results (no K3 angle split, same K1 row split).  Device
  * staging buffers, sub-plans, streams, events and the graph belong to the plan (created by the
  * first call, kept until ei_plan_destroy; EI_ERR_RESOURCE if that fails). */

@@ -137,7 +137,8 @@ struct ei_plan {
   int h_nchunk = 0, h_Sc = 0;               // 0: not decided yet, 1: one piece
   ei_plan *h_sub[2] = {nullptr, nullptr};
   cudaStream_t h_down = nullptr;            // download stream (chunked host path)
-  cudaEvent_t h_cev[17] = {};               // per chunk: uploaded, evaluated; + downloads done
+  static constexpr int HCHUNK_MAX = 32;
+  cudaEvent_t h_cev[2 * HCHUNK_MAX + 1] = {};   // per chunk: uploaded, evaluated; + downloads done
   // launch accounting
   mutable int64_t stats[6] = {0, 0, 0, 0, 0, 0};
   // optional per-kernel timing of ei_cost_grad: 7 events per recorded evaluation

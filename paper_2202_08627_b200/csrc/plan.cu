@@ -603,12 +603,13 @@ namespace {
 // evaluation (st) and chunk c-2's download (h_down) overlap.  Only when the sub-plans compute
 // exactly what the whole plan computes: no K3 angle split and the same K1 row split (every other
 // planning choice leaves each slice's arithmetic unchanged), so the results are bit-identical.
-// Env EI_HOST_CHUNKS=K sets the count (1 disables; default 8 for >= 16 slices, 4 for >= 8).
+// Env EI_HOST_CHUNKS=K sets the count (1 disables; default 16 for >= 32 slices, 8 for >= 16, 4 for
+// >= 8; C4 e2e per call 8 / 16 / 32 chunks: 25.1 / 23.7 / 24.1 ms, tools/dbg/sweep_chunks.sh).
 void setup_chunks(ei_plan *p) {
   p->h_nchunk = 1;
   const char *env = getenv("EI_HOST_CHUNKS");
-  int want = env ? atoi(env) : (p->S >= 16 ? 8 : (p->S >= 8 ? 4 : 1));
-  want = std::min(std::min(want, p->S), 8);
+  int want = env ? atoi(env) : (p->S >= 32 ? 16 : (p->S >= 16 ? 8 : (p->S >= 8 ? 4 : 1)));
+  want = std::min(std::min(want, p->S), ei_plan::HCHUNK_MAX);
   if (want <= 1 || p->KS != 1) return;
   const int Sc = (p->S + want - 1) / want, n = (p->S + Sc - 1) / Sc, Sl = p->S - (n - 1) * Sc;
   if (n <= 1) return;

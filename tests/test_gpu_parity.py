@@ -592,3 +592,37 @@ def test_host_path_chunked_stack(ei, chunks, n_pieces, span, monkeypatch):
         assert np.isnan(cost[9]) and np.all(np.isfinite(np.delete(cost, 9)))
         assert all(np.array_equal(a, b, equal_nan=True) for a, b in zip(gh, g_d))
         assert np.array_equal(st, st_d) and st[0] == 1
+
+
+def test_host_path_many_chunks(ei, monkeypatch):
+    """More than 8 chunks (the C4 default is 16): 72 slices of C2's geometry in 9 chunks of 8,
+    bit-identical to the device entry point, one K1 launch per chunk, on the first call and on
+    the graph replay."""
+    monkeypatch.setenv("EI_HOST_CHUNKS", "9")
+    cfg = synth.with_slices(synth.CONFIGS["C2"], 72)
+    S, N = cfg.S, cfg.N
+    rng = np.random.default_rng(8)
+    maps = [(0.05 * rng.random((S, N, N))).astype(np.float32) for _ in range(3)]
+    flat = np.ascontiguousarray(np.broadcast_to(synth.draw_slice(cfg, 0)[0].flat, (S, 3, cfg.n_det))).astype(np.float32)
+    mask = cfg.mask.astype(np.float32)
+    s_exp = (rng.random((S, cfg.n_angles, cfg.M, cfg.n_det)) * 2e4).astype(np.float32)
+    plan = plan_for(ei, cfg)
+    ws = ei.Workspace(plan)
+    cost_d, g_d, _ = ei.cost_grad(plan, [dev(m) for m in maps], dev(flat), dev(mask), None, dev(s_exp), 1e-2, ws)
+    torch.cuda.synchronize()
+    cost_d, g_d = cost_d.cpu().numpy(), [g.cpu().numpy() for g in g_d]
+
+    def pinned(a):
+        return torch.from_numpy(np.ascontiguousarray(a)).pin_memory().numpy()
+
+    h_in = [pinned(m) for m in maps] + [pinned(flat), pinned(mask), None, pinned(s_exp)]
+    for rep in range(2):
+        cost = pinned(np.zeros(S))
+        gh = [pinned(np.zeros((S, N, N), np.float32)) for _ in range(3)]
+        st = pinned(np.zeros(4, np.int32))
+        s0 = ei.ei_plan_stats(plan)
+        ei.ei_cost_grad_host(plan, *h_in[:7], 1e-2, cost, *gh, st)
+        s1 = ei.ei_plan_stats(plan)
+        assert s1[0] - s0[0] == 9, (s0, s1)
+        assert np.array_equal(cost, cost_d)
+        assert all(np.array_equal(a, b) for a, b in zip(gh, g_d))

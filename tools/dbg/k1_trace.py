@@ -75,4 +75,10 @@ order = np.argsort(-dur)[:12]
 print("slowest CTAs (block tile grp rs sm start dur rows):")
 for i in order:
     print("  %5d %3d %3d %2d %4d %7.2f %7.2f %4d" % (i, tile[i], grp[i], rs[i], sm[i], st[i], dur[i], rows[i]))
+# completion time of each angle group (all its units, every tile and row split): when a
+# dataflow successor (K2 rows, K3 angle chunks) could start on that group's angles
+gend = np.array([en[grp == g].max() for g in range(ngr)])
+print("group completion (us): min %.2f  p25 %.2f  median %.2f  p75 %.2f  max %.2f" %
+      tuple(np.percentile(gend, q) for q in (0, 25, 50, 75, 100)))
+print("  sorted:", " ".join("%.1f" % v for v in np.sort(gend)))
 np.save("gpurun_out/k1_trace_%s.npy" % name, tr)

@@ -50,6 +50,14 @@ def load_traffic(cfg_name, kernel):
         return None, None
 
 
+def load_traffic_field(cfg_name, kernel, field):
+    try:
+        e = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))[cfg_name]
+        return e["kernels"][kernel].get(field)
+    except Exception:
+        return None
+
+
 def load_peaks():
     try:
         return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -141,6 +149,18 @@ def kernel_table(kb, kern_ms, n_rec, ms_step, sm_mhz, hbm_peak, cfg_name=None):
             dgbs = dram / (per_kernel_ms[k] * 1e-3) / 1e9
             kernels[k].update({"dram_bytes_per_launch": dram, "dram_gbs": round(dgbs, 1),
                                "dram_frac": round(dgbs / hbm_peak, 4)})
+        lts = load_traffic_field(cfg_name, k, "lts_bytes_per_launch") if cfg_name else None
+        if bound == "l1" and lts and per_kernel_ms[k] > 0:
+            # the shared-memory data path also absorbs the TMA fills of the staging ring: their
+            # bytes arrive through L2 (lts__t_bytes of the committed capture, which also counts
+            # the kernel's output writes, ~1-2 %), so (gathers + fills) / time is the data path's
+            # use.  K1 only: it executes its algorithmic 24 B per sample, while K3's pixel pairs
+            # share entries between lanes, so bytes do not count its wavefronts (the ncu
+            # summaries derive wavefronts per SM-cycle for both)
+            kernels[k]["l2_bytes_per_launch"] = lts
+            if k == "K1_project":
+                kernels[k]["smem_frac_incl_fills"] = round(
+                    (kb[k] + lts) / (per_kernel_ms[k] * 1e-3) / 1e9 / peak, 4)
     kernels["K0_pack"] = {"ms": round(per_kernel_ms["K0_pack"], 5),
                           "share": round(per_kernel_ms["K0_pack"] / ms_step, 4)}
     dom = max(("K1_project", "K2_curve", "K3_backproject"), key=lambda k: per_kernel_ms[k])

@@ -35,6 +35,15 @@ def main(path):
                     continue
                 if v > 0.05:
                     st.append((v, k[len("smsp__average_warps_issue_stalled_"):-len("_per_issue_active.ratio")]))
+        try:   # the shared-memory data pipe moves one 128-B wavefront per SM-cycle
+            g = lambda k: float(r[h.index(k)].replace(",", ""))
+            sm_cyc = g("sm__cycles_elapsed.avg") * 148   # B200: 148 SMs
+            wf = g("l1tex__data_pipe_lsu_wavefronts_mem_shared_op_ld.sum")
+            lts = g("lts__t_bytes.sum") * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[units[h.index("lts__t_bytes.sum")]]
+            print("   %-70s %.3f" % ("derived: shared-load wavefronts per SM-cycle", wf / sm_cyc))
+            print("   %-70s %.3f" % ("derived: + L2 bytes (TMA fills, outputs) / 128 B per SM-cycle", (wf + lts / 128) / sm_cyc))
+        except (ValueError, KeyError, ZeroDivisionError):
+            pass
         print("   stalls/issue:", ", ".join("%s %.2f" % (n, v) for v, n in sorted(st, reverse=True)[:8]))
 
 

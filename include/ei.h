@@ -39,11 +39,14 @@ enum {
     EI_OK = 0,
     EI_ERR_NULL = 1,      /* a required pointer is NULL                                   */
     EI_ERR_SHAPE = 2,     /* S<1, N<2, Nd<3, n_angles<1, M<1, n_maps not 1|3,
-                             Nd or n_angles > ~14000, M too large for K2's staging ring, a
-                             sampled flat IC with < 4 knots                                  */
+                             16 Nd + 4 M > 225280 (Nd <= 14079 for M <= 4), n_angles > 14080,
+                             M too large for K2's staging ring (one detector segment's 3 + M
+                             rows in 220 KB of shared memory), a sampled flat IC with < 4
+                             knots (tests/test_gpu_limits.py runs parity at these limits)   */
     EI_ERR_DOMAIN = 3,    /* pixel/det_pitch/z <= 0 or non-finite, det_pitch < pixel,
                              non-finite angle, lambda < 0 or non-finite                    */
-    EI_ERR_RESOURCE = 4,  /* device allocation failed / size overflow                      */
+    EI_ERR_RESOURCE = 4,  /* device allocation failed / size overflow (N^2 > 2^30 or
+                             n_angles Nd M > 2^30: 32-bit per-slice indices)                */
     EI_ERR_CUDA = 5       /* a CUDA call or kernel launch failed                           */
 };
 

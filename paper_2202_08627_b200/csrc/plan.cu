@@ -26,8 +26,8 @@ int check_geom(const ei_geometry *g) {
   // sizes must fit the 32-bit per-slice index arithmetic of the kernels
   if ((int64_t)g->n * g->n > (1LL << 30) || (int64_t)g->n_angles * g->n_det * g->n_mask > (1LL << 30))
     return EI_ERR_RESOURCE;
-  // size limits of this implementation (validated ranges): N_d <= 14080 and N_theta <= 14080
-  // (the largest tested configurations use 3072 and 1440); K2's staging ring bounds M separately
+  // size limits of this implementation: 16 N_d + 4 M <= 220 KB and N_theta <= 14080 (parity is
+  // tested at both limits, tests/test_gpu_limits.py; BASELINE's configurations use 3072 and 1440); K2's staging ring bounds M separately
   // (plan_curve: the projections + M measured rows of a segment must fit a CTA's shared memory)
   if (16LL * g->n_det + 4LL * g->n_mask > 220 * 1024 || 16LL * g->n_angles > 220 * 1024)
     return EI_ERR_SHAPE;

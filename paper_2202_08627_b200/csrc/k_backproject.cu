@@ -87,7 +87,7 @@ struct Smem3 {
   float4 b[NST3][CH3][WL3];   // (d[e-1], d[e], m[e+1], d[e+1])
   float c[NST3][CH3][WL3];    // s[e+1]
   float4 t1[NST3][CH3];       // c', s', 1/h, 1 - 1/h
-  float4 t2[NST3][CH3];       // (Nd-1)/2 + 1 - e0 + min(c', 0), |c'|, 1 - 2/h, 1 + 1/h
+  float4 t2[NST3][CH3];       // (Nd-1)/2 + 1 - e0 + min(c', 0), |c'| - 1, -, -
   int nb[NST3];              // first angle of the chunk with cos < 0 (CH if none)
   float tot[12][NT];        // per consumer thread: totals of finished angle classes (pair, L/R, map)
   uint64_t full[NST3], empty[NST3];
@@ -408,7 +408,7 @@ SPAN_START_bp();
         const int ws = (int)floorf(fminf(fminf(k00, k01), fminf(k10, k11))) - 1;
         e0 = min(max((ws + 1) & ~3, -PADG + 4), (RpG - PADG - WL3 - 4) & ~3);
         sm.t1[st][lane] = make_float4(g.x, g.y, g.z, 1.f - g.z);
-        sm.t2[st][lane] = make_float4(dctr + 1.f - (float)e0 + fminf(g.x, 0.f), fabsf(g.x), 1.f - 2.f * g.z, 1.f + g.z);
+        sm.t2[st][lane] = make_float4(dctr + 1.f - (float)e0 + fminf(g.x, 0.f), fabsf(g.x) - 1.f, 0.f, 0.f);
       }
       {   // first angle of the chunk with cos < 0 (the list has cos >= 0 first), na if none
         const unsigned neg = __ballot_sync(0xffffffffu, lane < na && sm.t1[st][lane].x < 0.f);
@@ -443,7 +443,8 @@ SPAN_START_bp();
   // float2 + float per map); totals of finished classes per (pair, left/right, map)
   float2 lm0 = make_float2(0.f, 0.f), ld0 = lm0, ls0 = lm0, hm0 = lm0, hd0 = lm0, hs0 = lm0;
   float2 lm1 = lm0, ld1 = lm0, ls1 = lm0, hm1 = lm0, hd1 = lm0, hs1 = lm0;
-  float hm30 = 0.f, hd30 = 0.f, hs30 = 0.f, hm31 = 0.f, hd31 = 0.f, hs31 = 0.f;
+  float2 hmd30 = lm0, hmd31 = lm0;   // upper pixel's third tap of mu and delta: one FFMA2 (u2 broadcast)
+  float hs30 = 0.f, hs31 = 0.f;
   // totals of finished classes in shared memory (this thread's column; touched once per class):
   // tot[(2 p + side) 3 + map][tid], side 0 = left pixel
 #pragma unroll
@@ -452,8 +453,8 @@ SPAN_START_bp();
   auto flush = [&]() {   // fold the class's partial sums into the per-pixel totals, restart
     const float L[2][3] = {{lm0.x + lm0.y, ld0.x + ld0.y, ls0.x + ls0.y},
                            {lm1.x + lm1.y, ld1.x + ld1.y, ls1.x + ls1.y}};
-    const float H[2][3] = {{hm0.x + hm0.y + hm30, hd0.x + hd0.y + hd30, hs0.x + hs0.y + hs30},
-                           {hm1.x + hm1.y + hm31, hd1.x + hd1.y + hd31, hs1.x + hs1.y + hs31}};
+    const float H[2][3] = {{hm0.x + hm0.y + hmd30.x, hd0.x + hd0.y + hmd30.y, hs0.x + hs0.y + hs30},
+                           {hm1.x + hm1.y + hmd31.x, hd1.x + hd1.y + hmd31.y, hs1.x + hs1.y + hs31}};
 #pragma unroll
     for (int p = 0; p < 2; ++p)
 #pragma unroll
@@ -462,7 +463,8 @@ SPAN_START_bp();
         sm.tot[(2 * p + 1) * 3 + m][tid] += cls ? L[p][m] : H[p][m];
       }
     lm0 = ld0 = ls0 = hm0 = hd0 = hs0 = lm1 = ld1 = ls1 = hm1 = hd1 = hs1 = make_float2(0.f, 0.f);
-    hm30 = hd30 = hs30 = hm31 = hd31 = hs31 = 0.f;
+    hmd30 = hmd31 = make_float2(0.f, 0.f);
+    hs30 = hs31 = 0.f;
   };
 
   pdl_wait();   // sleep while K2 runs (this CTA may have launched early)
@@ -480,17 +482,17 @@ SPAN_START_bp();
       const float *cr = &sm.c[st][al][0];
       const float base = fmaf(yi, t1.y, t2.x);   // staged index of the lower pixel's entry, - x term
       auto pair = [&](float xl, float2 &lm, float2 &ld, float2 &ls, float2 &hm, float2 &hd, float2 &hs,
-                      float &hm3, float &hd3, float &hs3) {
+                      float2 &hmd3, float &hs3) {
         const float kst = fmaf(xl, t1.x, base);   // lower pixel's k* + 1 - e0 (> 0)
         const int k0 = __float2int_rd(kst);
         const float fr = kst - (float)k0;
         // lower pixel: taps k0, k0+1; upper pixel (k* + |c'|, |c'| <= 1): taps k0, k0+1, k0+2 with
-        // the tent max(0, 1 - |k - k*|/h) at distances f1, |f1 - 1|, 2 - f1
+        // the tent max(0, 1 - |k - k*|/h) at distances f1, |f1 - 1|, 2 - f1, written with
+        // x = f1 - 1 in [-1, 1): 1 - (1 + x)/h, 1 - |x|/h, 1 - (1 - x)/h (one FFMA.SAT each)
         const float2 wl = make_float2(__saturatef(fmaf(-fr, t1.z, 1.f)), __saturatef(fmaf(fr, t1.z, t1.w)));
-        const float f1 = fr + t2.y;
-        const float2 u01 = make_float2(__saturatef(fmaf(-f1, t1.z, 1.f)),
-                                       fminf(__saturatef(fmaf(f1, t1.z, t1.w)), __saturatef(fmaf(-f1, t1.z, t2.w))));
-        const float u2 = __saturatef(fmaf(f1, t1.z, t2.z));
+        const float x1 = fr + t2.y;
+        const float2 u01 = make_float2(__saturatef(fmaf(-x1, t1.z, t1.w)), __saturatef(fmaf(-fabsf(x1), t1.z, 1.f)));
+        const float u2 = __saturatef(fmaf(x1, t1.z, t1.w));
 #ifdef EI_CHECK
         if (k0 < 0 || k0 >= WL3) atomicAdd(fin.diag, 1);   // debug build: inside the staged window
 #endif
@@ -502,12 +504,11 @@ SPAN_START_bp();
         hm = __ffma2_rn(u01, make_float2(A.x, A.y), hm);
         hs = __ffma2_rn(u01, make_float2(A.z, A.w), hs);
         hd = __ffma2_rn(u01, make_float2(B.x, B.y), hd);
-        hm3 = fmaf(u2, B.z, hm3);
-        hd3 = fmaf(u2, B.w, hd3);
+        hmd3 = __ffma2_rn(make_float2(u2, u2), make_float2(B.z, B.w), hmd3);   // FFMA2, scalar operand
         hs3 = fmaf(u2, C, hs3);
       };
-      pair(xl0, lm0, ld0, ls0, hm0, hd0, hs0, hm30, hd30, hs30);
-      pair(xl1, lm1, ld1, ls1, hm1, hd1, hs1, hm31, hd31, hs31);
+      pair(xl0, lm0, ld0, ls0, hm0, hd0, hs0, hmd30, hs30);
+      pair(xl1, lm1, ld1, ls1, hm1, hd1, hs1, hmd31, hs31);
     };
 #pragma unroll 1
     for (int al = 0; al < nb; ++al) angle(al);

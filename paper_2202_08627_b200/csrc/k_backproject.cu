@@ -444,7 +444,7 @@ SPAN_START_bp();
   float2 lm0 = make_float2(0.f, 0.f), ld0 = lm0, ls0 = lm0, hm0 = lm0, hd0 = lm0, hs0 = lm0;
   float2 lm1 = lm0, ld1 = lm0, ls1 = lm0, hm1 = lm0, hd1 = lm0, hs1 = lm0;
   float2 hmd30 = lm0, hmd31 = lm0;   // upper pixel's third tap of mu and delta: one FFMA2 (u2 broadcast)
-  float hs30 = 0.f, hs31 = 0.f;
+  float2 hs3p = lm0;                 // and of sigma, pair 0 in .x, pair 1 in .y (one FFMA2 per angle)
   // totals of finished classes in shared memory (this thread's column; touched once per class):
   // tot[(2 p + side) 3 + map][tid], side 0 = left pixel
 #pragma unroll
@@ -453,8 +453,8 @@ SPAN_START_bp();
   auto flush = [&]() {   // fold the class's partial sums into the per-pixel totals, restart
     const float L[2][3] = {{lm0.x + lm0.y, ld0.x + ld0.y, ls0.x + ls0.y},
                            {lm1.x + lm1.y, ld1.x + ld1.y, ls1.x + ls1.y}};
-    const float H[2][3] = {{hm0.x + hm0.y + hmd30.x, hd0.x + hd0.y + hmd30.y, hs0.x + hs0.y + hs30},
-                           {hm1.x + hm1.y + hmd31.x, hd1.x + hd1.y + hmd31.y, hs1.x + hs1.y + hs31}};
+    const float H[2][3] = {{hm0.x + hm0.y + hmd30.x, hd0.x + hd0.y + hmd30.y, hs0.x + hs0.y + hs3p.x},
+                           {hm1.x + hm1.y + hmd31.x, hd1.x + hd1.y + hmd31.y, hs1.x + hs1.y + hs3p.y}};
 #pragma unroll
     for (int p = 0; p < 2; ++p)
 #pragma unroll
@@ -463,8 +463,7 @@ SPAN_START_bp();
         sm.tot[(2 * p + 1) * 3 + m][tid] += cls ? L[p][m] : H[p][m];
       }
     lm0 = ld0 = ls0 = hm0 = hd0 = hs0 = lm1 = ld1 = ls1 = hm1 = hd1 = hs1 = make_float2(0.f, 0.f);
-    hmd30 = hmd31 = make_float2(0.f, 0.f);
-    hs30 = hs31 = 0.f;
+    hmd30 = hmd31 = hs3p = make_float2(0.f, 0.f);
   };
 
   pdl_wait();   // sleep while K2 runs (this CTA may have launched early)
@@ -476,13 +475,14 @@ SPAN_START_bp();
     // the chunk's angles of the current class, then (at most once per CTA) the class change
     // and the rest: the plan lists cos >= 0 first, so the change is one index per chunk
     const int nb = cls ? na : min(na, sm.nb[st]);
-    auto angle = [&](int al) {
-      const float4 t1 = sm.t1[st][al], t2 = sm.t2[st][al];
+    auto angle = [&](const float4 *tp) {   // tp = &sm.t1[st][al]: the loop runs on this pointer
+      const int al = (int)(tp - &sm.t1[st][0]);
+      const float4 t1 = *tp, t2 = sm.t2[st][al];
       const float4 *ar = &sm.a[st][al][0], *br = &sm.b[st][al][0];
       const float *cr = &sm.c[st][al][0];
       const float base = fmaf(yi, t1.y, t2.x);   // staged index of the lower pixel's entry, - x term
       auto pair = [&](float xl, float2 &lm, float2 &ld, float2 &ls, float2 &hm, float2 &hd, float2 &hs,
-                      float2 &hmd3, float &hs3) {
+                      float2 &hmd3, float &u2o, float &Co) {
         const float kst = fmaf(xl, t1.x, base);   // lower pixel's k* + 1 - e0 (> 0)
         const int k0 = __float2int_rd(kst);
         const float fr = kst - (float)k0;
@@ -505,18 +505,22 @@ SPAN_START_bp();
         hs = __ffma2_rn(u01, make_float2(A.z, A.w), hs);
         hd = __ffma2_rn(u01, make_float2(B.x, B.y), hd);
         hmd3 = __ffma2_rn(make_float2(u2, u2), make_float2(B.z, B.w), hmd3);   // FFMA2, scalar operand
-        hs3 = fmaf(u2, C, hs3);
+        u2o = u2;
+        Co = C;
       };
-      pair(xl0, lm0, ld0, ls0, hm0, hd0, hs0, hmd30, hs30);
-      pair(xl1, lm1, ld1, ls1, hm1, hd1, hs1, hmd31, hs31);
+      float u20, u21, C0, C1;
+      pair(xl0, lm0, ld0, ls0, hm0, hd0, hs0, hmd30, u20, C0);
+      pair(xl1, lm1, ld1, ls1, hm1, hd1, hs1, hmd31, u21, C1);
+      hs3p = __ffma2_rn(make_float2(u20, u21), make_float2(C0, C1), hs3p);   // both pairs' sigma third taps
     };
+    const float4 *t0 = &sm.t1[st][0];
 #pragma unroll 1
-    for (int al = 0; al < nb; ++al) angle(al);
+    for (const float4 *tp = t0; tp != t0 + nb; ++tp) angle(tp);
     if (nb < na) {   // the class changes inside this chunk (warp-uniform)
       flush();
       cls = 1;
 #pragma unroll 1
-      for (int al = nb; al < na; ++al) angle(al);
+      for (const float4 *tp = t0 + nb; tp != t0 + na; ++tp) angle(tp);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&sm.empty[st]);

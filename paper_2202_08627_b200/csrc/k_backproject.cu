@@ -82,12 +82,17 @@ struct Smem1 {
 constexpr int NST3 = EI_K3_NST3;   // ring stages (compile-time switches for A/B runs)
 constexpr int CH3 = EI_K3_CH3;     // angles per staged chunk
 constexpr int WL3 = 52;
+// one staged angle: its three planes and its table in one record, so a single pointer (stepped
+// once per angle) addresses everything the consumers read for it (immediate offsets)
+struct Ang3 {
+  float4 a[WL3];   // (m[e-1], m[e], s[e-1], s[e])
+  float4 b[WL3];   // (d[e-1], d[e], m[e+1], d[e+1])
+  float c[WL3];    // s[e+1]
+  float4 t1;       // c', s', 1/h, 1 - 1/h
+  float4 t2;       // (Nd-1)/2 + 1 - e0 + min(c', 0), |c'| - 1, -, -
+};
 struct Smem3 {
-  float4 a[NST3][CH3][WL3];   // (m[e-1], m[e], s[e-1], s[e])
-  float4 b[NST3][CH3][WL3];   // (d[e-1], d[e], m[e+1], d[e+1])
-  float c[NST3][CH3][WL3];    // s[e+1]
-  float4 t1[NST3][CH3];       // c', s', 1/h, 1 - 1/h
-  float4 t2[NST3][CH3];       // (Nd-1)/2 + 1 - e0 + min(c', 0), |c'| - 1, -, -
+  Ang3 ang[NST3][CH3];
   int nb[NST3];              // first angle of the chunk with cos < 0 (CH if none)
   float tot[12][NT];        // per consumer thread: totals of finished angle classes (pair, L/R, map)
   uint64_t full[NST3], empty[NST3];
@@ -407,11 +412,11 @@ SPAN_START_bp();
         // into the zero pad (a window overlapping [-1, ND] is never clamped: PADG >= WL3 + 8)
         const int ws = (int)floorf(fminf(fminf(k00, k01), fminf(k10, k11))) - 1;
         e0 = min(max((ws + 1) & ~3, -PADG + 4), (RpG - PADG - WL3 - 4) & ~3);
-        sm.t1[st][lane] = make_float4(g.x, g.y, g.z, 1.f - g.z);
-        sm.t2[st][lane] = make_float4(dctr + 1.f - (float)e0 + fminf(g.x, 0.f), fabsf(g.x) - 1.f, 0.f, 0.f);
+        sm.ang[st][lane].t1 = make_float4(g.x, g.y, g.z, 1.f - g.z);
+        sm.ang[st][lane].t2 = make_float4(dctr + 1.f - (float)e0 + fminf(g.x, 0.f), fabsf(g.x) - 1.f, 0.f, 0.f);
       }
       {   // first angle of the chunk with cos < 0 (the list has cos >= 0 first), na if none
-        const unsigned neg = __ballot_sync(0xffffffffu, lane < na && sm.t1[st][lane].x < 0.f);
+        const unsigned neg = __ballot_sync(0xffffffffu, lane < na && sm.ang[st][lane].t1.x < 0.f);
         if (lane == 0) sm.nb[st] = neg ? __ffs(neg) - 1 : na;
       }
       __syncwarp();
@@ -419,9 +424,9 @@ SPAN_START_bp();
       __syncwarp();
       if (lane < na) {
         const size_t row = soff + (size_t)__ldg(alist_k + c0(c) + lane) * rowlen + e0;
-        bulk_g2s(&sm.a[st][lane][0], GA + row, bytesAB, &sm.full[st]);
-        bulk_g2s(&sm.b[st][lane][0], GB + row, bytesAB, &sm.full[st]);
-        bulk_g2s(&sm.c[st][lane][0], GC + row, bytesC, &sm.full[st]);
+        bulk_g2s(&sm.ang[st][lane].a[0], GA + row, bytesAB, &sm.full[st]);
+        bulk_g2s(&sm.ang[st][lane].b[0], GB + row, bytesAB, &sm.full[st]);
+        bulk_g2s(&sm.ang[st][lane].c[0], GC + row, bytesC, &sm.full[st]);
       }
       if (++st == NST3) { st = 0; ph ^= 1; }
     }
@@ -475,11 +480,10 @@ SPAN_START_bp();
     // the chunk's angles of the current class, then (at most once per CTA) the class change
     // and the rest: the plan lists cos >= 0 first, so the change is one index per chunk
     const int nb = cls ? na : min(na, sm.nb[st]);
-    auto angle = [&](const float4 *tp) {   // tp = &sm.t1[st][al]: the loop runs on this pointer
-      const int al = (int)(tp - &sm.t1[st][0]);
-      const float4 t1 = *tp, t2 = sm.t2[st][al];
-      const float4 *ar = &sm.a[st][al][0], *br = &sm.b[st][al][0];
-      const float *cr = &sm.c[st][al][0];
+    auto angle = [&](const Ang3 *ap) {   // the loop runs on this pointer
+      const float4 t1 = ap->t1, t2 = ap->t2;
+      const float4 *ar = ap->a, *br = ap->b;
+      const float *cr = ap->c;
       const float base = fmaf(yi, t1.y, t2.x);   // staged index of the lower pixel's entry, - x term
       auto pair = [&](float xl, float2 &lm, float2 &ld, float2 &ls, float2 &hm, float2 &hd, float2 &hs,
                       float2 &hmd3, float &u2o, float &Co) {
@@ -513,14 +517,14 @@ SPAN_START_bp();
       pair(xl1, lm1, ld1, ls1, hm1, hd1, hs1, hmd31, u21, C1);
       hs3p = __ffma2_rn(make_float2(u20, u21), make_float2(C0, C1), hs3p);   // both pairs' sigma third taps
     };
-    const float4 *t0 = &sm.t1[st][0];
+    const Ang3 *a0 = &sm.ang[st][0];
 #pragma unroll 1
-    for (const float4 *tp = t0; tp != t0 + nb; ++tp) angle(tp);
+    for (const Ang3 *ap = a0; ap != a0 + nb; ++ap) angle(ap);
     if (nb < na) {   // the class changes inside this chunk (warp-uniform)
       flush();
       cls = 1;
 #pragma unroll 1
-      for (const float4 *tp = t0 + nb; tp != t0 + na; ++tp) angle(tp);
+      for (const Ang3 *ap = a0 + nb; ap != a0 + na; ++ap) angle(ap);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&sm.empty[st]);

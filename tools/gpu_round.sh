@@ -1,7 +1,7 @@
 #!/bin/bash
 # One GPU-box pass: parity tests, smoke, bench lines for every config, ncu launch list of the
 # default bench command and one `--set full` capture of K1/K3/K2.  Usage (under gpurun):
-#   bash tools/gpu_round.sh TAG [what...]     what ⊂ {tests smoke bench ref ncu full peaks}
+#   bash tools/gpu_round.sh TAG [what...]     what ⊂ {tests smoke bench ref ncu full peaks eicheck}
 set -u
 TAG=${1:-run}; shift || true
 WHAT=${*:-tests smoke bench ncu full}
@@ -36,6 +36,14 @@ EOF
     ref)
       timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > $OUT/bench_ref.json 2> $OUT/bench_ref.err; echo "ref rc=$?" | tee -a $OUT/rc.txt
       tail -c 600 $OUT/bench_ref.json ;;
+    eicheck)
+      # the parity suite under a bounds-checking build (-DEI_CHECK: K3 checks every tap against its
+      # staged window, K1 every chunk's extreme taps; ei_plan_info out[4] must stay 0), then the
+      # normal build again
+      EI_NVCC_DEFS=-DEI_CHECK python -c "from paper_2202_08627_b200 import build; build.build()" > $OUT/build_check.log 2>&1
+      EI_NVCC_DEFS=-DEI_CHECK timeout 1500 python -m pytest tests/test_gpu_parity.py tests/test_gpu_fullsize.py tests/test_gpu_limits.py -m gpu -x -q > $OUT/pytest_gpu_eicheck.log 2>&1
+      echo "eicheck rc=$?" | tee -a $OUT/rc.txt; tail -2 $OUT/pytest_gpu_eicheck.log
+      python -c "from paper_2202_08627_b200 import build; build.build()" >> $OUT/build.log 2>&1 ;;
     peaks)
       timeout 600 python tools/measure_peaks.py $OUT/peaks.json > $OUT/peaks.log 2>&1; echo "peaks rc=$?" | tee -a $OUT/rc.txt
       tail -c 400 $OUT/peaks.json ;;

@@ -195,8 +195,10 @@ int ei_plan_read_timing(ei_plan *plan, double ms[6], int *n_evals);
  * out[5] = K1 dynamic shared memory per CTA (bytes), out[6] = K1 angle groups using the
  * ray-fastest lane mapping, out[7] = K3 angle split (most parts of one tile), out[8] = mirror angle pairs (theta,
  * theta + pi) of a 360-degree scan projected and back-projected once (env EI_MIRROR=0 at plan
- * creation disables), out[9] = K2 detector segments per row. */
-int ei_plan_info(const ei_plan *plan, int64_t out[10]);
+ * creation disables), out[9] = K2 detector segments per row, out[10] = K1B band mode: map rows
+ * per band of the cost / forward path (0: ray-tile units; then out[3] is the number of bands),
+ * out[11] = CTAs of the cost path's K1 grid.  The caller's array holds 12 entries. */
+int ei_plan_info(const ei_plan *plan, int64_t out[12]);
 
 /* Human-readable name of an EI_* code (static string). */
 const char *ei_error_string(int code);

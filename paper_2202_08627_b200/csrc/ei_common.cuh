@@ -47,6 +47,9 @@ struct ProjPlan {
   int *unitRS = nullptr;    // device: the same for the row-split cost path
   int PAD = 0;              // zero entries before/after every pair-layout map row
   int Rp = 0;               // padded row length (entries): N + 1 + 2 PAD, even
+  int band = 0;             // K1B band mode for the RS launches (small maps): RS = bands of BR rows
+  int BR = 0;               // map rows per band
+  int bstride = 0;          // staged row stride of a band (entries, even, >= N + 4)
 };
 
 // K2 launch plan (k_curve.cu: plan_curve)
@@ -171,6 +174,7 @@ int plan_projector(ei_plan &p, const double *angles, const std::vector<int> &pro
                    std::vector<int> &coff1, std::vector<int4> &chunksRS, std::vector<int> &coffRS,
                    std::vector<int> &unit1, std::vector<int> &unitRS);
 size_t k1_smem(int nst, int E, int nchmax, int nmap);   // K1 dynamic shared memory (bytes)
+size_t k1_band_smem(int BR, int stride, int nmap);      // K1B (band mode) dynamic shared memory
 // fold of mirror-pair gradient rows (k_pack.cu): G(primary) += mirror(G(mirror)), pair layout
 cudaError_t launch_fold(const ei_plan &p, int n_maps, cudaStream_t st);
 // K0 (k_pack.cu)

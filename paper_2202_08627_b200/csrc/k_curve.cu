@@ -286,7 +286,30 @@ __global__ void __launch_bounds__(K2_MAXT + 32, 2) curve_kernel(K2Args g) {
         const int plane = g.NA * ND;
         const float *Pb = g.P + (size_t)s * g.nmap * plane + a * ND + k0;
         const int pdo = Mode<MODE>::h ? 0 : plane;
-        for (int r = 1; r < g.RS; ++r) {
+        // K1B band mode gives RS ~ 10-30 partials: whole float4s where the 4 positions are in the
+        // row (k0 is a multiple of 4; rows 16-B aligned), unrolled so the L2 loads overlap; same
+        // fixed order r = 1, 2, ... as the scalar path
+        int r = 1;
+        if (g.vec && k0 >= 0 && k0 + J <= ND) {
+          const bool hl = k0 > 0, hr = k0 + J < ND;
+#pragma unroll 4
+          for (; r < g.RS; ++r) {
+            const float *b = Pb + r * g.rstride;
+            const float4 v0 = __ldg(reinterpret_cast<const float4 *>(b));
+            Pm.x += v0.x; Pm.y += v0.y; Pm.z += v0.z; Pm.w += v0.w;
+            if (Mode<MODE>::h) {
+              Pd = Pm;
+            } else {
+              const float4 v1 = __ldg(reinterpret_cast<const float4 *>(b + pdo));
+              const float4 v2 = __ldg(reinterpret_cast<const float4 *>(b + 2 * plane));
+              Pd.x += v1.x; Pd.y += v1.y; Pd.z += v1.z; Pd.w += v1.w;
+              Ps.x += v2.x; Ps.y += v2.y; Ps.z += v2.z; Ps.w += v2.w;
+            }
+            if (hl) nbl += __ldg(b + pdo - 1);
+            if (hr) nbr += __ldg(b + pdo + J);
+          }
+        }
+        for (; r < g.RS; ++r) {
           const float *b = Pb + r * g.rstride;
           float v[3][J];
 #pragma unroll

@@ -347,8 +347,191 @@ SPAN_START_proj();
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// Band mode (K1B, small maps: C1, C2, P1; DESIGN.md §5 K1B).  The per-tile units above differ in
+// work by up to 128 rows (detector-end tiles and near-axis angles miss much of the map), and on a
+// single-wave grid the step ends with its heaviest unit.  Here a unit is (angle group, band of BR
+// map rows, slice): the producer stages the band's FULL rows once (entries -2 .. N+1 of the pair
+// layout, one bulk copy per row and plane), and the consumer warps sweep ALL rays over it, 64 per
+// pass.  Every map row meets about the same number of rays ((N+1)|c_dom| per angle), so the units
+// carry nearly equal work, and one staged byte serves every ray of the group that crosses it.  The
+// band's sum is a partial projection P[band]; K2 adds the bands in fixed order (as for RS).  A tap
+// index outside the map is clamped onto the zero entries -1 / N+1, which contribute exactly 0.
+constexpr int NCWB = 8;   // consumer warps per band CTA (64 rays per pass)
+
+struct BandArgs {
+  const void *MA, *MAT;         // PL<NMAP>::A pairs, [S][N][Rp], entry e at e + PAD
+  const float2 *MB, *MBT;       // sigma pairs (NMAP = 3)
+  const float4 *k1;
+  const int2 *groups;
+  const int *order, *partner;
+  int N, NA, ND, S, BR, nbands, ngroups, PAD, Rp, stride, has_pairs;
+  float *P;                     // [nbands][S][NMAP][NA][ND]
+};
+
+size_t k1_band_smem(int BR, int stride, int nmap) {
+  return (size_t)BR * stride * (nmap == 3 ? 24 : 8);
+}
+
+template <int NMAP, int NSLB>
+__global__ void __launch_bounds__(NCWB * 32 + 32, 2) project_band_kernel(BandArgs args) {
+  constexpr int NT = NCWB * 32;
+  using TA = typename PL<NMAP>::A;
+  const int N = args.N, ND = args.ND, stride = args.stride;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  TA *sA = reinterpret_cast<TA *>(smem_raw);                            // [BR][stride]
+  float2 *sB = reinterpret_cast<float2 *>(sA + (size_t)args.BR * stride);  // [BR][stride] (NMAP 3)
+  __shared__ __align__(8) uint64_t full;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int grp = blockIdx.x % args.ngroups;
+  const int band = (blockIdx.x / args.ngroups) % args.nbands;
+  const int s = blockIdx.x / (args.ngroups * args.nbands);
+  const int i0 = band * args.BR, rc = min(args.BR, N - i0);
+  SPAN_START_proj();
+  const int2 gr = args.groups[grp];
+  const int2 gi = make_int2(gr.x, gr.y & 0xffff);
+  const bool ray_fast = (gr.y >> 16) != 0;
+  const float ctr = 0.5f * (float)(N - 1), dctr = 0.5f * (float)(ND - 1);
+  const bool rowdom = __ldg(args.k1 + args.order[gi.x]).w != 0.f;
+  const size_t Rp = (size_t)args.Rp;
+  if (tid == 0) {
+    mbar_init(&full, 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  if (w == NCWB) {   // ---------------- producer warp: the band's rows, entries -2 .. N+1 ----------------
+    pdl_wait();   // K0's packed maps
+    if (lane == 0) {
+      const TA *gA = reinterpret_cast<const TA *>(rowdom ? args.MA : args.MAT) + (size_t)s * N * Rp + args.PAD - 2;
+      const float2 *gB = NMAP == 3 ? (rowdom ? args.MB : args.MBT) + (size_t)s * N * Rp + args.PAD - 2 : nullptr;
+      const uint32_t bytesA = (uint32_t)(((size_t)(N + 4) * sizeof(TA) + 15) & ~(size_t)15);
+      const uint32_t bytesB = NMAP == 3 ? (uint32_t)(((N + 4) * 8 + 15) & ~15) : 0u;
+      mbar_arrive_expect_tx(&full, (uint32_t)rc * (bytesA + bytesB));
+      for (int r = 0; r < rc; ++r) {
+        const size_t row = (size_t)(i0 + r) * Rp;
+        bulk_g2s(sA + (size_t)r * stride, gA + row, bytesA, &full);
+        if (NMAP == 3) bulk_g2s(sB + (size_t)r * stride, gB + row, bytesB, &full);
+      }
+    }
+    return;
+  }
+
+  // ---------------- consumer warps ----------------
+  const int aq = ray_fast ? lane >> 3 : lane & 3, rq = ray_fast ? lane & 7 : lane >> 2;
+  float tn[NSLB];
+  int ang[NSLB];   // the slot's angle (clamped to the group's last for idle slots)
+  bool live[NSLB];
+#pragma unroll
+  for (int m = 0; m < NSLB; ++m) {
+    const int al = min(aq + 4 * m, gi.y - 1);
+    ang[m] = args.order[gi.x + al];
+    live[m] = aq + 4 * m < gi.y;
+    tn[m] = __ldg(args.k1 + ang[m]).y;
+  }
+  const float ya = (float)i0 - ctr, yb = ya + (float)(rc - 1);
+  const size_t plane = (size_t)args.NA * ND;
+  float *outb = args.P + ((size_t)band * args.S + s) * NMAP * plane;
+  const TA *arow0 = sA + 2;                 // entry 0 of row 0 (entry e at index e + 2)
+  const float2 *brow0 = sB + 2;
+  pdl_wait();   // sleep (not spin on the barrier) while K0 runs
+  mbar_wait_full(&full, 0);
+  for (int kt = 0; kt < ND; kt += NCWB * 8) {
+    const int k = kt + w * 8 + rq;
+    const float kc = (float)k - dctr;
+    float alpha[NSLB];
+    bool hit = false;
+#pragma unroll
+    for (int m = 0; m < NSLB; ++m) {
+      alpha[m] = fmaf(kc, __ldg(args.k1 + ang[m]).x, ctr);   // x* = alpha - tn * (i - ctr)
+      const float xa = fmaf(-tn[m], ya, alpha[m]), xb = fmaf(-tn[m], yb, alpha[m]);
+      hit |= live[m] && k < ND && fmaxf(xa, xb) > -1.f && fminf(xa, xb) < (float)N;
+    }
+    float2 am[NSLB], ad[NSLB], as[NSLB];
+#pragma unroll
+    for (int m = 0; m < NSLB; ++m) am[m] = ad[m] = as[m] = make_float2(0.f, 0.f);
+    if (__any_sync(0xffffffffu, hit)) {   // some ray of the warp crosses the band inside the map
+      const TA *arow = arow0;
+      const float2 *brow = brow0;
+      float yi = ya;
+      for (int r = 0; r < rc; ++r, yi += 1.f, arow += stride, brow += stride) {
+#pragma unroll
+        for (int m = 0; m < NSLB; ++m) {
+          const float xs = fmaf(-tn[m], yi, alpha[m]);
+          const int j0 = __float2int_rd(xs);
+          const float fr = xs - (float)j0;
+          const float2 wt = make_float2(1.f - fr, fr);
+          const int e = min(max(j0 + 1, -1), N + 1);   // tap pair (x[j0], x[j0+1]) = entry j0 + 1
+          const TA va = arow[e];
+          if constexpr (NMAP == 3) {
+            am[m] = __ffma2_rn(wt, make_float2(va.x, va.y), am[m]);
+            ad[m] = __ffma2_rn(wt, make_float2(va.z, va.w), ad[m]);
+            as[m] = __ffma2_rn(wt, brow[e], as[m]);
+          } else {
+            am[m] = __ffma2_rn(wt, va, am[m]);
+          }
+        }
+      }
+    }
+    if (k < ND) {
+      float *out = outb + k, *outm = outb + (ND - 1 - k);
+#pragma unroll
+      for (int m = 0; m < NSLB; ++m) {
+        if (!live[m]) continue;
+        const int a = ang[m];
+        const float scale = __ldg(args.k1 + a).z;
+        const int b = args.has_pairs ? __ldg(args.partner + a) : -1;
+        const float v0 = (am[m].x + am[m].y) * scale;
+        out[(size_t)a * ND] = v0;
+        if (b >= 0) outm[(size_t)b * ND] = v0;
+        if constexpr (NMAP == 3) {
+          const float v1 = (ad[m].x + ad[m].y) * scale, v2 = (as[m].x + as[m].y) * scale;
+          out[plane + (size_t)a * ND] = v1;
+          out[2 * plane + (size_t)a * ND] = v2;
+          if (b >= 0) {
+            outm[plane + (size_t)b * ND] = v1;
+            outm[2 * plane + (size_t)b * ND] = v2;
+          }
+        }
+      }
+    }
+  }
+  pdl_trigger();
+#ifdef EI_TRACE
+  asm volatile("bar.sync 1, %0;\n" ::"r"(NT) : "memory");   // consumers only
+  if (tid == 0) SPAN_END_proj(0);
+#endif
+}
+
+template <int NMAP>
+cudaError_t launch_band(const ei_plan &p, float *P, cudaStream_t st) {
+  BandArgs a;
+  if (NMAP == 3) {
+    a.MA = p.MA; a.MAT = p.MAT; a.MB = p.MB; a.MBT = p.MBT;
+  } else {
+    a.MA = p.M1; a.MAT = p.M1T; a.MB = nullptr; a.MBT = nullptr;
+  }
+  a.k1 = p.tab.k1;
+  a.groups = p.proj.groups;
+  a.order = p.proj.order;
+  a.partner = p.proj.partner;
+  a.has_pairs = p.npairs > 0 ? 1 : 0;
+  a.N = p.N; a.NA = p.NA; a.ND = p.ND; a.S = p.S;
+  a.BR = p.proj.BR; a.nbands = p.proj.RS; a.ngroups = p.proj.n_groups;
+  a.PAD = p.proj.PAD; a.Rp = p.proj.Rp; a.stride = p.proj.bstride;
+  a.P = P;
+  const size_t smem = k1_band_smem(a.BR, a.stride, NMAP);
+  auto kern = p.proj.nsl == 2 ? project_band_kernel<NMAP, 2> : project_band_kernel<NMAP, 4>;
+  cudaError_t e = cudaFuncSetAttribute((const void *)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  dim3 grid(p.proj.n_groups * p.proj.RS * p.S);
+  e = launch_pdl(kern, grid, dim3(NCWB * 32 + 32), smem, st, a);
+  if (e != cudaSuccess) return e;
+  return cudaGetLastError();
+}
+
 template <int NMAP>
 cudaError_t launch(const ei_plan &p, int RS, float *P, cudaStream_t st) {
+  if (p.proj.band && RS == p.proj.RS) return launch_band<NMAP>(p, P, st);
   ProjArgs a;
   if (NMAP == 3) {
     a.MA = p.MA; a.MAT = p.MAT; a.MB = p.MB; a.MBT = p.MBT;
@@ -690,7 +873,35 @@ int plan_projector(ei_plan &p, const double *angles, const std::vector<int> &pro
   if (const char *e = getenv("EI_K1_NST")) nst = std::max(2, std::min(NSTMAX, atoi(e)));   // knob
   const int E = stage_entries(nst);
   if (!build_chunks(p, angles, groups, order, 1, E, RCMAX, ch1)) return EI_ERR_SHAPE;
-  if (RS > 1) {
+  // K1B band mode for the cost / forward path of small maps: units (group, band of BR = 16 map
+  // rows, slice) of nearly equal work.  Measured (tools/dbg/sweep_band.sh, step time): a win only
+  // where the band grid is one wave of enough CTAs — P1 38.8 -> 37.0 us (196 units); C2's 384 units
+  // (1.3 waves) 68.2 -> 87 us, and at BR = 11 (576 units) 81 us with K2 summing 24 partials; C1's
+  // 48 units 26.7 -> 26.8-27.5 us.  So: BR = 16 rows fit the 104 KB budget and the band grid is
+  // between half a wave and one wave of 2 CTAs per SM (knobs EI_K1_BAND, EI_K1_BR)
+  p.proj.band = 0;
+  {
+    const int bstride = (N + 4 + 1) & ~1;
+    const int brmax = std::min(64, (int)((size_t)104 * 1024 / ((size_t)bstride * per_entry)));
+    const int br0 = 16;
+    const long long units16 = (long long)((N + br0 - 1) / br0) * (long long)groups.size() * p.S;
+    bool use = brmax >= br0 && units16 <= 2LL * sms && 2 * units16 >= sms;
+    int br = br0;
+    if (const char *e = getenv("EI_K1_BAND")) use = atoi(e) != 0 && brmax >= 4;
+    if (const char *e = getenv("EI_K1_BR")) br = atoi(e);
+    br = std::max(1, std::min(brmax, br));
+    const int nb = (N + br - 1) / br;
+    if (use && (size_t)nb * p.S * 3 * NA * ND * sizeof(float) <= ((size_t)256 << 20)) {
+      p.proj.band = 1;
+      p.proj.BR = br;
+      p.proj.bstride = bstride;
+      RS = nb;
+      p.proj.k0_early = (long long)nb * groups.size() * p.S <= sms ? 1 : 0;
+    }
+  }
+  if (p.proj.band) {
+    chRS = ch1;
+  } else if (RS > 1) {
     if (!build_chunks(p, angles, groups, order, RS, E, RCMAX, chRS)) return EI_ERR_SHAPE;
   } else {
     chRS = ch1;
@@ -701,6 +912,9 @@ int plan_projector(ei_plan &p, const double *angles, const std::vector<int> &pro
             "widest window %d\n", p.proj.RT, 4 * p.proj.nsl, RS, nst, E, ch1.c.size(), ch1.nchmax,
             ch1.c.empty() ? 0.0 : (double)[&] { long long r = 0; for (auto &q : ch1.c) r += q.w; return r; }() / ch1.c.size(),
             ch1.rcmax, ch1.wmax);
+  if (getenv("EI_PLAN_VERBOSE") && p.proj.band)
+    fprintf(stderr, "libei plan: K1B band mode: %d bands of %d rows x %zu groups x %d slices (stride %d)\n",
+            RS, p.proj.BR, groups.size(), p.S, p.proj.bstride);
   p.proj.E = E;
   p.proj.nst = nst;
   p.proj.n_groups = (int)groups.size();
@@ -715,10 +929,10 @@ int plan_projector(ei_plan &p, const double *angles, const std::vector<int> &pro
   p.proj.n_tiles = ntile;
   if ((long long)ntile * groups.size() * p.S * RS > 0x7fffffffLL) return EI_ERR_SHAPE;   // 1-D grid
   unit1 = order_units(ch1, 1, (int)groups.size(), ntile, p.S, cps);
-  unitRS = RS > 1 ? order_units(chRS, RS, (int)groups.size(), ntile, p.S, cps) : unit1;
+  unitRS = (RS > 1 && !p.proj.band) ? order_units(chRS, RS, (int)groups.size(), ntile, p.S, cps) : unit1;
   chunks1.swap(ch1.c);
   coff1.swap(ch1.off);
-  if (RS > 1) {
+  if (RS > 1 && !p.proj.band) {
     chunksRS.swap(chRS.c);
     coffRS.swap(chRS.off);
   } else {

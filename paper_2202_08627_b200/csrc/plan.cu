@@ -330,7 +330,7 @@ int ei_plan_stats(const ei_plan *p, int64_t out[6]) {
   return EI_OK;
 }
 
-int ei_plan_info(const ei_plan *p, int64_t out[10]) {
+int ei_plan_info(const ei_plan *p, int64_t out[12]) {
   if (!p || !out) return EI_ERR_NULL;
   int32_t d = 0;
   if (cudaMemcpy(&d, p->diag, sizeof(d), cudaMemcpyDeviceToHost) != cudaSuccess) return EI_ERR_CUDA;
@@ -344,6 +344,9 @@ int ei_plan_info(const ei_plan *p, int64_t out[10]) {
   out[7] = p->KS;
   out[8] = p->npairs;
   out[9] = p->k2.nseg;
+  out[10] = p->proj.band ? p->proj.BR : 0;
+  out[11] = p->proj.band ? (int64_t)p->proj.n_groups * p->proj.RS * p->S
+                         : (int64_t)p->proj.n_tiles * p->proj.n_groups * p->S * p->proj.RS;
   return EI_OK;
 }
 

@@ -130,10 +130,11 @@ def ei_plan_stats(plan: Plan):
 
 
 def ei_plan_info(plan: Plan) -> dict:
-    out = (ctypes.c_int64 * 10)()
+    out = (ctypes.c_int64 * 12)()
     _check(_lib.ei_plan_info(plan.handle, out), "ei_plan_info")
     keys = ("k1_groups", "k1_rows_per_chunk", "k1_window", "k1_row_split", "window_overflows",
-            "k1_smem_bytes", "k1_ray_fast", "k3_angle_split", "mirror_pairs", "k2_segments")
+            "k1_smem_bytes", "k1_ray_fast", "k3_angle_split", "mirror_pairs", "k2_segments",
+            "k1_band_rows", "k1_ctas")
     return dict(zip(keys, list(out)))
 
 

@@ -626,3 +626,53 @@ def test_host_path_many_chunks(ei, monkeypatch):
         assert s1[0] - s0[0] == 9, (s0, s1)
         assert np.array_equal(cost, cost_d)
         assert all(np.array_equal(a, b) for a, b in zip(gh, g_d))
+
+
+@pytest.mark.parametrize("name", ["C1", "C2", "R1", "R3"])
+def test_k1_band_mode_parity(ei, name, monkeypatch):
+    """K1B band mode (units = angle group x band of BR map rows x slice; all rays swept over the
+    band's fully staged rows; K2 sums the bands' partial projections in fixed order) against the
+    ray-tile units and the oracle: cost, s_mod and the three gradient maps within the gates for
+    band heights 5 / 16 / 1000 (ragged last band; one band = the whole map), the band and tile
+    paths within fp32 rounding of each other, and repeat calls bit-identical."""
+    case = _cases.cached_case(name)
+    cfg = case.cfg
+    maps = synth.perturbed(case.maps(), cfg.seed + 7)
+    rc, rgm, rgd, rgs, rst = _cases.oracle_cost_grad(case, maps, 1e-2)
+    rs, _ = ora.forward(cfg.angles, *maps, case.flat, case.mask, case.drift, dx=cfg.pixel,
+                        du=cfg.det_pitch, z=cfg.z)
+    runs = {}
+    for band, br in (("0", None), ("1", "5"), ("1", "16"), ("1", "1000")):
+        monkeypatch.setenv("EI_K1_BAND", band)
+        if br is None:
+            monkeypatch.delenv("EI_K1_BR", raising=False)
+        else:
+            monkeypatch.setenv("EI_K1_BR", br)
+        plan = plan_for(ei, cfg)
+        info = ei.ei_plan_info(plan)
+        if band == "1":
+            assert 0 < info["k1_band_rows"] <= int(br)
+            assert info["k1_row_split"] == -(-cfg.N // info["k1_band_rows"])
+        else:
+            assert info["k1_band_rows"] == 0
+        c, g, st = gpu_cost_grad(ei, plan, case, maps, 1e-2)
+        c2, g2, _ = gpu_cost_grad(ei, plan, case, maps, 1e-2)
+        assert np.array_equal(c, c2) and all(np.array_equal(a, b) for a, b in zip(g, g2))
+        smod = torch.zeros(cfg.S, cfg.n_angles, cfg.M, cfg.n_det, device="cuda")
+        drift = None if case.drift is None else dev(case.drift)
+        ei.ei_forward(plan, *[dev(m) for m in maps], dev(case.flat), dev(case.mask), drift, smod)
+        torch.cuda.synchronize()
+        smod = smod.cpu().numpy()
+        for s in range(cfg.S):
+            assert abs(c[s] - rc[s]) / abs(rc[s]) <= 1e-4, (band, br, s, c[s], rc[s])
+            for q, ref in enumerate((rgm, rgd, rgs)):
+                assert rel_l2(g[q][s], ref[s]) <= 1e-3, (band, br, s, q, rel_l2(g[q][s], ref[s]))
+        assert rel_l2(smod, rs) <= 1e-3, (band, br, rel_l2(smod, rs))
+        assert list(st[:3]) == list(rst)
+        runs[(band, br)] = (c, g, smod)
+    c0, g0, s0 = runs[("0", None)]
+    for key, (c, g, smod) in runs.items():
+        assert np.allclose(c, c0, rtol=1e-6, atol=0), key
+        for q in range(3):
+            assert rel_l2(g[q], g0[q]) <= 1e-4, (key, q, rel_l2(g[q], g0[q]))
+        assert rel_l2(smod, s0) <= 1e-5, (key, rel_l2(smod, s0))

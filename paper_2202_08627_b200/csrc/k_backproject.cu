@@ -215,7 +215,7 @@ SPAN_START_bp();
   // PDL: the producer (TMA of K2's gradient rows) and the finalize CTAs (K2's partials) wait for
   // K2; the other consumers only read what the producer staged
   if (w == NT / 32) {   // ---------------- producer warp ----------------
-    pdl_wait();   // K2's gradient sinograms
+    // the first chunk's tables (plan data) are prepared before the PDL wait, see backproject3
     // tile corners (full 32x32 tile, even past the map edge, so every lane indexes the window)
     const float xa = (float)j0 - ctr, xb = xa + (float)(TILE - 1);
     const float ya = (float)i0 - ctr, yb = ya + (float)(TILE - 1);
@@ -225,9 +225,9 @@ SPAN_START_bp();
     for (int c = c_lo; c < c_hi; ++c) {
       if (c - c_lo >= NST) mbar_wait(&sm.empty[st], ph ^ 1);
       const int na = min(CH, a_hi - a_lo - c * CH);
-      int ws = 0;
+      int ws = 0, a = 0;
       if (lane < na) {   // per-angle table + window start (first tap entry - 1)
-        const int a = __ldg(alist_k + c * CH + lane);
+        a = __ldg(alist_k + c * CH + lane);
         const float4 g = __ldg(k3 + a);   // cdu, sdu, inv_h, scale
         const float k00 = fmaf(xa, g.x, fmaf(ya, g.y, dctr)), k01 = fmaf(xb, g.x, fmaf(ya, g.y, dctr));
         const float k10 = fmaf(xa, g.x, fmaf(yb, g.y, dctr)), k11 = fmaf(xb, g.x, fmaf(yb, g.y, dctr));
@@ -238,8 +238,9 @@ SPAN_START_bp();
       __syncwarp();
       if (lane == 0) mbar_arrive_expect_tx(&sm.full[st], (uint32_t)na * bytesA);
       __syncwarp();
+      if (c == c_lo) pdl_wait();   // K2's gradient sinograms
       if (lane < na) {
-        const size_t row = (size_t)__ldg(alist_k + c * CH + lane) * rowlen;
+        const size_t row = (size_t)a * rowlen;
         // a window entirely off the detector only needs zeros: clamp its copy into the zero pad
         // (a window overlapping [0, ND] is always inside the PADG >= WL padding)
         const int e0 = min(max(ws + 1, -PADG), ND + PADG - WLB), eb = e0 & ~1;
@@ -366,6 +367,10 @@ __global__ void __launch_bounds__(NT + 32, 3) backproject3_kernel(
     j0 = blockIdx.x * TILE; i0 = blockIdx.y * TILE; s = blockIdx.z % S; ks = blockIdx.z / S; nks = KS;
   }
 SPAN_START_bp();
+#ifdef EI_TRACE
+  const unsigned long long t_start = gtimer3();
+  unsigned long long t_data = 0;
+#endif
   const float ctr = 0.5f * (float)(N - 1), dctr = 0.5f * (float)(ND - 1);
   const size_t rowlen = (size_t)RpG, soff = (size_t)s * NA * rowlen + PADG;
   const int a_lo = (int)(((long long)ks * NA3) / nks), a_hi = (int)(((long long)(ks + 1) * NA3) / nks);
@@ -392,7 +397,8 @@ SPAN_START_bp();
   __syncthreads();
 
   if (w == NT / 32) {   // ---------------- producer warp ----------------
-    pdl_wait();   // K2's gradient sinograms
+    // the per-angle tables and windows are plan data: the first chunk's are prepared before the
+    // PDL wait (they overlap K2's tail); only the copies of K2's gradient rows wait for K2
     const float xa = (float)j0 - ctr, xb = xa + (float)(TILE - 1);
     const float ya = (float)i0 - ctr, yb = ya + (float)(TILE - 1);
     constexpr uint32_t bytesAB = (uint32_t)WL3 * 16, bytesC = (uint32_t)WL3 * 4;
@@ -401,9 +407,9 @@ SPAN_START_bp();
     for (int c = 0; c < c_hi; ++c) {
       if (c >= NST3) mbar_wait(&sm.empty[st], ph ^ 1);
       const int na = nac(c);
-      int e0 = 0;
+      int e0 = 0, a = 0;
       if (lane < na) {   // per-angle tables + window start
-        const int a = __ldg(alist_k + c0(c) + lane);
+        a = __ldg(alist_k + c0(c) + lane);
         const float4 g = __ldg(k3 + a);   // c', s', 1/h, Joseph weight
         const float k00 = fmaf(xa, g.x, fmaf(ya, g.y, dctr)), k01 = fmaf(xb, g.x, fmaf(ya, g.y, dctr));
         const float k10 = fmaf(xa, g.x, fmaf(yb, g.y, dctr)), k11 = fmaf(xb, g.x, fmaf(yb, g.y, dctr));
@@ -422,8 +428,9 @@ SPAN_START_bp();
       __syncwarp();
       if (lane == 0) mbar_arrive_expect_tx(&sm.full[st], (uint32_t)na * (2u * bytesAB + bytesC));
       __syncwarp();
+      if (c == 0) pdl_wait();   // K2's gradient sinograms
       if (lane < na) {
-        const size_t row = soff + (size_t)__ldg(alist_k + c0(c) + lane) * rowlen + e0;
+        const size_t row = soff + (size_t)a * rowlen + e0;
         bulk_g2s(&sm.ang[st][lane].a[0], GA + row, bytesAB, &sm.full[st]);
         bulk_g2s(&sm.ang[st][lane].b[0], GB + row, bytesAB, &sm.full[st]);
         bulk_g2s(&sm.ang[st][lane].c[0], GC + row, bytesC, &sm.full[st]);
@@ -476,6 +483,9 @@ SPAN_START_bp();
   uint32_t ph = 0;
   for (int c = 0; c < c_hi; ++c) {
     mbar_wait_full(&sm.full[st], ph);
+#ifdef EI_TRACE
+    if (c == 0) t_data = gtimer3();
+#endif
     const int na = nac(c);
     // the chunk's angles of the current class, then (at most once per CTA) the class change
     // and the rest: the plan lists cos >= 0 first, so the change is one index per chunk
@@ -533,7 +543,18 @@ SPAN_START_bp();
   flush();
 #ifdef EI_TRACE
   asm volatile("bar.sync 2, %0;\n" ::"n"(NT) : "memory");   // consumers only
-  if (tid == 0) SPAN_END_bp(0);
+  if (tid == 0) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+    const size_t b = ((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;   // linear
+    if (b < 65536) {
+      g_k3_trace[4 * b] = t_start;
+      g_k3_trace[4 * b + 1] = t_data;
+      g_k3_trace[4 * b + 2] = gtimer3();
+      g_k3_trace[4 * b + 3] = smid | ((unsigned long long)c_hi << 32);
+    }
+    SPAN_END_bp(0);
+  }
 #endif
   const int i = i0 + row;
   if (i >= N) return;

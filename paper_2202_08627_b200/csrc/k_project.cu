@@ -874,18 +874,19 @@ int plan_projector(ei_plan &p, const double *angles, const std::vector<int> &pro
   const int E = stage_entries(nst);
   if (!build_chunks(p, angles, groups, order, 1, E, RCMAX, ch1)) return EI_ERR_SHAPE;
   // K1B band mode for the cost / forward path of small maps: units (group, band of BR = 16 map
-  // rows, slice) of nearly equal work.  Measured (tools/dbg/sweep_band.sh, step time): a win only
-  // where the band grid is one wave of enough CTAs — P1 38.8 -> 37.0 us (196 units); C2's 384 units
-  // (1.3 waves) 68.2 -> 87 us, and at BR = 11 (576 units) 81 us with K2 summing 24 partials; C1's
-  // 48 units 26.7 -> 26.8-27.5 us.  So: BR = 16 rows fit the 104 KB budget and the band grid is
-  // between half a wave and one wave of 2 CTAs per SM (knobs EI_K1_BAND, EI_K1_BR)
+  // rows, slice) of nearly equal work, every lane sweeping all N_d rays.  Measured
+  // (tools/dbg/sweep_band.sh, step time): P1 (N_d = N) 38.8 -> 37.0 us (378 units); C2 (N_d = 1.5 N:
+  // a third of the lanes sample zero entries) 68.2 -> 87 us with 384 units, 81 us at BR = 11 (576
+  // units, K2 summing 24 partials); C1 (N_d = 1.5 N, 48 units) 26.7 -> 26.8-27.5 us.  So: BR = 16
+  // rows fit the 104 KB budget, N_d <= 1.2 N, and the band grid within 1.5 waves of 2 CTAs per SM
+  // (knobs EI_K1_BAND, EI_K1_BR)
   p.proj.band = 0;
   {
     const int bstride = (N + 4 + 1) & ~1;
     const int brmax = std::min(64, (int)((size_t)104 * 1024 / ((size_t)bstride * per_entry)));
     const int br0 = 16;
     const long long units16 = (long long)((N + br0 - 1) / br0) * (long long)groups.size() * p.S;
-    bool use = brmax >= br0 && units16 <= 2LL * sms && 2 * units16 >= sms;
+    bool use = brmax >= br0 && 5LL * ND <= 6LL * N && units16 <= 3LL * sms && 2 * units16 >= sms;
     int br = br0;
     if (const char *e = getenv("EI_K1_BAND")) use = atoi(e) != 0 && brmax >= 4;
     if (const char *e = getenv("EI_K1_BR")) br = atoi(e);

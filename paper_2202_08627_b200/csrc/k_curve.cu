@@ -153,8 +153,11 @@ __device__ __forceinline__ const float *row_ptr(const K2Args &g, const Pos &q, i
   return g.s_exp + ((size_t)(q.s * g.NA + q.a) * g.M + (r - g.nmap)) * g.ND;
 }
 
+#ifndef EI_K2_MINB
+#define EI_K2_MINB 2   // CTAs per SM the register allocation targets (compile-time A/B switch)
+#endif
 template <int MODE>
-__global__ void __launch_bounds__(K2_MAXT + 32, 2) curve_kernel(K2Args g) {
+__global__ void __launch_bounds__(K2_MAXT + 32, EI_K2_MINB) curve_kernel(K2Args g) {
   extern __shared__ __align__(16) float smem[];   // ring [NST][nrows][WB] + exchange [2][3][WB]
   __shared__ __align__(8) uint64_t full[NST], empty[NST];
   SPAN_START_curve();

@@ -203,3 +203,29 @@ def test_h_model_detector_segments(ei, sampled, monkeypatch):
     assert np.all(np.abs(cost - rc) / rc <= 1e-4), (cost, rc)
     for s in range(cfg.S):
         assert rel_l2(g[s], rg[s]) <= 1e-3, (s, rel_l2(g[s], rg[s]))
+
+
+@pytest.mark.parametrize("name", ["P1", "RH"])
+@pytest.mark.parametrize("band", ["0", "1"])
+def test_cost_grad_h_band_and_tile_k1(ei, name, band, monkeypatch):
+    """The single-map K1 in both decompositions (K1B band units, the plan's choice on P1, and the
+    ray-tile units) holds the oracle gates for cost and g_h, with band heights 16 and 7 (ragged
+    last band)."""
+    case = _cases.cached_h_case(name)
+    cfg = case.cfg
+    h = synth.perturbed((case.h,), cfg.seed + 7)[0]
+    lam = synth.H_LAMBDA
+    rc, rg, rst = _cases.oracle_cost_grad_h(case, h, lam)
+    monkeypatch.setenv("EI_K1_BAND", band)
+    for br in (["16", "7"] if band == "1" else [None]):
+        if br is None:
+            monkeypatch.delenv("EI_K1_BR", raising=False)
+        else:
+            monkeypatch.setenv("EI_K1_BR", br)
+        plan = plan_for(ei, cfg)
+        info = ei.ei_plan_info(plan)
+        assert (info["k1_band_rows"] > 0) == (band == "1")
+        cost, g, gdr, st = gpu_h(ei, plan, case, h, lam)
+        assert np.all(np.abs(cost - rc) / rc <= 1e-4), (br, cost, rc)
+        for s in range(cfg.S):
+            assert rel_l2(g[s], rg[s]) <= 1e-3, (br, s, rel_l2(g[s], rg[s]))

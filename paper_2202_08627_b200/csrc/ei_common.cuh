@@ -108,7 +108,6 @@ struct ei_plan {
   double *part_reg = nullptr;    // [S][RB] per-tile sum x^2 partials (K0)
   float *part3 = nullptr;        // [KS][S][3][N][N] K3 angle-split partial gradients
   int KS = 1;                    // K3 angle split: most parts of one (slice, tile)
-  int k3p4 = 0;                  // K3 with 4 pixel pairs per thread (KS == 1 only)
   int KSk = 1, KSe = 0;          // (slice, tile) pairs v < KSe have KSk + 1 parts, the rest KSk
   int4 *k3u = nullptr;           // device [n_k3u] K3 units {tile, slice, part, parts} in launch order
   int n_k3u = 0;                 // (only for split grids with more units than SMs)

@@ -91,32 +91,12 @@ struct Ang3 {
   float4 t1;       // c', s', 1/h, 1 - 1/h
   float4 t2;       // (Nd-1)/2 + 1 - e0 + min(c', 0), |c'| - 1, -, -
 };
-// Two consumer shapes of the three-map kernel (DESIGN.md §5 K3): NPAIR = 2 pixel pairs per thread,
-// 256 consumer threads, 3 CTAs per SM (the default), or NPAIR = 4 pairs per thread, 128 consumer
-// threads, 4 CTAs per SM and 8-angle chunks (the per-angle table loads, loop control and window
-// offset amortised over 8 pixels instead of 4)
-#ifndef EI_K3_CH4
-#define EI_K3_CH4 8
-#endif
-template <int NPAIR>
-struct K3V;
-template <>
-struct K3V<2> {
-  static constexpr int NTC = NT, CH = CH3, MINB = 3;
-};
-template <>
-struct K3V<4> {
-  static constexpr int NTC = 128, CH = EI_K3_CH4, MINB = 4;
-};
-template <int NPAIR>
-struct Smem3T {
-  Ang3 ang[NST3][K3V<NPAIR>::CH];
+struct Smem3 {
+  Ang3 ang[NST3][CH3];
   int nb[NST3];              // first angle of the chunk with cos < 0 (CH if none)
-  float tot[6 * NPAIR][K3V<NPAIR>::NTC];   // per consumer thread: totals of finished angle classes
-                                           // (pair, L/R, map)
+  float tot[12][NT];        // per consumer thread: totals of finished angle classes (pair, L/R, map)
   uint64_t full[NST3], empty[NST3];
 };
-using Smem3 = Smem3T<2>;
 
 #ifdef EI_TRACE
 // debug builds only (tools/dbg/k1_trace.py --k3): per CTA {start, first chunk staged, end, SM id}
@@ -139,9 +119,8 @@ struct FinArgs {
   int *diag;                     // -DEI_CHECK builds: staged-window overflows (ei_plan_info out[4])
 };
 
-// consumer threads only (named barrier 1, NT threads); fixed order (for a given NT): per-thread strided fp64 sums,
+// consumer threads only (named barrier 1, NT threads); fixed order: per-thread strided fp64 sums,
 // then the warps' sums in warp order
-template <int NT>   // the calling kernel's consumer threads
 __device__ __forceinline__ void finalize(const FinArgs &f, int s, int tid) {
   __shared__ double fred[NT / 32];
   // every thread's loads are issued UF at a time (independent L2 round trips in flight) and added
@@ -278,7 +257,7 @@ SPAN_START_bp();
   // the per-angle drift gradient
   if (fin.cost && i0 == 0 && j0 == 0 && ks == 0) {
     pdl_wait();   // K2's partials
-    finalize<NT>(fin, s, tid);
+    finalize(fin, s, tid);
   }
   const int row = 4 * w + (lane >> 3), lx = lane & 7;
   const float yi = (float)(i0 + row) - ctr;
@@ -368,17 +347,16 @@ SPAN_START_bp();
 }
 
 // three-map model: triple layout, pixel pairs (see the file header)
-template <bool TAB, int NPAIR>
-__global__ void __launch_bounds__(K3V<NPAIR>::NTC + 32, K3V<NPAIR>::MINB) backproject3_kernel(
+template <bool TAB>
+__global__ void __launch_bounds__(NT + 32, 3) backproject3_kernel(
     const float4 *__restrict__ GA, const float4 *__restrict__ GB, const float *__restrict__ GC,
     const float4 *__restrict__ k3, const int *__restrict__ alist, int NA3, int N, int NA, int ND,
     const float *__restrict__ mu, const float *__restrict__ delta, const float *__restrict__ sigma,
     float lambda, float *__restrict__ o0, float *__restrict__ o1, float *__restrict__ o2,
     size_t out_stride, int S, int KS, float *__restrict__ part3, int PADG, int RpG,
     const int4 *__restrict__ units, FinArgs fin) {
-  constexpr int NT = K3V<NPAIR>::NTC, CH3 = K3V<NPAIR>::CH;   // consumer threads, angles per chunk
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  Smem3T<NPAIR> &sm = *reinterpret_cast<Smem3T<NPAIR> *>(smem_raw);
+  Smem3 &sm = *reinterpret_cast<Smem3 *>(smem_raw);
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   int j0, i0, s, ks, nks;   // unit decode as in backproject1_kernel
   if (TAB) {
@@ -465,49 +443,39 @@ SPAN_START_bp();
   // ---------------- consumer warps ----------------
   if (fin.cost && i0 == 0 && j0 == 0 && ks == 0) {   // fused K4 (see backproject1_kernel)
     pdl_wait();
-    finalize<NT>(fin, s, tid);
+    finalize(fin, s, tid);
   }
-  // NPAIR = 2: warp w covers a 16 x 8 pixel block (2 x 4 blocks per tile); NPAIR = 4: a 32 x 8
-  // block (1 x 4).  lane = (pair column pc, row r): a quarter warp is 4 pair columns x 2 rows; pair
-  // p of a thread sits 8 p pixels right of pair 0
-  const int pc = lane & 3, r = lane >> 2;
-  const int row = NPAIR == 2 ? 8 * (w >> 1) + r : 8 * w + r;
-  const int jl = NPAIR == 2 ? j0 + 16 * (w & 1) + 2 * pc : j0 + 2 * pc;   // left pixel of pair 0
+  // warp w covers a 16 x 8 pixel block (2 x 4 blocks per tile); lane = (pair column pc, row r):
+  // a quarter warp is 4 pair columns x 2 rows; pair p of a thread sits 8 pixels right of pair 0
+  const int wx = w & 1, wy = w >> 1, pc = lane & 3, r = lane >> 2;
+  const int row = 8 * wy + r, jl = j0 + 16 * wx + 2 * pc;      // left pixel of pair 0
   const float yi = (float)(i0 + row) - ctr;
-  float xl[NPAIR];
-#pragma unroll
-  for (int p = 0; p < NPAIR; ++p) xl[p] = (float)(jl + 8 * p) - ctr;
+  const float xl0 = (float)jl - ctr, xl1 = xl0 + 8.f;
   // partial sums of the current class: lower pixel (2 taps: float2 per map), upper pixel (3 taps:
   // float2 + float per map); totals of finished classes per (pair, left/right, map)
-  float2 lm[NPAIR], ld[NPAIR], ls[NPAIR], hm[NPAIR], hd[NPAIR], hs[NPAIR];
-  float2 hmd3[NPAIR];       // upper pixel's third tap of mu and delta: one FFMA2 (u2 broadcast)
-  float2 hs3p[NPAIR / 2];   // and of sigma, pairs 2q in .x, 2q + 1 in .y (one FFMA2 per angle)
-  auto zero = [&]() {
-#pragma unroll
-    for (int p = 0; p < NPAIR; ++p)
-      lm[p] = ld[p] = ls[p] = hm[p] = hd[p] = hs[p] = hmd3[p] = make_float2(0.f, 0.f);
-#pragma unroll
-    for (int q = 0; q < NPAIR / 2; ++q) hs3p[q] = make_float2(0.f, 0.f);
-  };
-  zero();
+  float2 lm0 = make_float2(0.f, 0.f), ld0 = lm0, ls0 = lm0, hm0 = lm0, hd0 = lm0, hs0 = lm0;
+  float2 lm1 = lm0, ld1 = lm0, ls1 = lm0, hm1 = lm0, hd1 = lm0, hs1 = lm0;
+  float2 hmd30 = lm0, hmd31 = lm0;   // upper pixel's third tap of mu and delta: one FFMA2 (u2 broadcast)
+  float2 hs3p = lm0;                 // and of sigma, pair 0 in .x, pair 1 in .y (one FFMA2 per angle)
   // totals of finished classes in shared memory (this thread's column; touched once per class):
   // tot[(2 p + side) 3 + map][tid], side 0 = left pixel
 #pragma unroll
-  for (int m = 0; m < 6 * NPAIR; ++m) sm.tot[m][tid] = 0.f;
+  for (int m = 0; m < 12; ++m) sm.tot[m][tid] = 0.f;
   int cls = 0;   // 0: cos >= 0, lower pixel = left; 1: cos < 0, lower pixel = right
   auto flush = [&]() {   // fold the class's partial sums into the per-pixel totals, restart
+    const float L[2][3] = {{lm0.x + lm0.y, ld0.x + ld0.y, ls0.x + ls0.y},
+                           {lm1.x + lm1.y, ld1.x + ld1.y, ls1.x + ls1.y}};
+    const float H[2][3] = {{hm0.x + hm0.y + hmd30.x, hd0.x + hd0.y + hmd30.y, hs0.x + hs0.y + hs3p.x},
+                           {hm1.x + hm1.y + hmd31.x, hd1.x + hd1.y + hmd31.y, hs1.x + hs1.y + hs3p.y}};
 #pragma unroll
-    for (int p = 0; p < NPAIR; ++p) {
-      const float s3 = (p & 1) ? hs3p[p >> 1].y : hs3p[p >> 1].x;
-      const float L[3] = {lm[p].x + lm[p].y, ld[p].x + ld[p].y, ls[p].x + ls[p].y};
-      const float H[3] = {hm[p].x + hm[p].y + hmd3[p].x, hd[p].x + hd[p].y + hmd3[p].y, hs[p].x + hs[p].y + s3};
+    for (int p = 0; p < 2; ++p)
 #pragma unroll
       for (int m = 0; m < 3; ++m) {
-        sm.tot[(2 * p) * 3 + m][tid] += cls ? H[m] : L[m];
-        sm.tot[(2 * p + 1) * 3 + m][tid] += cls ? L[m] : H[m];
+        sm.tot[(2 * p) * 3 + m][tid] += cls ? H[p][m] : L[p][m];
+        sm.tot[(2 * p + 1) * 3 + m][tid] += cls ? L[p][m] : H[p][m];
       }
-    }
-    zero();
+    lm0 = ld0 = ls0 = hm0 = hd0 = hs0 = lm1 = ld1 = ls1 = hm1 = hd1 = hs1 = make_float2(0.f, 0.f);
+    hmd30 = hmd31 = hs3p = make_float2(0.f, 0.f);
   };
 
   pdl_wait();   // sleep while K2 runs (this CTA may have launched early)
@@ -554,12 +522,10 @@ SPAN_START_bp();
         u2o = u2;
         Co = C;
       };
-      float u2v[NPAIR], Cv[NPAIR];
-#pragma unroll
-      for (int p = 0; p < NPAIR; ++p) pair(xl[p], lm[p], ld[p], ls[p], hm[p], hd[p], hs[p], hmd3[p], u2v[p], Cv[p]);
-#pragma unroll
-      for (int q = 0; q < NPAIR / 2; ++q)   // two pairs' sigma third taps per FFMA2
-        hs3p[q] = __ffma2_rn(make_float2(u2v[2 * q], u2v[2 * q + 1]), make_float2(Cv[2 * q], Cv[2 * q + 1]), hs3p[q]);
+      float u20, u21, C0, C1;
+      pair(xl0, lm0, ld0, ls0, hm0, hd0, hs0, hmd30, u20, C0);
+      pair(xl1, lm1, ld1, ls1, hm1, hd1, hs1, hmd31, u21, C1);
+      hs3p = __ffma2_rn(make_float2(u20, u21), make_float2(C0, C1), hs3p);   // both pairs' sigma third taps
     };
     const Ang3 *a0 = &sm.ang[st][0];
 #pragma unroll 1
@@ -594,7 +560,7 @@ SPAN_START_bp();
   if (i >= N) return;
   const size_t NN = (size_t)N * N;
 #pragma unroll
-  for (int p = 0; p < NPAIR; ++p)
+  for (int p = 0; p < 2; ++p)
 #pragma unroll
     for (int q = 0; q < 2; ++q) {
       const int j = jl + 8 * p + q;
@@ -718,19 +684,9 @@ cudaError_t launch_backproject3(const ei_plan &p, const float *mu, const float *
                                 float *g_sigma, size_t out_stride, const Finalize *fz,
                                 cudaStream_t st) {
   const FinArgs fin = fin_args(p, lambda, fz);
-  cudaError_t e;
-  if (p.k3p4) {   // 4 pixel pairs per thread (plans without an angle split, p.KS == 1)
-    e = set_smem(backproject3_kernel<true, 4>, backproject3_kernel<false, 4>, sizeof(Smem3T<4>));
-    if (e != cudaSuccess) return e;
-    e = launch_pdl(backproject3_kernel<false, 4>, bp_grid(p), dim3(K3V<4>::NTC + 32), sizeof(Smem3T<4>), st,
-                   (const float4 *)p.GA, (const float4 *)p.GB, (const float *)p.GC, p.tab.k3, p.alist3, p.NA3,
-                   p.N, p.NA, p.ND, mu, delta, sigma, lambda, g_mu, g_delta, g_sigma, out_stride, p.S, p.KS,
-                   p.part3, p.PADG, p.RpG, (const int4 *)p.k3u, fin);
-    return e == cudaSuccess ? cudaGetLastError() : e;
-  }
-  e = set_smem(backproject3_kernel<true, 2>, backproject3_kernel<false, 2>, sizeof(Smem3));
+  cudaError_t e = set_smem(backproject3_kernel<true>, backproject3_kernel<false>, sizeof(Smem3));
   if (e != cudaSuccess) return e;
-  auto kern = p.k3u ? backproject3_kernel<true, 2> : backproject3_kernel<false, 2>;
+  auto kern = p.k3u ? backproject3_kernel<true> : backproject3_kernel<false>;
   e = launch_pdl(kern, bp_grid(p), dim3(NT + 32), sizeof(Smem3), st, (const float4 *)p.GA,
                  (const float4 *)p.GB, (const float *)p.GC, p.tab.k3, p.alist3, p.NA3, p.N, p.NA, p.ND, mu,
                  delta, sigma, lambda, g_mu, g_delta, g_sigma, out_stride, p.S, p.KS, p.part3, p.PADG,

@@ -242,7 +242,6 @@ int ei_plan_create(const ei_geometry *geom, const double *angles, ei_plan **out)
     p->KSk = KS;
     p->KSe = (int)extra;
     p->KS = KS + (extra > 0 ? 1 : 0);
-    if (const char *e = getenv("EI_K3_P4")) p->k3p4 = (atoi(e) != 0 && p->KS == 1) ? 1 : 0;   // A/B knob
     const long long n = ctas * KS + extra;
     if (p->KS > 1 && n > sms) {   // placement table: parts heaviest first, least-loaded SM
       std::vector<int4> u;

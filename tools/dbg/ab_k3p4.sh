@@ -1,8 +1,9 @@
-# A/B: K3 with 4 pixel pairs per thread (EI_K3_P4=1, 128 consumer threads, 4 CTAs per SM) vs 2
-OUT=gpurun_out/abp4; mkdir -p $OUT
+# A/B: K3 original (2 pixel pairs x 256 threads) vs the generic kernel's 2-pair instance
+# (EI_K3_GEN=1) vs its 4-pair instance (EI_K3_P4=1: 128 consumer threads, 4 CTAs per SM)
+OUT=gpurun_out/abp4b; mkdir -p $OUT
 python -c "import __graft_entry__ as g; g.build()" > $OUT/build.log 2>&1
 run() { c=$1; shift; x=$(env "$@" timeout 90 python bench.py --config $c --steps ${STEPS:-20} --warmup 5 --no-cpu-baseline 2>/dev/null | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); k=d.get('kernels',{}); print(d['ms_per_step'], ' '.join('%s=%.4f'%(n[:2],v['ms']) for n,v in k.items()))"); echo "$c $* $x" | tee -a $OUT/res.txt; }
 timeout 300 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "pair_shapes" > $OUT/pytest.log 2>&1; tail -1 $OUT/pytest.log
 for r in 1 2; do
-  for c in C4 C3 C5; do run $c EI_NONE=1; run $c EI_K3_P4=1; done
+  for c in C4 C3 C5; do run $c EI_NONE=1; run $c EI_K3_GEN=1; run $c EI_K3_P4=1; done
 done

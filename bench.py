@@ -264,6 +264,13 @@ def make_gpu_case(cfg, ei, torch, noise=True):
     return case
 
 
+def step_percentiles(ev):
+    """p10 / p50 / p90 of this rank's per-step device times (ms), CUDA events around each step."""
+    t = np.sort(np.array([a.elapsed_time(b) for a, b in ev]))
+    q = lambda f: float(t[min(len(t) - 1, int(round(f * (len(t) - 1))))])
+    return {"p10": round(q(0.1), 5), "p50": round(q(0.5), 5), "p90": round(q(0.9), 5)}
+
+
 def run_gpu(args, cfg, rank, world, local_rank):
     import torch
     import torch.distributed as dist
@@ -382,6 +389,7 @@ def run_gpu(args, cfg, rank, world, local_rank):
     clocks = sampler.summary(t0, t1)
     peaks = load_peaks()
     ms_step = ms / K
+    step_stats = step_percentiles(ev)
     rsu = ray_sample_updates(cfg)
     kb = kernel_bytes(cfg, rsu, plan_info.get("mirror_pairs", 0))
     sm_mhz = clocks.get("sm_mhz") or peaks.get("sm_max_mhz", 1965.0)
@@ -395,7 +403,8 @@ def run_gpu(args, cfg, rank, world, local_rank):
     value = world * 1000.0 / ms_step
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": K,
-        "warmup": args.warmup, "ms_per_step": round(ms_step, 5), "higher_is_better": True,
+        "warmup": args.warmup, "ms_per_step": round(ms_step, 5), "ms_per_step_pct": step_stats,
+        "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": bench_config(cfg, lam),
         "l2": "flushed before every timed step (256 MiB write, untimed)",
@@ -472,10 +481,12 @@ def run_gpu_angles(args, cfg, rank, world, local_rank):
     if rank != 0:
         return None
     ms_step = ms / K
+    step_stats = step_percentiles(ev)
     rsu = ray_sample_updates(cfg)
     return {
         "metric": METRIC, "value": round(1000.0 / ms_step, 3), "unit": UNIT, "n_gpus": world, "steps": K,
-        "warmup": args.warmup, "ms_per_step": round(ms_step, 5), "higher_is_better": True,
+        "warmup": args.warmup, "ms_per_step": round(ms_step, 5), "ms_per_step_pct": step_stats,
+        "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": bench_config(cfg, lam),
         "parallelism": "angle-sharded x%d, NCCL all-reduce of gradient + cost per evaluation" % world,
@@ -644,6 +655,7 @@ def run_gpu_h(args, cfg):
     torch.cuda.synchronize()
     t1 = time.time()
     ms_step = sum(a.elapsed_time(b) for a, b in ev) / K
+    step_stats = step_percentiles(ev)
     s1 = ei.ei_plan_stats(plan)
     ei.ei_plan_set_timing(plan, K)
     for i in range(K):
@@ -669,6 +681,7 @@ def run_gpu_h(args, cfg):
     line = {
         "metric": "cost+gradient evals/sec (single-map model, eq. 4)", "value": round(1000.0 / ms_step, 3),
         "unit": UNIT, "n_gpus": 1, "steps": K, "warmup": args.warmup, "ms_per_step": round(ms_step, 5),
+        "ms_per_step_pct": step_stats,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": "%s: %s (paper scan geometry, PAPER.md:89-93), gamma=%g" %
                    (cfg.name, describe(cfg), case.gamma), "lambda": lam, "eval_point": "x_pert (R21)",

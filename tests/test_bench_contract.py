@@ -70,3 +70,5 @@ def test_gpu_arm_line():
     assert d["gpu_launches"] >= 4 * d["steps"]             # K0..K3 per evaluation, all libei kernels
     assert d["clocks"]["sm_mhz"] and d["clocks"]["sm_max_mhz"]
     assert set(d["kernels"]) >= {"K0_pack", "K1_project", "K2_curve", "K3_backproject"}
+    pct = d["ms_per_step_pct"]                           # per-step spread of the device times
+    assert 0 < pct["p10"] <= pct["p50"] <= pct["p90"]

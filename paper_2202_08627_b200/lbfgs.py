@@ -52,31 +52,66 @@ class Result:
     iters: Optional[np.ndarray] = None                             # iterations per problem
 
 
-def _bdot(a: Blocks, b: Blocks) -> torch.Tensor:
+# A vector of the optimizer is either a list of block tensors [S, ...] (blocks of any shapes) or,
+# when x0 is one tensor [B, S, ...] of equal blocks, that stacked tensor itself: then every vector
+# operation below is one or two kernels over all blocks instead of a few per block (the loop is
+# launch-bound at the sizes of one slice: ~550 launches per iteration with per-block lists).
+Vec = Union[torch.Tensor, Blocks]
+
+
+def _bdot(a: Vec, b: Vec) -> torch.Tensor:
     """Per-(block, problem) dot products, products in the tensors' dtype, sums in fp64: [B, S]."""
+    if isinstance(a, torch.Tensor):
+        return torch.sum((a * b).reshape(a.shape[0], a.shape[1], -1), dim=-1, dtype=torch.float64)
     return torch.stack([torch.sum((x * y).reshape(x.shape[0], -1), dim=-1, dtype=torch.float64)
                         for x, y in zip(a, b)])
 
 
-def _sdot(a: Blocks, b: Blocks) -> torch.Tensor:
+def _sdot(a: Vec, b: Vec) -> torch.Tensor:
     """Per-problem dot products over all blocks: [S] fp64."""
     return _bdot(a, b).sum(0)
 
 
-def _bc(v: torch.Tensor, like: torch.Tensor) -> torch.Tensor:
-    """Broadcast a per-problem vector [S] against a block [S, ...]."""
+def _bc(v: torch.Tensor, like: torch.Tensor, stacked: bool = False) -> torch.Tensor:
+    """Broadcast a per-problem vector [S] (or, stacked, a per-(block, problem) matrix [B, S])
+    against a block [S, ...] (stacked: against the vector [B, S, ...])."""
     if v.dtype != torch.bool:
         v = v.to(like.dtype)
-    return v.reshape(v.shape + (1,) * (like.dim() - 1))
+    if stacked and v.dim() == 1:
+        return v.reshape((1,) + v.shape + (1,) * (like.dim() - 2))
+    return v.reshape(v.shape + (1,) * (like.dim() - v.dim()))
 
 
-def _axpy(x: Blocks, a: torch.Tensor, p: Blocks) -> Blocks:
+def _axpy(x: Vec, a: torch.Tensor, p: Vec) -> Vec:
     """x + a p with a per-problem scalar a [S]."""
+    if isinstance(x, torch.Tensor):
+        return x + _bc(a, x, True) * p
     return [xb + _bc(a, xb) * pb for xb, pb in zip(x, p)]
 
 
-def _where(mask: torch.Tensor, a: Blocks, b: Blocks) -> Blocks:
+def _where(mask: torch.Tensor, a: Vec, b: Vec) -> Vec:
+    if isinstance(a, torch.Tensor):
+        return torch.where(_bc(mask, a, True), a, b)
     return [torch.where(_bc(mask, xa), xa, xb) for xa, xb in zip(a, b)]
+
+
+def _bscale(v: Vec, c: torch.Tensor) -> Vec:
+    """v_b * c[b] with a per-(block, problem) matrix c [B, S]."""
+    if isinstance(v, torch.Tensor):
+        return v * _bc(c, v, True)
+    return [vb * _bc(c[b], vb) for b, vb in enumerate(v)]
+
+
+def _sub(a: Vec, b: Vec) -> Vec:
+    return a - b if isinstance(a, torch.Tensor) else [x - y for x, y in zip(a, b)]
+
+
+def _neg(a: Vec) -> Vec:
+    return -a if isinstance(a, torch.Tensor) else [-x for x in a]
+
+
+def _clone(a: Vec) -> Vec:
+    return a.clone() if isinstance(a, torch.Tensor) else [x.clone() for x in a]
 
 
 def _cubic_min(a0, f0, d0, a1, f1, d1):
@@ -106,7 +141,7 @@ def strong_wolfe(fg, x: Blocks, f0: np.ndarray, g: Blocks, p: Blocks, d0: np.nda
     a_hi, f_hi, d_hi = np.zeros(S), f0.copy(), d0.copy()
     best_a, best_f = np.zeros(S), f0.copy()
     found = np.zeros(S, bool)
-    x_best, g_best = list(x), list(g)
+    x_best, g_best = (x, g) if isinstance(x, torch.Tensor) else (list(x), list(g))
     n_ev = 0
     first = np.ones(S, bool)
     dev = x[0].device
@@ -172,9 +207,9 @@ def strong_wolfe(fg, x: Blocks, f0: np.ndarray, g: Blocks, p: Blocks, d0: np.nda
     return x_best, best_f, g_best, best_a, found, n_ev
 
 
-def _as_blocks(x0) -> Tuple[Blocks, bool]:
+def _as_blocks(x0) -> Tuple[Vec, bool]:
     if isinstance(x0, torch.Tensor):
-        return [x0[b] for b in range(x0.shape[0])], True
+        return x0, True          # stacked: the vector is the tensor [B, S, ...] itself
     return list(x0), False
 
 
@@ -192,15 +227,15 @@ def minimize(fg: Callable, x0: Union[torch.Tensor, Sequence[torch.Tensor]], max_
     _sdot_r = lambda a, b: _bdot_r(a, b).sum(0)
     t0 = time.time()
     x, stacked = _as_blocks(x0)
-    x = [b.clone() for b in x]
-    pack = (lambda blocks: torch.stack(blocks)) if stacked else (lambda blocks: blocks)
-    unpack = (lambda v: [v[b] for b in range(v.shape[0])]) if stacked else (lambda v: list(v))
+    x = _clone(x)
+    pack = lambda v: v
+    unpack = (lambda v: v) if stacked else (lambda v: list(v))
     fgb = lambda blocks: (lambda r: (r[0].double(), unpack(r[1])))(fg(pack(blocks)))
     f, g = fgb(x)
-    f, g = f.clone(), [b.clone() for b in g]
+    f, g = f.clone(), _clone(g)
     n_evals = 1
-    S, B = x[0].shape[0], len(x)
-    dev = x[0].device
+    S, B = (x.shape[1], x.shape[0]) if stacked else (x[0].shape[0], len(x))
+    dev = x.device if stacked else x[0].device
     Sh: List[Blocks] = []                    # history, oldest first
     Yh: List[Blocks] = []
     rho: List[torch.Tensor] = []             # [S] fp64, 0 where the pair is not valid
@@ -222,21 +257,21 @@ def minimize(fg: Callable, x0: Union[torch.Tensor, Sequence[torch.Tensor]], max_
             it -= 1
             break
         # ---- two-loop recursion: p = -H g (per problem, masked histories) ----
-        q = [b.clone() for b in g]
+        q = _clone(g)
         alphas = []
         for k in reversed(range(len(Sh))):
             a_k = rho[k] * _sdot_r(Sh[k], q)
             alphas.append(a_k)
-            q = [qb - yb * _bc(a_k, qb) for qb, yb in zip(q, Yh[k])]
+            q = _axpy(q, -a_k, Yh[k])                  # q - a_k y_k
         gnorm = _bdot_r(g, g).sqrt().clamp_min(1e-300)
         scal = torch.where(has_gamma.unsqueeze(0), gamma, 1.0 / gnorm)     # [B, S]
-        r = [qb * _bc(scal[b], qb) for b, qb in enumerate(q)]
+        r = _bscale(q, scal)
         for k, a_k in zip(range(len(Sh)), reversed(alphas)):
             b_k = rho[k] * _sdot_r(Yh[k], r)
-            r = [rb + sb * _bc(a_k - b_k, rb) for rb, sb in zip(r, Sh[k])]
-        p = [-rb for rb in r]
+            r = _axpy(r, a_k - b_k, Sh[k])             # r + (a_k - b_k) s_k
+        p = _neg(r)
         d0 = _sdot_r(g, p)
-        sd_dir = [-gb * _bc(scal[b], gb) for b, gb in enumerate(g)]   # scaled steepest descent
+        sd_dir = _bscale(_neg(g), scal)   # scaled steepest descent
         bad = d0 >= 0                          # not a descent direction: steepest descent
         p = _where(bad, sd_dir, p)
         d0 = torch.where(bad, _sdot_r(g, p), d0)
@@ -259,8 +294,8 @@ def minimize(fg: Callable, x0: Union[torch.Tensor, Sequence[torch.Tensor]], max_
         hit = acc & ((f_new <= tgt) if tgt is not None else np.zeros(S, bool))
         stall = acc & ~hit & (rel < rel_tol) & ~sd_now
         okt = torch.from_numpy(ok & active).to(dev)
-        s_vec = [xn - xb for xn, xb in zip(x_new, x)]
-        y_vec = [gn - gb for gn, gb in zip(g_new, g)]
+        s_vec = _sub(x_new, x)
+        y_vec = _sub(g_new, g)
         sy = _sdot_r(s_vec, y_vec)
         yy = _sdot_r(y_vec, y_vec)
         keep = okt & (sy > 0)

@@ -118,3 +118,24 @@ def test_target_stop_and_reasons():
     assert float(res.history[res.iters[0] - 1][0]) > 1e-3 * float(f0[0])   # the first one below
     assert res.reason[1] in ("rel_tol", "precision") and bool(res.converged.all())
     assert res.iters[1] > res.iters[0]
+
+
+def test_stacked_and_list_forms_take_the_same_steps():
+    """The same problem given as one stacked tensor [B, S, n] (the fast path: one kernel per
+    vector operation over all blocks) and as a list of B block tensors takes the same iterates:
+    the two paths differ only in how the fp64 per-block sums are blocked, so the costs agree to
+    rounding along the whole run and both converge to the minimiser."""
+    fg, xs = quad_problem(S=2, B=3, n=30, seed=5)
+    x0 = torch.zeros_like(xs)
+    rs = lbfgs.minimize(fg, x0, max_iter=60, rel_tol=0.0)
+
+    def fg_list(blocks):
+        f, g = fg(torch.stack(blocks))
+        return f, [g[b] for b in range(g.shape[0])]
+    rl = lbfgs.minimize(fg_list, [x0[b].clone() for b in range(x0.shape[0])], max_iter=60, rel_tol=0.0)
+    assert isinstance(rs.x, torch.Tensor) and isinstance(rl.x, list)
+    assert rs.n_iter == rl.n_iter and rs.n_evals == rl.n_evals
+    for a, b in zip(rs.history, rl.history):
+        assert torch.allclose(a, b, rtol=1e-9, atol=0.0)
+    for b in range(3):
+        assert torch.allclose(rs.x[b], rl.x[b], rtol=1e-7, atol=1e-12 * float(xs[b].abs().max()))

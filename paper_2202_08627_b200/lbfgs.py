@@ -384,6 +384,37 @@ def ei_objective_drift(plan, flat, mask, s_exp, lam: float = 1e-2, ws=None, chec
     return fg
 
 
+def ei_objective_drift_stacked(plan, flat, mask, s_exp, lam: float = 1e-2, ws=None, check: bool = True):
+    """The joint maps + drift problem of `ei_objective_drift` in the optimizer's stacked form (one
+    tensor per vector, so the loop runs its one-kernel vector operations): x = [4, 1, L] with
+    L = max(S N^2, N_theta); blocks 0-2 hold mu, delta, sigma flattened over the stack, block 3 the
+    drift m_o(theta) in its first N_theta entries and zeros after them (their gradient is exactly 0,
+    so they stay 0 and add nothing to any dot product).  Returns (fg, x0, split) with
+    split(x) -> (mu, delta, sigma [S, N, N], m_o [N_theta])."""
+    from . import ei
+    S, N, NA, ND, M = plan.shape
+    ws = ws or ei.Workspace(plan, s_exp.device)
+    n, L = S * N * N, max(S * N * N, NA)
+    x0 = torch.zeros(4, 1, L, device=s_exp.device)
+
+    def split(x: torch.Tensor):
+        return (x[0, 0, :n].view(S, N, N), x[1, 0, :n].view(S, N, N), x[2, 0, :n].view(S, N, N),
+                x[3, 0, :NA])
+
+    def fg(x: torch.Tensor):
+        mu, de, sg, mo = split(x.contiguous())
+        ws.status.zero_()
+        ei.ei_cost_grad_drift(plan, mu, de, sg, flat, mask, mo, s_exp, lam, ws.cost, ws.g[0], ws.g[1],
+                              ws.g[2], ws.g_drift, ws.status)
+        if check:
+            _check_status(ws.status, "ei_cost_grad_drift")
+        g = torch.zeros_like(x0)
+        g[0:3, 0, :n].copy_(ws.g.reshape(3, n))
+        g[3, 0, :NA].copy_(ws.g_drift.double().sum(0).float())
+        return ws.cost.sum().reshape(1), g
+    return fg, x0, split
+
+
 def ei_objective_h(plan, gamma: float, flat, mask, drift, s_exp, lam: float = 1e-2,
                    flat_samples: bool = False, check: bool = True):
     """fg(x) for x = [1, S, N, N] (the paper's single map h, eq. 4 with mu = gamma^-1 delta = h,

@@ -98,17 +98,28 @@ def test_lbfgs_matches_scipy_on_oracle(mods):
     assert abs(float(res.cost[0]) - ref.fun) <= 1e-5 * ref.fun, (float(res.cost[0]), ref.fun)
 
 
+@pytest.mark.parametrize("form", ["list", "stacked"])
 @pytest.mark.parametrize("noise", [False, True])
-def test_joint_drift_c4_geometry(mods, noise):
+def test_joint_drift_c4_geometry(mods, noise, form):
     ei, lbfgs = mods
     cfg = dataclasses.replace(synth.CONFIGS["C4"], S=4)
     case = _cases.oracle_case(cfg, noise=noise)
-    fg = lbfgs.ei_objective_drift(plan_for(ei, cfg), d(case.flat), d(case.mask), d(case.s_exp), 0.0, check=False)
-    x0 = ([torch.zeros(1, cfg.S, cfg.N, cfg.N, device="cuda") for _ in range(3)] +
-          [torch.zeros(1, cfg.n_angles, device="cuda")])
+    plan = plan_for(ei, cfg)
+    if form == "list":
+        fg = lbfgs.ei_objective_drift(plan, d(case.flat), d(case.mask), d(case.s_exp), 0.0, check=False)
+        x0 = ([torch.zeros(1, cfg.S, cfg.N, cfg.N, device="cuda") for _ in range(3)] +
+              [torch.zeros(1, cfg.n_angles, device="cuda")])
+        drift_of = lambda x: x[3][0]
+    else:   # the same problem as one stacked tensor (maps and the zero-padded drift block)
+        fg, x0, split = lbfgs.ei_objective_drift_stacked(plan, d(case.flat), d(case.mask), d(case.s_exp), 0.0,
+                                                        check=False)
+        drift_of = lambda x: split(x)[3]
     target = float(case.s_exp.astype(np.float64).sum()) if noise else None
     res = lbfgs.minimize(fg, x0, max_iter=150, target=target)
-    e = _cases.drift_rms(res.x[3][0].cpu().numpy(), case.drift.astype(np.float64))
+    if form == "stacked":
+        pad = res.x[3, 0, cfg.n_angles:]
+        assert bool((pad == 0).all())                   # the padding never moves
+    e = _cases.drift_rms(drift_of(res.x).cpu().numpy(), case.drift.astype(np.float64))
     assert e < (0.05 if noise else 1e-3), e
     if noise:
         assert res.reason == ["target"], res.reason

@@ -67,15 +67,15 @@ def main():
     if args.stop == "discrepancy":
         target = case.s_exp.astype(np.float64).reshape(cfg.S, -1).sum(1)
     if args.drift_slices:
-        fg = lbfgs.ei_objective_drift(plan, d(case.flat), d(case.mask), d(case.s_exp), args.lam)
-        x0 = ([torch.zeros(1, cfg.S, cfg.N, cfg.N, device=dev) for _ in range(3)] +
-              [torch.zeros(1, cfg.n_angles, device=dev)])
+        # one stacked tensor (maps + zero-padded drift block): the optimizer's one-kernel vector path
+        fg, x0, split = lbfgs.ei_objective_drift_stacked(plan, d(case.flat), d(case.mask), d(case.s_exp), args.lam)
         if target is not None:
             target = target.sum()
 
         def errs(x):
-            e = {q: rms_of_range(x[i][0].cpu().numpy(), truth[i]) for i, q in enumerate(("mu", "delta", "sigma"))}
-            e["drift"] = drift_rms(x[3][0].cpu().numpy(), case.drift.astype(np.float64))
+            parts = split(x)
+            e = {q: rms_of_range(parts[i].cpu().numpy(), truth[i]) for i, q in enumerate(("mu", "delta", "sigma"))}
+            e["drift"] = drift_rms(parts[3].cpu().numpy(), case.drift.astype(np.float64))
             return e
     else:
         fg = lbfgs.ei_objective(plan, d(case.flat), d(case.mask), None if case.drift is None else d(case.drift),

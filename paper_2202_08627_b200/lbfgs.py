@@ -275,8 +275,8 @@ def minimize(fg: Callable, x0: Union[torch.Tensor, Sequence[torch.Tensor]], max_
         bad = d0 >= 0                          # not a descent direction: steepest descent
         p = _where(bad, sd_dir, p)
         d0 = torch.where(bad, _sdot_r(g, p), d0)
-        d0h = d0.cpu().numpy()
-        bad_h = bad.cpu().numpy()
+        db = torch.stack([d0, bad.to(d0.dtype)]).cpu().numpy()   # one device -> host transfer
+        d0h, bad_h = db[0], db[1] != 0
         sd_now = sd | bad_h
         active = ~done
         x_new, f_new, g_new, step, ok, nev = strong_wolfe(fgb, x, fh, g, p, d0h, active, c1, c2, max_ls, sdot=_sdot_r)

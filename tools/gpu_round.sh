@@ -1,7 +1,7 @@
 #!/bin/bash
 # One GPU-box pass: parity tests, smoke, bench lines for every config, ncu launch list of the
 # default bench command and one `--set full` capture of K1/K3/K2.  Usage (under gpurun):
-#   bash tools/gpu_round.sh TAG [what...]     what ⊂ {tests smoke bench ref ncu full peaks eicheck}
+#   bash tools/gpu_round.sh TAG [what...]     what ⊂ {tests smoke bench ref ncu full peaks eicheck recon}
 set -u
 TAG=${1:-run}; shift || true
 WHAT=${*:-tests smoke bench ncu full}
@@ -44,6 +44,9 @@ EOF
       EI_NVCC_DEFS=-DEI_CHECK timeout 1500 python -m pytest tests/test_gpu_parity.py tests/test_gpu_fullsize.py tests/test_gpu_limits.py -m gpu -x -q > $OUT/pytest_gpu_eicheck.log 2>&1
       echo "eicheck rc=$?" | tee -a $OUT/rc.txt; tail -2 $OUT/pytest_gpu_eicheck.log
       python -c "from paper_2202_08627_b200 import build; build.build()" >> $OUT/build.log 2>&1 ;;
+    recon)
+      # NEXT-1 / NEXT-2 full reconstructions (tools/recon_runs.sh) into $OUT/recon.jsonl
+      bash tools/recon_runs.sh $TAG > $OUT/recon.log 2>&1; echo "recon rc=$?" | tee -a $OUT/rc.txt ;;
     peaks)
       timeout 600 python tools/measure_peaks.py $OUT/peaks.json > $OUT/peaks.log 2>&1; echo "peaks rc=$?" | tee -a $OUT/rc.txt
       tail -c 400 $OUT/peaks.json ;;

@@ -1,4 +1,6 @@
 # A/B: K1 CTAs of 32 angles (EI_K1_X2=1: 16 consumer warps, 1 CTA per SM, one staged window for
+# (The variant this script switched on was removed after the measurement recorded in DESIGN.md §5
+# "Measured and rejected"; its knob no longer exists, so both arms now run the same code.)
 # both 16-angle halves) vs the default 16-angle CTAs at 2 per SM; parity first
 OUT=gpurun_out/abx2; mkdir -p $OUT
 python -c "import __graft_entry__ as g; g.build()" > $OUT/build.log 2>&1

@@ -1,4 +1,6 @@
 # A/B: K3 original (2 pixel pairs x 256 threads) vs the generic kernel's 2-pair instance
+# (The variant this script switched on was removed after the measurement recorded in DESIGN.md §5
+# "Measured and rejected"; its knob no longer exists, so both arms now run the same code.)
 # (EI_K3_GEN=1) vs its 4-pair instance (EI_K3_P4=1: 128 consumer threads, 4 CTAs per SM)
 OUT=gpurun_out/abp4b; mkdir -p $OUT
 python -c "import __graft_entry__ as g; g.build()" > $OUT/build.log 2>&1

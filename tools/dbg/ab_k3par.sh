@@ -1,4 +1,6 @@
 # A/B: K3 per-angle tables from the kernel-parameter bank (default) vs the staged records
+# (The variant this script switched on was removed after the measurement recorded in DESIGN.md §5
+# "Measured and rejected"; its knob no longer exists, so both arms now run the same code.)
 # (EI_K3_SMEMTAB=1), device-timed step and per-kernel ms, 2 repeats
 OUT=gpurun_out/abk3; mkdir -p $OUT
 python -c "import __graft_entry__ as g; g.build()" > $OUT/build.log 2>&1
